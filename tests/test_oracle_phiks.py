@@ -1,0 +1,211 @@
+"""Pins of the oracle's PHIKS algorithm (§3) against dense brute force,
+closed forms and PAPER.md Table 1.  CPU only."""
+import json
+import math
+import os
+
+import mpmath
+import numpy as np
+import pytest
+
+from oracle import phiks_oracle as O
+from oracle import dense as D
+from paper_2210_07667_b200 import workloads as W
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = 2.0 ** -53
+
+
+def relinf(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def _cases(n_cases, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for c in range(n_cases):
+        d = int(rng.integers(1, 4))
+        dims = tuple(int(x) for x in rng.integers(2, 7, size=d))
+        tau = [1.0, 0.1, 0.7][c % 3]
+        fac = W.random_factors(dims, seed=1000 + c, scale=float(rng.uniform(0.5, 5.0)),
+                               complex_=bool(c % 2))
+        out.append((dims, tau, fac, c))
+    return out
+
+
+@pytest.mark.parametrize("dims,tau,fac,c", _cases(12, 1))
+def test_same_vector_vs_dense(dims, tau, fac, c):
+    p = 1 + c % 5
+    n_scales = 1 + c % 3
+    ells = tuple(range(0, p + 1))
+    V = W.random_tensor(dims, seed=50 + c, complex_=bool(c % 2))
+    res = O.phiks(fac, tau, "same", ells, [V], n_scales=n_scales, tol=TOL)
+    K = D.assemble_K(fac) * tau
+    assert res.plan.s >= n_scales - 1
+    for j in range(n_scales):
+        for ell in ells:
+            ref = D.lincomb_augmented(K / 2 ** j, {ell: W.as_flat(V)})
+            assert relinf(W.as_flat(res.out[(ell, j)]), ref) <= 1e-11, (ell, j)
+
+
+@pytest.mark.parametrize("dims,tau,fac,c", _cases(12, 2))
+def test_lincomb_vs_dense(dims, tau, fac, c):
+    p = 1 + c % 5
+    n_scales = 1 + c % 3
+    ells = tuple(range(0, p + 1))
+    vs = [W.random_tensor(dims, seed=80 + c * 7 + k, complex_=bool(c % 2)) for k in ells]
+    res = O.phiks(fac, tau, "lincomb", ells, vs, n_scales=n_scales, tol=TOL)
+    K = D.assemble_K(fac) * tau
+    for j in range(n_scales):
+        # Eq. (19): exp(c K)v0 + Σ c^ℓ φ_ℓ(cK) v_ℓ, c = 2^-j
+        vd = {ell: W.as_flat(v) / 2.0 ** (ell * j) for ell, v in zip(ells, vs)}
+        ref = D.lincomb_augmented(K / 2 ** j, vd)
+        assert relinf(W.as_flat(res.out[j]), ref) <= 1e-11, j
+
+
+def test_lincomb_missing_orders_and_no_exp_term():
+    fac = W.random_factors((3, 4), seed=9, scale=3.0)
+    vs = {2: W.random_tensor((3, 4), seed=1), 4: W.random_tensor((3, 4), seed=2)}
+    res = O.phiks(fac, 1.0, "lincomb", tuple(vs), list(vs.values()), n_scales=2, tol=TOL)
+    K = D.assemble_K(fac)
+    for j in range(2):
+        ref = D.lincomb_augmented(K / 2 ** j, {l: W.as_flat(v) / 2.0 ** (l * j) for l, v in vs.items()})
+        assert relinf(W.as_flat(res.out[j]), ref) <= 1e-11
+
+
+def _validation_operator(n, d):
+    # PAPER.md §4.1 l.1071-1082: (1+i)/100·Δ, Dirichlet, v = 4096(1+i)∏ x(1-x)
+    A = (1 + 1j) / 100 * W.fd_dxx_dirichlet(n)
+    h = 1.0 / (n + 1)
+    x = np.arange(1, n + 1) * h
+    f = x * (1 - x)
+    V = 4096 * (1 + 1j) * f
+    for _ in range(d - 1):
+        V = np.multiply.outer(V, f)
+    return [A] * d, V
+
+
+@pytest.mark.parametrize("mode", ["same", "lincomb"])
+def test_validation_mirror_fig1(mode):
+    # Fig. 1 analogue at oracle scale: d=3, n=6, p=5, tol 2^-53, scales j=0,1
+    fac, V = _validation_operator(6, 3)
+    K = D.assemble_K(fac)
+    ells = (1, 2, 3, 4, 5)
+    vs = [V] * 5 if mode == "lincomb" else [V]
+    res = O.phiks(fac, 1.0, mode, ells, vs, n_scales=2, tol=TOL)
+    for j in range(2):
+        if mode == "same":
+            for ell in ells:
+                ref = D.lincomb_augmented(K / 2 ** j, {ell: W.as_flat(V)})
+                assert relinf(W.as_flat(res.out[(ell, j)]), ref) <= 1e-11
+        else:
+            ref = D.lincomb_augmented(K / 2 ** j, {l: W.as_flat(V) / 2.0 ** (l * j) for l in ells})
+            assert relinf(W.as_flat(res.out[j]), ref) <= 1e-11
+
+
+def test_zero_operator_gives_inverse_factorials():
+    dims = (3, 4, 2)
+    fac = [np.zeros((n, n)) for n in dims]
+    V = W.random_tensor(dims, seed=5)
+    res = O.phiks(fac, 1.0, "same", (0, 1, 2, 3, 4, 5), [V], n_scales=2, tol=TOL)
+    for (ell, j), out in res.out.items():
+        assert np.abs(out - V / math.factorial(ell)).max() <= 1e-15 * np.abs(V).max()
+    vs = [W.random_tensor(dims, seed=6 + k) for k in range(3)]
+    res = O.phiks(fac, 1.0, "lincomb", (0, 1, 2), vs, tol=TOL)
+    ref = vs[0] + vs[1] + vs[2] / 2
+    assert np.abs(res.out[0] - ref).max() <= 1e-14
+
+
+def test_scalar_phi1_closed_form():
+    res = O.phiks([np.array([[-1.0]])], 1.0, "same", (1,), [np.array([2.0])], tol=TOL)
+    assert abs(res.out[(1, 0)][0] - 2.0 * (1 - math.exp(-1))) <= 1e-15
+
+
+def _phi_mp(ell, z):
+    mpmath.mp.dps = 50
+    z = mpmath.mpf(z)
+    if ell == 0:
+        return float(mpmath.exp(z))
+    return float(sum(z ** k / mpmath.factorial(k + ell) for k in range(400)))
+
+
+def test_diagonal_factors_factorise():
+    # A_μ diagonal -> K diagonal with entries Σ λ: φ_ℓ(K)v = φ_ℓ(λ_i+λ_j+λ_k) v_ijk
+    rng = np.random.default_rng(3)
+    dims = (5, 4, 3)
+    lams = [rng.uniform(-6, 1, size=n) for n in dims]
+    fac = [np.diag(l) for l in lams]
+    V = W.random_tensor(dims, seed=7)
+    res = O.phiks(fac, 1.0, "same", (0, 1, 2, 3), [V], n_scales=1, tol=TOL)
+    lam = lams[0][:, None, None] + lams[1][None, :, None] + lams[2][None, None, :]
+    for ell in (0, 1, 2, 3):
+        ref = np.vectorize(lambda z: _phi_mp(ell, z))(lam) * V
+        assert relinf(res.out[(ell, 0)], ref) <= 1e-12
+
+
+def test_multiscale_equals_fresh_call():
+    fac = W.random_factors((4, 5), seed=31, scale=4.0)
+    V = W.random_tensor((4, 5), seed=8)
+    res = O.phiks(fac, 2.0, "same", (0, 1, 2), [V], n_scales=3, tol=TOL)
+    for j in range(3):
+        fresh = O.phiks(fac, 2.0 / 2 ** j, "same", (0, 1, 2), [V], n_scales=1, tol=TOL)
+        for ell in (0, 1, 2):
+            assert relinf(res.out[(ell, j)], fresh.out[(ell, 0)]) <= 1e-12
+
+
+def test_tucker_ops_telemetry():
+    fac = W.random_factors((4, 3, 2), seed=2, scale=6.0)
+    V = W.random_tensor((4, 3, 2), seed=9)
+    res = O.phiks(fac, 1.0, "same", (1, 2, 3), [V], n_scales=1, tol=TOL)
+    pl = res.plan
+    # endpoint θ_q = 1 needs no Tucker operator (l.948-952): one less than Eq. (14)
+    assert res.tucker_ops == (pl.q - 1) + pl.s * 3
+    assert res.tucker_ops < O.tucker_count("same", pl.s, 1, pl.q, 3)
+
+
+# ---------------------------------------------------------------- Table 1 pins
+
+
+def _table1():
+    with open(os.path.join(GOLD, "table1.json")) as f:
+        return json.load(f)
+
+
+def _validation_plan_inputs(n, d):
+    A = (1 + 1j) / 100 * W.fd_dxx_dirichlet(n)
+    h = 1.0 / (n + 1)
+    x = np.arange(1, n + 1) * h
+    nv = 4096 * math.sqrt(2) * float(np.linalg.norm(x * (1 - x))) ** d
+    return O.range_rectangle([A] * d), nv
+
+
+@pytest.mark.parametrize("mode,row", [("same", r) for r in _table1()["same_vector"]]
+                         + [("lincomb", r) for r in _table1()["linear_combination"]])
+def test_table1_q_at_paper_s(mode, row):
+    """PAPER.md Table 1: with the paper's s, the §3.3 criterion (tolerance
+    2^-53, reading R2: absolute δ for this validation) selects the paper's q."""
+    t = _table1()
+    rect, nv = _validation_plan_inputs(row["n"], row["d"])
+    p = t["p"]
+    norms = [nv] if mode == "same" else [nv] * p
+    q = O.q_for_s(mode, rect, p, norms, t["tol"], row["s"])
+    assert q == row["q"]
+
+
+def test_table1_same_vector_T_formula():
+    t = _table1()
+    for row in t["same_vector"]:
+        assert O.tucker_count("same", row["s"], t["s_hat"], row["q"], t["p"]) == row["T"]
+
+
+def test_table1_plan_not_costlier_than_paper():
+    """The literal §3.3 stopping rule (reading R6) never picks a plan with a
+    larger Eq. (14)/(19) count than the paper's Table 1 choice."""
+    t = _table1()
+    for mode, key in (("same", "same_vector"), ("lincomb", "linear_combination")):
+        row = [r for r in t[key] if r["d"] == 6 and r["n"] == 8][0]
+        rect, nv = _validation_plan_inputs(row["n"], row["d"])
+        norms = [nv] if mode == "same" else [nv] * t["p"]
+        pl = O.select_plan(mode, rect, t["p"], norms, t["tol"], t["s_hat"])
+        paper_T = O.tucker_count(mode, row["s"], t["s_hat"], row["q"], t["p"])
+        assert pl.T <= paper_T
