@@ -1,0 +1,190 @@
+/*
+ * phiks.h — C ABI of the B200-native PHIKS library (libphiks.so).
+ *
+ * PHIKS computes actions of φ-functions of a Kronecker sum
+ *     K = A_d ⊕ … ⊕ A_1 = Σ_μ I_d ⊗ … ⊗ A_μ ⊗ … ⊗ I_1      (§2 Eq. (3), l.214-219)
+ * without forming K, by Gauss–Lobatto–Legendre quadrature of the integral
+ *     φ_ℓ(X) = ∫_0^1 θ^{ℓ-1}/(ℓ-1)! exp((1-θ)X) dθ           (Eq. (2), l.78-82)
+ * at the scaled matrix τK/2^s, evaluated with Tucker operators (μ-mode
+ * products with exp((1-θ_i)τA_μ/2^s), Eq. (10), l.471-477), followed
+ * by the modified squaring recurrences (Eq. (12) l.554-563, Eq. (18) l.734-746).
+ * The choice of s and q follows §3.3 (l.779-960).  See DESIGN.md for readings.
+ *
+ * Memory layout ("vec ... stacks the columns"): an order-d
+ * tensor of size n_1×…×n_d is a contiguous fp64 array in column-major order,
+ * element (i_1,…,i_d) at offset i_1 + n_1*(i_2 + n_2*(… + n_{d-1}*i_d)).
+ * Matrices are n×n column-major fp64.
+ *
+ * Every compute step runs in CUDA kernels of this library (sm_100a).  There is
+ * no CPU fallback: without a CUDA device every entry point that computes
+ * returns PHIKS_ERR_CUDA.
+ *
+ * Error behaviour: every function returns a phiks_status; on error nothing is
+ * written to the outputs' contents beyond what kernels already wrote, and
+ * phiks_last_error() returns a human-readable message for the calling thread.
+ * Handles are not thread-safe: one handle must not be used by two host
+ * threads at once.  Distinct handles are independent.
+ */
+#ifndef PHIKS_H_
+#define PHIKS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PHIKS_OK = 0,
+  PHIKS_ERR_ARG = 1,        /* invalid argument (dimension, order, null pointer, ...) */
+  PHIKS_ERR_CUDA = 2,       /* CUDA runtime error or no CUDA device                  */
+  PHIKS_ERR_PLAN = 3,       /* §3.3 search found no admissible (s, q)                */
+  PHIKS_ERR_NOMEM = 4,      /* device or pinned-host allocation failed               */
+  PHIKS_ERR_WORKSPACE = 5,  /* caller workspace too small (see phiks_stats)          */
+  PHIKS_ERR_LIMIT = 6       /* request exceeds a compiled limit (PHIKS_MAX_*)        */
+} phiks_status;
+
+#define PHIKS_MAX_D 8       /* tensor order d                                        */
+#define PHIKS_MAX_P 6       /* highest φ order ℓ                                     */
+#define PHIKS_MAX_SCALES 16 /* output time scales ŝ                                  */
+#define PHIKS_MAX_N 4096    /* largest n_μ                                           */
+
+typedef enum {
+  /* φ_ℓ(τK/2^j) v for every ℓ in `ells`, j = 0..n_scales-1, one vector v
+     (§3.1, formulas (6) and (13)).  ℓ = 0 means exp(τK/2^j) v. */
+  PHIKS_MODE_SAME_VECTOR = 0,
+  /* exp(τK/2^j) v_0 + Σ_{ℓ≥1} φ_ℓ(τK/2^j) v_ℓ / 2^{ℓj}, j = 0..n_scales-1
+     (§3.2, formulas (7) and (19) with c = 1); vecs[i] pairs with ells[i]. */
+  PHIKS_MODE_LINCOMB = 1
+} phiks_mode;
+
+typedef enum {
+  PHIKS_MEM_DEVICE = 0, /* vecs/outs are device pointers; apply is stream-asynchronous  */
+  PHIKS_MEM_HOST = 1    /* vecs/outs are host pointers (pinned recommended); the library
+                           copies them through device staging and synchronises the
+                           stream before returning                                       */
+} phiks_mem_kind;
+
+/* Opaque handle: the factor matrices A_μ (copied to device at create), their
+   per-factor numerical-range data and cached plans/workspace. */
+typedef struct phiks_ctx* phiks_handle;
+
+typedef struct {
+  int mode;          /* phiks_mode                                                   */
+  int n_ells;        /* number of entries of ells, 1..PHIKS_MAX_P+1                   */
+  const int* ells;   /* host array of strictly increasing orders in [0, PHIKS_MAX_P]  */
+  int n_scales;      /* ŝ ≥ 1: outputs at τ/2^j, j = 0..ŝ-1 (forces s ≥ ŝ-1)         */
+  double tau;        /* time step τ > 0; the operator is τK                           */
+  double tol;        /* relative tolerance (reading R2); ≤ 0 → 2^-53        */
+  int force_s;       /* ≥ 0: use this s instead of the §3.3 search (testing); else -1 */
+  int force_q;       /* ≥ 2: use this q (with force_s); else -1                       */
+  int mem_kind;      /* phiks_mem_kind of vecs and outs                               */
+} phiks_request;
+
+typedef struct {
+  int s;             /* scaling parameter s                                            */
+  int q;             /* number of GLL quadrature nodes (0 when only ℓ = 0 requested)   */
+  int T_formula;     /* Tucker count of Eq. (14) (same vector) or Eq. (19) (lincomb)   */
+  int T_executed;    /* Tucker operators the library actually runs for the request     */
+} phiks_plan_info;
+
+typedef struct {
+  phiks_plan_info plan;     /* plan of the last apply                               */
+  int64_t kernel_launches;  /* CUDA kernels launched by the last apply              */
+  int64_t tucker_ops;       /* Tucker operators executed by the last apply          */
+  double mu_mode_flops;     /* 2·N·Σ_μ n_μ per Tucker operator, summed              */
+  double expm_flops;        /* flops of the small-matrix exponential stage          */
+  size_t workspace_bytes;   /* device workspace the last apply needed               */
+  int64_t total_kernel_launches; /* since create                                    */
+} phiks_stats;
+
+/* Create a handle for K = A_d ⊕ … ⊕ A_1.
+   d: 1..PHIKS_MAX_D.  n[μ]: 1..PHIKS_MAX_N, μ = 0..d-1 (paper's μ = 1..d).
+   A_host[μ]: host pointer to the n[μ]×n[μ] column-major real matrix A_μ; the
+   library copies it (caller keeps ownership).  Identical factors (bitwise) are
+   detected and share their exponentials.  Computes the per-factor numerical-
+   range rectangle data of PAPER.md l.925-936 (reading R1) on the host.
+   *out receives the handle; destroy it with phiks_destroy. */
+phiks_status phiks_create(int d, const int* n, const double* const* A_host, phiks_handle* out);
+
+/* Release the handle and every device/pinned buffer it owns.  NULL is a no-op. */
+phiks_status phiks_destroy(phiks_handle h);
+
+/* §3.3 plan for `req` without computing anything on the device.
+   vec_norms: host array of ||v_ℓ||_2 for ℓ = 1..p (lincomb mode, index ℓ-1;
+   0 for orders not present); ignored (may be NULL) in same-vector mode. */
+phiks_status phiks_plan(phiks_handle h, const phiks_request* req, const double* vec_norms,
+                        phiks_plan_info* out);
+
+/* Apply the request.
+   vecs: n_vecs pointers to input tensors (same-vector: n_vecs == 1;
+         lincomb: n_vecs == n_ells, vecs[i] is v_{ells[i]}).
+   outs: output tensors, caller-allocated, N doubles each, never aliasing vecs.
+         same-vector: n_ells*n_scales pointers, outs[j*n_ells + i] = φ_{ells[i]}(τK/2^j)v.
+         lincomb:     n_scales pointers, outs[j] = result at scale j.
+   workspace: device buffer of ws_bytes, or NULL to let the library allocate and
+         cache its own (grown on demand, freed by phiks_destroy).
+   stream: cudaStream_t (NULL = legacy default stream).
+   With PHIKS_MEM_DEVICE the call only enqueues work on `stream` (plus, in
+   lincomb mode, one device→host read of the vector norms for the §3.3 plan). */
+phiks_status phiks_apply(phiks_handle h, const phiks_request* req, int n_vecs,
+                         const double* const* vecs, double* const* outs, void* workspace,
+                         size_t ws_bytes, void* stream);
+
+/* Device workspace (bytes) phiks_apply needs for `req` under `plan`. */
+phiks_status phiks_workspace_size(phiks_handle h, const phiks_request* req,
+                                  const phiks_plan_info* plan, size_t* bytes);
+
+/* Telemetry of the last phiks_apply on this handle. */
+phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out);
+
+/* One batched μ-mode product (cost O(N n_μ)):
+   out_b = in_b ×_{mu+1} M_b for b = 0..batch-1, tensors of dims n[0..d-1],
+   M_b n[mu]×n[mu] column-major; all pointers device.  The building block of
+   the Tucker operator, exposed for tests and benchmarks. */
+phiks_status phiks_mode_product(int d, const int* n, int mu, int batch, const double* const* in,
+                                const double* const* M, double* const* out, void* stream);
+
+/* Tucker operator (Eq. (4)): out = in ×_1 M_0 ×_2 M_1 … ×_d M_{d-1},
+   device pointers; scratch: 2*N doubles of device memory (NULL if d == 1). */
+phiks_status phiks_tucker(int d, const int* n, const double* in, const double* const* M,
+                          double* out, double* scratch, void* stream);
+
+/* exp(c·A) for a device n×n column-major A into device E (scaling and squaring,
+   degree-16 Taylor with Paterson–Stockmeyer); scratch: 8*n*n doubles. */
+phiks_status phiks_expm(int n, const double* A, double c, double* E, double* scratch,
+                        void* stream);
+
+/* FP64 peak microbenchmark: launches `blocks` CTAs running `iters` iterations
+   of register-resident DMMA (kind 0) or DFMA (kind 1) chains; writes a
+   checksum to sink (device, one double per thread of the grid).  *flops
+   receives the number of floating-point operations the launch performs. */
+phiks_status phiks_fp64_peak_launch(int kind, int blocks, int64_t iters, double* sink,
+                                    void* stream, double* flops);
+
+/* Host-only §3.3 planning (no device needed): same as phiks_plan for the
+   factors A_host (real, column-major, host) without creating a handle. */
+phiks_status phiks_plan_host(int d, const int* n, const double* const* A_host, const phiks_request* req,
+                             const double* vec_norms, phiks_plan_info* out);
+
+/* Host-only §3.3 search on an explicit rectangle Ξ = (center_re + i center_im)
+   + [-hr, hr] + i[-hi, hi] ⊇ W(τK), absolute tolerance
+   delta, norms[k-1] = ||v_k|| (lincomb) or norms[0] = ||v|| (same vector).
+   s_fixed ≥ 0: only the smallest admissible q at that s is returned in out->q
+   (0 if none) with out->s = s_fixed; otherwise the full search from s_min.
+   Lets the planner be checked against PAPER.md Table 1 (complex operator). */
+phiks_status phiks_select_plan(int mode, double center_re, double center_im, double hr, double hi, int p,
+                               const double* norms, double delta, int s_hat, int s_min, int s_fixed,
+                               phiks_plan_info* out);
+
+/* Message for the last error on the calling thread ("" if none). */
+const char* phiks_last_error(void);
+
+/* Library version string. */
+const char* phiks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHIKS_H_ */

@@ -1,0 +1,191 @@
+"""B200-native PHIKS: actions of φ-functions of Kronecker sums on FP64 tensor cores.
+
+User API (thin marshalling over the C ABI of include/phiks.h; PyTorch only
+provides device memory and streams):
+
+    from paper_2210_07667_b200 import PhiKS
+    op = PhiKS([A1, A2, A3])                    # numpy factor matrices A_μ
+    outs = op.apply(tau, [0, 1, 2], [v])        # φ_ℓ(τK)v, torch fp64 cuda tensors
+    comb = op.apply(tau, [0, 1, 2], [v0, v1, v2], mode="lincomb")
+
+Tensors are column-major n_1×…×n_d (§2 vec convention): a torch
+tensor of shape (n_d, …, n_1) in C order, or any contiguous tensor with N
+elements in that order.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import MEM_DEVICE, MEM_HOST, MODE_LINCOMB, MODE_SAME_VECTOR, PhiksError
+
+__all__ = ["PhiKS", "PhiksError", "mode_product", "tucker", "expm", "fp64_peak_launch", "version"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _check_dev(t, N: Optional[int] = None):
+    torch = _torch()
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError("expected a contiguous float64 CUDA tensor")
+    if N is not None and t.numel() != N:
+        raise ValueError(f"tensor has {t.numel()} elements, expected {N}")
+    return t.data_ptr()
+
+
+def version() -> str:
+    return _lib.load().phiks_version().decode()
+
+
+class PhiKS:
+    """Handle on K = A_d ⊕ … ⊕ A_1 (phiks_create / phiks_destroy)."""
+
+    def __init__(self, factors: Sequence[np.ndarray]):
+        lib = _lib.load()
+        self.d = len(factors)
+        self.dims = tuple(int(np.asarray(a).shape[0]) for a in factors)
+        self.N = int(np.prod(self.dims))
+        self._A = [np.asfortranarray(np.asarray(a, dtype=np.float64)) for a in factors]
+        for a in self._A:
+            if a.ndim != 2 or a.shape[0] != a.shape[1]:
+                raise ValueError("factor matrices must be square")
+        n_arr = (ctypes.c_int * self.d)(*self.dims)
+        a_arr = _lib.ptr_array([a.ctypes.data for a in self._A])
+        h = ctypes.c_void_p()
+        _lib.check(lib.phiks_create(self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.load().phiks_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    def plan(self, tau: float, ells: Sequence[int], mode: str = "same", n_scales: int = 1,
+             tol: float = 0.0, vec_norms: Optional[Sequence[float]] = None) -> dict:
+        lib = _lib.load()
+        req = _lib.make_request(self._mode(mode), ells, n_scales, tau, tol)
+        info = _lib.PlanInfo()
+        norms = None
+        if vec_norms is not None:
+            norms = (ctypes.c_double * len(vec_norms))(*vec_norms)
+        _lib.check(lib.phiks_plan(self._h, ctypes.byref(req), norms, ctypes.byref(info)), "phiks_plan")
+        return {"s": info.s, "q": info.q, "T_formula": info.T_formula, "T_executed": info.T_executed}
+
+    @staticmethod
+    def _mode(mode) -> int:
+        if mode in ("same", MODE_SAME_VECTOR):
+            return MODE_SAME_VECTOR
+        if mode in ("lincomb", MODE_LINCOMB):
+            return MODE_LINCOMB
+        raise ValueError(f"unknown mode {mode!r}")
+
+    def apply(self, tau: float, ells: Sequence[int], vecs: Sequence, mode: str = "same", n_scales: int = 1,
+              tol: float = 0.0, outs: Optional[Sequence] = None, force_s: int = -1, force_q: int = -1,
+              stream=None, workspace=None):
+        """Run phiks_apply.  vecs/outs are contiguous fp64 CUDA tensors
+        (PHIKS_MEM_DEVICE) or numpy arrays (PHIKS_MEM_HOST; then outs are
+        returned as numpy arrays).  Returns the list of outputs: same-vector →
+        outs[j*len(ells)+i] = φ_{ells[i]}(τK/2^j)v; lincomb → outs[j]."""
+        lib = _lib.load()
+        m = self._mode(mode)
+        host = isinstance(vecs[0], np.ndarray)
+        nouts = len(ells) * n_scales if m == MODE_SAME_VECTOR else n_scales
+        if host:
+            vecs = [np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1, order="F")) for v in vecs]
+            for v in vecs:
+                if v.size != self.N:
+                    raise ValueError("vector size mismatch")
+            if outs is None:
+                outs = [np.empty(self.N) for _ in range(nouts)]
+            vptr = [v.ctypes.data for v in vecs]
+            optr = [o.ctypes.data for o in outs]
+            sptr = _stream_ptr(stream) if stream is not None else 0
+        else:
+            torch = _torch()
+            vptr = [_check_dev(v, self.N) for v in vecs]
+            if outs is None:
+                outs = [torch.empty(self.N, dtype=torch.float64, device=vecs[0].device) for _ in range(nouts)]
+            optr = [_check_dev(o, self.N) for o in outs]
+            sptr = _stream_ptr(stream)
+        req = _lib.make_request(m, ells, n_scales, tau, tol, force_s, force_q, MEM_HOST if host else MEM_DEVICE)
+        ws_ptr, ws_bytes = (None, 0)
+        if workspace is not None:
+            ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+        code = lib.phiks_apply(self._h, ctypes.byref(req), len(vecs), _lib.ptr_array(vptr), _lib.ptr_array(optr),
+                               ws_ptr, ws_bytes, sptr)
+        _lib.check(code, "phiks_apply")
+        return list(outs)
+
+    def stats(self) -> dict:
+        st = _lib.Stats()
+        _lib.check(_lib.load().phiks_get_stats(self._h, ctypes.byref(st)), "phiks_get_stats")
+        return {"s": st.plan.s, "q": st.plan.q, "T_formula": st.plan.T_formula, "T_executed": st.plan.T_executed,
+                "kernel_launches": st.kernel_launches, "tucker_ops": st.tucker_ops,
+                "mu_mode_flops": st.mu_mode_flops, "expm_flops": st.expm_flops,
+                "workspace_bytes": st.workspace_bytes, "total_kernel_launches": st.total_kernel_launches}
+
+
+# ----------------------------------------------------------------------
+def mode_product(dims: Sequence[int], mu: int, ins: Sequence, Ms: Sequence, outs: Sequence, stream=None):
+    """Batched μ-mode product out_b = in_b ×_{mu+1} M_b (0-based mu)."""
+    lib = _lib.load()
+    N = int(np.prod(dims))
+    n_arr = (ctypes.c_int * len(dims))(*dims)
+    _lib.check(lib.phiks_mode_product(len(dims), n_arr, int(mu), len(ins),
+                                      _lib.ptr_array([_check_dev(t, N) for t in ins]),
+                                      _lib.ptr_array([_check_dev(M) for M in Ms]),
+                                      _lib.ptr_array([_check_dev(t, N) for t in outs]), _stream_ptr(stream)),
+               "phiks_mode_product")
+
+
+def tucker(dims: Sequence[int], x, Ms: Sequence, out, scratch=None, stream=None):
+    lib = _lib.load()
+    torch = _torch()
+    N = int(np.prod(dims))
+    if scratch is None and len(dims) > 1:
+        scratch = torch.empty(2 * N, dtype=torch.float64, device=x.device)
+    n_arr = (ctypes.c_int * len(dims))(*dims)
+    _lib.check(lib.phiks_tucker(len(dims), n_arr, _check_dev(x, N), _lib.ptr_array([_check_dev(M) for M in Ms]),
+                                _check_dev(out, N), scratch.data_ptr() if scratch is not None else None,
+                                _stream_ptr(stream)), "phiks_tucker")
+
+
+def expm(A, c: float = 1.0, stream=None):
+    """exp(c·A) for a square fp64 CUDA matrix stored column-major (n*n elements)."""
+    lib = _lib.load()
+    torch = _torch()
+    n = int(round(A.numel() ** 0.5))
+    E = torch.empty_like(A)
+    scratch = torch.empty(8 * n * n, dtype=torch.float64, device=A.device)
+    _lib.check(lib.phiks_expm(n, _check_dev(A), float(c), E.data_ptr(), scratch.data_ptr(), _stream_ptr(stream)),
+               "phiks_expm")
+    return E
+
+
+def fp64_peak_launch(kind: int, blocks: int, iters: int, sink, stream=None) -> float:
+    """Launch the DMMA (kind 0) / DFMA (kind 1) microbenchmark; returns its flop count."""
+    lib = _lib.load()
+    fl = ctypes.c_double()
+    _lib.check(lib.phiks_fp64_peak_launch(int(kind), int(blocks), int(iters), _check_dev(sink), _stream_ptr(stream),
+                                          ctypes.byref(fl)), "phiks_fp64_peak_launch")
+    return fl.value

@@ -1,0 +1,107 @@
+"""ctypes binding of libphiks.so (include/phiks.h).  Argument marshalling only:
+every compute step runs in the library's CUDA kernels.  There is no fallback:
+if the library is missing or no CUDA device is present, calls raise."""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libphiks.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "phiks.h")
+
+MODE_SAME_VECTOR = 0
+MODE_LINCOMB = 1
+MEM_DEVICE = 0
+MEM_HOST = 1
+MAX_D, MAX_P, MAX_SCALES, MAX_N = 8, 6, 16, 4096
+
+_STATUS = {0: "PHIKS_OK", 1: "PHIKS_ERR_ARG", 2: "PHIKS_ERR_CUDA", 3: "PHIKS_ERR_PLAN",
+           4: "PHIKS_ERR_NOMEM", 5: "PHIKS_ERR_WORKSPACE", 6: "PHIKS_ERR_LIMIT"}
+
+
+class PhiksError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        super().__init__(f"{where}: {_STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Request(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int), ("n_ells", ctypes.c_int), ("ells", ctypes.POINTER(ctypes.c_int)),
+                ("n_scales", ctypes.c_int), ("tau", ctypes.c_double), ("tol", ctypes.c_double),
+                ("force_s", ctypes.c_int), ("force_q", ctypes.c_int), ("mem_kind", ctypes.c_int)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("s", ctypes.c_int), ("q", ctypes.c_int), ("T_formula", ctypes.c_int),
+                ("T_executed", ctypes.c_int)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("plan", PlanInfo), ("kernel_launches", ctypes.c_int64), ("tucker_ops", ctypes.c_int64),
+                ("mu_mode_flops", ctypes.c_double), ("expm_flops", ctypes.c_double),
+                ("workspace_bytes", ctypes.c_size_t), ("total_kernel_launches", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libphiks.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built — run __graft_entry__.build() (make -C paper_2210_07667_b200/csrc)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+    P = ctypes.POINTER
+    lib.phiks_create.argtypes = [i, P(i), P(vp), P(vp)]
+    lib.phiks_destroy.argtypes = [vp]
+    lib.phiks_plan.argtypes = [vp, P(Request), P(d), P(PlanInfo)]
+    lib.phiks_apply.argtypes = [vp, P(Request), i, P(vp), P(vp), vp, ctypes.c_size_t, vp]
+    lib.phiks_workspace_size.argtypes = [vp, P(Request), P(PlanInfo), P(ctypes.c_size_t)]
+    lib.phiks_get_stats.argtypes = [vp, P(Stats)]
+    lib.phiks_mode_product.argtypes = [i, P(i), i, i, P(vp), P(vp), P(vp), vp]
+    lib.phiks_tucker.argtypes = [i, P(i), vp, P(vp), vp, vp, vp]
+    lib.phiks_expm.argtypes = [i, vp, d, vp, vp, vp]
+    lib.phiks_fp64_peak_launch.argtypes = [i, i, ctypes.c_int64, vp, vp, P(d)]
+    lib.phiks_plan_host.argtypes = [i, P(i), P(vp), P(Request), P(d), P(PlanInfo)]
+    lib.phiks_select_plan.argtypes = [i, d, d, d, d, i, P(d), d, i, i, i, P(PlanInfo)]
+    lib.phiks_last_error.restype = ctypes.c_char_p
+    lib.phiks_version.restype = ctypes.c_char_p
+    for name in ("phiks_create", "phiks_destroy", "phiks_plan", "phiks_apply", "phiks_workspace_size",
+                 "phiks_get_stats", "phiks_mode_product", "phiks_tucker", "phiks_expm",
+                 "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def header_functions() -> list:
+    """Names of the functions include/phiks.h declares."""
+    import re
+    src = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"\b(phiks_[a-z0-9_]+)\s*\(", src)))
+
+
+def check(code: int, where: str) -> None:
+    if code != 0:
+        raise PhiksError(code, where, load().phiks_last_error().decode())
+
+
+def ptr_array(ptrs: Sequence[int]):
+    arr = (ctypes.c_void_p * max(len(ptrs), 1))()
+    for k, p in enumerate(ptrs):
+        arr[k] = ctypes.c_void_p(int(p))
+    return arr
+
+
+def make_request(mode: int, ells: Sequence[int], n_scales: int, tau: float, tol: float = 0.0,
+                 force_s: int = -1, force_q: int = -1, mem_kind: int = MEM_DEVICE):
+    ells_arr = (ctypes.c_int * len(ells))(*[int(e) for e in ells])
+    req = Request(mode, len(ells), ctypes.cast(ells_arr, ctypes.POINTER(ctypes.c_int)), int(n_scales),
+                  float(tau), float(tol), int(force_s), int(force_q), int(mem_kind))
+    req._keep = ells_arr  # keep the array alive with the struct
+    return req

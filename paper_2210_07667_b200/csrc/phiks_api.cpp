@@ -1,0 +1,1179 @@
+// C ABI and host orchestration of the PHIKS hot path (include/phiks.h).
+//
+// The host only plans and enqueues: every arithmetic step on tensors or
+// matrices runs in the CUDA kernels of kernels.cu.  One apply is
+//   A. small-matrix exponentials exp(c·τA_f) for the GLL nodes (Taylor degree
+//      16, Paterson–Stockmeyer, scaling and squaring) and the level matrices
+//      exp(τA_f/2^j) by repeated squaring,
+//   B. quadrature: one batched Tucker operator per node (Eq. (10)),
+//      weight-sum fused into the last mode's epilogue (Eq. (11) / Eq. (17)),
+//   C. squaring levels j = s..1 (Eq. (12) / Eq. (18)), recurrence fused into the
+//      last mode's epilogue, intermediate scales written on the way (Eq. (13)/(19)),
+//   D. exp(τK/2^j)v actions (one Tucker operator each, l.614-616).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "phiks_internal.h"
+#include "planner.h"
+
+using namespace phiks;
+
+namespace {
+
+thread_local std::string g_err;
+
+phiks_status fail(phiks_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(PHIKS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+double factorial(int k) {
+  double f = 1.0;
+  for (int i = 2; i <= k; ++i) f *= i;
+  return f;
+}
+
+struct Factor {
+  int n = 0;
+  double* dA = nullptr;   // device copy of A_f
+  double norm1 = 0.0;    // ||A_f||_1
+  plan::FactorRange fr{};
+};
+
+struct PlanKey {
+  int mode, p, n_scales;
+  double tau, tol;
+  std::vector<double> norms;
+  bool operator<(const PlanKey& o) const {
+    return std::tie(mode, p, n_scales, tau, tol, norms) < std::tie(o.mode, o.p, o.n_scales, o.tau, o.tol, o.norms);
+  }
+};
+
+}  // namespace
+
+struct phiks_ctx {
+  int d = 0;
+  int n[PHIKS_MAX_D] = {0};
+  int64_t N = 0;
+  std::vector<Factor> factors;
+  int fac_of_mode[PHIKS_MAX_D] = {0};
+  void* ws_own = nullptr;
+  size_t ws_own_bytes = 0;
+  double* h_pinned = nullptr;  // pinned host scratch (norms)
+  std::map<PlanKey, plan::Plan> plan_cache;
+  phiks_stats stats{};
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Bump allocator over the workspace; in measure mode it only counts.
+// ---------------------------------------------------------------------------
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, off = 0;
+  bool measure = true;
+  double* alloc_doubles(int64_t count) {
+    const size_t bytes = ((static_cast<size_t>(count) * sizeof(double)) + 255) & ~size_t(255);
+    char* p = measure ? nullptr : base + off;
+    off += bytes;
+    if (measure) return reinterpret_cast<double*>(static_cast<uintptr_t>(0x1000) + off);  // fake, never dereferenced
+    return reinterpret_cast<double*>(p);
+  }
+};
+
+// A source list with coefficients, kept on the host until a launch is built.
+struct Src {
+  const double* ptr;
+  double coef;
+};
+struct Out {
+  double* dst;
+  double beta;
+  std::vector<Src> srcs;
+};
+
+// One Tucker operator of a batch.
+struct TuckerItem {
+  const double* in = nullptr;
+  double in_scale = 1.0;  // folded into every last-mode beta
+  const double* mats[PHIKS_MAX_D] = {nullptr};
+  int group = 0;          // last-mode accumulation group
+  std::vector<Out> outs;  // last-mode epilogue
+};
+
+struct Exec {
+  phiks_ctx* h;
+  cudaStream_t st;
+  bool measure;
+  Arena* ar;
+  int64_t launches = 0;
+  int64_t tucker_ops = 0;
+  std::vector<double*> scr_pool[2];  // N-sized scratch reused by every tucker_batch
+  double mu_flops = 0.0, expm_flops = 0.0;
+  phiks_status status = PHIKS_OK;
+
+  bool ok() const { return status == PHIKS_OK; }
+  void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess && status == PHIKS_OK) {
+      status = PHIKS_ERR_CUDA;
+      g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    }
+  }
+
+  // ---- one mode-product launch from host-side term lists ----
+  struct LaunchTerm {
+    const double* in;
+    const double* M;
+    int group;
+    std::vector<Out> outs;
+  };
+  void mode_launch(int64_t L, int n, int64_t R, const std::vector<LaunchTerm>& terms) {
+    if (!ok() || terms.empty()) return;
+    // chunk so every launch fits ModeParams; a group's terms stay in order
+    size_t i = 0;
+    while (i < terms.size() && ok()) {
+      ModeParams* pp = new ModeParams();
+      ModeParams& p = *pp;
+      p.L = L;
+      p.R = R;
+      p.n = n;
+      p.ngroups = 0;
+      int nt = 0, no = 0, ns = 0;
+      std::map<int, int> gslot;  // group key -> slot in this launch
+      std::vector<std::vector<int>> gterms;
+      size_t j = i;
+      for (; j < terms.size(); ++j) {
+        const LaunchTerm& t = terms[j];
+        int need_s = 0;
+        for (const Out& o : t.outs) need_s += static_cast<int>(o.srcs.size());
+        const bool new_group = gslot.find(t.group) == gslot.end();
+        if (nt + 1 > kMaxTerms || no + static_cast<int>(t.outs.size()) > kMaxOuts || ns + need_s > kMaxSrcs ||
+            (new_group && static_cast<int>(gterms.size()) + 1 > kMaxGroups))
+          break;
+        if (new_group) {
+          gslot[t.group] = static_cast<int>(gterms.size());
+          gterms.emplace_back();
+        }
+        gterms[gslot[t.group]].push_back(static_cast<int>(j));
+        ++nt;
+        no += static_cast<int>(t.outs.size());
+        ns += need_s;
+      }
+      if (j == i) {
+        status = PHIKS_ERR_LIMIT;
+        g_err = "term exceeds launch descriptor limits";
+        delete pp;
+        return;
+      }
+      // lay out groups contiguously
+      int tt = 0, oo = 0, ss = 0;
+      for (size_t g = 0; g < gterms.size(); ++g) {
+        p.groups[g].t0 = tt;
+        for (int ti : gterms[g]) {
+          const LaunchTerm& t = terms[ti];
+          TermSpec& ts = p.terms[tt++];
+          ts.in = t.in;
+          ts.M = t.M;
+          ts.out0 = oo;
+          ts.nout = static_cast<int>(t.outs.size());
+          for (const Out& o : t.outs) {
+            OutSpec& os = p.outs[oo++];
+            os.dst = o.dst;
+            os.beta = o.beta;
+            os.src0 = ss;
+            os.nsrc = static_cast<int>(o.srcs.size());
+            for (const Src& s : o.srcs) p.srcs[ss++] = SrcRef{s.ptr, s.coef};
+          }
+        }
+        p.groups[g].t1 = tt;
+      }
+      p.ngroups = static_cast<int>(gterms.size());
+      if (!measure) check(launch_mode_product(p, st), "mode_product");
+      ++launches;
+      delete pp;
+      i = j;
+    }
+  }
+
+  void combine(int64_t count, const std::vector<Out>& outs) {
+    if (!ok() || outs.empty()) return;
+    size_t i = 0;
+    while (i < outs.size() && ok()) {
+      CombineParams* pp = new CombineParams();
+      CombineParams& p = *pp;
+      p.count = count;
+      p.nout = 0;
+      int ns = 0;
+      size_t j = i;
+      for (; j < outs.size(); ++j) {
+        const int need = static_cast<int>(outs[j].srcs.size());
+        if (p.nout + 1 > kMaxCombOuts || ns + need > kMaxCombSrcs) break;
+        OutSpec& os = p.outs[p.nout++];
+        os.dst = outs[j].dst;
+        os.beta = 0.0;
+        os.src0 = ns;
+        os.nsrc = need;
+        for (const Src& s : outs[j].srcs) p.srcs[ns++] = SrcRef{s.ptr, s.coef};
+      }
+      if (!measure) check(launch_combine(p, st), "combine");
+      ++launches;
+      delete pp;
+      i = j;
+    }
+  }
+
+  // ---- batched Tucker operators (Eq. (4)) ----
+  void tucker_batch(const std::vector<TuckerItem>& items) {
+    if (!ok() || items.empty()) return;
+    const int d = h->d;
+    const int64_t N = h->N;
+    // items per chunk bounded by the number of groups a non-last launch can hold
+    const size_t chunk = static_cast<size_t>(kMaxGroups);
+    const size_t nscr = std::min(items.size(), chunk);
+    auto& scr = scr_pool;
+    if (d >= 2)
+      while (scr[0].size() < nscr) scr[0].push_back(ar->alloc_doubles(N));
+    if (d >= 3)
+      while (scr[1].size() < nscr) scr[1].push_back(ar->alloc_doubles(N));
+    for (size_t c0 = 0; c0 < items.size() && ok(); c0 += chunk) {
+      const size_t c1 = std::min(items.size(), c0 + chunk);
+      int64_t L = 1;
+      for (int mu = 0; mu < d; ++mu) {
+        const int n = h->n[mu];
+        const int64_t R = N / (L * n);
+        std::vector<LaunchTerm> terms;
+        for (size_t b = c0; b < c1; ++b) {
+          const TuckerItem& it = items[b];
+          LaunchTerm t;
+          t.in = (mu == 0) ? it.in : scr[(mu - 1) % 2][b - c0];
+          t.M = it.mats[mu];
+          if (mu < d - 1) {
+            t.group = static_cast<int>(b - c0);
+            t.outs.push_back(Out{scr[mu % 2][b - c0], 1.0, {}});
+          } else {
+            t.group = it.group;
+            t.outs = it.outs;
+            if (it.in_scale != 1.0)
+              for (Out& o : t.outs) o.beta *= it.in_scale;
+          }
+          terms.push_back(std::move(t));
+        }
+        mode_launch(L, n, R, terms);
+        L *= n;
+      }
+      int64_t nsum = 0;
+      for (int mu = 0; mu < d; ++mu) nsum += h->n[mu];
+      tucker_ops += static_cast<int64_t>(c1 - c0);
+      mu_flops += static_cast<double>(c1 - c0) * 2.0 * static_cast<double>(N) * static_cast<double>(nsum);
+    }
+  }
+
+  // out_b = A_b · B_b (+ epilogue) for n×n matrices: mode-1 product of the
+  // "tensor" B (n, n) with matrix A.
+  void gemm_batch(int n, std::vector<LaunchTerm>& terms) {
+    mode_launch(1, n, n, terms);
+    expm_flops += 2.0 * n * static_cast<double>(n) * n * static_cast<double>(terms.size());
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Stage A: small-matrix exponentials exp(c_k · τA_f) for a list of (f, c)
+// requests.  Y = a·X (X = τA_f, a = c/2^σ, ||Y||_1 ≤ 1/2):
+//   exp(Y) ≈ Σ_{k=0}^{16} Y^k/k! = B0 + Y4(B1 + Y4(B2 + Y4(B3 + Y4/16!))),
+//   B_m = Σ_{r=0}^{3} Y^r/(4m+r)!  (Paterson–Stockmeyer), then σ squarings.
+// The powers X^2, X^3, X^4 are shared by every request of a factor.
+// ---------------------------------------------------------------------------
+struct ExpReq {
+  int f;
+  double c;
+  double* result = nullptr;  // filled in
+};
+
+void expm_batch(Exec& ex, double tau, std::vector<ExpReq>& reqs) {
+  phiks_ctx* h = ex.h;
+  const int nf = static_cast<int>(h->factors.size());
+  std::vector<char> used(nf, 0);
+  for (auto& r : reqs) used[r.f] = 1;
+  // per-factor powers
+  std::vector<double*> X1(nf, nullptr), X2(nf), X3(nf), X4(nf);
+  std::map<int, double*> Ident;
+  for (int f = 0; f < nf; ++f) {
+    if (!used[f]) continue;
+    const int n = h->factors[f].n;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    X1[f] = ex.ar->alloc_doubles(nn);
+    X2[f] = ex.ar->alloc_doubles(nn);
+    X3[f] = ex.ar->alloc_doubles(nn);
+    X4[f] = ex.ar->alloc_doubles(nn);
+    if (!Ident.count(n)) {
+      Ident[n] = ex.ar->alloc_doubles(nn);
+      if (!ex.measure) ex.check(launch_set_identity(Ident[n], n, 1.0, ex.st), "set_identity");
+      ++ex.launches;
+    }
+  }
+  // distinct n values
+  std::vector<int> ns;
+  for (int f = 0; f < nf; ++f)
+    if (used[f] && std::find(ns.begin(), ns.end(), h->factors[f].n) == ns.end()) ns.push_back(h->factors[f].n);
+  for (int n : ns) {
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    std::vector<Out> sc;
+    for (int f = 0; f < nf; ++f)
+      if (used[f] && h->factors[f].n == n) sc.push_back(Out{X1[f], 0.0, {Src{h->factors[f].dA, tau}}});
+    ex.combine(nn, sc);
+    std::vector<Exec::LaunchTerm> t2, t3, t4;
+    for (int f = 0; f < nf; ++f)
+      if (used[f] && h->factors[f].n == n) t2.push_back({X1[f], X1[f], f, {Out{X2[f], 1.0, {}}}});
+    ex.gemm_batch(n, t2);
+    for (int f = 0; f < nf; ++f)
+      if (used[f] && h->factors[f].n == n) {
+        t3.push_back({X1[f], X2[f], f, {Out{X3[f], 1.0, {}}}});   // X2·X1
+        t4.push_back({X2[f], X2[f], f, {Out{X4[f], 1.0, {}}}});   // X2·X2
+      }
+    for (auto& t : t4) t3.push_back(t);
+    for (size_t i = 0; i < t3.size(); ++i) t3[i].group = static_cast<int>(i);
+    ex.gemm_batch(n, t3);
+  }
+  // per request: scaling, Horner in X4, squarings
+  struct St {
+    double a;
+    int sigma;
+    double* buf[2];
+    int cur;
+  };
+  std::vector<St> sts(reqs.size());
+  int max_sigma = 0;
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    const Factor& F = h->factors[reqs[i].f];
+    const double nrm = std::fabs(reqs[i].c) * tau * F.norm1;
+    int sigma = 0;
+    if (nrm > 0.5) sigma = static_cast<int>(std::ceil(std::log2(nrm / 0.5)));
+    sts[i].sigma = sigma;
+    sts[i].a = reqs[i].c / std::ldexp(1.0, sigma);
+    const int64_t nn = static_cast<int64_t>(F.n) * F.n;
+    sts[i].buf[0] = ex.ar->alloc_doubles(nn);
+    sts[i].buf[1] = ex.ar->alloc_doubles(nn);
+    sts[i].cur = 0;
+    max_sigma = std::max(max_sigma, sigma);
+  }
+  auto coefs = [](double a, int base) {  // a^{base+r}/(base+r)!, r = 0..3
+    std::vector<double> c(4);
+    for (int r = 0; r < 4; ++r) c[r] = std::pow(a, base + r) / factorial(base + r);
+    return c;
+  };
+  for (int n : ns) {
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    // H = a^16/16! X4 + B3
+    std::vector<Out> h0;
+    for (size_t i = 0; i < reqs.size(); ++i) {
+      const int f = reqs[i].f;
+      if (h->factors[f].n != n) continue;
+      const double a = sts[i].a;
+      auto c = coefs(a, 12);
+      h0.push_back(Out{sts[i].buf[0], 0.0,
+                       {Src{X4[f], std::pow(a, 16) / factorial(16)}, Src{Ident[n], c[0]}, Src{X1[f], c[1]},
+                        Src{X2[f], c[2]}, Src{X3[f], c[3]}}});
+    }
+    ex.combine(nn, h0);
+    // three Horner GEMMs: H <- a^4 X4 H + B_m, m = 2, 1, 0
+    for (int m = 2; m >= 0; --m) {
+      std::vector<Exec::LaunchTerm> tl;
+      for (size_t i = 0; i < reqs.size(); ++i) {
+        const int f = reqs[i].f;
+        if (h->factors[f].n != n) continue;
+        const double a = sts[i].a;
+        auto c = coefs(a, 4 * m);
+        St& s = sts[i];
+        tl.push_back({s.buf[s.cur], X4[f], static_cast<int>(tl.size()),
+                      {Out{s.buf[s.cur ^ 1], std::pow(a, 4),
+                           {Src{Ident[n], c[0]}, Src{X1[f], c[1]}, Src{X2[f], c[2]}, Src{X3[f], c[3]}}}}});
+        s.cur ^= 1;
+      }
+      ex.gemm_batch(n, tl);
+    }
+    // σ squarings
+    for (int k = 0; k < max_sigma; ++k) {
+      std::vector<Exec::LaunchTerm> tl;
+      for (size_t i = 0; i < reqs.size(); ++i) {
+        const int f = reqs[i].f;
+        St& s = sts[i];
+        if (h->factors[f].n != n || s.sigma <= k) continue;
+        tl.push_back({s.buf[s.cur], s.buf[s.cur], static_cast<int>(tl.size()), {Out{s.buf[s.cur ^ 1], 1.0, {}}}});
+        s.cur ^= 1;
+      }
+      if (!tl.empty()) ex.gemm_batch(n, tl);
+    }
+  }
+  for (size_t i = 0; i < reqs.size(); ++i) reqs[i].result = sts[i].buf[sts[i].cur];
+}
+
+// ---------------------------------------------------------------------------
+// The whole φ-action (stages A-D) on device pointers.
+// vin[ℓ] (ℓ = 0..p) device input tensors or nullptr; out_same[ℓ][j] / out_lin[j]
+// device output tensors or nullptr (not requested).
+// ---------------------------------------------------------------------------
+struct Job {
+  int mode;
+  int p;
+  int n_scales;
+  double tau;
+  int s, q;
+  const double* vin[kMaxVecs] = {nullptr};
+  double* out_same[kMaxVecs][PHIKS_MAX_SCALES] = {{nullptr}};
+  double* out_lin[PHIKS_MAX_SCALES] = {nullptr};
+};
+
+void run_job(Exec& ex, const Job& jb) {
+  phiks_ctx* h = ex.h;
+  const int d = h->d;
+  const int p = jb.p, s = jb.s, q = jb.q;
+  const int64_t N = h->N;
+  const int nf = static_cast<int>(h->factors.size());
+  const bool same = jb.mode == PHIKS_MODE_SAME_VECTOR;
+
+  // ---- which level matrices exp(τA/2^j) are needed ----
+  bool want_phi0 = false;
+  if (same) {
+    for (int j = 0; j < jb.n_scales; ++j) want_phi0 |= jb.out_same[0][j] != nullptr;
+  } else {
+    want_phi0 = jb.vin[0] != nullptr;
+  }
+  int jmin = s;
+  if (p >= 1) jmin = std::min(jmin, 1);
+  if (want_phi0) jmin = 0;
+  if (p >= 1 && s == 0) jmin = 0;
+
+  std::vector<double> theta, w;
+  if (p >= 1) plan::gll_rule(q, theta, w);
+
+  // ---- Stage A ----
+  std::vector<ExpReq> reqs;
+  // node exponentials (θ_i ≠ 1): c_i = (1 − θ_i)/2^s; node 0 (θ = 0) gives exp(τA/2^s)
+  const int n_nodes = (p >= 1) ? q - 1 : 0;
+  for (int i = 0; i < n_nodes; ++i)
+    for (int f = 0; f < nf; ++f) reqs.push_back({f, (1.0 - theta[i]) / std::ldexp(1.0, s)});
+  if (p == 0)
+    for (int f = 0; f < nf; ++f) reqs.push_back({f, 1.0 / std::ldexp(1.0, s)});
+  expm_batch(ex, jb.tau, reqs);
+  if (!ex.ok()) return;
+  // nodeE[i][f]
+  std::vector<std::vector<const double*>> nodeE(n_nodes, std::vector<const double*>(nf));
+  for (int i = 0; i < n_nodes; ++i)
+    for (int f = 0; f < nf; ++f) nodeE[i][f] = reqs[static_cast<size_t>(i) * nf + f].result;
+  // level matrices Es[j][f], j = jmin..s
+  std::vector<std::vector<double*>> Es(s + 1, std::vector<double*>(nf, nullptr));
+  for (int f = 0; f < nf; ++f)
+    Es[s][f] = (p >= 1) ? const_cast<double*>(nodeE[0][f]) : reqs[f].result;
+  for (int j = s; j > jmin; --j) {
+    std::map<int, std::vector<Exec::LaunchTerm>> byn;
+    for (int f = 0; f < nf; ++f) {
+      const int n = h->factors[f].n;
+      Es[j - 1][f] = ex.ar->alloc_doubles(static_cast<int64_t>(n) * n);
+      auto& v = byn[n];
+      v.push_back({Es[j][f], Es[j][f], static_cast<int>(v.size()), {Out{Es[j - 1][f], 1.0, {}}}});
+    }
+    for (auto& kv : byn) ex.gemm_batch(kv.first, kv.second);
+  }
+  auto mats_for = [&](const std::vector<double*>& perf, const double** mats) {
+    for (int mu = 0; mu < d; ++mu) mats[mu] = perf[h->fac_of_mode[mu]];
+  };
+  auto node_mats = [&](int i, const double** mats) {
+    for (int mu = 0; mu < d; ++mu) mats[mu] = nodeE[i][h->fac_of_mode[mu]];
+  };
+
+  // ---- state buffers ----
+  // state[j][ℓ] for the scale j (ℓ = 1..p)
+  std::vector<std::vector<double*>> state(s + 1, std::vector<double*>(p + 1, nullptr));
+  std::vector<double*> pool[2];
+  auto ws_state = [&](int j, int ell) -> double* {
+    auto& pl = pool[j % 2];
+    while (static_cast<int>(pl.size()) <= ell) pl.push_back(nullptr);
+    if (!pl[ell]) pl[ell] = ex.ar->alloc_doubles(N);
+    return pl[ell];
+  };
+  for (int j = 0; j <= s; ++j)
+    for (int ell = 1; ell <= p; ++ell) {
+      double* u = (same && j < jb.n_scales) ? jb.out_same[ell][j] : nullptr;
+      state[j][ell] = u ? u : ws_state(j, ell);
+    }
+
+  if (p >= 1) {
+    // ---- Stage B: quadrature at scale s ----
+    const double wq = w[q - 1];  // θ_q = 1 term: exp(0) = I, no Tucker operator (l.948-952)
+    std::vector<TuckerItem> items;
+    if (same) {
+      for (int i = 0; i < n_nodes; ++i) {
+        TuckerItem it;
+        it.in = jb.vin[0];
+        node_mats(i, it.mats);
+        it.group = 0;
+        for (int ell = 1; ell <= p; ++ell) {
+          Out o;
+          o.dst = state[s][ell];
+          o.beta = w[i] * std::pow(theta[i], ell - 1) / factorial(ell - 1);
+          if (i == 0)
+            o.srcs.push_back(Src{jb.vin[0], wq / factorial(ell - 1)});
+          else
+            o.srcs.push_back(Src{o.dst, 1.0});
+          it.outs.push_back(o);
+        }
+        items.push_back(it);
+      }
+    } else {
+      // Ψ_ℓ^{(s)} = Σ_i w_i E_i x_iℓ,  x_iℓ = Σ_{k=1}^ℓ θ_i^{ℓ−k}/(ℓ−k)! v_{p+1−k}/2^{(ℓ−k+1)s}
+      auto xcoef = [&](double th, int ell, int k) {
+        return std::pow(th, ell - k) / factorial(ell - k) / std::ldexp(1.0, (ell - k + 1) * s);
+      };
+      std::vector<Out> prep;
+      std::vector<std::vector<TuckerItem>> per_ell(p + 1);
+      for (int ell = 1; ell <= p; ++ell) {
+        bool first = true;
+        for (int i = 0; i < n_nodes; ++i) {
+          std::vector<Src> comb;
+          for (int k = 1; k <= ell; ++k) {
+            const double* v = jb.vin[p + 1 - k];
+            const double c = xcoef(theta[i], ell, k);
+            if (v && c != 0.0) comb.push_back(Src{v, c});
+          }
+          if (comb.empty()) continue;
+          TuckerItem it;
+          node_mats(i, it.mats);
+          it.group = ell;
+          if (comb.size() == 1) {
+            it.in = comb[0].ptr;
+            it.in_scale = comb[0].coef;
+          } else {
+            double* x = ex.ar->alloc_doubles(N);
+            prep.push_back(Out{x, 0.0, comb});
+            it.in = x;
+          }
+          Out o;
+          o.dst = state[s][ell];
+          o.beta = w[i];
+          if (first) {
+            for (int k = 1; k <= ell; ++k) {
+              const double* v = jb.vin[p + 1 - k];
+              if (v) o.srcs.push_back(Src{v, wq * xcoef(1.0, ell, k)});
+            }
+          } else {
+            o.srcs.push_back(Src{o.dst, 1.0});
+          }
+          it.outs.push_back(o);
+          first = false;
+          per_ell[ell].push_back(it);
+        }
+        if (first) {  // no node contributed: Ψ_ℓ = w_q x_qℓ
+          Out o{state[s][ell], 0.0, {}};
+          for (int k = 1; k <= ell; ++k) {
+            const double* v = jb.vin[p + 1 - k];
+            if (v) o.srcs.push_back(Src{v, wq * xcoef(1.0, ell, k)});
+          }
+          prep.push_back(o);
+          if (ell == p && s < jb.n_scales && jb.out_lin[s]) {
+            o.dst = jb.out_lin[s];
+            prep.push_back(o);
+          }
+        }
+      }
+      ex.combine(N, prep);
+      for (int ell = 1; ell <= p; ++ell)
+        for (auto& it : per_ell[ell]) items.push_back(it);
+      if (s < jb.n_scales && jb.out_lin[s]) {
+        // scale s output = Ψ_p^{(s)} (+ exp term later): mirror the Ψ_p accumulation
+        for (auto& it : items)
+          if (it.group == p) {
+            Out o = it.outs[0];
+            o.dst = jb.out_lin[s];
+            for (auto& sr : o.srcs)
+              if (sr.ptr == state[s][p]) sr.ptr = jb.out_lin[s];
+            it.outs.push_back(o);
+          }
+      }
+    }
+    ex.tucker_batch(items);
+    if (!ex.ok()) return;
+
+    // ---- Stage C: squaring, j = s..1 ----
+    for (int j = s; j >= 1; --j) {
+      std::vector<TuckerItem> sq;
+      for (int ell = p; ell >= 1; --ell) {
+        TuckerItem it;
+        it.in = state[j][ell];
+        mats_for(Es[j], it.mats);
+        it.group = ell;
+        Out o;
+        o.dst = state[j - 1][ell];
+        if (same) {
+          const double sc = std::ldexp(1.0, -ell);
+          o.beta = sc;
+          for (int k = 1; k <= ell; ++k) o.srcs.push_back(Src{state[j][k], sc / factorial(ell - k)});
+        } else {
+          o.beta = 1.0;
+          for (int k = 1; k <= ell; ++k)
+            o.srcs.push_back(Src{state[j][k], 1.0 / (factorial(ell - k) * std::ldexp(1.0, (ell - k) * j))});
+        }
+        it.outs.push_back(o);
+        if (!same && ell == p && (j - 1) < jb.n_scales && jb.out_lin[j - 1]) {
+          Out o2 = o;
+          o2.dst = jb.out_lin[j - 1];
+          it.outs.push_back(o2);
+        }
+        sq.push_back(it);
+      }
+      ex.tucker_batch(sq);
+      if (!ex.ok()) return;
+    }
+  }
+
+  // ---- Stage D: exp(τK/2^j) actions ----
+  std::vector<TuckerItem> ex_items;
+  if (same) {
+    for (int j = 0; j < jb.n_scales; ++j) {
+      if (!jb.out_same[0][j]) continue;
+      TuckerItem it;
+      it.in = jb.vin[0];
+      mats_for(Es[j], it.mats);
+      it.group = j;
+      it.outs.push_back(Out{jb.out_same[0][j], 1.0, {}});
+      ex_items.push_back(it);
+    }
+  } else {
+    for (int j = 0; j < jb.n_scales; ++j) {
+      if (!jb.out_lin[j]) continue;
+      if (jb.vin[0]) {
+        TuckerItem it;
+        it.in = jb.vin[0];
+        mats_for(Es[j], it.mats);
+        it.group = j;
+        Out o{jb.out_lin[j], 1.0, {}};
+        if (p >= 1) o.srcs.push_back(Src{jb.out_lin[j], 1.0});
+        it.outs.push_back(o);
+        ex_items.push_back(it);
+      }
+    }
+  }
+  ex.tucker_batch(ex_items);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* phiks_last_error(void) { return g_err.c_str(); }
+const char* phiks_version(void) { return "phiks-b200 0.1.0 (sm_100a, fp64 DMMA)"; }
+
+phiks_status phiks_create(int d, const int* n, const double* const* A_host, phiks_handle* out) {
+  if (!out || !n || !A_host) return fail(PHIKS_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (d < 1 || d > PHIKS_MAX_D) return fail(PHIKS_ERR_ARG, "d out of range");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PHIKS_ERR_CUDA, "no CUDA device");
+  auto* h = new phiks_ctx();
+  h->d = d;
+  h->N = 1;
+  for (int mu = 0; mu < d; ++mu) {
+    if (n[mu] < 1 || n[mu] > PHIKS_MAX_N || !A_host[mu]) {
+      delete h;
+      return fail(PHIKS_ERR_ARG, "n[mu] out of range or null A");
+    }
+    h->n[mu] = n[mu];
+    h->N *= n[mu];
+  }
+  // dedupe bitwise-identical factors
+  std::vector<int> rep;
+  for (int mu = 0; mu < d; ++mu) {
+    int found = -1;
+    for (size_t f = 0; f < rep.size(); ++f) {
+      const int m2 = rep[f];
+      if (n[m2] == n[mu] &&
+          std::memcmp(A_host[m2], A_host[mu], sizeof(double) * static_cast<size_t>(n[mu]) * n[mu]) == 0) {
+        found = static_cast<int>(f);
+        break;
+      }
+    }
+    if (found < 0) {
+      Factor F;
+      F.n = n[mu];
+      const size_t bytes = sizeof(double) * static_cast<size_t>(F.n) * F.n;
+      if (cudaMalloc(&F.dA, bytes) != cudaSuccess) {
+        phiks_destroy(h);
+        return fail(PHIKS_ERR_NOMEM, "cudaMalloc A");
+      }
+      if (cudaMemcpy(F.dA, A_host[mu], bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(F.dA);
+        phiks_destroy(h);
+        return fail(PHIKS_ERR_CUDA, "copy A");
+      }
+      const double* A = A_host[mu];
+      double nrm = 0.0;
+      for (int j = 0; j < F.n; ++j) {
+        double c = 0.0;
+        for (int i = 0; i < F.n; ++i) c += std::fabs(A[i + static_cast<size_t>(j) * F.n]);
+        nrm = std::max(nrm, c);
+      }
+      F.norm1 = nrm;
+      F.fr = plan::factor_range(F.n, A);
+      h->factors.push_back(F);
+      rep.push_back(mu);
+      found = static_cast<int>(h->factors.size()) - 1;
+    }
+    h->fac_of_mode[mu] = found;
+  }
+  if (cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned), 64 * sizeof(double)) != cudaSuccess) {
+    phiks_destroy(h);
+    return fail(PHIKS_ERR_NOMEM, "pinned host scratch");
+  }
+  *out = h;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_destroy(phiks_handle h) {
+  if (!h) return PHIKS_OK;
+  for (auto& F : h->factors)
+    if (F.dA) cudaFree(F.dA);
+  if (h->ws_own) cudaFree(h->ws_own);
+  if (h->h_pinned) cudaFreeHost(h->h_pinned);
+  delete h;
+  return PHIKS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+phiks_status validate(phiks_handle h, const phiks_request* req, int& p) {
+  if (!h || !req) return fail(PHIKS_ERR_ARG, "null argument");
+  if (req->mode != PHIKS_MODE_SAME_VECTOR && req->mode != PHIKS_MODE_LINCOMB) return fail(PHIKS_ERR_ARG, "mode");
+  if (req->n_ells < 1 || req->n_ells > PHIKS_MAX_P + 1 || !req->ells) return fail(PHIKS_ERR_ARG, "n_ells");
+  if (req->n_scales < 1 || req->n_scales > PHIKS_MAX_SCALES) return fail(PHIKS_ERR_LIMIT, "n_scales");
+  if (!(req->tau > 0.0) || !std::isfinite(req->tau)) return fail(PHIKS_ERR_ARG, "tau must be > 0");
+  p = -1;
+  for (int i = 0; i < req->n_ells; ++i) {
+    const int e = req->ells[i];
+    if (e < 0 || e > PHIKS_MAX_P) return fail(PHIKS_ERR_LIMIT, "order out of range");
+    if (i > 0 && e <= req->ells[i - 1]) return fail(PHIKS_ERR_ARG, "ells must be strictly increasing");
+    p = std::max(p, e);
+  }
+  if (req->force_s >= 0 && p >= 1 && req->force_q < 2) return fail(PHIKS_ERR_ARG, "force_q < 2");
+  if (req->force_s >= 0 && req->force_s < req->n_scales - 1) return fail(PHIKS_ERR_ARG, "force_s < n_scales-1");
+  return PHIKS_OK;
+}
+
+phiks_status make_plan(phiks_handle h, const phiks_request* req, int p, const std::vector<double>& norms,
+                       plan::Plan& out) {
+  const int s_min = req->n_scales - 1;
+  if (req->force_s >= 0) {
+    out.s = req->force_s;
+    out.q = (p >= 1) ? req->force_q : 0;
+    out.T = plan::tucker_count(req->mode, out.s, req->n_scales, out.q, p);
+    out.ok = true;
+    return PHIKS_OK;
+  }
+  const double tol = req->tol > 0 ? req->tol : std::ldexp(1.0, -53);
+  PlanKey key{req->mode, p, req->n_scales, req->tau, tol, norms};
+  auto it = h->plan_cache.find(key);
+  if (it != h->plan_cache.end()) {
+    out = it->second;
+    return PHIKS_OK;
+  }
+  plan::Rect rect{};
+  double cr = 0.0, hr = 0.0, hi = 0.0;
+  for (int mu = 0; mu < h->d; ++mu) {
+    const auto& fr = h->factors[h->fac_of_mode[mu]].fr;
+    cr += req->tau * fr.sigma;
+    hr += req->tau * fr.hnorm;
+    hi += req->tau * fr.snorm;
+  }
+  rect.center = std::complex<double>(cr, 0.0);
+  rect.hr = hr;
+  rect.hi = hi;
+  if (p == 0) {
+    out = plan::select_plan(req->mode, rect, 0, norms, 0.0, req->n_scales, s_min);
+  } else if (req->mode == PHIKS_MODE_SAME_VECTOR) {
+    // reading R2: δ = tol·||v||, and ||v|| cancels in ||R||·||v|| ≤ δ 2^{ℓs}
+    out = plan::select_plan(req->mode, rect, p, std::vector<double>{1.0}, tol, req->n_scales, s_min);
+  } else {
+    double mx = 0.0;
+    for (double v : norms) mx = std::max(mx, v);
+    if (mx == 0.0) {
+      out.s = s_min;
+      out.q = 2;
+      out.T = plan::tucker_count(req->mode, s_min, req->n_scales, 2, p);
+      out.ok = true;
+    } else {
+      out = plan::select_plan(req->mode, rect, p, norms, tol * mx, req->n_scales, s_min);
+    }
+  }
+  if (!out.ok) return fail(PHIKS_ERR_PLAN, "no admissible (s, q) in the §3.3 search");
+  h->plan_cache[key] = out;
+  return PHIKS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+phiks_status phiks_plan(phiks_handle h, const phiks_request* req, const double* vec_norms, phiks_plan_info* out) {
+  int p = 0;
+  phiks_status st = validate(h, req, p);
+  if (st != PHIKS_OK) return st;
+  if (!out) return fail(PHIKS_ERR_ARG, "null out");
+  std::vector<double> norms;
+  if (req->mode == PHIKS_MODE_LINCOMB && p >= 1) {
+    if (!vec_norms) return fail(PHIKS_ERR_ARG, "lincomb plan needs vec_norms");
+    norms.assign(vec_norms, vec_norms + p);
+  }
+  plan::Plan pl;
+  st = make_plan(h, req, p, norms, pl);
+  if (st != PHIKS_OK) return st;
+  out->s = pl.s;
+  out->q = pl.q;
+  out->T_formula = pl.T;
+  const int nodes = p >= 1 ? pl.q - 1 : 0;
+  bool has0 = req->ells[0] == 0;
+  out->T_executed = (req->mode == PHIKS_MODE_SAME_VECTOR) ? nodes + pl.s * p + (has0 ? req->n_scales : 0)
+                                                         : nodes * p + pl.s * p + (has0 ? req->n_scales : 0);
+  return PHIKS_OK;
+}
+
+static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_vecs, const double* const* vecs,
+                               double* const* outs, void* workspace, size_t ws_bytes, void* stream,
+                               bool size_only, const phiks_plan_info* forced, size_t* size_out) {
+  int p = 0;
+  phiks_status st = validate(h, req, p);
+  if (st != PHIKS_OK) return st;
+  const bool same = req->mode == PHIKS_MODE_SAME_VECTOR;
+  const int nouts = same ? req->n_ells * req->n_scales : req->n_scales;
+  if (!size_only) {
+    if (same ? n_vecs != 1 : n_vecs != req->n_ells) return fail(PHIKS_ERR_ARG, "n_vecs");
+    if (!vecs || !outs) return fail(PHIKS_ERR_ARG, "null vecs/outs");
+    for (int i = 0; i < n_vecs; ++i)
+      if (!vecs[i]) return fail(PHIKS_ERR_ARG, "null vector");
+    for (int i = 0; i < nouts; ++i)
+      if (!outs[i]) return fail(PHIKS_ERR_ARG, "null output");
+  }
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const bool host_mem = req->mem_kind == PHIKS_MEM_HOST;
+  const int64_t N = h->N;
+  const size_t tbytes = static_cast<size_t>(N) * sizeof(double);
+
+  Arena ar;
+  Exec ex{h, cs, true, &ar};
+  Job jb{};
+  jb.mode = req->mode;
+  jb.p = p;
+  jb.n_scales = req->n_scales;
+  jb.tau = req->tau;
+
+  // staging for host memory
+  std::vector<double*> dv(n_vecs > 0 ? n_vecs : 0, nullptr), dout(nouts, nullptr);
+  auto bind = [&](bool measure) {
+    ar.off = 0;
+    ar.measure = measure;
+    ex.measure = measure;
+    // user buffers: host memory -> device staging in the workspace; sizing
+    // without pointers -> distinct fake addresses (never dereferenced)
+    auto fake = [](int k) { return reinterpret_cast<double*>(static_cast<uintptr_t>(0x7f0000000000ULL) + 4096ULL * k); };
+    for (int i = 0; i < static_cast<int>(dv.size()); ++i)
+      dv[i] = host_mem ? ar.alloc_doubles(N) : (size_only ? fake(i) : const_cast<double*>(vecs[i]));
+    for (int i = 0; i < nouts; ++i)
+      dout[i] = host_mem ? ar.alloc_doubles(N) : (size_only ? fake(64 + i) : outs[i]);
+    for (int i = 0; i < kMaxVecs; ++i) jb.vin[i] = nullptr;
+    if (same) {
+      jb.vin[0] = dv.empty() ? nullptr : dv[0];
+      for (int j = 0; j < req->n_scales; ++j)
+        for (int i = 0; i < req->n_ells; ++i) jb.out_same[req->ells[i]][j] = dout[j * req->n_ells + i];
+    } else {
+      for (int i = 0; i < req->n_ells; ++i) jb.vin[req->ells[i]] = dv.empty() ? nullptr : dv[i];
+      for (int j = 0; j < req->n_scales; ++j) jb.out_lin[j] = dout[j];
+    }
+  };
+  if (size_only) dv.assign(same ? 1 : req->n_ells, nullptr);
+
+  // ---- plan (lincomb needs ||v_ℓ||: one deterministic GPU reduction + D2H) ----
+  std::vector<double> norms;
+  plan::Plan pl;
+  if (forced) {
+    pl.s = forced->s;
+    pl.q = forced->q;
+    pl.ok = true;
+  } else if (!same && p >= 1 && req->force_s < 0 && !size_only) {
+    // norms of v_1..v_p from device data
+    std::vector<const double*> vv;
+    std::vector<int> which;
+    for (int ell = 1; ell <= p; ++ell) {
+      for (int i = 0; i < req->n_ells; ++i)
+        if (req->ells[i] == ell) {
+          vv.push_back(nullptr);
+          which.push_back(i);
+        }
+    }
+    // host-memory inputs are normed on the device after staging (below); device inputs now
+    norms.assign(p, 0.0);
+    if (!vv.empty()) {
+      // workspace may not exist yet: use a private scratch allocation
+      double* scratch = nullptr;
+      const size_t sbytes = sizeof(double) * (1024 * kMaxVecs + kMaxVecs);
+      CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sbytes, cs));
+      std::vector<double*> tmp;
+      if (host_mem) {
+        for (size_t k = 0; k < vv.size(); ++k) {
+          double* t = nullptr;
+          CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t), tbytes, cs));
+          CUDA_TRY(cudaMemcpyAsync(t, vecs[which[k]], tbytes, cudaMemcpyHostToDevice, cs));
+          tmp.push_back(t);
+          vv[k] = t;
+        }
+      } else {
+        for (size_t k = 0; k < vv.size(); ++k) vv[k] = vecs[which[k]];
+      }
+      CUDA_TRY(launch_sumsq(vv.data(), static_cast<int>(vv.size()), N, scratch, scratch + 1024 * kMaxVecs, cs));
+      CUDA_TRY(cudaMemcpyAsync(h->h_pinned, scratch + 1024 * kMaxVecs, sizeof(double) * vv.size(),
+                               cudaMemcpyDeviceToHost, cs));
+      for (double* t : tmp) CUDA_TRY(cudaFreeAsync(t, cs));
+      CUDA_TRY(cudaFreeAsync(scratch, cs));
+      CUDA_TRY(cudaStreamSynchronize(cs));
+      h->stats.kernel_launches = 2;
+      for (size_t k = 0; k < vv.size(); ++k) norms[req->ells[which[k]] - 1] = std::sqrt(h->h_pinned[k]);
+    }
+    st = make_plan(h, req, p, norms, pl);
+    if (st != PHIKS_OK) return st;
+  } else {
+    if (!same && p >= 1 && req->force_s < 0 && size_only) return fail(PHIKS_ERR_ARG, "lincomb sizing needs a plan");
+    st = make_plan(h, req, p, norms, pl);
+    if (st != PHIKS_OK) return st;
+  }
+  jb.s = pl.s;
+  jb.q = pl.q;
+
+  // ---- measure ----
+  bind(true);
+  run_job(ex, jb);
+  if (!ex.ok()) return ex.status;
+  const size_t need = ar.off;
+  if (size_out) *size_out = need;
+  if (size_only) return PHIKS_OK;
+
+  char* base = nullptr;
+  if (workspace) {
+    if (ws_bytes < need) {
+      h->stats.workspace_bytes = need;
+      return fail(PHIKS_ERR_WORKSPACE, "workspace too small");
+    }
+    base = static_cast<char*>(workspace);
+  } else {
+    if (h->ws_own_bytes < need) {
+      if (h->ws_own) {
+        CUDA_TRY(cudaStreamSynchronize(cs));
+        CUDA_TRY(cudaFree(h->ws_own));
+        h->ws_own = nullptr;
+        h->ws_own_bytes = 0;
+      }
+      if (cudaMalloc(&h->ws_own, need > 0 ? need : 256) != cudaSuccess)
+        return fail(PHIKS_ERR_NOMEM, "workspace cudaMalloc");
+      h->ws_own_bytes = need > 0 ? need : 256;
+    }
+    base = static_cast<char*>(h->ws_own);
+  }
+  // ---- execute ----
+  ar.base = base;
+  ar.cap = need;
+  Exec ex2{h, cs, false, &ar};
+  ex = ex2;
+  bind(false);
+  if (host_mem)
+    for (size_t i = 0; i < dv.size(); ++i)
+      CUDA_TRY(cudaMemcpyAsync(dv[i], vecs[i], tbytes, cudaMemcpyHostToDevice, cs));
+  run_job(ex, jb);
+  if (!ex.ok()) return ex.status;
+  if (host_mem) {
+    for (int i = 0; i < nouts; ++i) CUDA_TRY(cudaMemcpyAsync(outs[i], dout[i], tbytes, cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(cudaStreamSynchronize(cs));
+  }
+  phiks_stats& S = h->stats;
+  S.plan.s = pl.s;
+  S.plan.q = pl.q;
+  S.plan.T_formula = plan::tucker_count(req->mode, pl.s, req->n_scales, pl.q, p);
+  S.plan.T_executed = static_cast<int>(ex.tucker_ops);
+  S.kernel_launches = ex.launches + ((!same && p >= 1 && req->force_s < 0 && !forced) ? 2 : 0);
+  S.tucker_ops = ex.tucker_ops;
+  S.mu_mode_flops = ex.mu_flops;
+  S.expm_flops = ex.expm_flops;
+  S.workspace_bytes = need;
+  S.total_kernel_launches += S.kernel_launches;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_apply(phiks_handle h, const phiks_request* req, int n_vecs, const double* const* vecs,
+                         double* const* outs, void* workspace, size_t ws_bytes, void* stream) {
+  return apply_impl(h, req, n_vecs, vecs, outs, workspace, ws_bytes, stream, false, nullptr, nullptr);
+}
+
+phiks_status phiks_workspace_size(phiks_handle h, const phiks_request* req, const phiks_plan_info* plan,
+                                  size_t* bytes) {
+  if (!bytes) return fail(PHIKS_ERR_ARG, "null bytes");
+  return apply_impl(h, req, 0, nullptr, nullptr, nullptr, 0, nullptr, true, plan, bytes);
+}
+
+phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out) {
+  if (!h || !out) return fail(PHIKS_ERR_ARG, "null argument");
+  *out = h->stats;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_mode_product(int d, const int* n, int mu, int batch, const double* const* in,
+                                const double* const* M, double* const* out, void* stream) {
+  if (d < 1 || d > PHIKS_MAX_D || !n || mu < 0 || mu >= d || batch < 0 || (batch > 0 && (!in || !M || !out)))
+    return fail(PHIKS_ERR_ARG, "bad argument");
+  int64_t L = 1, R = 1;
+  for (int k = 0; k < mu; ++k) L *= n[k];
+  for (int k = mu + 1; k < d; ++k) R *= n[k];
+  size_t i = 0;
+  while (i < static_cast<size_t>(batch)) {
+    ModeParams* pp = new ModeParams();
+    pp->L = L;
+    pp->R = R;
+    pp->n = n[mu];
+    int g = 0;
+    for (; g < kMaxGroups && i < static_cast<size_t>(batch); ++g, ++i) {
+      pp->groups[g] = GroupSpec{g, g + 1};
+      pp->terms[g] = TermSpec{in[i], M[i], g, 1};
+      pp->outs[g] = OutSpec{out[i], 1.0, 0, 0};
+    }
+    pp->ngroups = g;
+    cudaError_t e = launch_mode_product(*pp, static_cast<cudaStream_t>(stream));
+    delete pp;
+    if (e != cudaSuccess) return fail(PHIKS_ERR_CUDA, std::string("mode_product: ") + cudaGetErrorString(e));
+  }
+  return PHIKS_OK;
+}
+
+phiks_status phiks_tucker(int d, const int* n, const double* in, const double* const* M, double* out,
+                          double* scratch, void* stream) {
+  if (d < 1 || d > PHIKS_MAX_D || !n || !in || !M || !out || (d > 1 && !scratch))
+    return fail(PHIKS_ERR_ARG, "bad argument");
+  int64_t N = 1;
+  for (int k = 0; k < d; ++k) N *= n[k];
+  const double* cur = in;
+  for (int mu = 0; mu < d; ++mu) {
+    double* dst = (mu == d - 1) ? out : scratch + (mu % 2) * N;
+    phiks_status st = phiks_mode_product(d, n, mu, 1, &cur, &M[mu], &dst, stream);
+    if (st != PHIKS_OK) return st;
+    cur = dst;
+  }
+  return PHIKS_OK;
+}
+
+phiks_status phiks_expm(int n, const double* A, double c, double* E, double* scratch, void* stream) {
+  if (n < 1 || n > PHIKS_MAX_N || !A || !E || !scratch) return fail(PHIKS_ERR_ARG, "bad argument");
+  // temporary single-factor context on caller memory
+  phiks_ctx h;
+  h.d = 1;
+  h.n[0] = n;
+  h.N = n;
+  Factor F;
+  F.n = n;
+  F.dA = const_cast<double*>(A);
+  // ||A||_1 needs host data: read back (small, test/bench API only)
+  std::vector<double> hA(static_cast<size_t>(n) * n);
+  CUDA_TRY(cudaMemcpy(hA.data(), A, sizeof(double) * hA.size(), cudaMemcpyDeviceToHost));
+  double nrm = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += std::fabs(hA[i + static_cast<size_t>(j) * n]);
+    nrm = std::max(nrm, s);
+  }
+  F.norm1 = nrm;
+  h.factors.push_back(F);
+  Arena ar;
+  ar.measure = true;
+  {
+    Exec exm{&h, static_cast<cudaStream_t>(stream), true, &ar};
+    std::vector<ExpReq> r0{{0, c}};
+    expm_batch(exm, 1.0, r0);
+  }
+  if (ar.off > sizeof(double) * 8 * static_cast<size_t>(n) * n) {
+    h.factors.clear();
+    return fail(PHIKS_ERR_WORKSPACE, "expm scratch too small");
+  }
+  ar.off = 0;
+  ar.base = reinterpret_cast<char*>(scratch);
+  ar.cap = sizeof(double) * 8 * static_cast<size_t>(n) * n;
+  ar.measure = false;
+  Exec ex{&h, static_cast<cudaStream_t>(stream), false, &ar};
+  std::vector<ExpReq> reqs{{0, c}};
+  expm_batch(ex, 1.0, reqs);
+  h.factors.clear();
+  if (!ex.ok()) return ex.status;
+  CUDA_TRY(cudaMemcpyAsync(E, reqs[0].result, sizeof(double) * static_cast<size_t>(n) * n, cudaMemcpyDeviceToDevice,
+                           static_cast<cudaStream_t>(stream)));
+  return PHIKS_OK;
+}
+
+phiks_status phiks_plan_host(int d, const int* n, const double* const* A_host, const phiks_request* req,
+                             const double* vec_norms, phiks_plan_info* out) {
+  if (!n || !A_host || !req || !out || d < 1 || d > PHIKS_MAX_D) return fail(PHIKS_ERR_ARG, "bad argument");
+  phiks_ctx h;  // host-only context: factor ranges, no device buffers
+  h.d = d;
+  h.N = 1;
+  for (int mu = 0; mu < d; ++mu) {
+    if (n[mu] < 1 || n[mu] > PHIKS_MAX_N || !A_host[mu]) return fail(PHIKS_ERR_ARG, "bad factor");
+    h.n[mu] = n[mu];
+    h.N *= n[mu];
+    Factor F;
+    F.n = n[mu];
+    F.fr = plan::factor_range(F.n, A_host[mu]);
+    h.factors.push_back(F);
+    h.fac_of_mode[mu] = mu;
+  }
+  return phiks_plan(&h, req, vec_norms, out);
+}
+
+phiks_status phiks_select_plan(int mode, double center_re, double center_im, double hr, double hi, int p,
+                               const double* norms, double delta, int s_hat, int s_min, int s_fixed,
+                               phiks_plan_info* out) {
+  if (!out || p < 0 || p > PHIKS_MAX_P || (p > 0 && !norms)) return fail(PHIKS_ERR_ARG, "bad argument");
+  plan::Rect rect{std::complex<double>(center_re, center_im), hr, hi};
+  const int nn = (mode == PHIKS_MODE_SAME_VECTOR) ? 1 : p;
+  std::vector<double> nv(norms, norms + (p > 0 ? nn : 0));
+  if (s_fixed >= 0) {
+    out->s = s_fixed;
+    out->q = p > 0 ? plan::q_for_s(mode, rect, p, nv, delta, s_fixed) : 0;
+    out->T_formula = plan::tucker_count(mode, s_fixed, s_hat, out->q, p);
+    out->T_executed = -1;
+    return PHIKS_OK;
+  }
+  plan::Plan pl = plan::select_plan(mode, rect, p, nv, delta, s_hat, s_min);
+  if (!pl.ok) return fail(PHIKS_ERR_PLAN, "no admissible (s, q)");
+  out->s = pl.s;
+  out->q = pl.q;
+  out->T_formula = pl.T;
+  out->T_executed = -1;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_fp64_peak_launch(int kind, int blocks, int64_t iters, double* sink, void* stream, double* flops) {
+  if (!sink || !flops || blocks < 1 || iters < 1 || (kind != 0 && kind != 1)) return fail(PHIKS_ERR_ARG, "bad argument");
+  cudaError_t e = launch_fp64_peak(kind, blocks, iters, sink, static_cast<cudaStream_t>(stream), flops);
+  if (e != cudaSuccess) return fail(PHIKS_ERR_CUDA, cudaGetErrorString(e));
+  return PHIKS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Internal declarations shared by the host orchestration (phiks_api.cpp) and
+// the CUDA kernels (kernels.cu).  Not part of the C ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "phiks.h"
+
+namespace phiks {
+
+constexpr int kMaxVecs = PHIKS_MAX_P + 1;
+
+// ---------------------------------------------------------------------------
+// Batched μ-mode product with a fused linear epilogue.
+//
+// A launch processes tensors viewed as (L, n, R) — L = Π_{ν<μ} n_ν (fastest),
+// n = n_μ, R = Π_{ν>μ} n_ν — computing for every term t of a group
+//     acc[l, j, r] = Σ_k M_t[j, k] · in_t[l, k, r]            (μ-mode product)
+// and then, for every output o of the term,
+//     dst_o[l, j, r] = beta_o · acc + Σ_s gamma_s · src_s[l, j, r].
+// Terms of one group run sequentially in the same CTA for a given output tile,
+// so a term may accumulate into a tensor an earlier term of its group wrote
+// (src == dst).  Different groups must not write the same tensor.
+// ---------------------------------------------------------------------------
+
+struct SrcRef {
+  const double* ptr;
+  double coef;
+};
+
+struct OutSpec {
+  double* dst;
+  double beta;   // coefficient of the accumulator
+  int src0;      // first SrcRef index
+  int nsrc;      // number of SrcRefs
+};
+
+struct TermSpec {
+  const double* in;
+  const double* M;  // n×n column-major, element (j,k) at j + k*n
+  int out0;
+  int nout;
+};
+
+struct GroupSpec {
+  int t0, t1;
+};
+
+constexpr int kMaxGroups = 64;
+constexpr int kMaxTerms = 96;
+constexpr int kMaxOuts = 160;
+constexpr int kMaxSrcs = 320;
+
+struct ModeParams {
+  int64_t L, R;
+  int n;
+  int ngroups;
+  GroupSpec groups[kMaxGroups];
+  TermSpec terms[kMaxTerms];
+  OutSpec outs[kMaxOuts];
+  SrcRef srcs[kMaxSrcs];
+};
+
+// Elementwise linear combinations: for every output o,
+//     dst_o[i] = Σ_s gamma_s · src_s[i],  i < count.
+constexpr int kMaxCombOuts = 64;
+constexpr int kMaxCombSrcs = 256;
+struct CombineParams {
+  int64_t count;
+  int nout;
+  OutSpec outs[kMaxCombOuts];  // beta unused
+  SrcRef srcs[kMaxCombSrcs];
+};
+
+// Kernel launchers (kernels.cu).  Return cudaError_t of the launch.
+cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st);
+cudaError_t launch_combine(const CombineParams& p, cudaStream_t st);
+// partial sums of squares of `count` doubles of each of `nvec` vectors
+// -> norms2[v] (device), deterministic two-pass reduction; scratch ≥ 1024*nvec doubles
+cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, double* scratch,
+                         double* norms2, cudaStream_t st);
+cudaError_t launch_set_identity(double* E, int n, double diag, cudaStream_t st);
+cudaError_t launch_fp64_peak(int kind, int blocks, int64_t iters, double* sink, cudaStream_t st,
+                             double* flops);
+
+}  // namespace phiks

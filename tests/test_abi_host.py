@@ -1,0 +1,108 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol
+include/phiks.h declares, and its host-side §3.3 planner agrees with the
+oracle's and with PAPER.md Table 1.  No compute calls."""
+import ctypes
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import phiks_oracle as O
+from paper_2210_07667_b200 import _lib
+from paper_2210_07667_b200 import workloads as W
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    names = _lib.header_functions()
+    assert len(names) >= 12
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert b"sm_100a" in lib.phiks_version()
+
+
+def test_create_fails_loudly_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = _lib.load()
+    A = np.asfortranarray(W.fd_dxx_dirichlet(4))
+    h = ctypes.c_void_p()
+    n = (ctypes.c_int * 1)(4)
+    code = lib.phiks_create(1, n, _lib.ptr_array([A.ctypes.data]), ctypes.byref(h))
+    assert code == 2  # PHIKS_ERR_CUDA
+    assert b"CUDA" in lib.phiks_last_error()
+
+
+def _select(mode, rect, p, norms, delta, s_hat=1, s_min=0, s_fixed=-1):
+    lib = _lib.load()
+    info = _lib.PlanInfo()
+    arr = (ctypes.c_double * max(len(norms), 1))(*norms)
+    code = lib.phiks_select_plan(0 if mode == "same" else 1, rect.center.real, rect.center.imag, rect.hr,
+                                 rect.hi, p, arr, delta, s_hat, s_min, s_fixed, ctypes.byref(info))
+    _lib.check(code, "phiks_select_plan")
+    return info
+
+
+def _table1():
+    with open(os.path.join(GOLD, "table1.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("mode,row", [("same", r) for r in _table1()["same_vector"]]
+                         + [("lincomb", r) for r in _table1()["linear_combination"]])
+def test_cpp_planner_table1_q_at_paper_s(mode, row):
+    """PAPER.md Table 1 (l.1416-1449): the library's §3.3 bound selects the
+    paper's q at the paper's s for every column."""
+    t = _table1()
+    n, d = row["n"], row["d"]
+    A = (1 + 1j) / 100 * W.fd_dxx_dirichlet(n)
+    rect = O.range_rectangle([A] * d)  # rectangle of the complex validation operator
+    h = 1.0 / (n + 1)
+    x = np.arange(1, n + 1) * h
+    nv = 4096 * math.sqrt(2) * float(np.linalg.norm(x * (1 - x))) ** d
+    norms = [nv] if mode == "same" else [nv] * t["p"]
+    info = _select(mode, rect, t["p"], norms, t["tol"], t["s_hat"], 0, row["s"])
+    assert info.q == row["q"]
+
+
+def _plan_host(pb, tol=0.0):
+    lib = _lib.load()
+    n = (ctypes.c_int * len(pb.dims))(*pb.dims)
+    A = [np.asfortranarray(a) for a in pb.A]
+    req = _lib.make_request(0 if pb.mode == "same" else 1, pb.ells, pb.n_scales, pb.tau, tol)
+    p = max(pb.ells)
+    norms = None
+    if pb.mode == "lincomb":
+        d = dict(zip(pb.ells, pb.vs))
+        norms = (ctypes.c_double * p)(*[float(np.linalg.norm(d[k].ravel())) if k in d else 0.0
+                                        for k in range(1, p + 1)])
+    info = _lib.PlanInfo()
+    _lib.check(lib.phiks_plan_host(len(pb.dims), n, _lib.ptr_array([a.ctypes.data for a in A]), ctypes.byref(req),
+                                   norms, ctypes.byref(info)), "phiks_plan_host")
+    return info
+
+
+@pytest.mark.parametrize("cfg,small", [(0, False), (1, True), (2, True), (3, True), (4, True),
+                                       (2, False), (3, False)])
+def test_cpp_planner_matches_oracle_on_configs(cfg, small):
+    for pb in W.config(cfg, small=small).problems:
+        ora = O.plan_for(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, pb.n_scales)
+        got = _plan_host(pb)
+        assert (got.s, got.q, got.T_formula) == (ora.s, ora.q, ora.T), pb.name
+
+
+def test_cpp_planner_random_factors_match_oracle():
+    rng = np.random.default_rng(7)
+    for c in range(6):
+        dims = tuple(int(x) for x in rng.integers(3, 9, size=int(rng.integers(1, 4))))
+        fac = W.random_factors(dims, seed=300 + c, scale=float(rng.uniform(0.5, 30.0)))
+        V = W.random_tensor(dims, seed=c)
+        pb = W.Problem("rand", dims, fac, 1.0, "same", (0, 1, 2, 3), [V], 1 + c % 3)
+        ora = O.plan_for(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, pb.n_scales)
+        got = _plan_host(pb)
+        assert (got.s, got.q) == (ora.s, ora.q)

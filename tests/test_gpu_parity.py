@@ -1,0 +1,189 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Tolerance (BASELINE.json north_star): fp64 relative
+2-norm error ≤ 1e-12 per output."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import phiks_oracle as O  # noqa: E402
+from paper_2210_07667_b200 import PhiKS, expm, fp64_peak_launch, mode_product, tucker  # noqa: E402
+from paper_2210_07667_b200 import workloads as W  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+DEV = "cuda:0"
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(W.as_flat(x))).to(DEV)
+
+
+def mat(M):
+    return torch.from_numpy(np.asfortranarray(M).reshape(-1, order="F").copy()).to(DEV)
+
+
+def rel2(got, ref):
+    ref = np.asarray(ref).ravel(order="F") if np.asarray(ref).ndim > 1 else np.asarray(ref)
+    got = got.detach().cpu().numpy() if isinstance(got, torch.Tensor) else got
+    return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+# ---------------------------------------------------------------- building blocks
+
+
+@pytest.mark.parametrize("dims", [(7,), (32, 32), (33, 17), (5, 130, 3), (64, 3, 65), (2, 3, 4, 5), (1, 9, 1),
+                                  (256, 40), (129, 2, 129)])
+def test_mode_product_every_mode(dims):
+    T = W.random_tensor(dims, seed=sum(dims))
+    for mu, n in enumerate(dims):
+        Ms = [np.random.default_rng(mu + 10 * k).standard_normal((n, n)) for k in range(2)]
+        ins = [dev(T), dev(2.0 * T)]
+        outs = [torch.empty_like(ins[0]) for _ in range(2)]
+        mode_product(dims, mu, ins, [mat(M) for M in Ms], outs)
+        torch.cuda.synchronize()
+        for k in range(2):
+            ref = O.mu_mode_product((1.0 + k) * T, Ms[k], mu)
+            assert rel2(outs[k], W.as_flat(ref)) <= 1e-14, (dims, mu, k)
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16), (31, 8, 45), (3, 3, 3, 3)])
+def test_tucker_matches_oracle(dims):
+    T = W.random_tensor(dims, seed=3)
+    Ms = [np.random.default_rng(i).standard_normal((n, n)) for i, n in enumerate(dims)]
+    out = torch.empty(int(np.prod(dims)), dtype=torch.float64, device=DEV)
+    tucker(dims, dev(T), [mat(M) for M in Ms], out)
+    assert rel2(out, W.as_flat(O.tucker(T, Ms))) <= 1e-14
+
+
+@pytest.mark.parametrize("n,scale,c", [(4, 1.0, 1.0), (32, 30.0, 0.37), (65, 400.0, 1.0), (256, 5e3, 0.01),
+                                       (300, 2.0, -1.0)])
+def test_expm_matches_oracle(n, scale, c):
+    A = W.random_factors([n], seed=n, scale=scale)[0]
+    E = expm(mat(A), c)
+    ref = O.expm_taylor(c * A)
+    err = np.abs(E.cpu().numpy().reshape(n, n, order="F") - ref).sum(axis=0).max() / max(O.norm1(ref), 1.0)
+    assert err <= 1e-12
+
+
+def test_expm_fd_operator():
+    A = 1e-4 * (W.fd_dxx_dirichlet(512) + 10 * W.fd_dx_dirichlet(512))
+    E = expm(mat(A), 0.25)
+    ref = O.expm_taylor(0.25 * A)
+    assert rel2(E, W.as_flat(ref)) <= 1e-13
+
+
+def test_fp64_peak_kernel_runs():
+    sink = torch.empty(148 * 256, dtype=torch.float64, device=DEV)
+    for kind in (0, 1):
+        fl = fp64_peak_launch(kind, 148, 100, sink)
+        torch.cuda.synchronize()
+        assert fl > 0 and torch.isfinite(sink).all()
+
+
+# ---------------------------------------------------------------- φ-actions
+
+
+def _run(pb, force=True, n_scales=None):
+    n_scales = pb.n_scales if n_scales is None else n_scales
+    ref = O.phiks(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, n_scales=n_scales)
+    op = PhiKS(pb.A)
+    kw = dict(force_s=ref.plan.s, force_q=ref.plan.q) if force else {}
+    outs = op.apply(pb.tau, pb.ells, [dev(v) for v in pb.vs], mode=pb.mode, n_scales=n_scales, **kw)
+    torch.cuda.synchronize()
+    return op, ref, outs
+
+
+def _compare(pb, ref, outs, n_scales):
+    worst = 0.0
+    for j in range(n_scales):
+        if pb.mode == "same":
+            for i, ell in enumerate(pb.ells):
+                e = rel2(outs[j * len(pb.ells) + i], W.as_flat(ref.out[(ell, j)]))
+                assert e <= TOL, (pb.name, ell, j, e)
+                worst = max(worst, e)
+        else:
+            e = rel2(outs[j], W.as_flat(ref.out[j]))
+            assert e <= TOL, (pb.name, j, e)
+            worst = max(worst, e)
+    return worst
+
+
+@pytest.mark.parametrize("cfg,small", [(0, False), (1, True), (2, True), (3, True), (4, True)])
+def test_configs_small_parity(cfg, small):
+    for pb in W.config(cfg, small=small).problems:
+        op, ref, outs = _run(pb, force=False)
+        st = op.stats()
+        assert (st["s"], st["q"]) == (ref.plan.s, ref.plan.q), pb.name   # library's own §3.3 plan
+        _compare(pb, ref, outs, pb.n_scales)
+        assert st["tucker_ops"] == ref.tucker_ops
+
+
+def _random_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for c in range(n):
+        d = int(rng.integers(1, 5))
+        dims = tuple(int(x) for x in rng.integers(1, 40 if d <= 2 else 14, size=d))
+        fac = W.random_factors(dims, seed=500 + c, scale=float(rng.uniform(0.1, 20.0)))
+        mode = "same" if c % 2 == 0 else "lincomb"
+        p = int(rng.integers(0, 7))
+        ells = tuple(sorted(set([p] + [int(x) for x in rng.integers(0, p + 1, size=2)])))
+        nsc = int(rng.integers(1, 4))
+        vs = [W.random_tensor(dims, seed=900 + 7 * c + k) for k in range(1 if mode == "same" else len(ells))]
+        out.append(W.Problem(f"rand{c}_{mode}_d{d}", dims, fac, float(rng.uniform(0.05, 2.0)), mode, ells, vs, nsc))
+    return out
+
+
+@pytest.mark.parametrize("pb", _random_cases(16, 42), ids=lambda pb: pb.name)
+def test_random_problems_parity(pb):
+    op, ref, outs = _run(pb, force=True)
+    _compare(pb, ref, outs, pb.n_scales)
+
+
+def test_host_memory_path_equals_device_path():
+    pb = W.config(2, small=True).problems[0]
+    op = PhiKS(pb.A)
+    d_outs = op.apply(pb.tau, pb.ells, [dev(pb.vs[0])], n_scales=pb.n_scales)
+    h_outs = op.apply(pb.tau, pb.ells, [np.asfortranarray(pb.vs[0])], n_scales=pb.n_scales)
+    torch.cuda.synchronize()
+    for a, b in zip(d_outs, h_outs):
+        assert np.array_equal(a.cpu().numpy(), b)
+
+
+def test_edge_cases():
+    # n_μ = 1 everywhere (N = 1): scalar K = Σ a_μ
+    fac = [np.array([[-0.3]]), np.array([[0.7]])]
+    V = np.array([[2.0]])
+    pb = W.Problem("scalar", (1, 1), fac, 1.0, "same", (0, 1, 2, 3), [V], 2)
+    op, ref, outs = _run(pb)
+    _compare(pb, ref, outs, 2)
+    z = 0.4
+    assert abs(outs[1].item() - 2.0 * (math.exp(z) - 1) / z) <= 1e-14 * 2
+    # K = 0: φ_ℓ(0)v = v/ℓ!
+    fac = [np.zeros((3, 3)), np.zeros((4, 4))]
+    V = W.random_tensor((3, 4), seed=1)
+    pb = W.Problem("zero", (3, 4), fac, 1.0, "same", (0, 1, 2, 3, 4, 5, 6), [V], 1)
+    op, ref, outs = _run(pb)
+    for i in range(7):
+        assert rel2(outs[i], W.as_flat(V) / math.factorial(i)) <= 1e-15
+    # zero vector
+    pb = W.Problem("zerov", (5, 6), W.random_factors((5, 6), seed=2, scale=3.0), 1.0, "lincomb", (0, 1, 2),
+                   [np.zeros((5, 6))] * 3, 1)
+    op = PhiKS(pb.A)
+    out = op.apply(1.0, (0, 1, 2), [dev(v) for v in pb.vs], mode="lincomb")
+    assert float(out[0].abs().max()) == 0.0
+
+
+def test_errors_are_loud():
+    from paper_2210_07667_b200 import PhiksError
+    op = PhiKS([W.fd_dxx_dirichlet(8)])
+    v = torch.zeros(8, dtype=torch.float64, device=DEV)
+    with pytest.raises(PhiksError):
+        op.apply(1.0, (2, 1), [v])          # not increasing
+    with pytest.raises(PhiksError):
+        op.apply(-1.0, (1,), [v])           # tau <= 0
+    with pytest.raises(PhiksError):
+        op.apply(1.0, (7,), [v])            # order above PHIKS_MAX_P
