@@ -152,7 +152,7 @@ phiks_status phiks_tucker(int d, const int* n, const double* in, const double* c
                           double* out, double* scratch, void* stream);
 
 /* exp(c·A) for a device n×n column-major A into device E (scaling and squaring,
-   degree-16 Taylor with Paterson–Stockmeyer); scratch: 8*n*n doubles. */
+   degree-16 Taylor with Paterson–Stockmeyer); scratch: 8*n*n + 256 doubles. */
 phiks_status phiks_expm(int n, const double* A, double c, double* E, double* scratch,
                         void* stream);
 

@@ -176,7 +176,7 @@ def expm(A, c: float = 1.0, stream=None):
     torch = _torch()
     n = int(round(A.numel() ** 0.5))
     E = torch.empty_like(A)
-    scratch = torch.empty(8 * n * n, dtype=torch.float64, device=A.device)
+    scratch = torch.empty(8 * n * n + 256, dtype=torch.float64, device=A.device)
     _lib.check(lib.phiks_expm(n, _check_dev(A), float(c), E.data_ptr(), scratch.data_ptr(), _stream_ptr(stream)),
                "phiks_expm")
     return E

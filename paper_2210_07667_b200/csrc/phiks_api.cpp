@@ -370,14 +370,14 @@ void expm_batch(Exec& ex, double tau, std::vector<ExpReq>& reqs) {
     sts[i].cur = 0;
     max_sigma = std::max(max_sigma, sigma);
   }
-  auto coefs = [](double a, int base) {  // a^{base+r}/(base+r)!, r = 0..3
+  auto coefs = [](double a, int base) {  // B_m coefficients a^r/(base+r)!, r = 0..3 (base = 4m)
     std::vector<double> c(4);
-    for (int r = 0; r < 4; ++r) c[r] = std::pow(a, base + r) / factorial(base + r);
+    for (int r = 0; r < 4; ++r) c[r] = std::pow(a, r) / factorial(base + r);
     return c;
   };
   for (int n : ns) {
     const int64_t nn = static_cast<int64_t>(n) * n;
-    // H = a^16/16! X4 + B3
+    // H = Y4/16! + B3 = a^4/16! X4 + B3
     std::vector<Out> h0;
     for (size_t i = 0; i < reqs.size(); ++i) {
       const int f = reqs[i].f;
@@ -385,7 +385,7 @@ void expm_batch(Exec& ex, double tau, std::vector<ExpReq>& reqs) {
       const double a = sts[i].a;
       auto c = coefs(a, 12);
       h0.push_back(Out{sts[i].buf[0], 0.0,
-                       {Src{X4[f], std::pow(a, 16) / factorial(16)}, Src{Ident[n], c[0]}, Src{X1[f], c[1]},
+                       {Src{X4[f], std::pow(a, 4) / factorial(16)}, Src{Ident[n], c[0]}, Src{X1[f], c[1]},
                         Src{X2[f], c[2]}, Src{X3[f], c[3]}}});
     }
     ex.combine(nn, h0);
@@ -1109,13 +1109,13 @@ phiks_status phiks_expm(int n, const double* A, double c, double* E, double* scr
     std::vector<ExpReq> r0{{0, c}};
     expm_batch(exm, 1.0, r0);
   }
-  if (ar.off > sizeof(double) * 8 * static_cast<size_t>(n) * n) {
+  if (ar.off > sizeof(double) * (8 * static_cast<size_t>(n) * n + 256)) {
     h.factors.clear();
     return fail(PHIKS_ERR_WORKSPACE, "expm scratch too small");
   }
   ar.off = 0;
   ar.base = reinterpret_cast<char*>(scratch);
-  ar.cap = sizeof(double) * 8 * static_cast<size_t>(n) * n;
+  ar.cap = sizeof(double) * (8 * static_cast<size_t>(n) * n + 256);
   ar.measure = false;
   Exec ex{&h, static_cast<cudaStream_t>(stream), false, &ar};
   std::vector<ExpReq> reqs{{0, c}};
