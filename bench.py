@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""PHIKS benchmark (driver contract: one JSON line on rank 0).
+
+Workload: BASELINE.json configs[3] — d=3, n=256^3 (N≈16.8M, 134 MB per
+vector), fp64, two independent Kronecker sums (Brusselator species, block-
+diagonal K̂, §4.4), each A_μ = D_s·(Neumann FD Laplacian), D_u=2e-3,
+D_v=1e-3, τ=5e-3; φ_0..φ_2 (same-vector mode) on one U[0,3] vector per species
+(seed 3).  One step = the φ-action of both species (planning, small-matrix
+exponentials, quadrature, squaring, exp action), inputs resident in HBM.
+
+metric: fp64 μ-mode GFLOP/s (2·N·Σ_μ n_μ per executed Tucker operator) of the
+whole φ-action, plus φ-action wall time (ms_per_step).
+
+  python bench.py [--gpus N --steps K --warmup W]      # this framework (CUDA)
+  python bench.py --impl reference ...                 # the CPU oracle (reference arm)
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 μ-mode GFLOP/s & φ-action time, 3D 256³"
+UNIT = "GFLOP/s"
+WORKLOAD = ("configs[3]: d=3, n=256^3, fp64, Brusselator-shaped block-diagonal K (2 species, "
+            "A_mu = D_s*Neumann FD Laplacian, D_u=2e-3, D_v=1e-3), tau=5e-3, phi_0..phi_2 same-vector, "
+            "v ~ U[0,3] seed 3")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            js = json.load(f)
+        return js.get("mode_product_dram_bytes_per_launch"), js.get("source")
+    except Exception:
+        return None, None
+
+
+# ---------------------------------------------------------------------------
+def run_oracle_sample(problems):
+    """The oracle (as it stands) on a bounded sample; returns (flops, seconds)."""
+    from oracle import phiks_oracle as O
+    flops = 0.0
+    t0 = time.perf_counter()
+    for pb in problems:
+        res = O.phiks(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, n_scales=pb.n_scales)
+        flops += res.tucker_ops * 2.0 * np.prod(pb.dims) * sum(pb.dims)
+    return flops, time.perf_counter() - t0
+
+
+def blas_threads():
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        return int(max(i.get("num_threads", 1) for i in info)) if info else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2210_07667_b200 import workloads as W
+    wl = W.config(3)
+    sample = [wl.problems[0]]  # bounded sample: species 0 (u) φ-action at full 256^3
+    for _ in range(args.warmup):
+        run_oracle_sample(sample)
+    tot_f, tot_t = 0.0, 0.0
+    for _ in range(args.steps):
+        f, t = run_oracle_sample(sample)
+        tot_f += f
+        tot_t += t
+    value = tot_f / tot_t / 1e9
+    ms = tot_t / args.steps * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": "species 0 only per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+                         "sample": "one species (u) φ_0..φ_2 action at full 256^3 per step (numpy/OpenBLAS fp64)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def b200_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_07667_b200 import PhiKS, fp64_peak_launch
+    from paper_2210_07667_b200 import workloads as W
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+
+    # ---- workload (each rank: the full configs[3] problem; replicas) ----
+    wl = W.config(3)
+    ops, vins, outs, host_in, host_out = [], [], [], [], []
+    for pb in wl.problems:
+        op = PhiKS(pb.A)
+        ops.append(op)
+        x = W.as_flat(pb.vs[0])
+        vins.append(torch.from_numpy(x.copy()).to(dev))
+        outs.append([torch.empty_like(vins[-1]) for _ in pb.ells])
+        hi = torch.empty(x.size, dtype=torch.float64, pin_memory=True)
+        hi.numpy()[:] = x
+        host_in.append(hi)
+        host_out.append([torch.empty(x.size, dtype=torch.float64, pin_memory=True) for _ in pb.ells])
+
+    def step():
+        for op, pb, v, o in zip(ops, wl.problems, vins, outs):
+            op.apply(pb.tau, pb.ells, [v], mode=pb.mode, n_scales=pb.n_scales, outs=o, stream=stream)
+
+    def step_host():
+        for op, pb, v, o in zip(ops, wl.problems, host_in, host_out):
+            op.apply(pb.tau, pb.ells, [v.numpy()], mode=pb.mode, n_scales=pb.n_scales, outs=[t.numpy() for t in o])
+
+    # ---- measured FP64 tensor-core peak (DMMA microbenchmark) ----
+    sink = torch.empty(148 * 4 * 256, dtype=torch.float64, device=dev)
+    fp64_peak_launch(0, 148 * 4, 2000, sink)
+    torch.cuda.synchronize()
+    peaks = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fl = fp64_peak_launch(0, 148 * 4, 40000, sink)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        peaks.append(fl / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    peak_tf = max(peaks)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    flops_step = sum(op.stats()["mu_mode_flops"] for op in ops)
+    plans = [{"s": op.stats()["s"], "q": op.stats()["q"], "T_executed": op.stats()["T_executed"]} for op in ops]
+
+    # ---- timed region (device-resident inputs) ----
+    for op in ops:
+        op.set_profiling(True)
+    launches0 = sum(op.stats()["total_kernel_launches"] for op in ops)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_local = e0.elapsed_time(e1) / 1e3
+    st = [op.stats() for op in ops]
+    launches = sum(s["total_kernel_launches"] for s in st) - launches0
+    mp_ms = sum(s["mode_product_ms"] for s in st)
+    mp_fl = sum(s["mode_product_flops"] for s in st)
+    mp_n = sum(s["mode_product_launches"] for s in st)
+    for op in ops:
+        op.set_profiling(False)
+    t = t_local
+    if world > 1:
+        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    value = flops_step * world * args.steps / t / 1e9
+
+    # ---- end-to-end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        step_host()
+        torch.cuda.synchronize()
+        k = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            step_host()
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        N = int(np.prod(wl.problems[0].dims))
+        e2e = {"value": flops_step * world * k / te / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": sum(8 * N for _ in wl.problems),
+               "d2h_bytes_per_step": sum(8 * N * len(pb.ells) for pb in wl.problems),
+               "ms_per_step": te / k * 1e3, "timing": "host wall clock around the C-ABI calls (host-memory mode)"}
+
+    # ---- CPU baseline: the oracle, rank 0, N = 1 only ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        f, tc = run_oracle_sample(wl.problems)
+        cpu = {"value": f / tc / 1e9, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+               "sample": "the full step (both species, 256^3) once, numpy/OpenBLAS fp64", "seconds": tc}
+
+    traffic, tsrc = load_traffic()
+    ach = mp_fl / (mp_ms / 1e3) / 1e12 if mp_ms > 0 else None
+    roof = {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": (ach / peak_tf) if ach else None, "traffic": traffic,
+            "kernel": "mode_product_kernel (FP64 DMMA.8x8x4)",
+            "peak_source": "measured in this run: phiks_fp64_peak_launch DMMA microbenchmark (max of 3)",
+            "per_launch_ms": mp_ms / max(mp_n, 1), "launches_timed": mp_n,
+            "share_of_step": (mp_ms / 1e3) / t_local if t_local > 0 else None,
+            "traffic_source": tsrc}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (134 MB per vector > 126 MB L2)", "plans": plans,
+                       "mu_mode_gflop_per_step": flops_step / 1e9},
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

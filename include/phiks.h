@@ -97,6 +97,11 @@ typedef struct {
   double expm_flops;        /* flops of the small-matrix exponential stage          */
   size_t workspace_bytes;   /* device workspace the last apply needed               */
   int64_t total_kernel_launches; /* since create                                    */
+  /* filled only when profiling is on (phiks_set_profiling): CUDA-event timing of
+     every μ-mode-product kernel launch of the last apply, on the apply's stream */
+  int64_t mode_product_launches;  /* launches of the μ-mode product kernel          */
+  double mode_product_ms;         /* sum of their event-measured durations (ms)     */
+  double mode_product_flops;      /* algorithmic flops of those launches (2·rows·n²) */
 } phiks_stats;
 
 /* Create a handle for K = A_d ⊕ … ⊕ A_1.
@@ -135,6 +140,11 @@ phiks_status phiks_apply(phiks_handle h, const phiks_request* req, int n_vecs,
 /* Device workspace (bytes) phiks_apply needs for `req` under `plan`. */
 phiks_status phiks_workspace_size(phiks_handle h, const phiks_request* req,
                                   const phiks_plan_info* plan, size_t* bytes);
+
+/* on != 0: bracket every μ-mode-product launch of subsequent applies with CUDA
+   events on the apply's stream (for the roofline report); phiks_get_stats then
+   waits for those events.  Off by default. */
+phiks_status phiks_set_profiling(phiks_handle h, int on);
 
 /* Telemetry of the last phiks_apply on this handle. */
 phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out);

@@ -142,7 +142,12 @@ class PhiKS:
         return {"s": st.plan.s, "q": st.plan.q, "T_formula": st.plan.T_formula, "T_executed": st.plan.T_executed,
                 "kernel_launches": st.kernel_launches, "tucker_ops": st.tucker_ops,
                 "mu_mode_flops": st.mu_mode_flops, "expm_flops": st.expm_flops,
-                "workspace_bytes": st.workspace_bytes, "total_kernel_launches": st.total_kernel_launches}
+                "workspace_bytes": st.workspace_bytes, "total_kernel_launches": st.total_kernel_launches,
+                "mode_product_launches": st.mode_product_launches, "mode_product_ms": st.mode_product_ms,
+                "mode_product_flops": st.mode_product_flops}
+
+    def set_profiling(self, on: bool = True):
+        _lib.check(_lib.load().phiks_set_profiling(self._h, 1 if on else 0), "phiks_set_profiling")
 
 
 # ----------------------------------------------------------------------

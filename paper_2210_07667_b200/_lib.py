@@ -41,7 +41,9 @@ class PlanInfo(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("plan", PlanInfo), ("kernel_launches", ctypes.c_int64), ("tucker_ops", ctypes.c_int64),
                 ("mu_mode_flops", ctypes.c_double), ("expm_flops", ctypes.c_double),
-                ("workspace_bytes", ctypes.c_size_t), ("total_kernel_launches", ctypes.c_int64)]
+                ("workspace_bytes", ctypes.c_size_t), ("total_kernel_launches", ctypes.c_int64),
+                ("mode_product_launches", ctypes.c_int64), ("mode_product_ms", ctypes.c_double),
+                ("mode_product_flops", ctypes.c_double)]
 
 
 _lib = None
@@ -69,11 +71,12 @@ def load() -> ctypes.CDLL:
     lib.phiks_fp64_peak_launch.argtypes = [i, i, ctypes.c_int64, vp, vp, P(d)]
     lib.phiks_plan_host.argtypes = [i, P(i), P(vp), P(Request), P(d), P(PlanInfo)]
     lib.phiks_select_plan.argtypes = [i, d, d, d, d, i, P(d), d, i, i, i, P(PlanInfo)]
+    lib.phiks_set_profiling.argtypes = [vp, i]
     lib.phiks_last_error.restype = ctypes.c_char_p
     lib.phiks_version.restype = ctypes.c_char_p
     for name in ("phiks_create", "phiks_destroy", "phiks_plan", "phiks_apply", "phiks_workspace_size",
                  "phiks_get_stats", "phiks_mode_product", "phiks_tucker", "phiks_expm",
-                 "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan"):
+                 "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan", "phiks_set_profiling"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

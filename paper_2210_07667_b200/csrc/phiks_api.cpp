@@ -75,6 +75,11 @@ struct phiks_ctx {
   double* h_pinned = nullptr;  // pinned host scratch (norms)
   std::map<PlanKey, plan::Plan> plan_cache;
   phiks_stats stats{};
+  // profiling: event pairs around μ-mode-product launches of the last apply
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<double> ev_flops;
+  int ev_used = 0;
 };
 
 namespace {
@@ -202,7 +207,19 @@ struct Exec {
         p.groups[g].t1 = tt;
       }
       p.ngroups = static_cast<int>(gterms.size());
+      if (!measure && h->profiling) {
+        if (h->ev_used == static_cast<int>(h->ev.size())) {
+          cudaEvent_t a, b;
+          check(cudaEventCreate(&a), "cudaEventCreate");
+          check(cudaEventCreate(&b), "cudaEventCreate");
+          h->ev.emplace_back(a, b);
+          h->ev_flops.push_back(0.0);
+        }
+        h->ev_flops[h->ev_used] = 2.0 * static_cast<double>(L * R) * n * static_cast<double>(n) * nt;
+        check(cudaEventRecord(h->ev[h->ev_used].first, st), "cudaEventRecord");
+      }
       if (!measure) check(launch_mode_product(p, st), "mode_product");
+      if (!measure && h->profiling) check(cudaEventRecord(h->ev[h->ev_used++].second, st), "cudaEventRecord");
       ++launches;
       delete pp;
       i = j;
@@ -750,6 +767,10 @@ phiks_status phiks_destroy(phiks_handle h) {
     if (F.dA) cudaFree(F.dA);
   if (h->ws_own) cudaFree(h->ws_own);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
+  for (auto& e : h->ev) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
   delete h;
   return PHIKS_OK;
 }
@@ -1035,6 +1056,26 @@ phiks_status phiks_workspace_size(phiks_handle h, const phiks_request* req, cons
 phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out) {
   if (!h || !out) return fail(PHIKS_ERR_ARG, "null argument");
   *out = h->stats;
+  out->mode_product_launches = 0;
+  out->mode_product_ms = 0.0;
+  out->mode_product_flops = 0.0;
+  if (h->profiling) {
+    for (int i = 0; i < h->ev_used; ++i) {
+      CUDA_TRY(cudaEventSynchronize(h->ev[i].second));
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, h->ev[i].first, h->ev[i].second));
+      out->mode_product_ms += ms;
+      out->mode_product_flops += h->ev_flops[i];
+    }
+    out->mode_product_launches = h->ev_used;
+  }
+  return PHIKS_OK;
+}
+
+phiks_status phiks_set_profiling(phiks_handle h, int on) {
+  if (!h) return fail(PHIKS_ERR_ARG, "null handle");
+  h->profiling = on != 0;
+  h->ev_used = 0;
   return PHIKS_OK;
 }
 
