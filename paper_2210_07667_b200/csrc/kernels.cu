@@ -10,6 +10,8 @@
 //  * combine_kernel      — elementwise multi-output linear combinations.
 //  * sumsq kernels       — deterministic ||v||_2^2 for the §3.3 plan (lincomb).
 //  * fp64_peak_kernel    — DMMA / DFMA throughput microbenchmark (roofline).
+#include <cstdlib>
+
 #include "phiks_internal.h"
 
 namespace phiks {
@@ -44,9 +46,25 @@ __device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, doub
 // off(m,k) = (m mod L) + L·k + L·n·(m div L); B operand = M^T tile (k, j) at
 // j + k·n.  KMAJ (L == 1): off(m,k) = m·n + k, the contraction index is the
 // contiguous one, so the loader walks k across threads.
+//
+// Persistent: the grid is sized to the resident CTA count; CTA b walks the
+// work units (group, tile) b, b+G, …, and inside a unit the group's terms.
+// The cp.async prologue of the next (unit, term) is issued before the current
+// epilogue, so global loads overlap the epilogue and the next mainloop starts
+// on resident data.
 // ---------------------------------------------------------------------------
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool KMAJ>
-__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
+// off(m) of row m: (m mod L) + L·n·(m div L); 32-bit division when it fits
+__device__ __forceinline__ int64_t row_offset(int64_t m, int64_t L, int64_t Ln, bool small) {
+  if (small) {
+    const uint32_t mu = static_cast<uint32_t>(m), Lu = static_cast<uint32_t>(L);
+    const uint32_t q = mu / Lu;
+    return static_cast<int64_t>(mu - q * Lu) + Ln * q;
+  }
+  return (m % L) + Ln * (m / L);
+}
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool KMAJ>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     mode_product_kernel(const __grid_constant__ ModeParams p) {
   constexpr int NT = WARPS_M * WARPS_N * 32;
   constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
@@ -54,9 +72,10 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
   constexpr int SA = BM + 4, SB = BN + 4;  // padded strides: 64-bit fragment loads conflict-free
   constexpr int A_PER_T = BM * BK / NT, B_PER_T = BK * BN / NT;
   static_assert(WM % 8 == 0 && WN % 8 == 0 && BK % 4 == 0, "tile shape");
-  static_assert(NT % BM == 0 || KMAJ, "non-KMAJ loader assumes NT % BM == 0");
+  static_assert(KMAJ || NT % BM == 0, "non-KMAJ loader assumes NT % BM == 0");
   static_assert(NT % BK == 0, "KMAJ loader assumes NT % BK == 0");
   static_assert(NT % BN == 0, "B loader assumes NT % BN == 0");
+  static_assert(A_PER_T >= 1 && B_PER_T >= 1 && A_PER_T <= 32, "tile/CTA shape");
 
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -66,12 +85,12 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
   const int64_t L = p.L;
   const int64_t Mtot = L * p.R;
   const int64_t Ln = L * static_cast<int64_t>(n);
+  const bool small = (Mtot < (int64_t(1) << 31)) && (L < (int64_t(1) << 31));
   const int tilesN = (n + BN - 1) / BN;
-  const int64_t tile = blockIdx.x;
-  const int tn = static_cast<int>(tile % tilesN);
-  const int64_t m0 = (tile / tilesN) * BM;
-  const int j0 = tn * BN;
-  const GroupSpec g = p.groups[blockIdx.y];
+  const int64_t tilesM = (Mtot + BM - 1) / BM;
+  const int64_t tiles = tilesM * tilesN;
+  const int64_t units = tiles * p.ngroups;
+  const int KT = (n + BK - 1) / BK;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -79,166 +98,241 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
   const int wn0 = (warp % WARPS_N) * WN;
   const int lg = lane >> 2, lt = lane & 3;
 
-  // ---- per-thread loader bookkeeping (independent of the term) ----
-  // A (non-KMAJ): this thread loads row mm = tid % BM at k = tid / BM + i*(NT/BM)
-  // A (KMAJ):     this thread loads k = tid % BK at rows mm = tid / BK + i*(NT/BK)
-  // B:            this thread loads column jj = tid % BN at k = tid / BN + i*(NT/BN)
-  int64_t a_off0;      // element offset of this thread's first A element at k0 = 0
-  bool a_rowok;        // non-KMAJ: row valid
-  int a_k;             // k index of the first element (relative to k0)
-  if (!KMAJ) {
-    const int64_t m = m0 + (tid % BM);
-    a_rowok = m < Mtot;
-    a_k = tid / BM;
-    a_off0 = a_rowok ? (m % L) + Ln * (m / L) + L * a_k : 0;
-  } else {
-    a_rowok = true;
-    a_k = tid % BK;
-    a_off0 = (m0 + tid / BK) * n + a_k;
-  }
-  const int b_j = j0 + tid % BN;
-  const int b_k = tid / BN;
-  const bool b_jok = b_j < n;
-
-  const int KT = (n + BK - 1) / BK;
-
-  for (int t = g.t0; t < g.t1; ++t) {
-    const TermSpec term = p.terms[t];
-    const double* __restrict__ in = term.in;
-    const double* __restrict__ M = term.M;
-
-    auto load_stage = [&](int stage, int kt) {
-      const int k0 = kt * BK;
-      double* as = As + stage * BK * SA;
-      double* bs = Bs + stage * BK * SB;
-      if (KMAJ) {
-        const bool kok = (k0 + a_k) < n;
-        const double* src = in + a_off0 + k0;
+  // ---- per-(unit, term) loader context: base pointers and validity, computed once ----
+  struct Ld {
+    int64_t unit;
+    int t;                 // absolute term index
+    const double* a;       // this thread's first A element at k = 0
+    const double* b;       // this thread's first B element at k = 0
+    uint32_t amask;        // KMAJ: row-valid bits per i;  non-KMAJ: bit 0 = row valid
+    bool bok;              // B column valid
+  };
+  auto make_ld = [&](int64_t unit, int t) -> Ld {
+    Ld c;
+    c.unit = unit;
+    c.t = t;
+    c.amask = 0;
+    c.bok = false;
+    c.a = nullptr;
+    c.b = nullptr;
+    if (unit >= units) return c;
+    const int64_t tile = unit % tiles;
+    const int64_t m0 = (tile / tilesN) * BM;
+    const int j0 = static_cast<int>(tile % tilesN) * BN;
+    const double* in = p.terms[t].in;
+    const double* M = p.terms[t].M;
+    if (KMAJ) {
+      const int64_t mrow = m0 + tid / BK;
+      c.a = in + mrow * n + (tid % BK);
 #pragma unroll
-        for (int i = 0; i < A_PER_T; ++i) {
-          const int mm = tid / BK + i * (NT / BK);
-          const bool v = kok && (m0 + mm < Mtot);
-          cp_async8(as + a_k * SA + mm, v ? src + static_cast<int64_t>(i) * (NT / BK) * n : in, v);
-        }
-      } else {
-        const double* src = in + a_off0 + L * k0;
+      for (int i = 0; i < A_PER_T; ++i)
+        if (mrow + i * (NT / BK) < Mtot) c.amask |= 1u << i;
+    } else {
+      const int64_t m = m0 + tid % BM;
+      const bool ok = m < Mtot;
+      c.amask = ok ? 1u : 0u;
+      c.a = in + (ok ? row_offset(m, L, Ln, small) : 0) + L * (tid / BM);
+    }
+    const int jj = j0 + tid % BN;
+    c.bok = jj < n;
+    c.b = M + (c.bok ? jj : 0) + static_cast<int64_t>(tid / BN) * n;
+    return c;
+  };
+  auto advance = [&](const Ld& c) -> Ld {
+    if (c.t + 1 < p.groups[c.unit / tiles].t1) return make_ld(c.unit, c.t + 1);
+    const int64_t nu = c.unit + gridDim.x;
+    return make_ld(nu, nu < units ? p.groups[nu / tiles].t0 : 0);
+  };
+  auto load_stage = [&](const Ld& c, int stage, int kt) {
+    const int k0 = kt * BK;
+    double* as = As + stage * BK * SA;
+    double* bs = Bs + stage * BK * SB;
+    if (KMAJ) {
+      const int kk = tid % BK;
+      const bool kok = (k0 + kk) < n;
 #pragma unroll
-        for (int i = 0; i < A_PER_T; ++i) {
-          const int kk = a_k + i * (NT / BM);
-          const bool v = a_rowok && (k0 + kk < n);
-          cp_async8(as + kk * SA + (tid % BM), v ? src + L * (i * (NT / BM)) : in, v);
-        }
+      for (int i = 0; i < A_PER_T; ++i) {
+        const bool v = kok && ((c.amask >> i) & 1u);
+        const int mm = tid / BK + i * (NT / BK);
+        cp_async8(as + kk * SA + mm, v ? c.a + k0 + static_cast<int64_t>(i) * (NT / BK) * n : c.a - (tid % BK), v);
       }
-      {
-        const double* src = M + b_j + static_cast<int64_t>(k0 + b_k) * n;
+    } else {
+      const int mm = tid % BM;
 #pragma unroll
-        for (int i = 0; i < B_PER_T; ++i) {
-          const int kk = b_k + i * (NT / BN);
-          const bool v = b_jok && (k0 + kk < n);
-          cp_async8(bs + kk * SB + (tid % BN), v ? src + static_cast<int64_t>(i) * (NT / BN) * n : M, v);
-        }
+      for (int i = 0; i < A_PER_T; ++i) {
+        const int kk = tid / BM + i * (NT / BM);
+        const bool v = (c.amask & 1u) && (k0 + kk < n);
+        cp_async8(as + kk * SA + mm, v ? c.a + L * (k0 + i * (NT / BM)) : p.terms[c.t].in, v);
       }
-    };
+    }
+    {
+      const int jj = tid % BN;
+#pragma unroll
+      for (int i = 0; i < B_PER_T; ++i) {
+        const int kk = tid / BN + i * (NT / BN);
+        const bool v = c.bok && (k0 + kk < n);
+        cp_async8(bs + kk * SB + jj, v ? c.b + static_cast<int64_t>(k0 + i * (NT / BN)) * n : p.terms[c.t].M, v);
+      }
+    }
+  };
+  auto prologue = [&](const Ld& c) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (c.unit < units && s < KT) load_stage(c, s, s);
+      cp_async_commit();
+    }
+  };
 
-    double acc[MI][NI][2];
+  if (static_cast<int64_t>(blockIdx.x) >= units) return;
+  Ld cur = make_ld(blockIdx.x, p.groups[blockIdx.x / tiles].t0);
+  prologue(cur);
+
+  double acc[MI][NI][2];
+  while (cur.unit < units) {
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < KT) load_stage(s, s);
-      cp_async_commit();
-    }
 
     for (int kt = 0; kt < KT; ++kt) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
       {
         const int nk = kt + STAGES - 1;
-        if (nk < KT) load_stage(nk % STAGES, nk);
+        if (nk < KT) load_stage(cur, nk % STAGES, nk);
         cp_async_commit();
       }
       const double* as = As + (kt % STAGES) * BK * SA + lt * SA + wm0 + lg;
       const double* bs = Bs + (kt % STAGES) * BK * SB + lt * SB + wn0 + lg;
-      double a[2][MI], b[2][NI];
-#pragma unroll
-      for (int mi = 0; mi < MI; ++mi) a[0][mi] = as[mi * 8];
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni) b[0][ni] = bs[ni * 8];
 #pragma unroll
       for (int k4 = 0; k4 < BK / 4; ++k4) {
-        const int cur = k4 & 1;
-        if (k4 + 1 < BK / 4) {
+        double a[MI], b[NI];
 #pragma unroll
-          for (int mi = 0; mi < MI; ++mi) a[cur ^ 1][mi] = as[(k4 + 1) * 4 * SA + mi * 8];
+        for (int mi = 0; mi < MI; ++mi) a[mi] = as[k4 * 4 * SA + mi * 8];
 #pragma unroll
-          for (int ni = 0; ni < NI; ++ni) b[cur ^ 1][ni] = bs[(k4 + 1) * 4 * SB + ni * 8];
-        }
+        for (int ni = 0; ni < NI; ++ni) b[ni] = bs[k4 * 4 * SB + ni * 8];
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < NI; ++ni)
-            dmma8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[cur][mi], b[cur][ni]);
+          for (int ni = 0; ni < NI; ++ni) dmma8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
       }
     }
     cp_async_wait<0>();
-    __syncthreads();  // smem is reused by the next term's prologue
+    __syncthreads();  // every warp is done with the stages: refill them for the next unit
 
-    // ---- fused linear epilogue ----
-    for (int o = term.out0; o < term.out0 + term.nout; ++o) {
-      const OutSpec os = p.outs[o];
-      double* __restrict__ dst = os.dst;
+    const Ld done = cur;
+    cur = advance(cur);
+    prologue(cur);  // overlaps the epilogue below
+
+    // ---- fused linear epilogue (registers → global, loads batched per row) ----
+    {
+      const int64_t tile = done.unit % tiles;
+      const int64_t m0 = (tile / tilesN) * BM;
+      const int j0 = static_cast<int>(tile % tilesN) * BN;
+      const TermSpec& term = p.terms[done.t];
+      for (int o = term.out0; o < term.out0 + term.nout; ++o) {
+        const OutSpec& os = p.outs[o];
+        double* dst = os.dst;
+        const double beta = os.beta;
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) {
-        const int64_t m = m0 + wm0 + mi * 8 + lg;
-        if (m >= Mtot) continue;
-        const int64_t rowoff = KMAJ ? m * n : (m % L) + Ln * (m / L);
+        for (int mi = 0; mi < MI; ++mi) {
+          const int64_t m = m0 + wm0 + mi * 8 + lg;
+          if (m >= Mtot) continue;
+          const int64_t rowoff = KMAJ ? m * n : row_offset(m, L, Ln, small);
+          double v[NI][2];
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
+          for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int j = j0 + wn0 + ni * 8 + 2 * lt + e;
-            if (j >= n) continue;
-            const int64_t off = rowoff + (KMAJ ? static_cast<int64_t>(j) : L * j);
-            double v = os.beta * acc[mi][ni][e];
-            for (int s = os.src0; s < os.src0 + os.nsrc; ++s) v += p.srcs[s].coef * p.srcs[s].ptr[off];
-            dst[off] = v;
+            for (int e = 0; e < 2; ++e) v[ni][e] = beta * acc[mi][ni][e];
+          const int jb = j0 + wn0 + 2 * lt;
+          for (int s = os.src0; s < os.src0 + os.nsrc; ++s) {
+            const double* src = p.srcs[s].ptr + rowoff;
+            const double cf = p.srcs[s].coef;
+            double x[NI][2];
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int j = jb + ni * 8 + e;
+                x[ni][e] = (j < n) ? src[KMAJ ? static_cast<int64_t>(j) : L * j] : 0.0;
+              }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) v[ni][e] += cf * x[ni][e];
           }
+          double* drow = dst + rowoff;
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int j = jb + ni * 8 + e;
+              if (j < n) drow[KMAJ ? static_cast<int64_t>(j) : L * j] = v[ni][e];
+            }
         }
       }
     }
   }
+  cp_async_wait<0>();
 }
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB>
 static cudaError_t launch_cfg(const ModeParams& p, cudaStream_t st) {
   constexpr int NT = WARPS_M * WARPS_N * 32;
   constexpr size_t smem = static_cast<size_t>(STAGES) * BK * ((BM + 4) + (BN + 4)) * sizeof(double);
+  static int sms = 0;
+  static int occ[2] = {0, 0};
   const int64_t Mtot = p.L * p.R;
-  const int64_t tiles = ((Mtot + BM - 1) / BM) * ((p.n + BN - 1) / BN);
-  if (tiles > 0x7fffffffLL || p.ngroups > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(p.ngroups));
-  if (p.L == 1) {
-    auto k = mode_product_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, true>;
+  const int64_t units = ((Mtot + BM - 1) / BM) * ((p.n + BN - 1) / BN) * p.ngroups;
+  const bool kmaj = p.L == 1;
+  auto k = kmaj ? mode_product_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, true>
+                : mode_product_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, false>;
+  if (occ[kmaj] == 0) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, NT, smem, st>>>(p);
-  } else {
-    auto k = mode_product_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, NT, smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, NT, smem, st>>>(p);
+    occ[kmaj] = o > 0 ? o : 1;
   }
+  int64_t grid = static_cast<int64_t>(sms) * occ[kmaj];
+  if (grid > units) grid = units;
+  if (grid < 1) return cudaSuccess;
+  k<<<static_cast<unsigned>(grid), NT, smem, st>>>(p);
   return cudaGetLastError();
+}
+
+static int tile_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PHIKS_TILE");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
   if (p.ngroups == 0) return cudaSuccess;
-  if (p.n > 64) return launch_cfg<128, 128, 16, 2, 4, 4>(p, st);
-  if (p.n > 32) return launch_cfg<128, 64, 16, 4, 2, 4>(p, st);
-  return launch_cfg<64, 32, 16, 4, 2, 4>(p, st);
+  const int64_t Mtot = p.L * p.R;
+  if (p.n > 64) {
+    switch (tile_variant()) {
+      case 1: return launch_cfg<128, 64, 16, 2, 2, 4, 2>(p, st);
+      case 3: return launch_cfg<64, 64, 16, 2, 2, 4, 3>(p, st);
+      case 5: return launch_cfg<128, 128, 16, 4, 4, 4, 1>(p, st);
+      case 6: return launch_cfg<128, 64, 16, 4, 2, 4, 2>(p, st);
+      case 7: return launch_cfg<64, 128, 16, 2, 4, 4, 2>(p, st);
+      case 8: return launch_cfg<128, 128, 16, 4, 4, 3, 1>(p, st);
+      default: break;
+    }
+    // small problems (e.g. the n×n GEMMs of the exponential stage): more CTAs
+    if (Mtot * ((p.n + 127) / 128) * p.ngroups < 148 * 4) return launch_cfg<64, 64, 16, 2, 2, 4, 3>(p, st);
+    return launch_cfg<128, 128, 16, 2, 4, 4, 1>(p, st);
+  }
+  if (p.n > 32) return launch_cfg<128, 64, 16, 4, 2, 4, 1>(p, st);
+  return launch_cfg<64, 32, 16, 4, 2, 4, 1>(p, st);
 }
 
 // ---------------------------------------------------------------------------
