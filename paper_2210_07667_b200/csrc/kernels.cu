@@ -10,6 +10,8 @@
 //  * combine_kernel      — elementwise multi-output linear combinations.
 //  * sumsq kernels       — deterministic ||v||_2^2 for the §3.3 plan (lincomb).
 //  * fp64_peak_kernel    — DMMA / DFMA throughput microbenchmark (roofline).
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
+
 #include <cstdlib>
 
 #include "phiks_internal.h"
@@ -305,6 +307,356 @@ static cudaError_t launch_cfg(const ModeParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ===========================================================================
+// TMA + mbarrier variant (the regular, large case).  One elected thread issues
+// the two bulk-tensor copies of every K-chunk (A tile of the tensor, B tile of
+// the matrix) into a STAGES-deep ring; all warps run DMMA and release a stage
+// by arriving on its "empty" mbarrier, so the mainloop has no CTA-wide
+// barrier and no per-thread address arithmetic.  The boxes are 4 elements
+// wider than the tile so the smem rows come out padded (conflict-free 64-bit
+// fragment loads) without a swizzle.
+// ===========================================================================
+struct TmaMaps {
+  CUtensorMap a[kMaxTerms];
+  CUtensorMap b[kMaxTerms];
+};
+
+namespace {
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+}  // namespace
+
+template <int BM, int BN, int BK, int KMAJ>
+struct TmaGeom {
+  static constexpr int SA = KMAJ ? (BK + 4) : (BM + 4);          // smem row stride of A
+  static constexpr int A_ELEMS = KMAJ ? BM * (BK + 4) : BK * (BM + 4);
+  static constexpr int SB = BN + 4;
+  static constexpr int B_ELEMS = BK * (BN + 4);
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static_assert((A_ELEMS * 8) % 128 == 0 && (B_ELEMS * 8) % 128 == 0, "128B-aligned stage tiles");
+};
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool KMAJ>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
+    mode_product_tma_kernel(const __grid_constant__ ModeParams p, const __grid_constant__ TmaMaps tm) {
+  constexpr int NWARPS = WARPS_M * WARPS_N;
+  constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
+  constexpr int MI = WM / 8, NI = WN / 8;
+  using G = TmaGeom<BM, BN, BK, KMAJ>;
+  constexpr unsigned STAGE_BYTES = G::STAGE_ELEMS * 8;
+
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_ELEMS);
+  uint64_t* empty = full + STAGES;
+
+  const int n = p.n;
+  const int64_t L = p.L, R = p.R;
+  const int64_t Ln = L * static_cast<int64_t>(n);
+  const int tilesN = (n + BN - 1) / BN;
+  const int64_t rowtilesPerSlab = KMAJ ? (R + BM - 1) / BM : (L + BM - 1) / BM;
+  const int64_t rowtiles = KMAJ ? rowtilesPerSlab : rowtilesPerSlab * R;
+  const int64_t tiles = rowtiles * tilesN;
+  const int64_t units = tiles * p.ngroups;
+  const int KT = (n + BK - 1) / BK;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm0 = (warp / WARPS_N) * WM;
+  const int wn0 = (warp % WARPS_N) * WN;
+  const int lg = lane >> 2, lt = lane & 3;
+
+  if (static_cast<int64_t>(blockIdx.x) >= units) return;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // tile geometry of a unit: row origin (l0, r) or r0, column origin j0
+  struct Tile {
+    int64_t l0, r;  // non-KMAJ: rows l0..l0+BM of slab r; KMAJ: rows r..r+BM (l0 unused)
+    int j0;
+  };
+  auto tile_of = [&](int64_t unit) -> Tile {
+    const int64_t tile = unit % tiles;
+    const int64_t rt = tile / tilesN;
+    Tile T;
+    T.j0 = static_cast<int>(tile % tilesN) * BN;
+    if (KMAJ) {
+      T.l0 = 0;
+      T.r = rt * BM;
+    } else {
+      T.r = rt / rowtilesPerSlab;
+      T.l0 = (rt % rowtilesPerSlab) * BM;
+    }
+    return T;
+  };
+
+  // ---- producer cursor (thread 0 only) ----
+  int64_t p_unit = blockIdx.x;
+  int p_t = p.groups[p_unit / tiles].t0, p_kt = 0;
+  int64_t p_it = 0;  // chunks issued
+  auto produce_one = [&]() {
+    if (p_unit >= units) return;
+    const int s = static_cast<int>(p_it % STAGES);
+    if (p_it >= STAGES) mbar_wait(&empty[s], static_cast<unsigned>(((p_it / STAGES) - 1) & 1));
+    const Tile T = tile_of(p_unit);
+    double* as = smem + s * G::STAGE_ELEMS;
+    double* bs = as + G::A_ELEMS;
+    mbar_expect_tx(&full[s], STAGE_BYTES);
+    const int k0 = p_kt * BK;
+    if (KMAJ)
+      tma_load_2d(as, &tm.a[p_t], k0, static_cast<int>(T.r), &full[s]);
+    else
+      tma_load_3d(as, &tm.a[p_t], static_cast<int>(T.l0), k0, static_cast<int>(T.r), &full[s]);
+    tma_load_2d(bs, &tm.b[p_t], T.j0, k0, &full[s]);
+    ++p_it;
+    if (++p_kt == KT) {
+      p_kt = 0;
+      if (p_t + 1 < p.groups[p_unit / tiles].t1) {
+        ++p_t;
+      } else {
+        p_unit += gridDim.x;
+        if (p_unit < units) p_t = p.groups[p_unit / tiles].t0;
+      }
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < STAGES - 1; ++s) produce_one();
+
+  int64_t it = 0;  // chunks consumed
+  double acc[MI][NI][2];
+  for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    const GroupSpec g = p.groups[unit / tiles];
+    const Tile T = tile_of(unit);
+    for (int t = g.t0; t < g.t1; ++t) {
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int kt = 0; kt < KT; ++kt, ++it) {
+        const int s = static_cast<int>(it % STAGES);
+        mbar_wait(&full[s], static_cast<unsigned>((it / STAGES) & 1));
+        const double* as = smem + s * G::STAGE_ELEMS;
+        const double* bs = as + G::A_ELEMS + lt * G::SB + wn0 + lg;
+        const double* aw = KMAJ ? as + (wm0 + lg) * G::SA + lt : as + lt * G::SA + wm0 + lg;
+#pragma unroll
+        for (int k4 = 0; k4 < BK / 4; ++k4) {
+          double a[MI], b[NI];
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) a[mi] = KMAJ ? aw[mi * 8 * G::SA + k4 * 4] : aw[k4 * 4 * G::SA + mi * 8];
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) b[ni] = bs[k4 * 4 * G::SB + ni * 8];
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (tid == 0) produce_one();
+      }
+
+      // ---- fused linear epilogue ----
+      const TermSpec& term = p.terms[t];
+      for (int o = term.out0; o < term.out0 + term.nout; ++o) {
+        const OutSpec& os = p.outs[o];
+        double* dst = os.dst;
+        const double beta = os.beta;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+          const int64_t rl = wm0 + mi * 8 + lg;
+          int64_t rowoff;
+          if (KMAJ) {
+            const int64_t r = T.r + rl;
+            if (r >= R) continue;
+            rowoff = r * n;
+          } else {
+            const int64_t l = T.l0 + rl;
+            if (l >= L) continue;
+            rowoff = l + Ln * T.r;
+          }
+          double v[NI][2];
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) v[ni][e] = beta * acc[mi][ni][e];
+          const int jb = T.j0 + wn0 + 2 * lt;
+          for (int s = os.src0; s < os.src0 + os.nsrc; ++s) {
+            const double* src = p.srcs[s].ptr + rowoff;
+            const double cf = p.srcs[s].coef;
+            double x[NI][2];
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int j = jb + ni * 8 + e;
+                x[ni][e] = (j < n) ? src[KMAJ ? static_cast<int64_t>(j) : L * j] : 0.0;
+              }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) v[ni][e] += cf * x[ni][e];
+          }
+          double* drow = dst + rowoff;
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int j = jb + ni * 8 + e;
+              if (j < n) drow[KMAJ ? static_cast<int64_t>(j) : L * j] = v[ni][e];
+            }
+        }
+      }
+    }
+  }
+}
+
+// ---- host side: tensor-map encoding through the runtime's driver entry point ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+
+static bool encode(CUtensorMap* m, const double* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                   const cuuint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
+  const bool kmaj = p.L == 1;
+  const int n = p.n;
+  // TMA preconditions: 16-byte strides and base addresses; rows long enough to tile
+  if (n % 2 != 0) return false;
+  if (!kmaj && (p.L % 2 != 0 || p.L < BM / 2)) return false;
+  if (p.L * p.R > (int64_t(1) << 31) * 8) return false;
+  int nterms = 0;
+  for (int g = 0; g < p.ngroups; ++g) nterms = p.groups[g].t1 > nterms ? p.groups[g].t1 : nterms;
+  static TmaMaps maps;  // host staging (launch copies the parameter block)
+  for (int t = 0; t < nterms; ++t) {
+    if ((reinterpret_cast<uintptr_t>(p.terms[t].in) | reinterpret_cast<uintptr_t>(p.terms[t].M)) & 15) return false;
+  }
+  for (int t = 0; t < nterms; ++t) {
+    bool ok;
+    if (kmaj) {
+      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(p.R)};
+      const cuuint64_t str[1] = {static_cast<cuuint64_t>(n) * 8};
+      const cuuint32_t box[2] = {BK + 4, BM};
+      ok = encode(&maps.a[t], p.terms[t].in, 2, dims, str, box);
+    } else {
+      const cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.L), static_cast<cuuint64_t>(n),
+                                  static_cast<cuuint64_t>(p.R)};
+      const cuuint64_t str[2] = {static_cast<cuuint64_t>(p.L) * 8, static_cast<cuuint64_t>(p.L) * n * 8};
+      const cuuint32_t box[3] = {BM + 4, BK, 1};
+      ok = encode(&maps.a[t], p.terms[t].in, 3, dims, str, box);
+    }
+    const cuuint64_t bd[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n)};
+    const cuuint64_t bs[1] = {static_cast<cuuint64_t>(n) * 8};
+    const cuuint32_t bb[2] = {BN + 4, BK};
+    ok = ok && encode(&maps.b[t], p.terms[t].M, 2, bd, bs, bb);
+    if (!ok) return false;
+  }
+  constexpr int NT = WARPS_M * WARPS_N * 32;
+  static int sms = 0;
+  static bool attr[2] = {false, false};
+  const int64_t rowtiles = kmaj ? (p.R + BM - 1) / BM : ((p.L + BM - 1) / BM) * p.R;
+  const int64_t units = rowtiles * ((n + BN - 1) / BN) * p.ngroups;
+  if (kmaj) {
+    using Gm = TmaGeom<BM, BN, BK, 1>;
+    constexpr size_t smem = static_cast<size_t>(STAGES) * Gm::STAGE_ELEMS * 8 + 2 * STAGES * 8;
+    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, true>;
+    if (!attr[1]) {
+      *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (*err != cudaSuccess) return true;
+      attr[1] = true;
+    }
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t grid = units < sms ? units : sms;
+    k<<<static_cast<unsigned>(grid), NT, smem, st>>>(p, maps);
+  } else {
+    using Gm = TmaGeom<BM, BN, BK, 0>;
+    constexpr size_t smem = static_cast<size_t>(STAGES) * Gm::STAGE_ELEMS * 8 + 2 * STAGES * 8;
+    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, false>;
+    if (!attr[0]) {
+      *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (*err != cudaSuccess) return true;
+      attr[0] = true;
+    }
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t grid = units < sms ? units : sms;
+    k<<<static_cast<unsigned>(grid), NT, smem, st>>>(p, maps);
+  }
+  *err = cudaGetLastError();
+  return true;
+}
+
 static int tile_variant() {
   static int v = -1;
   if (v < 0) {
@@ -317,6 +669,17 @@ static int tile_variant() {
 cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
   if (p.ngroups == 0) return cudaSuccess;
   const int64_t Mtot = p.L * p.R;
+  const int var = tile_variant();
+  if (p.n > 64 && (var == 0 || var >= 10)) {
+    cudaError_t err = cudaSuccess;
+    const int64_t big = Mtot * ((p.n + 127) / 128) * p.ngroups;
+    bool done = false;
+    if (var == 11)
+      done = launch_tma<128, 64, 16, 4, 2, 5>(p, st, &err);
+    else if (big >= 148 * 4)
+      done = launch_tma<128, 128, 16, 2, 4, 5>(p, st, &err);
+    if (done) return err;
+  }
   if (p.n > 64) {
     switch (tile_variant()) {
       case 1: return launch_cfg<128, 64, 16, 2, 2, 4, 2>(p, st);

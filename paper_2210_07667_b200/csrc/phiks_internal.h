@@ -48,10 +48,10 @@ struct GroupSpec {
   int t0, t1;
 };
 
-constexpr int kMaxGroups = 64;
-constexpr int kMaxTerms = 96;
-constexpr int kMaxOuts = 160;
-constexpr int kMaxSrcs = 320;
+constexpr int kMaxGroups = 48;
+constexpr int kMaxTerms = 48;   // also the TMA descriptor count per launch
+constexpr int kMaxOuts = 128;
+constexpr int kMaxSrcs = 224;
 
 struct ModeParams {
   int64_t L, R;

@@ -35,7 +35,9 @@ def rel2(got, ref):
 
 
 @pytest.mark.parametrize("dims", [(7,), (32, 32), (33, 17), (5, 130, 3), (64, 3, 65), (2, 3, 4, 5), (1, 9, 1),
-                                  (256, 40), (129, 2, 129)])
+                                  (256, 40), (129, 2, 129),
+                                  # large enough for the TMA/mbarrier path (n > 64, even strides)
+                                  (256, 300), (130, 130, 40), (96, 200, 66), (100, 100, 70), (66, 258, 34)])
 def test_mode_product_every_mode(dims):
     T = W.random_tensor(dims, seed=sum(dims))
     for mu, n in enumerate(dims):
