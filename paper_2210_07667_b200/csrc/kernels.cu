@@ -373,8 +373,8 @@ struct TmaGeom {
   static_assert((A_ELEMS * 8) % 128 == 0 && (B_ELEMS * 8) % 128 == 0, "128B-aligned stage tiles");
 };
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool KMAJ>
-__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, 1)
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool KMAJ>
+__global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     mode_product_tma_kernel(const __grid_constant__ ModeParams p, const __grid_constant__ TmaMaps tm) {
   constexpr int NWARPS = WARPS_M * WARPS_N;
   constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
@@ -581,7 +581,7 @@ static bool encode(CUtensorMap* m, const double* ptr, int rank, const cuuint64_t
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB>
 static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   const bool kmaj = p.L == 1;
   const int n = p.n;
@@ -623,7 +623,7 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   if (kmaj) {
     using Gm = TmaGeom<BM, BN, BK, 1>;
     constexpr size_t smem = static_cast<size_t>(STAGES) * Gm::STAGE_ELEMS * 8 + 2 * STAGES * 8;
-    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, true>;
+    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, true>;
     if (!attr[1]) {
       *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (*err != cudaSuccess) return true;
@@ -634,12 +634,12 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int64_t grid = units < sms ? units : sms;
+    const int64_t grid = units < (int64_t)sms * MINB ? units : (int64_t)sms * MINB;
     k<<<static_cast<unsigned>(grid), NT, smem, st>>>(p, maps);
   } else {
     using Gm = TmaGeom<BM, BN, BK, 0>;
     constexpr size_t smem = static_cast<size_t>(STAGES) * Gm::STAGE_ELEMS * 8 + 2 * STAGES * 8;
-    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, false>;
+    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, false>;
     if (!attr[0]) {
       *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (*err != cudaSuccess) return true;
@@ -650,7 +650,7 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int64_t grid = units < sms ? units : sms;
+    const int64_t grid = units < (int64_t)sms * MINB ? units : (int64_t)sms * MINB;
     k<<<static_cast<unsigned>(grid), NT, smem, st>>>(p, maps);
   }
   *err = cudaGetLastError();
@@ -675,9 +675,21 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
     const int64_t big = Mtot * ((p.n + 127) / 128) * p.ngroups;
     bool done = false;
     if (var == 11)
-      done = launch_tma<128, 64, 16, 4, 2, 5>(p, st, &err);
+      done = launch_tma<128, 64, 16, 2, 2, 4, 2>(p, st, &err);
+    else if (var == 12)
+      done = launch_tma<128, 64, 16, 2, 2, 3, 2>(p, st, &err);
+    else if (var == 13)
+      done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);
+    else if (var == 14)
+      done = launch_tma<128, 128, 16, 4, 4, 5, 1>(p, st, &err);
+    else if (var == 15)
+      done = launch_tma<64, 128, 16, 2, 4, 4, 2>(p, st, &err);
+    else if (var == 16)
+      done = launch_tma<128, 64, 16, 4, 2, 3, 2>(p, st, &err);
+    else if (var == 10)
+      done = launch_tma<128, 128, 16, 2, 4, 5, 1>(p, st, &err);
     else if (big >= 148 * 4)
-      done = launch_tma<128, 128, 16, 2, 4, 5>(p, st, &err);
+      done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);  // default: 2 CTAs/SM overlap epilogues
     if (done) return err;
   }
   if (p.n > 64) {
@@ -718,6 +730,73 @@ cudaError_t launch_combine(const CombineParams& p, cudaStream_t st) {
   int64_t blocks = (p.count + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   combine_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Matrix-form combination, two elements (16 B) per thread per step; sources
+// stream once, the nout accumulators stay in registers.
+// ---------------------------------------------------------------------------
+template <int NOUT>
+__global__ void __launch_bounds__(256) multi_combine_kernel(const __grid_constant__ MultiCombineParams p) {
+  const int64_t n2 = p.count / 2;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    double2 acc[NOUT];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) acc[o] = make_double2(0.0, 0.0);
+    int s = 0;
+    for (; s + 4 <= p.nsrc; s += 4) {
+      double2 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __ldcs(reinterpret_cast<const double2*>(p.src[s + u]) + i);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+          const double c = p.coef[o][s + u];
+          acc[o].x += c * x[u].x;
+          acc[o].y += c * x[u].y;
+        }
+    }
+    for (; s < p.nsrc; ++s) {
+      const double2 x = __ldcs(reinterpret_cast<const double2*>(p.src[s]) + i);
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) {
+        acc[o].x += p.coef[o][s] * x.x;
+        acc[o].y += p.coef[o][s] * x.y;
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o)
+      if (o < p.nout) reinterpret_cast<double2*>(p.dst[o])[i] = acc[o];
+  }
+  // odd tail element
+  if (p.count & 1) {
+    const int64_t i = p.count - 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (int o = 0; o < p.nout; ++o) {
+        double v = 0.0;
+        for (int s = 0; s < p.nsrc; ++s) v += p.coef[o][s] * p.src[s][i];
+        p.dst[o][i] = v;
+      }
+  }
+}
+
+cudaError_t launch_multi_combine(const MultiCombineParams& p, cudaStream_t st) {
+  if (p.nout == 0 || p.count == 0) return cudaSuccess;
+  bool aligned = true;
+  for (int s = 0; s < p.nsrc; ++s) aligned &= (reinterpret_cast<uintptr_t>(p.src[s]) & 15) == 0;
+  for (int o = 0; o < p.nout; ++o) aligned &= (reinterpret_cast<uintptr_t>(p.dst[o]) & 15) == 0;
+  if (!aligned) return cudaErrorMisalignedAddress;
+  int64_t blocks = (p.count / 2 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  switch (p.nout <= 2 ? 2 : (p.nout <= 4 ? 4 : 8)) {
+    case 2: multi_combine_kernel<2><<<static_cast<unsigned>(blocks), 256, 0, st>>>(p); break;
+    case 4: multi_combine_kernel<4><<<static_cast<unsigned>(blocks), 256, 0, st>>>(p); break;
+    default: multi_combine_kernel<8><<<static_cast<unsigned>(blocks), 256, 0, st>>>(p); break;
+  }
   return cudaGetLastError();
 }
 

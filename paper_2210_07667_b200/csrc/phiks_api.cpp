@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -128,6 +129,8 @@ struct Exec {
   int64_t launches = 0;
   int64_t tucker_ops = 0;
   std::vector<double*> scr_pool[2];  // N-sized scratch reused by every tucker_batch
+  std::vector<double*> y_pool;       // per-item Tucker results of split batches
+  int split = 0;                     // 1: quadrature sums as a separate pass, 2: also squaring
   double mu_flops = 0.0, expm_flops = 0.0;
   phiks_status status = PHIKS_OK;
 
@@ -251,6 +254,92 @@ struct Exec {
       delete pp;
       i = j;
     }
+  }
+
+  // ---- matrix-form combination dst_o = Σ_s coef[o][s] src_s ----
+  void mcombine(int64_t count, const std::vector<const double*>& srcs, const std::vector<double*>& dsts,
+                const std::vector<std::vector<double>>& coef) {
+    if (!ok() || dsts.empty()) return;
+    if (static_cast<int>(srcs.size()) <= kMcMaxSrc) {
+      for (size_t o0 = 0; o0 < dsts.size(); o0 += kMcMaxOut) {
+        MultiCombineParams* pp = new MultiCombineParams();
+        std::memset(pp, 0, sizeof(MultiCombineParams));
+        pp->count = count;
+        pp->nsrc = static_cast<int>(srcs.size());
+        for (size_t k = 0; k < srcs.size(); ++k) pp->src[k] = srcs[k];
+        pp->nout = static_cast<int>(std::min(dsts.size() - o0, static_cast<size_t>(kMcMaxOut)));
+        for (int o = 0; o < pp->nout; ++o) {
+          pp->dst[o] = dsts[o0 + o];
+          for (size_t k = 0; k < srcs.size(); ++k) pp->coef[o][k] = coef[o0 + o][k];
+        }
+        if (!measure) check(launch_multi_combine(*pp, st), "multi_combine");
+        ++launches;
+        delete pp;
+      }
+      return;
+    }
+    // many sources: per output, chunks of 63 sources accumulating into the output
+    for (size_t o = 0; o < dsts.size(); ++o) {
+      std::vector<Out> one;
+      for (size_t k0 = 0; k0 < srcs.size(); k0 += 63) {
+        Out ou{dsts[o], 0.0, {}};
+        if (k0 > 0) ou.srcs.push_back(Src{dsts[o], 1.0});
+        for (size_t k = k0; k < std::min(srcs.size(), k0 + 63); ++k)
+          if (coef[o][k] != 0.0) ou.srcs.push_back(Src{srcs[k], coef[o][k]});
+        combine(count, {ou});
+      }
+    }
+  }
+
+  // A batch whose last-mode epilogues run as a separate streaming pass: every
+  // item writes its raw Tucker result Y_b, then the epilogue recurrences (in
+  // group order, accumulations included) are evaluated symbolically into one
+  // matrix-form combination over {Y_b} ∪ external sources.
+  void tucker_batch_split(const std::vector<TuckerItem>& items) {
+    if (!ok() || items.empty()) return;
+    const int64_t N = h->N;
+    while (y_pool.size() < items.size()) y_pool.push_back(ar->alloc_doubles(N));
+    std::vector<TuckerItem> raw(items.size());
+    typedef std::vector<std::pair<const double*, double>> Lin;
+    std::map<const double*, Lin> val;
+    std::vector<double*> order;
+    auto add = [](Lin& acc, const double* ptr, double c) {
+      for (auto& t : acc)
+        if (t.first == ptr) {
+          t.second += c;
+          return;
+        }
+      acc.emplace_back(ptr, c);
+    };
+    for (size_t b = 0; b < items.size(); ++b) {
+      raw[b] = items[b];
+      raw[b].in_scale = 1.0;
+      raw[b].group = static_cast<int>(b);
+      raw[b].outs.assign(1, Out{y_pool[b], 1.0, {}});
+      for (const Out& o : items[b].outs) {
+        Lin lin;
+        add(lin, y_pool[b], o.beta * items[b].in_scale);
+        for (const Src& sr : o.srcs) {
+          auto it = val.find(sr.ptr);
+          if (it != val.end())
+            for (auto& t : it->second) add(lin, t.first, sr.coef * t.second);
+          else
+            add(lin, sr.ptr, sr.coef);
+        }
+        if (!val.count(o.dst)) order.push_back(o.dst);
+        val[o.dst] = lin;
+      }
+    }
+    tucker_batch(raw);
+    std::vector<const double*> srcs;
+    for (double* d : order)
+      for (auto& t : val[d])
+        if (std::find(srcs.begin(), srcs.end(), t.first) == srcs.end()) srcs.push_back(t.first);
+    std::vector<std::vector<double>> coef(order.size(), std::vector<double>(srcs.size(), 0.0));
+    for (size_t o = 0; o < order.size(); ++o)
+      for (auto& t : val[order[o]])
+        coef[o][std::find(srcs.begin(), srcs.end(), t.first) - srcs.begin()] = t.second;
+    mcombine(N, srcs, order, coef);
   }
 
   // ---- batched Tucker operators (Eq. (4)) ----
@@ -621,7 +710,10 @@ void run_job(Exec& ex, const Job& jb) {
           }
       }
     }
-    ex.tucker_batch(items);
+    if (ex.split >= 1)
+      ex.tucker_batch_split(items);
+    else
+      ex.tucker_batch(items);
     if (!ex.ok()) return;
 
     // ---- Stage C: squaring, j = s..1 ----
@@ -651,7 +743,10 @@ void run_job(Exec& ex, const Job& jb) {
         }
         sq.push_back(it);
       }
-      ex.tucker_batch(sq);
+      if (ex.split >= 2)
+        ex.tucker_batch_split(sq);
+      else
+        ex.tucker_batch(sq);
       if (!ex.ok()) return;
     }
   }
@@ -897,6 +992,13 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
 
   Arena ar;
   Exec ex{h, cs, true, &ar};
+  static const int split_mode = [] {
+    // default 2: quadrature sums and squaring recurrences as a streaming pass
+    // (measured faster on B200 than the fused epilogue); 0 = fused
+    const char* e = getenv("PHIKS_SPLIT");
+    return e ? atoi(e) : 2;
+  }();
+  ex.split = split_mode;
   Job jb{};
   jb.mode = req->mode;
   jb.p = p;
@@ -1018,6 +1120,7 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
   ar.cap = need;
   Exec ex2{h, cs, false, &ar};
   ex = ex2;
+  ex.split = split_mode;
   bind(false);
   if (host_mem)
     for (size_t i = 0; i < dv.size(); ++i)

@@ -74,9 +74,23 @@ struct CombineParams {
   SrcRef srcs[kMaxCombSrcs];
 };
 
+// Matrix-form combination: dst_o[i] = Σ_s coef[o][s] · src_s[i] for o < nout,
+// every source read once per element (quadrature / squaring sums when they are
+// not fused into an epilogue).
+constexpr int kMcMaxSrc = 64;
+constexpr int kMcMaxOut = 8;
+struct MultiCombineParams {
+  int64_t count;
+  int nsrc, nout;
+  const double* src[kMcMaxSrc];
+  double* dst[kMcMaxOut];
+  double coef[kMcMaxOut][kMcMaxSrc];
+};
+
 // Kernel launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st);
 cudaError_t launch_combine(const CombineParams& p, cudaStream_t st);
+cudaError_t launch_multi_combine(const MultiCombineParams& p, cudaStream_t st);
 // partial sums of squares of `count` doubles of each of `nvec` vectors
 // -> norms2[v] (device), deterministic two-pass reduction; scratch ≥ 1024*nvec doubles
 cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, double* scratch,
