@@ -188,6 +188,87 @@ phiks_status phiks_select_plan(int mode, double center_re, double center_im, dou
                                const double* norms, double delta, int s_hat, int s_min, int s_fixed,
                                phiks_plan_info* out);
 
+/* ------------------------------------------------------------------------
+ * Slab sharding across the GPUs of one NVSwitch box (the
+ * north star of BASELINE.json: "a slab partition of the tensor ... along the
+ * outermost mode, with modes 1..d-1 contracted locally and the mode-d product
+ * done through an all-to-all transpose").
+ *
+ * Rank r of P owns the contiguous slab i_d ∈ [r·n_d/P, (r+1)·n_d/P) of every
+ * tensor: N/P doubles, column-major with dims (n_1, …, n_{d-1}, n_d/P) — i.e.
+ * elements [r·N/P, (r+1)·N/P) of the global column-major array.  Each Tucker
+ * operator (Eq. (4); the μ-mode products commute, l.252-270) runs
+ * modes 1..d-2 on the slab, then the mode-(d-1) product whose epilogue stores
+ * every output column straight into the peer rank that owns it in the
+ * transposed layout (slab of mode d-1, dims (n_1..n_{d-2}, n_{d-1}/P, n_d)),
+ * a device-side barrier, the mode-d product there (local), whose epilogue
+ * stores back into the slab layout on the owner, and a second barrier: the
+ * all-to-all transposition is fused into the producing kernels' stores over
+ * NVLink peer memory.  The quadrature sums, squaring recurrences and scale
+ * outputs are then elementwise on the slab.
+ *
+ * Memory: each rank allocates a symmetric region (control block + pools of
+ * 2·16 slab-sized tensors) that its peers map through CUDA IPC.
+ * ------------------------------------------------------------------------ */
+#define PHIKS_IPC_HANDLE_BYTES 64
+
+/* Create rank `rank` of a `world`-way slab-sharded handle for the GLOBAL
+   dims n[0..d-1] and factors A_host (every rank passes the same factors).
+   world = 1 gives an ordinary handle.  world > 1 needs d ≥ 2,
+   world ≤ 8 and n[d-1], n[d-2] divisible by world (PHIKS_ERR_ARG otherwise).
+   Before the first apply the peers must be attached with
+   phiks_shard_open_peers (one process per GPU) or phiks_shard_set_peer_bases
+   (one process).  phiks_apply on the handle then takes and returns local
+   slabs (phiks_shard_info's local_count doubles each); every rank must issue
+   the same sequence of applies with the same request (the applies meet in
+   device-side barriers; a rank that does not arrive within 20 s makes the
+   barrier give up and the handle report PHIKS_ERR_CUDA from
+   phiks_get_stats / host-memory applies). */
+phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_host, int rank, int world,
+                                  phiks_handle* out);
+
+/* rank, world, local slab size in doubles, bytes of the symmetric region
+   (any output pointer may be NULL). */
+phiks_status phiks_shard_info(phiks_handle h, int* rank, int* world, int64_t* local_count,
+                              size_t* sym_bytes);
+
+/* Writes PHIKS_IPC_HANDLE_BYTES bytes: the CUDA IPC handle of this rank's
+   symmetric region (zeros for world = 1).  Exchange them between the ranks
+   (e.g. an all-gather over torch.distributed) and pass the gathered array to
+   phiks_shard_open_peers. */
+phiks_status phiks_shard_ipc_handle(phiks_handle h, void* handle_out);
+
+/* handles: world × PHIKS_IPC_HANDLE_BYTES bytes, slot k = rank k's handle
+   (own slot ignored).  Maps every peer's region (cudaIpcOpenMemHandle; the
+   GPUs must be peer-capable, i.e. NVLink/NVSwitch). */
+phiks_status phiks_shard_open_peers(phiks_handle h, const void* handles);
+
+/* Device base address of this rank's symmetric region (NULL for world = 1). */
+phiks_status phiks_shard_base(phiks_handle h, void** base);
+
+/* Same-process alternative to open_peers: bases[k] = rank k's region
+   (phiks_shard_base of the handle of rank k), bases[rank] must be own. */
+phiks_status phiks_shard_set_peer_bases(phiks_handle h, void* const* bases);
+
+/* Host-only geometry of the two peer-store launches of a sharded Tucker
+   operator (no device needed): n = GLOBAL dims, stage 0 = the mode-(d-1)
+   product on the slab, stage 1 = the mode-d product on the transposed slab.
+   out7 = {L, n, R, cb, rstride, roff, colstride}: the launch views its input
+   as (L, n, R) column-major and sends output element (l, j, r) to rank
+   k = j / cb at element offset l + rstride·r + roff + colstride·(j − k·cb)
+   of the destination tensor.  The library's own launches use exactly this. */
+phiks_status phiks_shard_layout(int d, const int* n, int rank, int world, int stage, int64_t* out7);
+
+/* Emulation of `world` ranks on ONE GPU (tests): hs[k] is rank k (all in this
+   process, peers set with phiks_shard_set_peer_bases).  Runs every rank's
+   apply phase by phase on one stream — rank 0's kernels up to its next
+   barrier, then rank 1's, … — so the barriers are implied by stream order and
+   no kernel waits on another.  Same kernels, same peer-store epilogues and
+   same plan as the multi-GPU path.  vecs: world × n_vecs device pointers
+   (rank-major); outs: world × (outputs per rank) device pointers. */
+phiks_status phiks_apply_ranks_serial(const phiks_handle* hs, int world, const phiks_request* req, int n_vecs,
+                                      const double* const* vecs, double* const* outs, void* stream);
+
 /* Message for the last error on the calling thread ("" if none). */
 const char* phiks_last_error(void);
 

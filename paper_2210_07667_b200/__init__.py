@@ -22,7 +22,8 @@ import numpy as np
 from . import _lib
 from ._lib import MEM_DEVICE, MEM_HOST, MODE_LINCOMB, MODE_SAME_VECTOR, PhiksError
 
-__all__ = ["PhiKS", "PhiksError", "mode_product", "tucker", "expm", "fp64_peak_launch", "version"]
+__all__ = ["PhiKS", "ShardedPhiKS", "PhiksError", "mode_product", "tucker", "expm", "fp64_peak_launch", "version",
+           "apply_ranks_serial"]
 
 
 def _torch():
@@ -53,11 +54,11 @@ def version() -> str:
 class PhiKS:
     """Handle on K = A_d ⊕ … ⊕ A_1 (phiks_create / phiks_destroy)."""
 
-    def __init__(self, factors: Sequence[np.ndarray]):
+    def __init__(self, factors: Sequence[np.ndarray], rank: int = 0, world: int = 1):
         lib = _lib.load()
         self.d = len(factors)
         self.dims = tuple(int(np.asarray(a).shape[0]) for a in factors)
-        self.N = int(np.prod(self.dims))
+        self.rank, self.world = int(rank), int(world)
         self._A = [np.asfortranarray(np.asarray(a, dtype=np.float64)) for a in factors]
         for a in self._A:
             if a.ndim != 2 or a.shape[0] != a.shape[1]:
@@ -65,8 +66,14 @@ class PhiKS:
         n_arr = (ctypes.c_int * self.d)(*self.dims)
         a_arr = _lib.ptr_array([a.ctypes.data for a in self._A])
         h = ctypes.c_void_p()
-        _lib.check(lib.phiks_create(self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create")
+        if self.world == 1:
+            _lib.check(lib.phiks_create(self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create")
+        else:
+            _lib.check(lib.phiks_create_sharded(self.d, n_arr, a_arr, self.rank, self.world, ctypes.byref(h)),
+                       "phiks_create_sharded")
         self._h = h
+        # N: elements of the tensors apply() takes (the local slab when sharded)
+        self.N = int(np.prod(self.dims)) // self.world
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -194,3 +201,6 @@ def fp64_peak_launch(kind: int, blocks: int, iters: int, sink, stream=None) -> f
     _lib.check(lib.phiks_fp64_peak_launch(int(kind), int(blocks), int(iters), _check_dev(sink), _stream_ptr(stream),
                                           ctypes.byref(fl)), "phiks_fp64_peak_launch")
     return fl.value
+
+
+from .sharding import ShardedPhiKS, apply_ranks_serial  # noqa: E402

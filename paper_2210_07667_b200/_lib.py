@@ -16,6 +16,8 @@ MODE_LINCOMB = 1
 MEM_DEVICE = 0
 MEM_HOST = 1
 MAX_D, MAX_P, MAX_SCALES, MAX_N = 8, 6, 16, 4096
+IPC_HANDLE_BYTES = 64
+MAX_RANKS = 8
 
 _STATUS = {0: "PHIKS_OK", 1: "PHIKS_ERR_ARG", 2: "PHIKS_ERR_CUDA", 3: "PHIKS_ERR_PLAN",
            4: "PHIKS_ERR_NOMEM", 5: "PHIKS_ERR_WORKSPACE", 6: "PHIKS_ERR_LIMIT"}
@@ -72,11 +74,21 @@ def load() -> ctypes.CDLL:
     lib.phiks_plan_host.argtypes = [i, P(i), P(vp), P(Request), P(d), P(PlanInfo)]
     lib.phiks_select_plan.argtypes = [i, d, d, d, d, i, P(d), d, i, i, i, P(PlanInfo)]
     lib.phiks_set_profiling.argtypes = [vp, i]
+    lib.phiks_create_sharded.argtypes = [i, P(i), P(vp), i, i, P(vp)]
+    lib.phiks_shard_info.argtypes = [vp, P(i), P(i), P(ctypes.c_int64), P(ctypes.c_size_t)]
+    lib.phiks_shard_ipc_handle.argtypes = [vp, vp]
+    lib.phiks_shard_open_peers.argtypes = [vp, vp]
+    lib.phiks_shard_base.argtypes = [vp, P(vp)]
+    lib.phiks_shard_set_peer_bases.argtypes = [vp, P(vp)]
+    lib.phiks_apply_ranks_serial.argtypes = [P(vp), i, P(Request), i, P(vp), P(vp), vp]
+    lib.phiks_shard_layout.argtypes = [i, P(i), i, i, i, P(ctypes.c_int64)]
     lib.phiks_last_error.restype = ctypes.c_char_p
     lib.phiks_version.restype = ctypes.c_char_p
     for name in ("phiks_create", "phiks_destroy", "phiks_plan", "phiks_apply", "phiks_workspace_size",
                  "phiks_get_stats", "phiks_mode_product", "phiks_tucker", "phiks_expm",
-                 "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan", "phiks_set_profiling"):
+                 "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan", "phiks_set_profiling",
+                 "phiks_create_sharded", "phiks_shard_info", "phiks_shard_ipc_handle", "phiks_shard_open_peers",
+                 "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_shard_layout"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

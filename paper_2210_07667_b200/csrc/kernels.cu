@@ -40,6 +40,13 @@ __device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, doub
       : "d"(a), "d"(b));
 }
 
+// Peer-memory store of the slab-sharded epilogue (phiks_internal.h, Remap).
+__device__ __forceinline__ void remote_store(const Remap& rm, const OutSpec& os, int64_t rowb, int j, double v) {
+  const int k = j / rm.cb;
+  double* base = reinterpret_cast<double*>(rm.base[k] + reinterpret_cast<uintptr_t>(os.dst));
+  base[rowb + rm.colstride * static_cast<int64_t>(j - k * rm.cb)] = v;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -236,6 +243,24 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
         const OutSpec& os = p.outs[o];
         double* dst = os.dst;
         const double beta = os.beta;
+        if (p.remap.world > 0) {  // slab-sharded: stores into the owner rank's region
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) {
+            const int64_t m = m0 + wm0 + mi * 8 + lg;
+            if (m >= Mtot) continue;
+            const int64_t l = KMAJ ? 0 : m % L, r = KMAJ ? m : m / L;
+            const int64_t rowb = l + p.remap.rstride * r + p.remap.roff;
+            const int jb = j0 + wn0 + 2 * lt;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int j = jb + ni * 8 + e;
+                if (j < n) remote_store(p.remap, os, rowb, j, beta * acc[mi][ni][e]);
+              }
+          }
+          continue;
+        }
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
           const int64_t m = m0 + wm0 + mi * 8 + lg;
@@ -276,6 +301,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     }
   }
   cp_async_wait<0>();
+  if (p.remap.world > 0) __threadfence_system();  // peer stores visible before the barrier kernel
 }
 
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB>
@@ -373,7 +399,7 @@ struct TmaGeom {
   static_assert((A_ELEMS * 8) % 128 == 0 && (B_ELEMS * 8) % 128 == 0, "128B-aligned stage tiles");
 };
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool KMAJ>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool KMAJ, bool REMOTE = false>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     mode_product_tma_kernel(const __grid_constant__ ModeParams p, const __grid_constant__ TmaMaps tm) {
   constexpr int NWARPS = WARPS_M * WARPS_N;
@@ -503,6 +529,32 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
         const OutSpec& os = p.outs[o];
         double* dst = os.dst;
         const double beta = os.beta;
+        if (REMOTE) {  // slab-sharded: stores into the owner rank's region
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) {
+            const int64_t rl = wm0 + mi * 8 + lg;
+            int64_t l, r;
+            if (KMAJ) {
+              l = 0;
+              r = T.r + rl;
+              if (r >= R) continue;
+            } else {
+              l = T.l0 + rl;
+              r = T.r;
+              if (l >= L) continue;
+            }
+            const int64_t rowb = l + p.remap.rstride * r + p.remap.roff;
+            const int jb = T.j0 + wn0 + 2 * lt;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int j = jb + ni * 8 + e;
+                if (j < n) remote_store(p.remap, os, rowb, j, beta * acc[mi][ni][e]);
+              }
+          }
+          continue;
+        }
 #pragma unroll
         for (int mi = 0; mi < MI; ++mi) {
           const int64_t rl = wm0 + mi * 8 + lg;
@@ -550,6 +602,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
       }
     }
   }
+  if (REMOTE) __threadfence_system();  // peer stores visible before the barrier kernel
 }
 
 // ---- host side: tensor-map encoding through the runtime's driver entry point ----
@@ -581,7 +634,7 @@ static bool encode(CUtensorMap* m, const double* ptr, int rank, const cuuint64_t
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool REMOTE = false>
 static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   const bool kmaj = p.L == 1;
   const int n = p.n;
@@ -623,7 +676,7 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   if (kmaj) {
     using Gm = TmaGeom<BM, BN, BK, 1>;
     constexpr size_t smem = static_cast<size_t>(STAGES) * Gm::STAGE_ELEMS * 8 + 2 * STAGES * 8;
-    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, true>;
+    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, true, REMOTE>;
     if (!attr[1]) {
       *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (*err != cudaSuccess) return true;
@@ -639,7 +692,7 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   } else {
     using Gm = TmaGeom<BM, BN, BK, 0>;
     constexpr size_t smem = static_cast<size_t>(STAGES) * Gm::STAGE_ELEMS * 8 + 2 * STAGES * 8;
-    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, false>;
+    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, false, REMOTE>;
     if (!attr[0]) {
       *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (*err != cudaSuccess) return true;
@@ -670,6 +723,11 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
   if (p.ngroups == 0) return cudaSuccess;
   const int64_t Mtot = p.L * p.R;
   const int var = tile_variant();
+  if (p.remap.world > 0 && p.n > 64) {  // slab-sharded peer-store epilogue: default tile only
+    cudaError_t err = cudaSuccess;
+    if (launch_tma<64, 128, 16, 2, 2, 4, 2, true>(p, st, &err)) return err;
+    return launch_cfg<64, 64, 16, 2, 2, 4, 3>(p, st);
+  }
   if (p.n > 64 && (var == 0 || var >= 10)) {
     cudaError_t err = cudaSuccess;
     const int64_t big = Mtot * ((p.n + 127) / 128) * p.ngroups;
@@ -903,6 +961,59 @@ cudaError_t launch_fp64_peak(int kind, int blocks, int64_t iters, double* sink, 
     fp64_peak_kernel<1><<<blocks, 256, 0, st>>>(iters, sink);
     *flops = static_cast<double>(blocks) * 256.0 * static_cast<double>(iters) * 32.0 * 2.0;
   }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Cross-rank barrier and small scatter of the slab-sharded path (peer memory
+// mapped through CUDA IPC; every pointer below may live on another GPU).
+// ---------------------------------------------------------------------------
+__global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
+  const int t = threadIdx.x;
+  __threadfence_system();
+  __syncthreads();
+  if (t < p.world) {
+    uint64_t* slot = p.peer_flags[t] + p.rank;  // my slot in peer t's array
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(slot), "l"(p.epoch) : "memory");
+  }
+  if (t < p.world) {
+    const uint64_t* mine = p.peer_flags[p.rank] + t;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t0));
+    while (true) {
+      uint64_t v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(mine) : "memory");
+      if (v >= p.epoch) break;
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
+      if (now - t0 > p.timeout_ns) {
+        atomicExch(p.err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+cudaError_t launch_barrier(const BarrierParams& p, cudaStream_t st) {
+  if (p.world <= 1) return cudaSuccess;
+  barrier_kernel<<<1, 32, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+__global__ void scatter_small_kernel(const __grid_constant__ ScatterParams p) {
+  for (int i = threadIdx.x; i < p.cnt * p.world; i += blockDim.x) {
+    const int k = i / p.cnt, c = i % p.cnt;
+    p.dst[k][p.rank * p.cnt + c] = p.src[c];
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+cudaError_t launch_scatter_small(const ScatterParams& p, cudaStream_t st) {
+  scatter_small_kernel<<<1, 128, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -15,7 +15,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
+#include <memory>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -81,7 +83,30 @@ struct phiks_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> ev_flops;
   int ev_used = 0;
+  // ---- slab sharding along the outermost mode (phiks_create_sharded) ----
+  // n[] holds the LOCAL dims of layout S_d (n[d-1] = gn[d-1]/world); the
+  // transposed layout S_{d-1} has dims (n_1..n_{d-2}, gn[d-2]/world, gn[d-1]).
+  int rank = 0, world = 1;
+  int gn[PHIKS_MAX_D] = {0};
+  char* sym = nullptr;  // own symmetric region: control block + T/Y pools
+  size_t sym_bytes = 0;
+  size_t sym_slot = 0;  // bytes per pooled local tensor
+  char* peer[kMaxRanks] = {nullptr};
+  bool peer_ipc[kMaxRanks] = {false};
+  bool peers_ready = false;
+  uint64_t epoch = 0;
+  bool sharded() const { return world > 1; }
 };
+
+namespace {
+// symmetric region layout (identical on every rank)
+constexpr size_t kCtrlFlags = 0;                                   // uint64 flags[kMaxRanks]
+constexpr size_t kCtrlErr = kMaxRanks * sizeof(uint64_t);          // int err
+constexpr size_t kCtrlNorms = 256;                                 // double norms[kMaxRanks][kMaxVecs]
+constexpr size_t kCtrlBytes = 4096;
+constexpr int kShardChunk = 16;  // Tucker operators per sharded sub-batch (T and Y pools)
+constexpr uint64_t kBarrierTimeoutNs = 20ull * 1000 * 1000 * 1000;
+}  // namespace
 
 namespace {
 
@@ -100,6 +125,29 @@ struct Arena {
     return reinterpret_cast<double*>(p);
   }
 };
+
+// Geometry of the two peer-store launches of a slab-sharded Tucker operator
+// (DESIGN.md §0(e)).  gn: global dims.  stage 0: the mode-(d-1) product on the
+// slab (layout S_d) storing into layout S_{d-1}; stage 1: the mode-d product
+// on layout S_{d-1} storing back into S_d.  Output element (l, j, r) of the
+// (L, n, R) launch goes to rank k = j / cb at offset
+//   l + rstride·r + roff + colstride·(j − k·cb).
+struct ShardStage {
+  int64_t L, n, R, cb, rstride, roff, colstride;
+};
+ShardStage shard_stage(int d, const int* gn, int rank, int world, int stage) {
+  int64_t L0 = 1;
+  for (int mu = 0; mu + 2 < d; ++mu) L0 *= gn[mu];
+  const int64_t na = gn[d - 2], nd = gn[d - 1];
+  const int64_t cb = na / world, cd = nd / world;
+  ShardStage s{};
+  if (stage == 0) {
+    s = ShardStage{L0, na, cd, cb, L0 * cb, L0 * cb * rank * cd, L0};
+  } else {
+    s = ShardStage{L0 * cb, nd, 1, cd, 0, L0 * cb * rank, L0 * na};
+  }
+  return s;
+}
 
 // A source list with coefficients, kept on the host until a launch is built.
 struct Src {
@@ -133,6 +181,16 @@ struct Exec {
   int split = 0;                     // 1: quadrature sums as a separate pass, 2: also squaring
   double mu_flops = 0.0, expm_flops = 0.0;
   phiks_status status = PHIKS_OK;
+  int64_t barriers = 0;
+
+  // Recorded ops: with `rec` set, launches are appended instead of issued (the
+  // phase-interleaved emulation of several ranks on one GPU replays them).
+  struct Op {
+    bool barrier;
+    std::function<cudaError_t(cudaStream_t)> fn;
+    const char* what;
+  };
+  std::vector<Op>* rec = nullptr;
 
   bool ok() const { return status == PHIKS_OK; }
   void check(cudaError_t e, const char* what) {
@@ -140,6 +198,32 @@ struct Exec {
       status = PHIKS_ERR_CUDA;
       g_err = std::string(what) + ": " + cudaGetErrorString(e);
     }
+  }
+  void emit(const char* what, std::function<cudaError_t(cudaStream_t)> fn) {
+    ++launches;
+    if (measure || !ok()) return;
+    if (rec)
+      rec->push_back(Op{false, std::move(fn), what});
+    else
+      check(fn(st), what);
+  }
+  // cross-rank barrier of a sharded handle (device-side, stream-ordered)
+  void barrier() {
+    ++barriers;
+    if (measure || !ok() || !h->sharded()) return;
+    ++launches;
+    if (rec) {
+      rec->push_back(Op{true, nullptr, "barrier"});
+      return;
+    }
+    BarrierParams bp{};
+    bp.rank = h->rank;
+    bp.world = h->world;
+    bp.epoch = ++h->epoch;
+    bp.timeout_ns = kBarrierTimeoutNs;
+    for (int k = 0; k < h->world; ++k) bp.peer_flags[k] = reinterpret_cast<uint64_t*>(h->peer[k] + kCtrlFlags);
+    bp.err = reinterpret_cast<int*>(h->sym + kCtrlErr);
+    check(launch_barrier(bp, st), "barrier");
   }
 
   // ---- one mode-product launch from host-side term lists ----
@@ -149,7 +233,7 @@ struct Exec {
     int group;
     std::vector<Out> outs;
   };
-  void mode_launch(int64_t L, int n, int64_t R, const std::vector<LaunchTerm>& terms) {
+  void mode_launch(int64_t L, int n, int64_t R, const std::vector<LaunchTerm>& terms, const Remap* rm = nullptr) {
     if (!ok() || terms.empty()) return;
     // chunk so every launch fits ModeParams; a group's terms stay in order
     size_t i = 0;
@@ -160,6 +244,7 @@ struct Exec {
       p.R = R;
       p.n = n;
       p.ngroups = 0;
+      if (rm) p.remap = *rm;
       int nt = 0, no = 0, ns = 0;
       std::map<int, int> gslot;  // group key -> slot in this launch
       std::vector<std::vector<int>> gterms;
@@ -210,6 +295,17 @@ struct Exec {
         p.groups[g].t1 = tt;
       }
       p.ngroups = static_cast<int>(gterms.size());
+      if (rec) {
+        ++launches;
+        if (!measure) {
+          std::shared_ptr<ModeParams> sp(pp);
+          rec->push_back(Op{false, [sp](cudaStream_t s) { return launch_mode_product(*sp, s); }, "mode_product"});
+        } else {
+          delete pp;
+        }
+        i = j;
+        continue;
+      }
       if (!measure && h->profiling) {
         if (h->ev_used == static_cast<int>(h->ev.size())) {
           cudaEvent_t a, b;
@@ -249,9 +345,8 @@ struct Exec {
         os.nsrc = need;
         for (const Src& s : outs[j].srcs) p.srcs[ns++] = SrcRef{s.ptr, s.coef};
       }
-      if (!measure) check(launch_combine(p, st), "combine");
-      ++launches;
-      delete pp;
+      std::shared_ptr<CombineParams> sp(pp);
+      emit("combine", [sp](cudaStream_t s) { return launch_combine(*sp, s); });
       i = j;
     }
   }
@@ -272,9 +367,8 @@ struct Exec {
           pp->dst[o] = dsts[o0 + o];
           for (size_t k = 0; k < srcs.size(); ++k) pp->coef[o][k] = coef[o0 + o][k];
         }
-        if (!measure) check(launch_multi_combine(*pp, st), "multi_combine");
-        ++launches;
-        delete pp;
+        std::shared_ptr<MultiCombineParams> sp(pp);
+        emit("multi_combine", [sp](cudaStream_t s) { return launch_multi_combine(*sp, s); });
       }
       return;
     }
@@ -294,12 +388,29 @@ struct Exec {
   // A batch whose last-mode epilogues run as a separate streaming pass: every
   // item writes its raw Tucker result Y_b, then the epilogue recurrences (in
   // group order, accumulations included) are evaluated symbolically into one
-  // matrix-form combination over {Y_b} ∪ external sources.
+  // matrix-form combination over {Y_b} ∪ external sources.  Sharded handles
+  // always take this path, kShardChunk items at a time (the Y_b then live in
+  // the symmetric region); a later chunk accumulates into the outputs.
   void tucker_batch_split(const std::vector<TuckerItem>& items) {
     if (!ok() || items.empty()) return;
     const int64_t N = h->N;
-    while (y_pool.size() < items.size()) y_pool.push_back(ar->alloc_doubles(N));
-    std::vector<TuckerItem> raw(items.size());
+    const bool shard = h->sharded();
+    const size_t chunk = shard ? static_cast<size_t>(kShardChunk) : items.size();
+    if (!shard)
+      while (y_pool.size() < items.size()) y_pool.push_back(ar->alloc_doubles(N));
+    // symbolic keys of the Y_b: the real buffers (local) or tags (sharded, pooled per chunk)
+    auto ykey = [&](size_t b) -> const double* {
+      return shard ? reinterpret_cast<const double*>(static_cast<uintptr_t>(16 + 16 * b)) : y_pool[b];
+    };
+    auto yitem = [&](const double* key) -> int64_t {  // item index of a Y key, -1 for externals
+      if (shard) {
+        const uintptr_t v = reinterpret_cast<uintptr_t>(key);
+        return (v >= 16 && v < 16 + 16 * items.size() && v % 16 == 0) ? static_cast<int64_t>(v / 16 - 1) : -1;
+      }
+      for (size_t b = 0; b < items.size(); ++b)
+        if (y_pool[b] == key) return static_cast<int64_t>(b);
+      return -1;
+    };
     typedef std::vector<std::pair<const double*, double>> Lin;
     std::map<const double*, Lin> val;
     std::vector<double*> order;
@@ -312,13 +423,9 @@ struct Exec {
       acc.emplace_back(ptr, c);
     };
     for (size_t b = 0; b < items.size(); ++b) {
-      raw[b] = items[b];
-      raw[b].in_scale = 1.0;
-      raw[b].group = static_cast<int>(b);
-      raw[b].outs.assign(1, Out{y_pool[b], 1.0, {}});
       for (const Out& o : items[b].outs) {
         Lin lin;
-        add(lin, y_pool[b], o.beta * items[b].in_scale);
+        add(lin, ykey(b), o.beta * items[b].in_scale);
         for (const Src& sr : o.srcs) {
           auto it = val.find(sr.ptr);
           if (it != val.end())
@@ -330,16 +437,138 @@ struct Exec {
         val[o.dst] = lin;
       }
     }
-    tucker_batch(raw);
-    std::vector<const double*> srcs;
-    for (double* d : order)
-      for (auto& t : val[d])
-        if (std::find(srcs.begin(), srcs.end(), t.first) == srcs.end()) srcs.push_back(t.first);
-    std::vector<std::vector<double>> coef(order.size(), std::vector<double>(srcs.size(), 0.0));
-    for (size_t o = 0; o < order.size(); ++o)
-      for (auto& t : val[order[o]])
-        coef[o][std::find(srcs.begin(), srcs.end(), t.first) - srcs.begin()] = t.second;
-    mcombine(N, srcs, order, coef);
+    for (size_t c0 = 0; c0 < items.size() && ok(); c0 += chunk) {
+      const size_t c1 = std::min(items.size(), c0 + chunk);
+      std::vector<TuckerItem> raw(items.begin() + c0, items.begin() + c1);
+      for (size_t b = 0; b < raw.size(); ++b) {
+        raw[b].in_scale = 1.0;
+        raw[b].group = static_cast<int>(b);
+        raw[b].outs.assign(1, Out{shard ? nullptr : y_pool[c0 + b], 1.0, {}});
+      }
+      if (shard)
+        tucker_raw_sharded(raw);
+      else
+        tucker_batch(raw);
+      // the combination restricted to this chunk's Y_b (+ externals in the first chunk)
+      auto real = [&](const double* key) -> const double* {
+        const int64_t b = yitem(key);
+        if (b < 0) return key;
+        return shard ? symY(static_cast<int>(b - static_cast<int64_t>(c0))) : y_pool[b];
+      };
+      std::vector<const double*> srcs;
+      std::vector<double*> dsts;
+      std::vector<std::vector<std::pair<const double*, double>>> rows;
+      for (double* dptr : order) {
+        std::vector<std::pair<const double*, double>> row;
+        for (auto& t : val[dptr]) {
+          const int64_t b = yitem(t.first);
+          const bool in_chunk = b >= static_cast<int64_t>(c0) && b < static_cast<int64_t>(c1);
+          if (in_chunk || (b < 0 && c0 == 0)) row.emplace_back(real(t.first), t.second);
+        }
+        if (c0 > 0) {
+          if (row.empty()) continue;
+          row.emplace_back(dptr, 1.0);
+        }
+        dsts.push_back(dptr);
+        rows.push_back(row);
+      }
+      for (auto& row : rows)
+        for (auto& t : row)
+          if (std::find(srcs.begin(), srcs.end(), t.first) == srcs.end()) srcs.push_back(t.first);
+      std::vector<std::vector<double>> coef(dsts.size(), std::vector<double>(srcs.size(), 0.0));
+      for (size_t o = 0; o < dsts.size(); ++o)
+        for (auto& t : rows[o]) coef[o][std::find(srcs.begin(), srcs.end(), t.first) - srcs.begin()] += t.second;
+      mcombine(N, srcs, dsts, coef);
+    }
+  }
+
+  // ---- slab-sharded raw Tucker operators (≤ kShardChunk items) ----
+  // Local layout S_d: dims (n_1..n_{d-1}, n_d/P), the rank's slab of the outermost
+  // mode.  Modes 1..d-2 are local; the mode-(d-1) product stores its output in
+  // layout S_{d-1} (dims (n_1..n_{d-2}, n_{d-1}/P, n_d)) on the rank owning each
+  // output column; after a barrier the mode-d product is local there and stores
+  // back into layout S_d on the owner of each output column; a second barrier
+  // makes Y_b complete.  Items write Y_b = symY(b).
+  double* symT(int i) const { return reinterpret_cast<double*>(h->sym + kCtrlBytes + i * h->sym_slot); }
+  double* symY(int i) const {
+    return reinterpret_cast<double*>(h->sym + kCtrlBytes + (kShardChunk + i) * h->sym_slot);
+  }
+  void tucker_raw_sharded(const std::vector<TuckerItem>& items) {
+    if (!ok() || items.empty()) return;
+    const int d = h->d, P = h->world, rk = h->rank;
+    const int64_t N = h->N;
+    const size_t nb = items.size();
+    auto& scr = scr_pool;
+    if (d >= 3)
+      while (scr[0].size() < nb) scr[0].push_back(ar->alloc_doubles(N));
+    if (d >= 4)
+      while (scr[1].size() < nb) scr[1].push_back(ar->alloc_doubles(N));
+    int64_t L = 1;
+    for (int mu = 0; mu + 2 < d; ++mu) {
+      const int n = h->n[mu];
+      std::vector<LaunchTerm> terms;
+      for (size_t b = 0; b < nb; ++b) {
+        LaunchTerm t;
+        t.in = (mu == 0) ? items[b].in : scr[(mu - 1) % 2][b];
+        t.M = items[b].mats[mu];
+        t.group = static_cast<int>(b);
+        t.outs.push_back(Out{scr[mu % 2][b], 1.0, {}});
+        terms.push_back(std::move(t));
+      }
+      mode_launch(L, n, N / (L * n), terms);
+      L *= n;
+    }
+    const ShardStage s0 = shard_stage(d, h->gn, rk, P, 0), s1 = shard_stage(d, h->gn, rk, P, 1);
+    auto remap_of = [&](const ShardStage& s) {
+      Remap r{};
+      r.world = P;
+      r.cb = static_cast<int>(s.cb);
+      r.rstride = s.rstride;
+      r.roff = s.roff;
+      r.colstride = s.colstride;
+      for (int k = 0; k < P; ++k) r.base[k] = h->peer[k];
+      return r;
+    };
+    const Remap ra = remap_of(s0), rb = remap_of(s1);
+    (void)L;
+    {
+      std::vector<LaunchTerm> terms;
+      for (size_t b = 0; b < nb; ++b) {
+        LaunchTerm t;
+        t.in = (d == 2) ? items[b].in : scr[(d - 3) % 2][b];
+        t.M = items[b].mats[d - 2];
+        t.group = static_cast<int>(b);
+        t.outs.push_back(Out{reinterpret_cast<double*>(kCtrlBytes + b * h->sym_slot), 1.0, {}});
+        terms.push_back(std::move(t));
+      }
+      mode_launch(s0.L, static_cast<int>(s0.n), s0.R, terms, &ra);
+    }
+    barrier();
+    {
+      std::vector<LaunchTerm> terms;
+      for (size_t b = 0; b < nb; ++b) {
+        LaunchTerm t;
+        t.in = symT(static_cast<int>(b));
+        t.M = items[b].mats[d - 1];
+        t.group = static_cast<int>(b);
+        t.outs.push_back(Out{reinterpret_cast<double*>(kCtrlBytes + (kShardChunk + b) * h->sym_slot), 1.0, {}});
+        terms.push_back(std::move(t));
+      }
+      mode_launch(s1.L, static_cast<int>(s1.n), s1.R, terms, &rb);
+    }
+    barrier();
+    int64_t nsum = 0;
+    for (int mu = 0; mu < d; ++mu) nsum += h->gn[mu];
+    tucker_ops += static_cast<int64_t>(nb);
+    mu_flops += static_cast<double>(nb) * 2.0 * static_cast<double>(N) * static_cast<double>(nsum);
+  }
+
+  // every batch of run_job: sharded handles always split
+  void batch(const std::vector<TuckerItem>& items, bool split_it) {
+    if (h->sharded() || split_it)
+      tucker_batch_split(items);
+    else
+      tucker_batch(items);
   }
 
   // ---- batched Tucker operators (Eq. (4)) ----
@@ -427,8 +656,8 @@ void expm_batch(Exec& ex, double tau, std::vector<ExpReq>& reqs) {
     X4[f] = ex.ar->alloc_doubles(nn);
     if (!Ident.count(n)) {
       Ident[n] = ex.ar->alloc_doubles(nn);
-      if (!ex.measure) ex.check(launch_set_identity(Ident[n], n, 1.0, ex.st), "set_identity");
-      ++ex.launches;
+      double* I = Ident[n];
+      ex.emit("set_identity", [I, n](cudaStream_t s) { return launch_set_identity(I, n, 1.0, s); });
     }
   }
   // distinct n values
@@ -710,10 +939,7 @@ void run_job(Exec& ex, const Job& jb) {
           }
       }
     }
-    if (ex.split >= 1)
-      ex.tucker_batch_split(items);
-    else
-      ex.tucker_batch(items);
+    ex.batch(items, ex.split >= 1);
     if (!ex.ok()) return;
 
     // ---- Stage C: squaring, j = s..1 ----
@@ -743,10 +969,7 @@ void run_job(Exec& ex, const Job& jb) {
         }
         sq.push_back(it);
       }
-      if (ex.split >= 2)
-        ex.tucker_batch_split(sq);
-      else
-        ex.tucker_batch(sq);
+      ex.batch(sq, ex.split >= 2);
       if (!ex.ok()) return;
     }
   }
@@ -778,7 +1001,7 @@ void run_job(Exec& ex, const Job& jb) {
       }
     }
   }
-  ex.tucker_batch(ex_items);
+  ex.batch(ex_items, false);
 }
 
 }  // namespace
@@ -806,6 +1029,7 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
       return fail(PHIKS_ERR_ARG, "n[mu] out of range or null A");
     }
     h->n[mu] = n[mu];
+    h->gn[mu] = n[mu];
     h->N *= n[mu];
   }
   // dedupe bitwise-identical factors
@@ -862,6 +1086,9 @@ phiks_status phiks_destroy(phiks_handle h) {
     if (F.dA) cudaFree(F.dA);
   if (h->ws_own) cudaFree(h->ws_own);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
+  for (int k = 0; k < kMaxRanks; ++k)
+    if (h->peer_ipc[k] && h->peer[k]) cudaIpcCloseMemHandle(h->peer[k]);
+  if (h->sym) cudaFree(h->sym);
   for (auto& e : h->ev) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -969,45 +1196,154 @@ phiks_status phiks_plan(phiks_handle h, const phiks_request* req, const double* 
   return PHIKS_OK;
 }
 
-static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_vecs, const double* const* vecs,
-                               double* const* outs, void* workspace, size_t ws_bytes, void* stream,
-                               bool size_only, const phiks_plan_info* forced, size_t* size_out) {
-  int p = 0;
-  phiks_status st = validate(h, req, p);
-  if (st != PHIKS_OK) return st;
-  const bool same = req->mode == PHIKS_MODE_SAME_VECTOR;
-  const int nouts = same ? req->n_ells * req->n_scales : req->n_scales;
-  if (!size_only) {
-    if (same ? n_vecs != 1 : n_vecs != req->n_ells) return fail(PHIKS_ERR_ARG, "n_vecs");
-    if (!vecs || !outs) return fail(PHIKS_ERR_ARG, "null vecs/outs");
-    for (int i = 0; i < n_vecs; ++i)
-      if (!vecs[i]) return fail(PHIKS_ERR_ARG, "null vector");
-    for (int i = 0; i < nouts; ++i)
-      if (!outs[i]) return fail(PHIKS_ERR_ARG, "null output");
-  }
-  cudaStream_t cs = static_cast<cudaStream_t>(stream);
-  const bool host_mem = req->mem_kind == PHIKS_MEM_HOST;
-  const int64_t N = h->N;
-  const size_t tbytes = static_cast<size_t>(N) * sizeof(double);
-
+// One apply on one handle, split into phases so that several emulated ranks
+// can be driven phase by phase (phiks_apply_ranks_serial).
+struct ApplyRun {
+  phiks_handle h = nullptr;
+  const phiks_request* req = nullptr;
+  int p = 0, n_vecs = 0, nouts = 0;
+  bool same = true, host_mem = false, size_only = false;
+  const double* const* vecs = nullptr;
+  double* const* outs = nullptr;
+  cudaStream_t cs = nullptr;
+  int64_t N = 0;
+  size_t tbytes = 0;
   Arena ar;
-  Exec ex{h, cs, true, &ar};
-  static const int split_mode = [] {
-    // default 2: quadrature sums and squaring recurrences as a streaming pass
-    // (measured faster on B200 than the fused epilogue); 0 = fused
-    const char* e = getenv("PHIKS_SPLIT");
-    return e ? atoi(e) : 2;
-  }();
-  ex.split = split_mode;
+  Exec ex{};
   Job jb{};
-  jb.mode = req->mode;
-  jb.p = p;
-  jb.n_scales = req->n_scales;
-  jb.tau = req->tau;
+  std::vector<double*> dv, dout;
+  plan::Plan pl;
+  int split = 2;
+  // lincomb norms
+  bool need_norms = false;
+  std::vector<int> which;        // index into vecs of v_1..v_p present
+  double* nscratch = nullptr;    // device: 1024*kMaxVecs partials + kMaxVecs norms²
+  std::vector<double*> ntmp;     // host-memory inputs staged for the norms
+  int norm_launches = 0;
 
-  // staging for host memory
-  std::vector<double*> dv(n_vecs > 0 ? n_vecs : 0, nullptr), dout(nouts, nullptr);
-  auto bind = [&](bool measure) {
+  phiks_status init(phiks_handle h_, const phiks_request* req_, int n_vecs_, const double* const* vecs_,
+                    double* const* outs_, void* stream, bool size_only_) {
+    h = h_;
+    req = req_;
+    phiks_status st = validate(h, req, p);
+    if (st != PHIKS_OK) return st;
+    n_vecs = n_vecs_;
+    vecs = vecs_;
+    outs = outs_;
+    size_only = size_only_;
+    same = req->mode == PHIKS_MODE_SAME_VECTOR;
+    nouts = same ? req->n_ells * req->n_scales : req->n_scales;
+    if (!size_only) {
+      if (same ? n_vecs != 1 : n_vecs != req->n_ells) return fail(PHIKS_ERR_ARG, "n_vecs");
+      if (!vecs || !outs) return fail(PHIKS_ERR_ARG, "null vecs/outs");
+      for (int i = 0; i < n_vecs; ++i)
+        if (!vecs[i]) return fail(PHIKS_ERR_ARG, "null vector");
+      for (int i = 0; i < nouts; ++i)
+        if (!outs[i]) return fail(PHIKS_ERR_ARG, "null output");
+    }
+    if (h->sharded() && !h->peers_ready) return fail(PHIKS_ERR_ARG, "sharded handle: peers not opened");
+    cs = static_cast<cudaStream_t>(stream);
+    host_mem = req->mem_kind == PHIKS_MEM_HOST;
+    N = h->N;
+    tbytes = static_cast<size_t>(N) * sizeof(double);
+    static const int split_mode = [] {
+      // default 2: quadrature sums and squaring recurrences as a streaming pass
+      // (measured faster on B200 than the fused epilogue); 0 = fused
+      const char* e = getenv("PHIKS_SPLIT");
+      return e ? atoi(e) : 2;
+    }();
+    split = split_mode;
+    jb.mode = req->mode;
+    jb.p = p;
+    jb.n_scales = req->n_scales;
+    jb.tau = req->tau;
+    if (size_only) dv.assign(same ? 1 : req->n_ells, nullptr);
+    else dv.assign(n_vecs > 0 ? n_vecs : 0, nullptr);
+    dout.assign(nouts, nullptr);
+    need_norms = !same && p >= 1 && req->force_s < 0 && !size_only;
+    return PHIKS_OK;
+  }
+
+  // ---- lincomb plan input: ||v_ℓ||₂ (deterministic GPU reduction; sharded:
+  // local sums of squares scattered to every rank, summed in rank order) ----
+  phiks_status norms_enqueue(bool do_barrier) {
+    if (!need_norms) return PHIKS_OK;
+    std::vector<const double*> vv;
+    for (int ell = 1; ell <= p; ++ell)
+      for (int i = 0; i < req->n_ells; ++i)
+        if (req->ells[i] == ell) which.push_back(i);
+    if (which.empty()) return PHIKS_OK;
+    const size_t sbytes = sizeof(double) * (1024 * kMaxVecs + kMaxVecs);
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&nscratch), sbytes, cs));
+    for (size_t k = 0; k < which.size(); ++k) {
+      if (host_mem) {
+        double* t = nullptr;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t), tbytes, cs));
+        CUDA_TRY(cudaMemcpyAsync(t, vecs[which[k]], tbytes, cudaMemcpyHostToDevice, cs));
+        ntmp.push_back(t);
+        vv.push_back(t);
+      } else {
+        vv.push_back(vecs[which[k]]);
+      }
+    }
+    CUDA_TRY(launch_sumsq(vv.data(), static_cast<int>(vv.size()), N, nscratch, nscratch + 1024 * kMaxVecs, cs));
+    norm_launches = 2;
+    if (h->sharded()) {
+      ScatterParams sp{};
+      sp.rank = h->rank;
+      sp.world = h->world;
+      sp.cnt = static_cast<int>(which.size());
+      sp.src = nscratch + 1024 * kMaxVecs;
+      for (int k = 0; k < h->world; ++k) sp.dst[k] = reinterpret_cast<double*>(h->peer[k] + kCtrlNorms);
+      CUDA_TRY(launch_scatter_small(sp, cs));
+      ++norm_launches;
+      if (do_barrier) {
+        Arena a0;
+        Exec eb{h, cs, false, &a0};
+        eb.barrier();
+        if (!eb.ok()) return eb.status;
+        ++norm_launches;
+      }
+    }
+    return PHIKS_OK;
+  }
+  // read back (synchronises the stream) and plan; `ctrl` = the control block
+  // holding the gathered partial sums (sharded) — any rank's, they are equal
+  phiks_status norms_finish(const char* ctrl) {
+    std::vector<double> norms(p, 0.0);
+    if (!which.empty()) {
+      const int nv = static_cast<int>(which.size());
+      const int W = h->sharded() ? h->world : 1;
+      const double* srcp = h->sharded() ? reinterpret_cast<const double*>(ctrl + kCtrlNorms)
+                                        : nscratch + 1024 * kMaxVecs;
+      CUDA_TRY(cudaMemcpyAsync(h->h_pinned, srcp, sizeof(double) * nv * W, cudaMemcpyDeviceToHost, cs));
+      for (double* t : ntmp) CUDA_TRY(cudaFreeAsync(t, cs));
+      ntmp.clear();
+      CUDA_TRY(cudaFreeAsync(nscratch, cs));
+      nscratch = nullptr;
+      CUDA_TRY(cudaStreamSynchronize(cs));
+      for (int k = 0; k < nv; ++k) {
+        double s2 = 0.0;
+        for (int r = 0; r < W; ++r) s2 += h->h_pinned[r * nv + k];
+        norms[req->ells[which[k]] - 1] = std::sqrt(s2);
+      }
+    }
+    return make_plan(h, req, p, norms, pl);
+  }
+
+  phiks_status plan_direct(const phiks_plan_info* forced) {
+    if (forced) {
+      pl.s = forced->s;
+      pl.q = forced->q;
+      pl.ok = true;
+      return PHIKS_OK;
+    }
+    if (!same && p >= 1 && req->force_s < 0 && size_only) return fail(PHIKS_ERR_ARG, "lincomb sizing needs a plan");
+    std::vector<double> norms;
+    return make_plan(h, req, p, norms, pl);
+  }
+
+  void bind(bool measure) {
     ar.off = 0;
     ar.measure = measure;
     ex.measure = measure;
@@ -1016,8 +1352,7 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
     auto fake = [](int k) { return reinterpret_cast<double*>(static_cast<uintptr_t>(0x7f0000000000ULL) + 4096ULL * k); };
     for (int i = 0; i < static_cast<int>(dv.size()); ++i)
       dv[i] = host_mem ? ar.alloc_doubles(N) : (size_only ? fake(i) : const_cast<double*>(vecs[i]));
-    for (int i = 0; i < nouts; ++i)
-      dout[i] = host_mem ? ar.alloc_doubles(N) : (size_only ? fake(64 + i) : outs[i]);
+    for (int i = 0; i < nouts; ++i) dout[i] = host_mem ? ar.alloc_doubles(N) : (size_only ? fake(64 + i) : outs[i]);
     for (int i = 0; i < kMaxVecs; ++i) jb.vin[i] = nullptr;
     if (same) {
       jb.vin[0] = dv.empty() ? nullptr : dv[0];
@@ -1027,81 +1362,29 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
       for (int i = 0; i < req->n_ells; ++i) jb.vin[req->ells[i]] = dv.empty() ? nullptr : dv[i];
       for (int j = 0; j < req->n_scales; ++j) jb.out_lin[j] = dout[j];
     }
-  };
-  if (size_only) dv.assign(same ? 1 : req->n_ells, nullptr);
-
-  // ---- plan (lincomb needs ||v_ℓ||: one deterministic GPU reduction + D2H) ----
-  std::vector<double> norms;
-  plan::Plan pl;
-  if (forced) {
-    pl.s = forced->s;
-    pl.q = forced->q;
-    pl.ok = true;
-  } else if (!same && p >= 1 && req->force_s < 0 && !size_only) {
-    // norms of v_1..v_p from device data
-    std::vector<const double*> vv;
-    std::vector<int> which;
-    for (int ell = 1; ell <= p; ++ell) {
-      for (int i = 0; i < req->n_ells; ++i)
-        if (req->ells[i] == ell) {
-          vv.push_back(nullptr);
-          which.push_back(i);
-        }
-    }
-    // host-memory inputs are normed on the device after staging (below); device inputs now
-    norms.assign(p, 0.0);
-    if (!vv.empty()) {
-      // workspace may not exist yet: use a private scratch allocation
-      double* scratch = nullptr;
-      const size_t sbytes = sizeof(double) * (1024 * kMaxVecs + kMaxVecs);
-      CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sbytes, cs));
-      std::vector<double*> tmp;
-      if (host_mem) {
-        for (size_t k = 0; k < vv.size(); ++k) {
-          double* t = nullptr;
-          CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t), tbytes, cs));
-          CUDA_TRY(cudaMemcpyAsync(t, vecs[which[k]], tbytes, cudaMemcpyHostToDevice, cs));
-          tmp.push_back(t);
-          vv[k] = t;
-        }
-      } else {
-        for (size_t k = 0; k < vv.size(); ++k) vv[k] = vecs[which[k]];
-      }
-      CUDA_TRY(launch_sumsq(vv.data(), static_cast<int>(vv.size()), N, scratch, scratch + 1024 * kMaxVecs, cs));
-      CUDA_TRY(cudaMemcpyAsync(h->h_pinned, scratch + 1024 * kMaxVecs, sizeof(double) * vv.size(),
-                               cudaMemcpyDeviceToHost, cs));
-      for (double* t : tmp) CUDA_TRY(cudaFreeAsync(t, cs));
-      CUDA_TRY(cudaFreeAsync(scratch, cs));
-      CUDA_TRY(cudaStreamSynchronize(cs));
-      h->stats.kernel_launches = 2;
-      for (size_t k = 0; k < vv.size(); ++k) norms[req->ells[which[k]] - 1] = std::sqrt(h->h_pinned[k]);
-    }
-    st = make_plan(h, req, p, norms, pl);
-    if (st != PHIKS_OK) return st;
-  } else {
-    if (!same && p >= 1 && req->force_s < 0 && size_only) return fail(PHIKS_ERR_ARG, "lincomb sizing needs a plan");
-    st = make_plan(h, req, p, norms, pl);
-    if (st != PHIKS_OK) return st;
   }
-  jb.s = pl.s;
-  jb.q = pl.q;
 
-  // ---- measure ----
-  bind(true);
-  run_job(ex, jb);
-  if (!ex.ok()) return ex.status;
-  const size_t need = ar.off;
-  if (size_out) *size_out = need;
-  if (size_only) return PHIKS_OK;
+  phiks_status measure(size_t* need) {
+    jb.s = pl.s;
+    jb.q = pl.q;
+    ex = Exec{h, cs, true, &ar};
+    ex.split = split;
+    bind(true);
+    run_job(ex, jb);
+    if (!ex.ok()) return ex.status;
+    *need = ar.off;
+    return PHIKS_OK;
+  }
 
-  char* base = nullptr;
-  if (workspace) {
-    if (ws_bytes < need) {
-      h->stats.workspace_bytes = need;
-      return fail(PHIKS_ERR_WORKSPACE, "workspace too small");
+  phiks_status workspace(void* workspace, size_t ws_bytes, size_t need, char** base) {
+    if (workspace) {
+      if (ws_bytes < need) {
+        h->stats.workspace_bytes = need;
+        return fail(PHIKS_ERR_WORKSPACE, "workspace too small");
+      }
+      *base = static_cast<char*>(workspace);
+      return PHIKS_OK;
     }
-    base = static_cast<char*>(workspace);
-  } else {
     if (h->ws_own_bytes < need) {
       if (h->ws_own) {
         CUDA_TRY(cudaStreamSynchronize(cs));
@@ -1113,35 +1396,96 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
         return fail(PHIKS_ERR_NOMEM, "workspace cudaMalloc");
       h->ws_own_bytes = need > 0 ? need : 256;
     }
-    base = static_cast<char*>(h->ws_own);
+    *base = static_cast<char*>(h->ws_own);
+    return PHIKS_OK;
   }
-  // ---- execute ----
-  ar.base = base;
-  ar.cap = need;
-  Exec ex2{h, cs, false, &ar};
-  ex = ex2;
-  ex.split = split_mode;
-  bind(false);
-  if (host_mem)
-    for (size_t i = 0; i < dv.size(); ++i)
-      CUDA_TRY(cudaMemcpyAsync(dv[i], vecs[i], tbytes, cudaMemcpyHostToDevice, cs));
-  run_job(ex, jb);
-  if (!ex.ok()) return ex.status;
-  if (host_mem) {
-    for (int i = 0; i < nouts; ++i) CUDA_TRY(cudaMemcpyAsync(outs[i], dout[i], tbytes, cudaMemcpyDeviceToHost, cs));
-    CUDA_TRY(cudaStreamSynchronize(cs));
+
+  // enqueue (rec == nullptr) or record the whole job on the bound workspace
+  phiks_status execute(char* base, size_t need, std::vector<Exec::Op>* rec) {
+    ar.base = base;
+    ar.cap = need;
+    ex = Exec{h, cs, false, &ar};
+    ex.split = split;
+    ex.rec = rec;
+    bind(false);
+    if (host_mem)
+      for (size_t i = 0; i < dv.size(); ++i) {
+        double* dst = dv[i];
+        const double* srcp = vecs[i];
+        const size_t nb = tbytes;
+        ex.emit("h2d", [dst, srcp, nb](cudaStream_t s) {
+          return cudaMemcpyAsync(dst, srcp, nb, cudaMemcpyHostToDevice, s);
+        });
+      }
+    run_job(ex, jb);
+    if (!ex.ok()) return ex.status;
+    if (host_mem)
+      for (int i = 0; i < nouts; ++i) {
+        double* dst = outs[i];
+        const double* srcp = dout[i];
+        const size_t nb = tbytes;
+        ex.emit("d2h", [dst, srcp, nb](cudaStream_t s) {
+          return cudaMemcpyAsync(dst, srcp, nb, cudaMemcpyDeviceToHost, s);
+        });
+      }
+    if (host_mem) ex.launches -= static_cast<int64_t>(dv.size()) + nouts;  // copies are not kernels
+    return PHIKS_OK;
   }
-  phiks_stats& S = h->stats;
-  S.plan.s = pl.s;
-  S.plan.q = pl.q;
-  S.plan.T_formula = plan::tucker_count(req->mode, pl.s, req->n_scales, pl.q, p);
-  S.plan.T_executed = static_cast<int>(ex.tucker_ops);
-  S.kernel_launches = ex.launches + ((!same && p >= 1 && req->force_s < 0 && !forced) ? 2 : 0);
-  S.tucker_ops = ex.tucker_ops;
-  S.mu_mode_flops = ex.mu_flops;
-  S.expm_flops = ex.expm_flops;
-  S.workspace_bytes = need;
-  S.total_kernel_launches += S.kernel_launches;
+
+  void finish_stats(size_t need) {
+    phiks_stats& S = h->stats;
+    S.plan.s = pl.s;
+    S.plan.q = pl.q;
+    S.plan.T_formula = plan::tucker_count(req->mode, pl.s, req->n_scales, pl.q, p);
+    S.plan.T_executed = static_cast<int>(ex.tucker_ops);
+    S.kernel_launches = ex.launches + norm_launches;
+    S.tucker_ops = ex.tucker_ops;
+    S.mu_mode_flops = ex.mu_flops;
+    S.expm_flops = ex.expm_flops;
+    S.workspace_bytes = need;
+    S.total_kernel_launches += S.kernel_launches;
+  }
+};
+
+// error flag of the cross-rank barrier (sticky; read with a synchronous copy)
+phiks_status check_barrier_flag(phiks_handle h) {
+  if (!h->sharded() || !h->sym) return PHIKS_OK;
+  int err = 0;
+  CUDA_TRY(cudaMemcpy(&err, h->sym + kCtrlErr, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) return fail(PHIKS_ERR_CUDA, "cross-rank barrier timed out (a peer rank did not arrive)");
+  return PHIKS_OK;
+}
+
+static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_vecs, const double* const* vecs,
+                               double* const* outs, void* workspace, size_t ws_bytes, void* stream,
+                               bool size_only, const phiks_plan_info* forced, size_t* size_out) {
+  ApplyRun run;
+  phiks_status st = run.init(h, req, n_vecs, vecs, outs, stream, size_only);
+  if (st != PHIKS_OK) return st;
+  if (!forced && run.need_norms) {
+    st = run.norms_enqueue(true);
+    if (st != PHIKS_OK) return st;
+    st = run.norms_finish(h->sym);
+  } else {
+    st = run.plan_direct(forced);
+  }
+  if (st != PHIKS_OK) return st;
+  size_t need = 0;
+  st = run.measure(&need);
+  if (st != PHIKS_OK) return st;
+  if (size_out) *size_out = need;
+  if (size_only) return PHIKS_OK;
+  char* base = nullptr;
+  st = run.workspace(workspace, ws_bytes, need, &base);
+  if (st != PHIKS_OK) return st;
+  st = run.execute(base, need, nullptr);
+  if (st != PHIKS_OK) return st;
+  if (run.host_mem) {
+    CUDA_TRY(cudaStreamSynchronize(run.cs));
+    st = check_barrier_flag(h);
+    if (st != PHIKS_OK) return st;
+  }
+  run.finish_stats(need);
   return PHIKS_OK;
 }
 
@@ -1158,6 +1502,10 @@ phiks_status phiks_workspace_size(phiks_handle h, const phiks_request* req, cons
 
 phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out) {
   if (!h || !out) return fail(PHIKS_ERR_ARG, "null argument");
+  {
+    phiks_status st = check_barrier_flag(h);
+    if (st != PHIKS_OK) return st;
+  }
   *out = h->stats;
   out->mode_product_launches = 0;
   out->mode_product_ms = 0.0;
@@ -1280,6 +1628,7 @@ phiks_status phiks_plan_host(int d, const int* n, const double* const* A_host, c
   for (int mu = 0; mu < d; ++mu) {
     if (n[mu] < 1 || n[mu] > PHIKS_MAX_N || !A_host[mu]) return fail(PHIKS_ERR_ARG, "bad factor");
     h.n[mu] = n[mu];
+    h.gn[mu] = n[mu];
     h.N *= n[mu];
     Factor F;
     F.n = n[mu];
@@ -1317,6 +1666,189 @@ phiks_status phiks_fp64_peak_launch(int kind, int blocks, int64_t iters, double*
   if (!sink || !flops || blocks < 1 || iters < 1 || (kind != 0 && kind != 1)) return fail(PHIKS_ERR_ARG, "bad argument");
   cudaError_t e = launch_fp64_peak(kind, blocks, iters, sink, static_cast<cudaStream_t>(stream), flops);
   if (e != cudaSuccess) return fail(PHIKS_ERR_CUDA, cudaGetErrorString(e));
+  return PHIKS_OK;
+}
+
+
+// ===========================================================================
+// Slab sharding across the GPUs of one box
+// ===========================================================================
+phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_host, int rank, int world,
+                                  phiks_handle* out) {
+  if (!out || !n) return fail(PHIKS_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return fail(PHIKS_ERR_ARG, "rank/world");
+  if (world > 1) {
+    if (d < 2) return fail(PHIKS_ERR_ARG, "sharding needs d >= 2");
+    if (n[d - 1] % world != 0 || n[d - 2] % world != 0)
+      return fail(PHIKS_ERR_ARG, "n_d and n_{d-1} must be divisible by world");
+  }
+  phiks_handle h = nullptr;
+  phiks_status st = phiks_create(d, n, A_host, &h);
+  if (st != PHIKS_OK) return st;
+  h->rank = rank;
+  h->world = world;
+  if (world > 1) {
+    h->n[d - 1] = n[d - 1] / world;
+    h->N /= world;
+    h->sym_slot = (static_cast<size_t>(h->N) * sizeof(double) + 255) & ~size_t(255);
+    h->sym_bytes = kCtrlBytes + 2 * kShardChunk * h->sym_slot;
+    if (cudaMalloc(reinterpret_cast<void**>(&h->sym), h->sym_bytes) != cudaSuccess) {
+      phiks_destroy(h);
+      return fail(PHIKS_ERR_NOMEM, "symmetric region cudaMalloc");
+    }
+    if (cudaMemset(h->sym, 0, kCtrlBytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+      phiks_destroy(h);
+      return fail(PHIKS_ERR_CUDA, "symmetric region init");
+    }
+    h->peer[rank] = h->sym;
+  } else {
+    h->peers_ready = true;
+  }
+  *out = h;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_shard_info(phiks_handle h, int* rank, int* world, int64_t* local_count, size_t* sym_bytes) {
+  if (!h) return fail(PHIKS_ERR_ARG, "null handle");
+  if (rank) *rank = h->rank;
+  if (world) *world = h->world;
+  if (local_count) *local_count = h->N;
+  if (sym_bytes) *sym_bytes = h->sym_bytes;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_shard_ipc_handle(phiks_handle h, void* handle_out) {
+  if (!h || !handle_out) return fail(PHIKS_ERR_ARG, "null argument");
+  std::memset(handle_out, 0, PHIKS_IPC_HANDLE_BYTES);
+  if (!h->sharded()) return PHIKS_OK;
+  static_assert(sizeof(cudaIpcMemHandle_t) <= PHIKS_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t ih;
+  CUDA_TRY(cudaIpcGetMemHandle(&ih, h->sym));
+  std::memcpy(handle_out, &ih, sizeof(ih));
+  return PHIKS_OK;
+}
+
+phiks_status phiks_shard_open_peers(phiks_handle h, const void* handles) {
+  if (!h || !handles) return fail(PHIKS_ERR_ARG, "null argument");
+  if (!h->sharded()) {
+    h->peers_ready = true;
+    return PHIKS_OK;
+  }
+  const char* hb = static_cast<const char*>(handles);
+  for (int k = 0; k < h->world; ++k) {
+    if (k == h->rank) continue;
+    if (h->peer_ipc[k] && h->peer[k]) {
+      cudaIpcCloseMemHandle(h->peer[k]);
+      h->peer[k] = nullptr;
+      h->peer_ipc[k] = false;
+    }
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, hb + static_cast<size_t>(k) * PHIKS_IPC_HANDLE_BYTES, sizeof(ih));
+    void* ptr = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess));
+    h->peer[k] = static_cast<char*>(ptr);
+    h->peer_ipc[k] = true;
+  }
+  h->peers_ready = true;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_shard_base(phiks_handle h, void** base) {
+  if (!h || !base) return fail(PHIKS_ERR_ARG, "null argument");
+  *base = h->sym;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_shard_set_peer_bases(phiks_handle h, void* const* bases) {
+  if (!h || !bases) return fail(PHIKS_ERR_ARG, "null argument");
+  if (!h->sharded()) {
+    h->peers_ready = true;
+    return PHIKS_OK;
+  }
+  if (bases[h->rank] != h->sym) return fail(PHIKS_ERR_ARG, "bases[rank] must be this handle's region");
+  for (int k = 0; k < h->world; ++k) {
+    if (!bases[k]) return fail(PHIKS_ERR_ARG, "null peer base");
+    h->peer[k] = static_cast<char*>(bases[k]);
+  }
+  h->peers_ready = true;
+  return PHIKS_OK;
+}
+
+phiks_status phiks_apply_ranks_serial(const phiks_handle* hs, int world, const phiks_request* req, int n_vecs,
+                                      const double* const* vecs, double* const* outs, void* stream) {
+  if (!hs || world < 1 || world > kMaxRanks || !req || !vecs || !outs) return fail(PHIKS_ERR_ARG, "bad argument");
+  for (int k = 0; k < world; ++k) {
+    if (!hs[k] || hs[k]->world != world || hs[k]->rank != k) return fail(PHIKS_ERR_ARG, "hs[k] must be rank k of world");
+    if (req->mem_kind != PHIKS_MEM_DEVICE) return fail(PHIKS_ERR_ARG, "ranks_serial takes device memory");
+  }
+  const bool same = req->mode == PHIKS_MODE_SAME_VECTOR;
+  const int nouts = same ? req->n_ells * req->n_scales : req->n_scales;
+  std::vector<ApplyRun> runs(world);
+  for (int k = 0; k < world; ++k) {
+    phiks_status st = runs[k].init(hs[k], req, n_vecs, vecs + static_cast<size_t>(k) * n_vecs,
+                                   outs + static_cast<size_t>(k) * nouts, stream, false);
+    if (st != PHIKS_OK) return st;
+  }
+  // plan: norms phase of every rank (no barrier: stream order), then read
+  if (runs[0].need_norms) {
+    for (int k = 0; k < world; ++k) {
+      phiks_status st = runs[k].norms_enqueue(false);
+      if (st != PHIKS_OK) return st;
+    }
+    for (int k = 0; k < world; ++k) {
+      phiks_status st = runs[k].norms_finish(hs[0]->sym);
+      if (st != PHIKS_OK) return st;
+    }
+  } else {
+    for (int k = 0; k < world; ++k) {
+      phiks_status st = runs[k].plan_direct(nullptr);
+      if (st != PHIKS_OK) return st;
+    }
+  }
+  std::vector<std::vector<Exec::Op>> ops(world);
+  std::vector<size_t> need(world, 0);
+  for (int k = 0; k < world; ++k) {
+    phiks_status st = runs[k].measure(&need[k]);
+    if (st != PHIKS_OK) return st;
+    char* base = nullptr;
+    st = runs[k].workspace(nullptr, 0, need[k], &base);
+    if (st != PHIKS_OK) return st;
+    st = runs[k].execute(base, need[k], &ops[k]);
+    if (st != PHIKS_OK) return st;
+  }
+  // replay phase by phase: the segment between two barriers of every rank
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  std::vector<size_t> pos(world, 0);
+  bool more = true;
+  while (more) {
+    more = false;
+    for (int k = 0; k < world; ++k) {
+      auto& v = ops[k];
+      while (pos[k] < v.size() && !v[pos[k]].barrier) {
+        cudaError_t e = v[pos[k]].fn(cs);
+        if (e != cudaSuccess) return fail(PHIKS_ERR_CUDA, std::string(v[pos[k]].what) + ": " + cudaGetErrorString(e));
+        ++pos[k];
+      }
+      if (pos[k] < v.size()) {
+        ++pos[k];  // the barrier itself: implied by stream order
+        more = true;
+      }
+    }
+  }
+  for (int k = 0; k < world; ++k) runs[k].finish_stats(need[k]);
+  return PHIKS_OK;
+}
+
+
+phiks_status phiks_shard_layout(int d, const int* n, int rank, int world, int stage, int64_t* out7) {
+  if (!n || !out7 || d < 2 || d > PHIKS_MAX_D || world < 1 || world > kMaxRanks || rank < 0 || rank >= world ||
+      (stage != 0 && stage != 1))
+    return fail(PHIKS_ERR_ARG, "bad argument");
+  if (n[d - 1] % world != 0 || n[d - 2] % world != 0) return fail(PHIKS_ERR_ARG, "dims not divisible by world");
+  const ShardStage s = shard_stage(d, n, rank, world, stage);
+  const int64_t v[7] = {s.L, s.n, s.R, s.cb, s.rstride, s.roff, s.colstride};
+  for (int i = 0; i < 7; ++i) out7[i] = v[i];
   return PHIKS_OK;
 }
 

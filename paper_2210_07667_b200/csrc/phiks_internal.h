@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include "phiks.h"
@@ -52,11 +53,28 @@ constexpr int kMaxGroups = 48;
 constexpr int kMaxTerms = 48;   // also the TMA descriptor count per launch
 constexpr int kMaxOuts = 128;
 constexpr int kMaxSrcs = 224;
+constexpr int kMaxRanks = 8;    // slab-sharded handles: ranks of one NVSwitch box
+
+// Remote (peer-memory) epilogue of the slab-sharded Tucker operator: when
+// world > 0 every output of the launch is written to the symmetric region of
+// the rank that owns its column j of the μ-mode product,
+//     k = j / cb,   dst = base[k] + (size_t)OutSpec::dst (a byte offset)
+//                        + l + rstride·r + roff + colstride·(j − k·cb),
+// (l, j, r) the (L, n, R) coordinates of the element.  This folds the
+// slab↔slab transposition of the mode-d product into the
+// stores of the producing mode product.  Remote outputs carry no sources.
+struct Remap {
+  int world;  // 0: local outputs (OutSpec::dst is a pointer)
+  int cb;     // columns per destination rank
+  int64_t rstride, roff, colstride;
+  char* base[kMaxRanks];
+};
 
 struct ModeParams {
   int64_t L, R;
   int n;
   int ngroups;
+  Remap remap;
   GroupSpec groups[kMaxGroups];
   TermSpec terms[kMaxTerms];
   OutSpec outs[kMaxOuts];
@@ -96,6 +114,26 @@ cudaError_t launch_multi_combine(const MultiCombineParams& p, cudaStream_t st);
 cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, double* scratch,
                          double* norms2, cudaStream_t st);
 cudaError_t launch_set_identity(double* E, int n, double diag, cudaStream_t st);
+
+// Cross-rank barrier of a slab-sharded handle (one CTA): writes `epoch` into
+// slot [rank] of every peer's flag array (st.release.sys over NVLink), then
+// waits until every slot of its own array is ≥ epoch (ld.acquire.sys).  Gives
+// up after `timeout_ns` and sets *err = 1 instead of hanging.
+struct BarrierParams {
+  int rank, world;
+  uint64_t epoch;
+  uint64_t timeout_ns;
+  uint64_t* peer_flags[kMaxRanks];  // peer k's flag array (own one at k == rank)
+  int* err;                          // own region: sticky timeout flag
+};
+cudaError_t launch_barrier(const BarrierParams& p, cudaStream_t st);
+// dst_k[rank*cnt + i] = src[i] for every peer k (small, one CTA)
+struct ScatterParams {
+  int rank, world, cnt;
+  const double* src;
+  double* dst[kMaxRanks];
+};
+cudaError_t launch_scatter_small(const ScatterParams& p, cudaStream_t st);
 cudaError_t launch_fp64_peak(int kind, int blocks, int64_t iters, double* sink, cudaStream_t st,
                              double* flops);
 

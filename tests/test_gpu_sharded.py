@@ -1,0 +1,128 @@
+"""GPU parity of the slab-sharded path on ONE GPU.
+
+The ranks are emulated in one process (phiks_apply_ranks_serial): every rank
+has its own handle, symmetric region and workspace, and the peer-store
+epilogues write into the other ranks' regions exactly as over NVLink; the
+phases run rank after rank on one stream, so the cross-rank barriers are
+implied by stream order and no kernel waits on another (B200_PROFILING.md).
+The gathered slabs must match the oracle to the north-star tolerance
+(relative 2-norm ≤ 1e-12) and the single-GPU path bit for bit (the μ-mode
+products accumulate every element in the same order).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import phiks_oracle as O  # noqa: E402
+from paper_2210_07667_b200 import PhiKS, ShardedPhiKS, apply_ranks_serial  # noqa: E402
+from paper_2210_07667_b200 import workloads as W  # noqa: E402
+from paper_2210_07667_b200.sharding import split_slabs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+DEV = "cuda:0"
+
+
+def rel2(got, ref):
+    return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+def run_sharded(pb, world, n_scales=None, force=None):
+    n_scales = pb.n_scales if n_scales is None else n_scales
+    ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
+    ShardedPhiKS.connect_local(ranks)
+    flat = [W.as_flat(v) for v in pb.vs]
+    vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, world)[r])).to(DEV) for x in flat]
+            for r in range(world)]
+    outs = apply_ranks_serial(ranks, pb.tau, pb.ells, vecs, mode=pb.mode, n_scales=n_scales)
+    torch.cuda.synchronize()
+    gathered = [torch.cat([outs[r][i] for r in range(world)]).cpu().numpy() for i in range(len(outs[0]))]
+    stats = [r.stats() for r in ranks]
+    for r in ranks:
+        r.close()
+    return gathered, stats
+
+
+def run_single(pb, n_scales=None):
+    n_scales = pb.n_scales if n_scales is None else n_scales
+    op = PhiKS(pb.A)
+    outs = op.apply(pb.tau, pb.ells, [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).to(DEV) for v in pb.vs],
+                    mode=pb.mode, n_scales=n_scales)
+    torch.cuda.synchronize()
+    return [o.cpu().numpy() for o in outs], op.stats()
+
+
+def compare_oracle(pb, outs, n_scales):
+    ref = O.phiks(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, n_scales=n_scales)
+    for j in range(n_scales):
+        if pb.mode == "same":
+            for i, ell in enumerate(pb.ells):
+                e = rel2(outs[j * len(pb.ells) + i], W.as_flat(ref.out[(ell, j)]))
+                assert e <= TOL, (pb.name, ell, j, e)
+        else:
+            e = rel2(outs[j], W.as_flat(ref.out[j]))
+            assert e <= TOL, (pb.name, j, e)
+    return ref
+
+
+CASES = [(2, 3), (2, 2), (3, 1), (4, 4), (2, 4)]
+
+
+@pytest.mark.parametrize("cfg,world", [(0, 2), (0, 4), (2, 2), (2, 4), (2, 8), (3, 2), (3, 8), (4, 2), (4, 8), (1, 4)])
+def test_sharded_configs_small(cfg, world):
+    for pb in W.config(cfg, small=True).problems:
+        outs, stats = run_sharded(pb, world)
+        ref = compare_oracle(pb, outs, pb.n_scales)
+        assert all((s["s"], s["q"]) == (ref.plan.s, ref.plan.q) for s in stats)
+        single, _ = run_single(pb)
+        for a, b in zip(outs, single):
+            assert np.array_equal(a, b), pb.name   # same accumulation order as one GPU
+
+
+def _random_sharded_cases():
+    rng = np.random.default_rng(77)
+    cases = []
+    for c in range(8):
+        world = int(rng.choice([2, 4, 8]))
+        d = int(rng.integers(2, 5))
+        dims = [int(x) for x in rng.integers(2, 9 if d >= 4 else 20, size=d)]
+        dims[-1] = world * int(rng.integers(1, 4))
+        dims[-2] = world * int(rng.integers(1, 4))
+        dims = tuple(dims)
+        mode = "same" if c % 2 == 0 else "lincomb"
+        p = int(rng.integers(1, 5))
+        ells = tuple(sorted(set([p] + [int(x) for x in rng.integers(0, p + 1, size=2)])))
+        vs = [W.random_tensor(dims, seed=300 + 11 * c + k) for k in range(1 if mode == "same" else len(ells))]
+        fac = W.random_factors(dims, seed=40 + c, scale=float(rng.uniform(0.5, 8.0)))
+        cases.append((W.Problem(f"srand{c}_{mode}_w{world}_d{d}", dims, fac, float(rng.uniform(0.1, 1.5)), mode,
+                                ells, vs, int(rng.integers(1, 3))), world))
+    return cases
+
+
+@pytest.mark.parametrize("case", _random_sharded_cases(), ids=lambda c: c[0].name)
+def test_sharded_random_problems(case):
+    pb, world = case
+    outs, _ = run_sharded(pb, world)
+    compare_oracle(pb, outs, pb.n_scales)
+
+
+def test_sharded_many_nodes_chunks():
+    # (q-1)·p > 16 quadrature Tucker operators: more than one sub-batch of the T/Y pools
+    dims = (8, 8, 8)
+    fac = W.random_factors(dims, seed=9, scale=40.0)
+    ells = (0, 1, 2, 3, 4, 5, 6)
+    vs = [W.random_tensor(dims, seed=k) for k in range(len(ells))]
+    pb = W.Problem("chunks", dims, fac, 1.0, "lincomb", ells, vs, 1)
+    plan = O.plan_for(fac, 1.0, "lincomb", ells, vs, 1)
+    assert (plan.q - 1) * 6 > 16, plan
+    outs, _ = run_sharded(pb, 4)
+    compare_oracle(pb, outs, 1)
+
+
+def test_sharded_world1_is_plain_handle():
+    pb = W.config(2, small=True).problems[0]
+    outs, _ = run_sharded(pb, 1)
+    single, _ = run_single(pb)
+    for a, b in zip(outs, single):
+        assert np.array_equal(a, b)
