@@ -109,7 +109,7 @@ def load_traffic():
     try:
         with open(path) as f:
             js = json.load(f)
-        return js.get("mode_product_dram_bytes_per_launch"), js.get("source")
+        return js.get("dram_bytes_per_gflop"), js.get("source")
     except Exception:
         return None, None
 
@@ -168,8 +168,9 @@ def b200_arm(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2210_07667_b200 import PhiKS, fp64_peak_launch
+    from paper_2210_07667_b200 import PhiKS, ShardedPhiKS, fp64_peak_launch
     from paper_2210_07667_b200 import workloads as W
+    from paper_2210_07667_b200.sharding import split_slabs
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -178,13 +179,15 @@ def b200_arm(args):
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
 
-    # ---- workload (each rank: the full configs[3] problem; replicas) ----
+    # ---- workload: configs[3]; N > 1 slab-shards every tensor along mode 3 ----
     wl = W.config(3)
     ops, vins, outs, host_in, host_out = [], [], [], [], []
     for pb in wl.problems:
-        op = PhiKS(pb.A)
+        op = ShardedPhiKS(pb.A, rank, world) if world > 1 else PhiKS(pb.A)
         ops.append(op)
         x = W.as_flat(pb.vs[0])
+        if world > 1:
+            x = np.ascontiguousarray(split_slabs(x, world)[rank])
         vins.append(torch.from_numpy(x.copy()).to(dev))
         outs.append([torch.empty_like(vins[-1]) for _ in pb.ells])
         hi = torch.empty(x.size, dtype=torch.float64, pin_memory=True)
@@ -268,7 +271,7 @@ def b200_arm(args):
             tt = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
-        N = int(np.prod(wl.problems[0].dims))
+        N = int(np.prod(wl.problems[0].dims)) // world
         e2e = {"value": flops_step * world * k / te / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": sum(8 * N for _ in wl.problems),
                "d2h_bytes_per_step": sum(8 * N * len(pb.ells) for pb in wl.problems),
@@ -281,11 +284,15 @@ def b200_arm(args):
         cpu = {"value": f / tc / 1e9, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
                "sample": "the full step (both species, 256^3) once, numpy/OpenBLAS fp64", "seconds": tc}
 
-    traffic, tsrc = load_traffic()
+    bpg, tsrc = load_traffic()
+    # dram bytes per launch: the committed ncu capture's bytes per algorithmic GFLOP
+    # of this kernel, times the average GFLOP of the launches timed here
+    traffic = bpg * (mp_fl / max(mp_n, 1) / 1e9) if (bpg and mp_n) else None
     ach = mp_fl / (mp_ms / 1e3) / 1e12 if mp_ms > 0 else None
     roof = {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": (ach / peak_tf) if ach else None, "traffic": traffic,
-            "kernel": "mode_product_kernel (FP64 DMMA.8x8x4)",
+            "kernel": "mode_product_tma_kernel (FP64 DMMA.8x8x4, TMA + mbarrier ring), all μ-mode-product launches",
+            "algorithmic_bytes_per_launch": 16.0 * (mp_fl / max(mp_n, 1)) / (2.0 * 256),
             "peak_source": "measured in this run: phiks_fp64_peak_launch DMMA microbenchmark (max of 3)",
             "per_launch_ms": mp_ms / max(mp_n, 1), "launches_timed": mp_n,
             "share_of_step": (mp_ms / 1e3) / t_local if t_local > 0 else None,
@@ -294,8 +301,10 @@ def b200_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "parallelism": f"replicas{world}" if world > 1 else "single",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD,
+                       "parallelism": f"slab{world} (mode-3 slabs, transposition fused into peer stores)"
+                       if world > 1 else "single",
                        "l2": "inputs larger than L2 (134 MB per vector > 126 MB L2)", "plans": plans,
                        "mu_mode_gflop_per_step": flops_step / 1e9},
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,

@@ -95,6 +95,7 @@ struct phiks_ctx {
   bool peer_ipc[kMaxRanks] = {false};
   bool peers_ready = false;
   uint64_t epoch = 0;
+  uint64_t norm_phase = 0;  // parity selects the norm-slot buffer (a fast rank may run one apply ahead)
   bool sharded() const { return world > 1; }
 };
 
@@ -102,8 +103,11 @@ namespace {
 // symmetric region layout (identical on every rank)
 constexpr size_t kCtrlFlags = 0;                                   // uint64 flags[kMaxRanks]
 constexpr size_t kCtrlErr = kMaxRanks * sizeof(uint64_t);          // int err
-constexpr size_t kCtrlNorms = 256;                                 // double norms[kMaxRanks][kMaxVecs]
+constexpr size_t kCtrlNorms = 256;                                 // double norms[2][kMaxRanks][kMaxVecs]
+constexpr size_t kCtrlNormsBuf = kMaxRanks * kMaxVecs * sizeof(double);
 constexpr size_t kCtrlBytes = 4096;
+static_assert(kCtrlNorms + 2 * kCtrlNormsBuf <= kCtrlBytes, "control block layout");
+static_assert(kCtrlErr + sizeof(int) <= kCtrlNorms, "control block layout");
 constexpr int kShardChunk = 16;  // Tucker operators per sharded sub-batch (T and Y pools)
 constexpr uint64_t kBarrierTimeoutNs = 20ull * 1000 * 1000 * 1000;
 }  // namespace
@@ -1220,6 +1224,7 @@ struct ApplyRun {
   double* nscratch = nullptr;    // device: 1024*kMaxVecs partials + kMaxVecs norms²
   std::vector<double*> ntmp;     // host-memory inputs staged for the norms
   int norm_launches = 0;
+  size_t norm_off = kCtrlNorms;  // this apply's norm-slot buffer in the control block
 
   phiks_status init(phiks_handle h_, const phiks_request* req_, int n_vecs_, const double* const* vecs_,
                     double* const* outs_, void* stream, bool size_only_) {
@@ -1289,12 +1294,13 @@ struct ApplyRun {
     CUDA_TRY(launch_sumsq(vv.data(), static_cast<int>(vv.size()), N, nscratch, nscratch + 1024 * kMaxVecs, cs));
     norm_launches = 2;
     if (h->sharded()) {
+      norm_off = kCtrlNorms + (h->norm_phase++ & 1) * kCtrlNormsBuf;
       ScatterParams sp{};
       sp.rank = h->rank;
       sp.world = h->world;
       sp.cnt = static_cast<int>(which.size());
       sp.src = nscratch + 1024 * kMaxVecs;
-      for (int k = 0; k < h->world; ++k) sp.dst[k] = reinterpret_cast<double*>(h->peer[k] + kCtrlNorms);
+      for (int k = 0; k < h->world; ++k) sp.dst[k] = reinterpret_cast<double*>(h->peer[k] + norm_off);
       CUDA_TRY(launch_scatter_small(sp, cs));
       ++norm_launches;
       if (do_barrier) {
@@ -1314,7 +1320,7 @@ struct ApplyRun {
     if (!which.empty()) {
       const int nv = static_cast<int>(which.size());
       const int W = h->sharded() ? h->world : 1;
-      const double* srcp = h->sharded() ? reinterpret_cast<const double*>(ctrl + kCtrlNorms)
+      const double* srcp = h->sharded() ? reinterpret_cast<const double*>(ctrl + norm_off)
                                         : nscratch + 1024 * kMaxVecs;
       CUDA_TRY(cudaMemcpyAsync(h->h_pinned, srcp, sizeof(double) * nv * W, cudaMemcpyDeviceToHost, cs));
       for (double* t : ntmp) CUDA_TRY(cudaFreeAsync(t, cs));
