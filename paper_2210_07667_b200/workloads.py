@@ -120,7 +120,7 @@ class Workload:
     problems: List[Problem]
 
 
-def config(idx: int, small: bool = False) -> Workload:
+def config(idx: int, small: bool = False, with_vectors: bool = True) -> Workload:
     """BASELINE.json configs[idx].  small=True shrinks the grid (same operator
     family, same recipe) so the oracle finishes in seconds — used by the
     parity tests; the full sizes are the bench / sampled-parity workloads."""
@@ -161,7 +161,7 @@ def config(idx: int, small: bool = False) -> Workload:
         dims = (24, 24, 16) if small else (512, 512, 256)
         eps, alpha = 1.0, (10.0, 10.0, -10.0)
         A = [eps * fd_dxx_dirichlet(nm) + a * fd_dx_dirichlet(nm) for nm, a in zip(dims, alpha)]
-        vs = _uniform_list(dims, 5, -1.0, 1.0, seed=4)
+        vs = _uniform_list(dims, 5, -1.0, 1.0, seed=4) if with_vectors else []
         p = Problem(f"cfg4_d3_{dims[0]}x{dims[1]}x{dims[2]}_adr_etdrk4", tuple(dims), A, 1e-4,
                     "lincomb", (0, 1, 2, 3, 4), vs, 1)
         return Workload("cfg4", [p])
