@@ -61,9 +61,14 @@ typedef enum {
 
 typedef enum {
   PHIKS_MEM_DEVICE = 0, /* vecs/outs are device pointers; apply is stream-asynchronous  */
-  PHIKS_MEM_HOST = 1    /* vecs/outs are host pointers (pinned recommended); the library
+  PHIKS_MEM_HOST = 1,   /* vecs/outs are host pointers (pinned recommended); the library
                            copies them through device staging and synchronises the
                            stream before returning                                       */
+  PHIKS_MEM_HOST_ASYNC = 2 /* as PHIKS_MEM_HOST but returns at once: the copies run on the
+                           handle's own copy streams (inputs overlap the exponential stage,
+                           exp(τK)v is copied out while the φ_ℓ≥1 part runs, and the
+                           copies overlap the next apply of another handle); vecs/outs
+                           MUST be pinned and stay untouched until phiks_wait(h)        */
 } phiks_mem_kind;
 
 /* Opaque handle: the factor matrices A_μ (copied to device at create), their
@@ -112,6 +117,10 @@ typedef struct {
    range rectangle data of PAPER.md l.925-936 (reading R1) on the host.
    *out receives the handle; destroy it with phiks_destroy. */
 phiks_status phiks_create(int d, const int* n, const double* const* A_host, phiks_handle* out);
+
+/* Block until the last apply on h (its kernels and host copies) has finished;
+   reports a cross-rank barrier timeout of a sharded handle as PHIKS_ERR_CUDA. */
+phiks_status phiks_wait(phiks_handle h);
 
 /* Release the handle and every device/pinned buffer it owns.  NULL is a no-op. */
 phiks_status phiks_destroy(phiks_handle h);

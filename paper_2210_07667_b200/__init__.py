@@ -108,11 +108,13 @@ class PhiKS:
 
     def apply(self, tau: float, ells: Sequence[int], vecs: Sequence, mode: str = "same", n_scales: int = 1,
               tol: float = 0.0, outs: Optional[Sequence] = None, force_s: int = -1, force_q: int = -1,
-              stream=None, workspace=None):
+              stream=None, workspace=None, host_async: bool = False):
         """Run phiks_apply.  vecs/outs are contiguous fp64 CUDA tensors
         (PHIKS_MEM_DEVICE) or numpy arrays (PHIKS_MEM_HOST; then outs are
-        returned as numpy arrays).  Returns the list of outputs: same-vector →
-        outs[j*len(ells)+i] = φ_{ells[i]}(τK/2^j)v; lincomb → outs[j]."""
+        returned as numpy arrays).  host_async=True (numpy arrays over PINNED
+        memory only) returns before the copies finish (PHIKS_MEM_HOST_ASYNC);
+        call wait() before reading the outputs.  Returns the list of outputs:
+        same-vector → outs[j*len(ells)+i] = φ_{ells[i]}(τK/2^j)v; lincomb → outs[j]."""
         lib = _lib.load()
         m = self._mode(mode)
         host = isinstance(vecs[0], np.ndarray)
@@ -134,7 +136,8 @@ class PhiKS:
                 outs = [torch.empty(self.N, dtype=torch.float64, device=vecs[0].device) for _ in range(nouts)]
             optr = [_check_dev(o, self.N) for o in outs]
             sptr = _stream_ptr(stream)
-        req = _lib.make_request(m, ells, n_scales, tau, tol, force_s, force_q, MEM_HOST if host else MEM_DEVICE)
+        kind = (_lib.MEM_HOST_ASYNC if host_async else MEM_HOST) if host else MEM_DEVICE
+        req = _lib.make_request(m, ells, n_scales, tau, tol, force_s, force_q, kind)
         ws_ptr, ws_bytes = (None, 0)
         if workspace is not None:
             ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
@@ -155,6 +158,10 @@ class PhiKS:
 
     def set_profiling(self, on: bool = True):
         _lib.check(_lib.load().phiks_set_profiling(self._h, 1 if on else 0), "phiks_set_profiling")
+
+    def wait(self):
+        """Block until the last apply (kernels and host copies) has finished."""
+        _lib.check(_lib.load().phiks_wait(self._h), "phiks_wait")
 
 
 # ----------------------------------------------------------------------

@@ -96,6 +96,9 @@ struct phiks_ctx {
   bool peers_ready = false;
   uint64_t epoch = 0;
   uint64_t norm_phase = 0;  // parity selects the norm-slot buffer (a fast rank may run one apply ahead)
+  // host-memory applies: copy streams and their ordering events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_h2d = nullptr, ev_d2h = nullptr, ev_cdone = nullptr, ev_ready = nullptr;
   bool sharded() const { return world > 1; }
 };
 
@@ -195,6 +198,10 @@ struct Exec {
     const char* what;
   };
   std::vector<Op>* rec = nullptr;
+  // host-memory applies: called (execute pass only) when the staged inputs are
+  // first needed and when some outputs are final (their copy-out can start)
+  std::function<void()> on_inputs;
+  std::function<void(const std::vector<double*>&)> on_outputs;
 
   bool ok() const { return status == PHIKS_OK; }
   void check(cudaError_t e, const char* what) {
@@ -834,6 +841,29 @@ void run_job(Exec& ex, const Job& jb) {
     for (int mu = 0; mu < d; ++mu) mats[mu] = nodeE[i][h->fac_of_mode[mu]];
   };
 
+  // inputs staged from host memory are needed from here on (stage A overlaps their copy)
+  if (ex.on_inputs) ex.on_inputs();
+
+  // ---- Stage D (same vector) first: exp(τK/2^j)v needs only the level
+  // matrices, so a host-memory apply can copy it out while B and C run ----
+  if (same) {
+    std::vector<TuckerItem> ex_items;
+    std::vector<double*> ready;
+    for (int j = 0; j < jb.n_scales; ++j) {
+      if (!jb.out_same[0][j]) continue;
+      TuckerItem it;
+      it.in = jb.vin[0];
+      mats_for(Es[j], it.mats);
+      it.group = j;
+      it.outs.push_back(Out{jb.out_same[0][j], 1.0, {}});
+      ex_items.push_back(it);
+      ready.push_back(jb.out_same[0][j]);
+    }
+    ex.batch(ex_items, false);
+    if (!ex.ok()) return;
+    if (ex.on_outputs && !ready.empty()) ex.on_outputs(ready);
+  }
+
   // ---- state buffers ----
   // state[j][ℓ] for the scale j (ℓ = 1..p)
   std::vector<std::vector<double*>> state(s + 1, std::vector<double*>(p + 1, nullptr));
@@ -978,19 +1008,9 @@ void run_job(Exec& ex, const Job& jb) {
     }
   }
 
-  // ---- Stage D: exp(τK/2^j) actions ----
+  // ---- Stage D (linear combination): exp(τK/2^j)v_0 added to the result ----
   std::vector<TuckerItem> ex_items;
-  if (same) {
-    for (int j = 0; j < jb.n_scales; ++j) {
-      if (!jb.out_same[0][j]) continue;
-      TuckerItem it;
-      it.in = jb.vin[0];
-      mats_for(Es[j], it.mats);
-      it.group = j;
-      it.outs.push_back(Out{jb.out_same[0][j], 1.0, {}});
-      ex_items.push_back(it);
-    }
-  } else {
+  if (!same) {
     for (int j = 0; j < jb.n_scales; ++j) {
       if (!jb.out_lin[j]) continue;
       if (jb.vin[0]) {
@@ -1092,6 +1112,10 @@ phiks_status phiks_destroy(phiks_handle h) {
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
   for (int k = 0; k < kMaxRanks; ++k)
     if (h->peer_ipc[k] && h->peer[k]) cudaIpcCloseMemHandle(h->peer[k]);
+  for (cudaEvent_t e : {h->ev_h2d, h->ev_d2h, h->ev_cdone, h->ev_ready})
+    if (e) cudaEventDestroy(e);
+  if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_out) cudaStreamDestroy(h->s_out);
   if (h->sym) cudaFree(h->sym);
   for (auto& e : h->ev) {
     cudaEventDestroy(e.first);
@@ -1111,6 +1135,8 @@ phiks_status validate(phiks_handle h, const phiks_request* req, int& p) {
   if (req->n_ells < 1 || req->n_ells > PHIKS_MAX_P + 1 || !req->ells) return fail(PHIKS_ERR_ARG, "n_ells");
   if (req->n_scales < 1 || req->n_scales > PHIKS_MAX_SCALES) return fail(PHIKS_ERR_LIMIT, "n_scales");
   if (!(req->tau > 0.0) || !std::isfinite(req->tau)) return fail(PHIKS_ERR_ARG, "tau must be > 0");
+  if (req->mem_kind != PHIKS_MEM_DEVICE && req->mem_kind != PHIKS_MEM_HOST && req->mem_kind != PHIKS_MEM_HOST_ASYNC)
+    return fail(PHIKS_ERR_ARG, "mem_kind");
   p = -1;
   for (int i = 0; i < req->n_ells; ++i) {
     const int e = req->ells[i];
@@ -1206,7 +1232,7 @@ struct ApplyRun {
   phiks_handle h = nullptr;
   const phiks_request* req = nullptr;
   int p = 0, n_vecs = 0, nouts = 0;
-  bool same = true, host_mem = false, size_only = false;
+  bool same = true, host_mem = false, host_async = false, size_only = false;
   const double* const* vecs = nullptr;
   double* const* outs = nullptr;
   cudaStream_t cs = nullptr;
@@ -1248,7 +1274,8 @@ struct ApplyRun {
     }
     if (h->sharded() && !h->peers_ready) return fail(PHIKS_ERR_ARG, "sharded handle: peers not opened");
     cs = static_cast<cudaStream_t>(stream);
-    host_mem = req->mem_kind == PHIKS_MEM_HOST;
+    host_mem = req->mem_kind == PHIKS_MEM_HOST || req->mem_kind == PHIKS_MEM_HOST_ASYNC;
+    host_async = req->mem_kind == PHIKS_MEM_HOST_ASYNC;
     N = h->N;
     tbytes = static_cast<size_t>(N) * sizeof(double);
     static const int split_mode = [] {
@@ -1414,28 +1441,51 @@ struct ApplyRun {
     ex.split = split;
     ex.rec = rec;
     bind(false);
-    if (host_mem)
-      for (size_t i = 0; i < dv.size(); ++i) {
-        double* dst = dv[i];
-        const double* srcp = vecs[i];
-        const size_t nb = tbytes;
-        ex.emit("h2d", [dst, srcp, nb](cudaStream_t s) {
-          return cudaMemcpyAsync(dst, srcp, nb, cudaMemcpyHostToDevice, s);
-        });
+    if (host_mem && rec) return fail(PHIKS_ERR_ARG, "recorded applies take device memory");
+    if (host_mem) {
+      // copies on the handle's own streams: H2D overlaps stage A, the copy-out of
+      // an output overlaps the rest of the job (and the next apply)
+      if (!h->s_in) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&h->ev_h2d, &h->ev_d2h, &h->ev_cdone, &h->ev_ready})
+          CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(h->ev_d2h, h->s_out));
+        CUDA_TRY(cudaEventRecord(h->ev_cdone, cs));
       }
+      CUDA_TRY(cudaStreamWaitEvent(h->s_in, h->ev_cdone, 0));  // previous apply is done with the staging
+      for (size_t i = 0; i < dv.size(); ++i)
+        CUDA_TRY(cudaMemcpyAsync(dv[i], vecs[i], tbytes, cudaMemcpyHostToDevice, h->s_in));
+      CUDA_TRY(cudaEventRecord(h->ev_h2d, h->s_in));
+      CUDA_TRY(cudaStreamWaitEvent(cs, h->ev_d2h, 0));  // previous apply's copy-out has drained
+      copied.assign(nouts, false);
+      ex.on_inputs = [this]() { ex.check(cudaStreamWaitEvent(cs, h->ev_h2d, 0), "wait h2d"); };
+      ex.on_outputs = [this](const std::vector<double*>& ready) { copy_out(ready); };
+    }
     run_job(ex, jb);
     if (!ex.ok()) return ex.status;
-    if (host_mem)
-      for (int i = 0; i < nouts; ++i) {
-        double* dst = outs[i];
-        const double* srcp = dout[i];
-        const size_t nb = tbytes;
-        ex.emit("d2h", [dst, srcp, nb](cudaStream_t s) {
-          return cudaMemcpyAsync(dst, srcp, nb, cudaMemcpyDeviceToHost, s);
-        });
-      }
-    if (host_mem) ex.launches -= static_cast<int64_t>(dv.size()) + nouts;  // copies are not kernels
+    if (host_mem) {
+      std::vector<double*> rest;
+      for (int i = 0; i < nouts; ++i)
+        if (!copied[i]) rest.push_back(dout[i]);
+      copy_out(rest);
+      if (!ex.ok()) return ex.status;
+      CUDA_TRY(cudaEventRecord(h->ev_d2h, h->s_out));
+      CUDA_TRY(cudaEventRecord(h->ev_cdone, cs));
+    }
     return PHIKS_OK;
+  }
+  std::vector<bool> copied;
+  void copy_out(const std::vector<double*>& ready) {
+    if (ready.empty()) return;
+    ex.check(cudaEventRecord(h->ev_ready, cs), "record ready");
+    ex.check(cudaStreamWaitEvent(h->s_out, h->ev_ready, 0), "wait ready");
+    for (double* p : ready)
+      for (int i = 0; i < nouts; ++i)
+        if (dout[i] == p && !copied[i]) {
+          ex.check(cudaMemcpyAsync(outs[i], dout[i], tbytes, cudaMemcpyDeviceToHost, h->s_out), "d2h");
+          copied[i] = true;
+        }
   }
 
   void finish_stats(size_t need) {
@@ -1486,7 +1536,8 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
   if (st != PHIKS_OK) return st;
   st = run.execute(base, need, nullptr);
   if (st != PHIKS_OK) return st;
-  if (run.host_mem) {
+  if (run.host_mem && !run.host_async) {
+    CUDA_TRY(cudaEventSynchronize(h->ev_d2h));
     CUDA_TRY(cudaStreamSynchronize(run.cs));
     st = check_barrier_flag(h);
     if (st != PHIKS_OK) return st;
@@ -1856,6 +1907,14 @@ phiks_status phiks_shard_layout(int d, const int* n, int rank, int world, int st
   const int64_t v[7] = {s.L, s.n, s.R, s.cb, s.rstride, s.roff, s.colstride};
   for (int i = 0; i < 7; ++i) out7[i] = v[i];
   return PHIKS_OK;
+}
+
+
+phiks_status phiks_wait(phiks_handle h) {
+  if (!h) return fail(PHIKS_ERR_ARG, "null handle");
+  if (h->ev_d2h) CUDA_TRY(cudaEventSynchronize(h->ev_d2h));
+  if (h->ev_cdone) CUDA_TRY(cudaEventSynchronize(h->ev_cdone));
+  return check_barrier_flag(h);
 }
 
 }  // extern "C"

@@ -99,6 +99,9 @@ class ShardedPhiKS:
     def set_profiling(self, on: bool = True):
         self.op.set_profiling(on)
 
+    def wait(self):
+        self.op.wait()
+
     def close(self):
         self.op.close()
 

@@ -155,6 +155,29 @@ def test_host_memory_path_equals_device_path():
         assert np.array_equal(a.cpu().numpy(), b)
 
 
+def test_host_async_path_equals_device_path():
+    # PHIKS_MEM_HOST_ASYNC: pinned buffers, copies on the handle's streams, two
+    # handles in flight (the bench's e2e pattern), then wait()
+    pbs = W.config(3, small=True).problems
+    ops = [PhiKS(pb.A) for pb in pbs]
+    pins, pouts, ref = [], [], []
+    for op, pb in zip(ops, pbs):
+        x = W.as_flat(pb.vs[0])
+        hi = torch.empty(x.size, dtype=torch.float64, pin_memory=True)
+        hi.numpy()[:] = x
+        pins.append(hi)
+        pouts.append([torch.empty(x.size, dtype=torch.float64, pin_memory=True) for _ in pb.ells])
+        ref.append([o.cpu().numpy() for o in op.apply(pb.tau, pb.ells, [dev(pb.vs[0])])])
+    for rep in range(2):
+        for op, pb, hi, ho in zip(ops, pbs, pins, pouts):
+            op.apply(pb.tau, pb.ells, [hi.numpy()], outs=[t.numpy() for t in ho], host_async=True)
+        for op in ops:
+            op.wait()
+        for ho, r in zip(pouts, ref):
+            for a, b in zip(ho, r):
+                assert np.array_equal(a.numpy(), b)
+
+
 def test_edge_cases():
     # n_μ = 1 everywhere (N = 1): scalar K = Σ a_μ
     fac = [np.array([[-0.3]]), np.array([[0.7]])]
