@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
         for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       for (int kt = 0; kt < KT; ++kt, ++it) {
         const uint32_t s = it % STAGES;
-        if (!(p.dbg & 1)) mbar_wait(&full[s], (it / STAGES) & 1);
+        mbar_wait(&full[s], (it / STAGES) & 1);
         const double* as = smem + s * G::STAGE_ELEMS;
         const double* bs = as + G::A_ELEMS + lt * G::SB + wn0 + lg;
         const double* aw = KMAJ ? as + (wm0 + lg) * G::SA + lt : as + lt * G::SA + wm0 + lg;
@@ -537,10 +537,6 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
       }
 
       // ---- fused linear epilogue ----
-      if (p.dbg & 2) {
-        if (acc[0][0][0] == 1.2345e-300) p.outs[0].dst[0] = acc[MI - 1][NI - 1][1];
-        continue;
-      }
       const TermSpec& term = p.terms[t];
       for (int o = term.out0; o < term.out0 + term.nout; ++o) {
         const OutSpec& os = p.outs[o];
@@ -745,21 +741,8 @@ static int tile_variant() {
   return v;
 }
 
-cudaError_t launch_mode_product(const ModeParams& p_in, cudaStream_t st) {
-  if (p_in.ngroups == 0) return cudaSuccess;
-  static const int dbg = [] {
-    const char* e = getenv("PHIKS_DBG");  // timing experiments only: 1 = no data wait, 2 = no epilogue
-    return e ? atoi(e) : 0;
-  }();
-  const ModeParams* pp = &p_in;
-  ModeParams* pd = nullptr;
-  if (dbg) {
-    pd = new ModeParams(p_in);
-    pd->dbg = dbg;
-    pp = pd;
-  }
-  struct Del { ModeParams* q; ~Del() { delete q; } } del{pd};
-  const ModeParams& p = *pp;
+cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
+  if (p.ngroups == 0) return cudaSuccess;
   const int64_t Mtot = p.L * p.R;
   const int var = tile_variant();
   if (p.remap.world > 0 && p.n > 64) {  // slab-sharded peer-store epilogue: default tile only

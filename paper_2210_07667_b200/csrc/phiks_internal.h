@@ -74,7 +74,6 @@ struct ModeParams {
   int64_t L, R;
   int n;
   int ngroups;
-  int dbg;  // timing experiments (PHIKS_DBG), 0 in production
   Remap remap;
   GroupSpec groups[kMaxGroups];
   TermSpec terms[kMaxTerms];
