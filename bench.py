@@ -249,6 +249,8 @@ def b200_arm(args):
     mp_ms = sum(s["mode_product_ms"] for s in st)
     mp_fl = sum(s["mode_product_flops"] for s in st)
     mp_n = sum(s["mode_product_launches"] for s in st)
+    ex_ms = sum(s["expm_ms"] for s in st)
+    ex_n = sum(s["expm_launches"] for s in st)
     for op in ops:
         op.set_profiling(False)
     t = t_local
@@ -299,11 +301,12 @@ def b200_arm(args):
     ach = mp_fl / (mp_ms / 1e3) / 1e12 if mp_ms > 0 else None
     roof = {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": (ach / peak_tf) if ach else None, "traffic": traffic,
-            "kernel": "mode_product_tma_kernel (FP64 DMMA.8x8x4, TMA + mbarrier ring), all μ-mode-product launches",
+            "kernel": "mode_product_tma_kernel (FP64 DMMA.8x8x4, TMA + mbarrier ring): the Tucker-operator launches",
             "algorithmic_bytes_per_launch": 16.0 * (mp_fl / max(mp_n, 1)) / (2.0 * 256),
             "peak_source": "measured in this run: phiks_fp64_peak_launch DMMA microbenchmark (max of 3)",
             "per_launch_ms": mp_ms / max(mp_n, 1), "launches_timed": mp_n,
             "share_of_step": (mp_ms / 1e3) / t_local if t_local > 0 else None,
+            "expm_stage": {"launches": ex_n, "share_of_step": (ex_ms / 1e3) / t_local if t_local > 0 else None},
             "traffic_source": tsrc}
     if rank == 0:
         line = {

@@ -104,9 +104,11 @@ typedef struct {
   int64_t total_kernel_launches; /* since create                                    */
   /* filled only when profiling is on (phiks_set_profiling): CUDA-event timing of
      every μ-mode-product kernel launch of the last apply, on the apply's stream */
-  int64_t mode_product_launches;  /* launches of the μ-mode product kernel          */
+  int64_t mode_product_launches;  /* Tucker-operator μ-mode-product launches          */
   double mode_product_ms;         /* sum of their event-measured durations (ms)     */
   double mode_product_flops;      /* algorithmic flops of those launches (2·rows·n²) */
+  int64_t expm_launches;          /* small-GEMM launches of the exponential stage   */
+  double expm_ms;                 /* sum of their event-measured durations (ms)     */
 } phiks_stats;
 
 /* Create a handle for K = A_d ⊕ … ⊕ A_1.

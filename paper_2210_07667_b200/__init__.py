@@ -154,7 +154,8 @@ class PhiKS:
                 "mu_mode_flops": st.mu_mode_flops, "expm_flops": st.expm_flops,
                 "workspace_bytes": st.workspace_bytes, "total_kernel_launches": st.total_kernel_launches,
                 "mode_product_launches": st.mode_product_launches, "mode_product_ms": st.mode_product_ms,
-                "mode_product_flops": st.mode_product_flops}
+                "mode_product_flops": st.mode_product_flops, "expm_launches": st.expm_launches,
+                "expm_ms": st.expm_ms}
 
     def set_profiling(self, on: bool = True):
         _lib.check(_lib.load().phiks_set_profiling(self._h, 1 if on else 0), "phiks_set_profiling")

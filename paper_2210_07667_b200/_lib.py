@@ -46,7 +46,8 @@ class Stats(ctypes.Structure):
                 ("mu_mode_flops", ctypes.c_double), ("expm_flops", ctypes.c_double),
                 ("workspace_bytes", ctypes.c_size_t), ("total_kernel_launches", ctypes.c_int64),
                 ("mode_product_launches", ctypes.c_int64), ("mode_product_ms", ctypes.c_double),
-                ("mode_product_flops", ctypes.c_double)]
+                ("mode_product_flops", ctypes.c_double), ("expm_launches", ctypes.c_int64),
+                ("expm_ms", ctypes.c_double)]
 
 
 _lib = None

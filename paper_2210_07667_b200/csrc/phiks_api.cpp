@@ -82,6 +82,7 @@ struct phiks_ctx {
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> ev_flops;
+  std::vector<char> ev_expm;  // 1: a small-GEMM launch of the exponential stage
   int ev_used = 0;
   // ---- slab sharding along the outermost mode (phiks_create_sharded) ----
   // n[] holds the LOCAL dims of layout S_d (n[d-1] = gn[d-1]/world); the
@@ -324,8 +325,10 @@ struct Exec {
           check(cudaEventCreate(&b), "cudaEventCreate");
           h->ev.emplace_back(a, b);
           h->ev_flops.push_back(0.0);
+          h->ev_expm.push_back(0);
         }
         h->ev_flops[h->ev_used] = 2.0 * static_cast<double>(L * R) * n * static_cast<double>(n) * nt;
+        h->ev_expm[h->ev_used] = in_expm ? 1 : 0;
         check(cudaEventRecord(h->ev[h->ev_used].first, st), "cudaEventRecord");
       }
       if (!measure) check(launch_mode_product(p, st), "mode_product");
@@ -630,8 +633,11 @@ struct Exec {
 
   // out_b = A_b · B_b (+ epilogue) for n×n matrices: mode-1 product of the
   // "tensor" B (n, n) with matrix A.
+  bool in_expm = false;
   void gemm_batch(int n, std::vector<LaunchTerm>& terms) {
+    in_expm = true;
     mode_launch(1, n, n, terms);
+    in_expm = false;
     expm_flops += 2.0 * n * static_cast<double>(n) * n * static_cast<double>(terms.size());
   }
 };
@@ -1567,15 +1573,22 @@ phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out) {
   out->mode_product_launches = 0;
   out->mode_product_ms = 0.0;
   out->mode_product_flops = 0.0;
+  out->expm_launches = 0;
+  out->expm_ms = 0.0;
   if (h->profiling) {
     for (int i = 0; i < h->ev_used; ++i) {
       CUDA_TRY(cudaEventSynchronize(h->ev[i].second));
       float ms = 0.f;
       CUDA_TRY(cudaEventElapsedTime(&ms, h->ev[i].first, h->ev[i].second));
-      out->mode_product_ms += ms;
-      out->mode_product_flops += h->ev_flops[i];
+      if (h->ev_expm[i]) {
+        out->expm_ms += ms;
+        ++out->expm_launches;
+      } else {
+        out->mode_product_ms += ms;
+        out->mode_product_flops += h->ev_flops[i];
+        ++out->mode_product_launches;
+      }
     }
-    out->mode_product_launches = h->ev_used;
   }
   return PHIKS_OK;
 }
