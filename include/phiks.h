@@ -257,6 +257,10 @@ phiks_status phiks_shard_open_peers(phiks_handle h, const void* handles);
 /* Device base address of this rank's symmetric region (NULL for world = 1). */
 phiks_status phiks_shard_base(phiks_handle h, void** base);
 
+/* Device address under which this process sees rank k's region (after
+   open_peers / set_peer_bases; k == rank gives the own region). */
+phiks_status phiks_shard_peer_base(phiks_handle h, int k, void** base);
+
 /* Same-process alternative to open_peers: bases[k] = rank k's region
    (phiks_shard_base of the handle of rank k), bases[rank] must be own. */
 phiks_status phiks_shard_set_peer_bases(phiks_handle h, void* const* bases);

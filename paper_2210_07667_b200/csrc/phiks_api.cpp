@@ -1930,4 +1930,11 @@ phiks_status phiks_wait(phiks_handle h) {
   return check_barrier_flag(h);
 }
 
+
+phiks_status phiks_shard_peer_base(phiks_handle h, int k, void** base) {
+  if (!h || !base || k < 0 || k >= h->world) return fail(PHIKS_ERR_ARG, "bad argument");
+  *base = h->peer[k];
+  return PHIKS_OK;
+}
+
 }  // extern "C"

@@ -65,6 +65,11 @@ class ShardedPhiKS:
         _lib.check(_lib.load().phiks_shard_base(self.op._h, ctypes.byref(b)), "phiks_shard_base")
         return int(b.value or 0)
 
+    def peer_base(self, k: int) -> int:
+        b = ctypes.c_void_p()
+        _lib.check(_lib.load().phiks_shard_peer_base(self.op._h, int(k), ctypes.byref(b)), "phiks_shard_peer_base")
+        return int(b.value or 0)
+
     def open_peers(self, handles: Sequence[bytes]):
         if len(handles) != self.world:
             raise ValueError("one handle per rank")
