@@ -752,7 +752,6 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
   }
   if (p.n > 64 && (var == 0 || var >= 10)) {
     cudaError_t err = cudaSuccess;
-    const int64_t big = Mtot * ((p.n + 127) / 128) * p.ngroups;
     bool done = false;
     if (var == 11)
       done = launch_tma<128, 64, 16, 2, 2, 4, 2>(p, st, &err);
@@ -768,8 +767,13 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
       done = launch_tma<128, 64, 16, 4, 2, 3, 2>(p, st, &err);
     else if (var == 10)
       done = launch_tma<128, 128, 16, 2, 4, 5, 1>(p, st, &err);
-    else if (big >= 148 * 4)
-      done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);  // default: 2 CTAs/SM overlap epilogues
+    else if (var == 0) {
+      const int64_t units = ((Mtot + 63) / 64) * ((p.n + 127) / 128) * p.ngroups;
+      if (units >= 148 * 2)
+        done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);  // default: 2 CTAs/SM overlap epilogues
+      else  // less than a wave (e.g. the n×n GEMMs of the exponential stage): 64×64 tiles, 3 CTAs/SM
+        done = launch_tma<64, 64, 16, 2, 2, 4, 3>(p, st, &err);
+    }
     if (done) return err;
   }
   if (p.n > 64) {
