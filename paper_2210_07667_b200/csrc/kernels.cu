@@ -996,11 +996,16 @@ cudaError_t launch_fp64_peak(int kind, int blocks, int64_t iters, double* sink, 
 // ---------------------------------------------------------------------------
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
+  __shared__ uint64_t epoch;
+  if (t == 0) {
+    epoch = *p.epoch + 1;  // only this (stream-ordered) kernel touches the counter
+    *p.epoch = epoch;
+  }
   __threadfence_system();
   __syncthreads();
   if (t < p.world) {
     uint64_t* slot = p.peer_flags[t] + p.rank;  // my slot in peer t's array
-    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(slot), "l"(p.epoch) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(slot), "l"(epoch) : "memory");
   }
   if (t < p.world) {
     const uint64_t* mine = p.peer_flags[p.rank] + t;
@@ -1009,7 +1014,7 @@ __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
     while (true) {
       uint64_t v;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(mine) : "memory");
-      if (v >= p.epoch) break;
+      if (v >= epoch) break;
       uint64_t now;
       asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(now));
       if (now - t0 > p.timeout_ns) {

@@ -95,8 +95,16 @@ struct phiks_ctx {
   char* peer[kMaxRanks] = {nullptr};
   bool peer_ipc[kMaxRanks] = {false};
   bool peers_ready = false;
-  uint64_t epoch = 0;
   uint64_t norm_phase = 0;  // parity selects the norm-slot buffer (a fast rank may run one apply ahead)
+  // CUDA graphs of whole applies (device memory, profiling off): captured on
+  // s_cap the first time a request/plan/pointer set is seen, replayed after
+  struct GraphEntry {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t s_cap = nullptr;
+  int64_t graph_replays = 0;
   // host-memory applies: copy streams and their ordering events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_h2d = nullptr, ev_d2h = nullptr, ev_cdone = nullptr, ev_ready = nullptr;
@@ -107,11 +115,12 @@ namespace {
 // symmetric region layout (identical on every rank)
 constexpr size_t kCtrlFlags = 0;                                   // uint64 flags[kMaxRanks]
 constexpr size_t kCtrlErr = kMaxRanks * sizeof(uint64_t);          // int err
+constexpr size_t kCtrlEpoch = 128;                                 // uint64 barrier count
 constexpr size_t kCtrlNorms = 256;                                 // double norms[2][kMaxRanks][kMaxVecs]
 constexpr size_t kCtrlNormsBuf = kMaxRanks * kMaxVecs * sizeof(double);
 constexpr size_t kCtrlBytes = 4096;
 static_assert(kCtrlNorms + 2 * kCtrlNormsBuf <= kCtrlBytes, "control block layout");
-static_assert(kCtrlErr + sizeof(int) <= kCtrlNorms, "control block layout");
+static_assert(kCtrlErr + sizeof(int) <= kCtrlEpoch && kCtrlEpoch + 8 <= kCtrlNorms, "control block layout");
 constexpr int kShardChunk = 16;  // Tucker operators per sharded sub-batch (T and Y pools)
 constexpr uint64_t kBarrierTimeoutNs = 20ull * 1000 * 1000 * 1000;
 }  // namespace
@@ -222,8 +231,9 @@ struct Exec {
   // cross-rank barrier of a sharded handle (device-side, stream-ordered)
   void barrier() {
     ++barriers;
-    if (measure || !ok() || !h->sharded()) return;
+    if (!ok() || !h->sharded()) return;
     ++launches;
+    if (measure) return;
     if (rec) {
       rec->push_back(Op{true, nullptr, "barrier"});
       return;
@@ -231,7 +241,7 @@ struct Exec {
     BarrierParams bp{};
     bp.rank = h->rank;
     bp.world = h->world;
-    bp.epoch = ++h->epoch;
+    bp.epoch = reinterpret_cast<uint64_t*>(h->sym + kCtrlEpoch);
     bp.timeout_ns = kBarrierTimeoutNs;
     for (int k = 0; k < h->world; ++k) bp.peer_flags[k] = reinterpret_cast<uint64_t*>(h->peer[k] + kCtrlFlags);
     bp.err = reinterpret_cast<int*>(h->sym + kCtrlErr);
@@ -1120,6 +1130,8 @@ phiks_status phiks_destroy(phiks_handle h) {
     if (h->peer_ipc[k] && h->peer[k]) cudaIpcCloseMemHandle(h->peer[k]);
   for (cudaEvent_t e : {h->ev_h2d, h->ev_d2h, h->ev_cdone, h->ev_ready})
     if (e) cudaEventDestroy(e);
+  for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+  if (h->s_cap) cudaStreamDestroy(h->s_cap);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
   if (h->sym) cudaFree(h->sym);
@@ -1425,6 +1437,8 @@ struct ApplyRun {
       return PHIKS_OK;
     }
     if (h->ws_own_bytes < need) {
+      for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);  // they reference the old workspace
+      h->graphs.clear();
       if (h->ws_own) {
         CUDA_TRY(cudaStreamSynchronize(cs));
         CUDA_TRY(cudaFree(h->ws_own));
@@ -1540,6 +1554,57 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
   char* base = nullptr;
   st = run.workspace(workspace, ws_bytes, need, &base);
   if (st != PHIKS_OK) return st;
+  static const bool graphs_on = [] {
+    const char* e = getenv("PHIKS_GRAPHS");
+    return !(e && atoi(e) == 0);
+  }();
+  if (graphs_on && !run.host_mem && !h->profiling) {
+    const cudaStream_t cs = run.cs;
+    // key: everything the recorded launches depend on
+    std::vector<uint64_t> key;
+    auto bits = [](double x) {
+      uint64_t u;
+      std::memcpy(&u, &x, sizeof(u));
+      return u;
+    };
+    key.insert(key.end(), {static_cast<uint64_t>(req->mode), static_cast<uint64_t>(req->n_scales), bits(req->tau),
+                           bits(req->tol), static_cast<uint64_t>(run.pl.s), static_cast<uint64_t>(run.pl.q),
+                           static_cast<uint64_t>(run.split), reinterpret_cast<uint64_t>(base), need});
+    for (int i = 0; i < req->n_ells; ++i) key.push_back(static_cast<uint64_t>(req->ells[i]));
+    for (int i = 0; i < n_vecs; ++i) key.push_back(reinterpret_cast<uint64_t>(vecs[i]));
+    for (int i = 0; i < run.nouts; ++i) key.push_back(reinterpret_cast<uint64_t>(outs[i]));
+    cudaGraphExec_t exec = nullptr;
+    for (auto& g : h->graphs)
+      if (g.key == key) exec = g.exec;
+    if (!exec) {
+      if (!h->s_cap) CUDA_TRY(cudaStreamCreateWithFlags(&h->s_cap, cudaStreamNonBlocking));
+      if (h->graphs.size() >= 32) {
+        CUDA_TRY(cudaStreamSynchronize(cs));
+        for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+        h->graphs.clear();
+      }
+      run.cs = h->s_cap;
+      CUDA_TRY(cudaStreamBeginCapture(h->s_cap, cudaStreamCaptureModeThreadLocal));
+      st = run.execute(base, need, nullptr);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(h->s_cap, &graph);
+      run.cs = cs;
+      if (st != PHIKS_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (ce != cudaSuccess) return fail(PHIKS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) return fail(PHIKS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+      h->graphs.push_back({key, exec});
+    } else {
+      ++h->graph_replays;
+    }
+    CUDA_TRY(cudaGraphLaunch(exec, cs));
+    run.finish_stats(need);
+    return PHIKS_OK;
+  }
   st = run.execute(base, need, nullptr);
   if (st != PHIKS_OK) return st;
   if (run.host_mem && !run.host_async) {

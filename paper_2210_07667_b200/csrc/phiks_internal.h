@@ -115,13 +115,13 @@ cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, dou
                          double* norms2, cudaStream_t st);
 cudaError_t launch_set_identity(double* E, int n, double diag, cudaStream_t st);
 
-// Cross-rank barrier of a slab-sharded handle (one CTA): writes `epoch` into
-// slot [rank] of every peer's flag array (st.release.sys over NVLink), then
-// waits until every slot of its own array is ≥ epoch (ld.acquire.sys).  Gives
-// up after `timeout_ns` and sets *err = 1 instead of hanging.
+// Cross-rank barrier of a slab-sharded handle (one CTA): e = ++*epoch, writes e
+// into slot [rank] of every peer's flag array (st.release.sys over NVLink), then
+// waits until every slot of its own array is ≥ e (ld.acquire.sys).  Gives up
+// after `timeout_ns` and sets *err = 1 instead of hanging.
 struct BarrierParams {
   int rank, world;
-  uint64_t epoch;
+  uint64_t* epoch;  // own region: the barrier count, advanced by the kernel itself (graph-replayable)
   uint64_t timeout_ns;
   uint64_t* peer_flags[kMaxRanks];  // peer k's flag array (own one at k == rank)
   int* err;                          // own region: sticky timeout flag

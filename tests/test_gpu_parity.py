@@ -155,6 +155,22 @@ def test_host_memory_path_equals_device_path():
         assert np.array_equal(a.cpu().numpy(), b)
 
 
+def test_graph_replay_is_bitwise_identical():
+    # the second apply on the same buffers replays the captured CUDA graph
+    for pb in (W.config(0).problems[0], W.config(1, small=True).problems[0]):
+        op = PhiKS(pb.A)
+        vs = [dev(v) for v in pb.vs]
+        outs = [torch.empty(op.N, dtype=torch.float64, device=DEV) for _ in range(len(pb.ells) if pb.mode == "same"
+                                                                                 else 1)]
+        first = [o.cpu().numpy().copy() for o in op.apply(pb.tau, pb.ells, vs, mode=pb.mode, outs=outs)]
+        for o in outs:
+            o.zero_()
+        again = [o.cpu().numpy() for o in op.apply(pb.tau, pb.ells, vs, mode=pb.mode, outs=outs)]
+        fresh = [o.cpu().numpy() for o in op.apply(pb.tau, pb.ells, vs, mode=pb.mode)]
+        for a, b, c in zip(first, again, fresh):
+            assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
 def test_host_async_path_equals_device_path():
     # PHIKS_MEM_HOST_ASYNC: pinned buffers, copies on the handle's streams, two
     # handles in flight (the bench's e2e pattern), then wait()
