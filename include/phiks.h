@@ -103,7 +103,8 @@ typedef struct {
   size_t workspace_bytes;   /* device workspace the last apply needed               */
   int64_t total_kernel_launches; /* since create                                    */
   /* filled only when profiling is on (phiks_set_profiling): CUDA-event timing of
-     every μ-mode-product kernel launch of the last apply, on the apply's stream */
+     every μ-mode-product kernel launch since profiling was switched on (summed
+     over the applies in between), on each apply's stream */
   int64_t mode_product_launches;  /* Tucker-operator μ-mode-product launches          */
   double mode_product_ms;         /* sum of their event-measured durations (ms)     */
   double mode_product_flops;      /* algorithmic flops of those launches (2·rows·n²) */

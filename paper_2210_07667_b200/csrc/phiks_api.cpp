@@ -11,6 +11,7 @@
 //      last mode's epilogue, intermediate scales written on the way (Eq. (13)/(19)),
 //   D. exp(τK/2^j)v actions (one Tucker operator each, l.614-616).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1535,6 +1536,9 @@ phiks_status check_barrier_flag(phiks_handle h) {
 static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_vecs, const double* const* vecs,
                                double* const* outs, void* workspace, size_t ws_bytes, void* stream,
                                bool size_only, const phiks_plan_info* forced, size_t* size_out) {
+  static const bool hostprof = getenv("PHIKS_HOSTPROF") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
   ApplyRun run;
   phiks_status st = run.init(h, req, n_vecs, vecs, outs, stream, size_only);
   if (st != PHIKS_OK) return st;
@@ -1546,9 +1550,22 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
     st = run.plan_direct(forced);
   }
   if (st != PHIKS_OK) return st;
+  const auto t1 = now();
   size_t need = 0;
   st = run.measure(&need);
   if (st != PHIKS_OK) return st;
+  const auto t2 = now();
+  struct HostProf {
+    bool on;
+    std::chrono::steady_clock::time_point t0, t1, t2;
+    ~HostProf() {
+      if (!on) return;
+      const auto t3 = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      fprintf(stderr, "PHIKS_HOSTPROF plan+norms %.1f us, measure %.1f us, enqueue %.1f us\n", us(t0, t1), us(t1, t2),
+              us(t2, t3));
+    }
+  } hostprof_guard{hostprof, t0, t1, t2};
   if (size_out) *size_out = need;
   if (size_only) return PHIKS_OK;
   char* base = nullptr;

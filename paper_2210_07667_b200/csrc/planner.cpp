@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdint>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -274,12 +276,17 @@ int tucker_count(int mode, int s, int s_hat, int q, int p) {
 namespace {
 
 // bounds B[li] (ℓ = li+1) for one q at the scaled rectangle; min over r.
+// The radii are independent: evaluated in parallel (OpenMP), reduced in order.
 void bounds_for_q(const Rect& rect, int q, int p, const std::vector<cd>& wpts, double wmax,
                   std::vector<double>& B, std::vector<std::vector<cd>>& Ecache,
                   std::vector<int>& Enz, std::vector<char>& Einf) {
   B.assign(p, INFINITY);
   const int nb = static_cast<int>(wpts.size());
+  for (int ri = 0; ri < kNr; ++ri) kq_on_ellipse(q, ri, n_zeta(r_grid(ri), wmax));  // memoise serially
+  std::vector<std::vector<double>> Br(kNr, std::vector<double>(p, INFINITY));
+#pragma omp parallel for schedule(dynamic, 1)
   for (int ri = 0; ri < kNr; ++ri) {
+    std::vector<double>& Bri = Br[ri];
     const double r = r_grid(ri);
     const int nz = n_zeta(r, wmax);
     // E[m*nb + b] = exp((1 - z_m) w_b), cached per r across q
@@ -330,9 +337,32 @@ void bounds_for_q(const Rect& rect, int q, int p, const std::vector<cd>& wpts, d
         mx = std::max(mx, v);
       }
       const double val = fin ? mx * kSpectral / nz : INFINITY;
-      if (std::isfinite(val)) B[li] = std::min(B[li], val);
+      if (std::isfinite(val)) Bri[li] = val;
     }
   }
+  for (int ri = 0; ri < kNr; ++ri)
+    for (int li = 0; li < p; ++li) B[li] = std::min(B[li], Br[ri][li]);
+}
+
+// B for (scaled rectangle, q, p), memoised: the bound depends on neither the
+// vector norms nor the tolerance, so a new right-hand side (a new time step of
+// an integrator) re-plans with comparisons only.
+struct BoundCache {
+  std::mutex mu;
+  std::map<std::vector<uint64_t>, std::vector<double>> map;
+};
+BoundCache& bound_cache() {
+  static BoundCache* c = new BoundCache();
+  return *c;
+}
+std::vector<uint64_t> bound_key(const Rect& rc, int q, int p) {
+  auto bits = [](double x) {
+    uint64_t u;
+    std::memcpy(&u, &x, sizeof(u));
+    return u;
+  };
+  return {bits(rc.center.real()), bits(rc.center.imag()), bits(rc.hr), bits(rc.hi), static_cast<uint64_t>(q),
+          static_cast<uint64_t>(p)};
 }
 
 std::vector<cd> boundary(const Rect& rc) {
@@ -363,7 +393,23 @@ int q_for_s(int mode, const Rect& rect, int p, const std::vector<double>& norms,
   std::vector<char> Einf(kNr, 0);
   std::vector<double> B;
   for (int q = kQmin; q <= kQmax; ++q) {
-    bounds_for_q(rc, q, p, w, wmax, B, Ecache, Enz, Einf);
+    const std::vector<uint64_t> key = bound_key(rc, q, p);
+    bool have = false;
+    {
+      BoundCache& bc = bound_cache();
+      std::lock_guard<std::mutex> lk(bc.mu);
+      auto it = bc.map.find(key);
+      if (it != bc.map.end()) {
+        B = it->second;
+        have = true;
+      }
+    }
+    if (!have) {
+      bounds_for_q(rc, q, p, w, wmax, B, Ecache, Enz, Einf);
+      BoundCache& bc = bound_cache();
+      std::lock_guard<std::mutex> lk(bc.mu);
+      bc.map[key] = B;
+    }
     bool ok = true;
     for (int ell = 1; ell <= p && ok; ++ell) {
       if (mode == kSame) {
