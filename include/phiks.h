@@ -233,7 +233,7 @@ phiks_status phiks_select_plan(int mode, double center_re, double center_im, dou
    (one process).  phiks_apply on the handle then takes and returns local
    slabs (phiks_shard_info's local_count doubles each); every rank must issue
    the same sequence of applies with the same request (the applies meet in
-   device-side barriers; a rank that does not arrive within 20 s makes the
+   device-side barriers; a rank that does not arrive within 60 s makes the
    barrier give up and the handle report PHIKS_ERR_CUDA from
    phiks_get_stats / host-memory applies). */
 phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_host, int rank, int world,

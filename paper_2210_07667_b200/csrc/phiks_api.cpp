@@ -123,7 +123,7 @@ constexpr size_t kCtrlBytes = 4096;
 static_assert(kCtrlNorms + 2 * kCtrlNormsBuf <= kCtrlBytes, "control block layout");
 static_assert(kCtrlErr + sizeof(int) <= kCtrlEpoch && kCtrlEpoch + 8 <= kCtrlNorms, "control block layout");
 constexpr int kShardChunk = 16;  // Tucker operators per sharded sub-batch (T and Y pools)
-constexpr uint64_t kBarrierTimeoutNs = 20ull * 1000 * 1000 * 1000;
+constexpr uint64_t kBarrierTimeoutNs = 60ull * 1000 * 1000 * 1000;
 }  // namespace
 
 namespace {
