@@ -732,12 +732,15 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   return true;
 }
 
+// PHIKS_TILE (A/B experiments, scripts/sweep_run.sh): 0 = the default below;
+// 1 = the cp.async kernel only (the pre-TMA baseline); 10 = TMA 128×128 tiles,
+// 8 warps, 1 CTA/SM; 12 = TMA 128×64 tiles, 3 stages.  DESIGN.md §4 and
+// profiles/r01_tile_sweep.jsonl, r01_kernel_experiments.json record the sweep.
 static int tile_variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char* e = getenv("PHIKS_TILE");
-    v = e ? atoi(e) : 0;
-  }
+    return e ? atoi(e) : 0;
+  }();
   return v;
 }
 
@@ -750,24 +753,14 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
     if (launch_tma<64, 128, 16, 2, 2, 4, 2, true>(p, st, &err)) return err;
     return launch_cfg<64, 64, 16, 2, 2, 4, 3>(p, st);
   }
-  if (p.n > 64 && (var == 0 || var >= 10)) {
+  if (p.n > 64 && var != 1) {
     cudaError_t err = cudaSuccess;
     bool done = false;
-    if (var == 11)
-      done = launch_tma<128, 64, 16, 2, 2, 4, 2>(p, st, &err);
-    else if (var == 12)
-      done = launch_tma<128, 64, 16, 2, 2, 3, 2>(p, st, &err);
-    else if (var == 13)
-      done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);
-    else if (var == 14)
-      done = launch_tma<128, 128, 16, 4, 4, 5, 1>(p, st, &err);
-    else if (var == 15)
-      done = launch_tma<64, 128, 16, 2, 4, 4, 2>(p, st, &err);
-    else if (var == 16)
-      done = launch_tma<128, 64, 16, 4, 2, 3, 2>(p, st, &err);
-    else if (var == 10)
+    if (var == 10) {
       done = launch_tma<128, 128, 16, 2, 4, 5, 1>(p, st, &err);
-    else if (var == 0) {
+    } else if (var == 12) {
+      done = launch_tma<128, 64, 16, 2, 2, 3, 2>(p, st, &err);
+    } else {
       const int64_t units = ((Mtot + 63) / 64) * ((p.n + 127) / 128) * p.ngroups;
       if (units >= 148 * 2)
         done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);  // default: 2 CTAs/SM overlap epilogues
@@ -776,17 +769,8 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
     }
     if (done) return err;
   }
+  // cp.async kernel: shapes TMA cannot take (odd n, odd or short L, misaligned pointers), n ≤ 64
   if (p.n > 64) {
-    switch (tile_variant()) {
-      case 1: return launch_cfg<128, 64, 16, 2, 2, 4, 2>(p, st);
-      case 3: return launch_cfg<64, 64, 16, 2, 2, 4, 3>(p, st);
-      case 5: return launch_cfg<128, 128, 16, 4, 4, 4, 1>(p, st);
-      case 6: return launch_cfg<128, 64, 16, 4, 2, 4, 2>(p, st);
-      case 7: return launch_cfg<64, 128, 16, 2, 4, 4, 2>(p, st);
-      case 8: return launch_cfg<128, 128, 16, 4, 4, 3, 1>(p, st);
-      default: break;
-    }
-    // small problems (e.g. the n×n GEMMs of the exponential stage): more CTAs
     if (Mtot * ((p.n + 127) / 128) * p.ngroups < 148 * 4) return launch_cfg<64, 64, 16, 2, 2, 4, 3>(p, st);
     return launch_cfg<128, 128, 16, 2, 4, 4, 1>(p, st);
   }
