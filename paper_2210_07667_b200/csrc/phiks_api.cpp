@@ -447,7 +447,21 @@ struct Exec {
         }
       acc.emplace_back(ptr, c);
     };
+    // items with one output, no sources, whose destination nothing else in the
+    // batch reads or writes, write it directly (no Y buffer, no combination)
+    std::vector<char> direct(items.size(), 0);
+    if (!shard) {
+      std::map<const double*, int> refs;
+      for (const TuckerItem& it : items)
+        for (const Out& o : it.outs) {
+          ++refs[o.dst];
+          for (const Src& sr : o.srcs) ++refs[sr.ptr];
+        }
+      for (size_t b = 0; b < items.size(); ++b)
+        direct[b] = items[b].outs.size() == 1 && items[b].outs[0].srcs.empty() && refs[items[b].outs[0].dst] == 1;
+    }
     for (size_t b = 0; b < items.size(); ++b) {
+      if (direct[b]) continue;
       for (const Out& o : items[b].outs) {
         Lin lin;
         add(lin, ykey(b), o.beta * items[b].in_scale);
@@ -466,9 +480,11 @@ struct Exec {
       const size_t c1 = std::min(items.size(), c0 + chunk);
       std::vector<TuckerItem> raw(items.begin() + c0, items.begin() + c1);
       for (size_t b = 0; b < raw.size(); ++b) {
+        const double beta = direct[c0 + b] ? raw[b].outs[0].beta * raw[b].in_scale : 1.0;
+        double* dst = direct[c0 + b] ? raw[b].outs[0].dst : (shard ? nullptr : y_pool[c0 + b]);
         raw[b].in_scale = 1.0;
         raw[b].group = static_cast<int>(b);
-        raw[b].outs.assign(1, Out{shard ? nullptr : y_pool[c0 + b], 1.0, {}});
+        raw[b].outs.assign(1, Out{dst, beta, {}});
       }
       if (shard)
         tucker_raw_sharded(raw);
@@ -861,24 +877,30 @@ void run_job(Exec& ex, const Job& jb) {
   // inputs staged from host memory are needed from here on (stage A overlaps their copy)
   if (ex.on_inputs) ex.on_inputs();
 
-  // ---- Stage D (same vector) first: exp(τK/2^j)v needs only the level
-  // matrices, so a host-memory apply can copy it out while B and C run ----
+  // ---- Stage D (same vector): exp(τK/2^j)v needs only the level matrices and
+  // reads the same v as the quadrature, so with p ≥ 1 it joins the quadrature
+  // batch (one launch per mode for both); a host-memory apply copies it out
+  // while the squaring runs ----
+  std::vector<TuckerItem> d_items;
+  std::vector<double*> d_ready;
   if (same) {
-    std::vector<TuckerItem> ex_items;
-    std::vector<double*> ready;
     for (int j = 0; j < jb.n_scales; ++j) {
       if (!jb.out_same[0][j]) continue;
       TuckerItem it;
       it.in = jb.vin[0];
       mats_for(Es[j], it.mats);
-      it.group = j;
+      it.group = 1000 + j;
       it.outs.push_back(Out{jb.out_same[0][j], 1.0, {}});
-      ex_items.push_back(it);
-      ready.push_back(jb.out_same[0][j]);
+      d_items.push_back(it);
+      d_ready.push_back(jb.out_same[0][j]);
     }
-    ex.batch(ex_items, false);
-    if (!ex.ok()) return;
-    if (ex.on_outputs && !ready.empty()) ex.on_outputs(ready);
+    if (p == 0) {
+      ex.batch(d_items, false);
+      if (!ex.ok()) return;
+      if (ex.on_outputs && !d_ready.empty()) ex.on_outputs(d_ready);
+      d_items.clear();
+      d_ready.clear();
+    }
   }
 
   // ---- state buffers ----
@@ -990,7 +1012,10 @@ void run_job(Exec& ex, const Job& jb) {
           }
       }
     }
+    for (auto& it : d_items) items.push_back(it);
     ex.batch(items, ex.split >= 1);
+    if (!ex.ok()) return;
+    if (ex.on_outputs && !d_ready.empty()) ex.on_outputs(d_ready);
     if (!ex.ok()) return;
 
     // ---- Stage C: squaring, j = s..1 ----
