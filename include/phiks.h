@@ -125,6 +125,19 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
    reports a cross-rank barrier timeout of a sharded handle as PHIKS_ERR_CUDA. */
 phiks_status phiks_wait(phiks_handle h);
 
+/* Complex K (§4.1 validates PHIKS on the complex operator
+   (1+i)/100·Δ): as phiks_create, but A_host[μ] points to an n[μ]×n[μ]
+   column-major complex matrix stored as interleaved (re, im) doubles
+   (C99 double complex / numpy complex128 layout).  Tensors given to
+   phiks_apply are then complex too: N interleaved (re, im) pairs, N = Π n_μ.
+   The library works in real arithmetic on the 2n×2n real form of each factor
+   (exp of the real form = real form of exp); a complex μ-mode product is the
+   first-mode product with that real form (μ = 1), or two real products
+   X ×_μ Re(M) + J(X ×_μ Im(M)) (μ ≥ 2, J: re ← −im, im ← re) fused in one
+   launch.  The §3.3 rectangle uses the complex trace shift (reading R1).
+   Not available for sharded handles. */
+phiks_status phiks_create_complex(int d, const int* n, const double* const* A_host, phiks_handle* out);
+
 /* Release the handle and every device/pinned buffer it owns.  NULL is a no-op. */
 phiks_status phiks_destroy(phiks_handle h);
 
@@ -189,6 +202,10 @@ phiks_status phiks_fp64_peak_launch(int kind, int blocks, int64_t iters, double*
    factors A_host (real, column-major, host) without creating a handle. */
 phiks_status phiks_plan_host(int d, const int* n, const double* const* A_host, const phiks_request* req,
                              const double* vec_norms, phiks_plan_info* out);
+
+/* phiks_plan_host for complex factors (interleaved, as phiks_create_complex). */
+phiks_status phiks_plan_host_complex(int d, const int* n, const double* const* A_host, const phiks_request* req,
+                                     const double* vec_norms, phiks_plan_info* out);
 
 /* Host-only §3.3 search on an explicit rectangle Ξ = (center_re + i center_im)
    + [-hr, hr] + i[-hi, hi] ⊇ W(τK), absolute tolerance

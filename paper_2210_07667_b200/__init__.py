@@ -38,10 +38,11 @@ def _stream_ptr(stream) -> int:
     return int(stream.cuda_stream)
 
 
-def _check_dev(t, N: Optional[int] = None):
+def _check_dev(t, N: Optional[int] = None, complex_: bool = False):
     torch = _torch()
-    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-        raise TypeError("expected a contiguous float64 CUDA tensor")
+    dt = torch.complex128 if complex_ else torch.float64
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dt and t.is_contiguous()):
+        raise TypeError(f"expected a contiguous {dt} CUDA tensor")
     if N is not None and t.numel() != N:
         raise ValueError(f"tensor has {t.numel()} elements, expected {N}")
     return t.data_ptr()
@@ -59,14 +60,21 @@ class PhiKS:
         self.d = len(factors)
         self.dims = tuple(int(np.asarray(a).shape[0]) for a in factors)
         self.rank, self.world = int(rank), int(world)
-        self._A = [np.asfortranarray(np.asarray(a, dtype=np.float64)) for a in factors]
+        # complex factors (§4.1's validation operator is complex): complex128 throughout
+        self.complex = any(np.iscomplexobj(a) for a in factors)
+        dt = np.complex128 if self.complex else np.float64
+        self._A = [np.asfortranarray(np.asarray(a, dtype=dt)) for a in factors]
         for a in self._A:
             if a.ndim != 2 or a.shape[0] != a.shape[1]:
                 raise ValueError("factor matrices must be square")
         n_arr = (ctypes.c_int * self.d)(*self.dims)
         a_arr = _lib.ptr_array([a.ctypes.data for a in self._A])
         h = ctypes.c_void_p()
-        if self.world == 1:
+        if self.complex:
+            if self.world != 1:
+                raise ValueError("complex factors are not supported on sharded handles")
+            _lib.check(lib.phiks_create_complex(self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create_complex")
+        elif self.world == 1:
             _lib.check(lib.phiks_create(self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create")
         else:
             _lib.check(lib.phiks_create_sharded(self.d, n_arr, a_arr, self.rank, self.world, ctypes.byref(h)),
@@ -119,22 +127,24 @@ class PhiKS:
         m = self._mode(mode)
         host = isinstance(vecs[0], np.ndarray)
         nouts = len(ells) * n_scales if m == MODE_SAME_VECTOR else n_scales
+        dt = np.complex128 if self.complex else np.float64
         if host:
-            vecs = [np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1, order="F")) for v in vecs]
+            vecs = [np.ascontiguousarray(np.asarray(v, dtype=dt).reshape(-1, order="F")) for v in vecs]
             for v in vecs:
                 if v.size != self.N:
                     raise ValueError("vector size mismatch")
             if outs is None:
-                outs = [np.empty(self.N) for _ in range(nouts)]
+                outs = [np.empty(self.N, dtype=dt) for _ in range(nouts)]
             vptr = [v.ctypes.data for v in vecs]
             optr = [o.ctypes.data for o in outs]
             sptr = _stream_ptr(stream) if stream is not None else 0
         else:
             torch = _torch()
-            vptr = [_check_dev(v, self.N) for v in vecs]
+            tdt = torch.complex128 if self.complex else torch.float64
+            vptr = [_check_dev(v, self.N, self.complex) for v in vecs]
             if outs is None:
-                outs = [torch.empty(self.N, dtype=torch.float64, device=vecs[0].device) for _ in range(nouts)]
-            optr = [_check_dev(o, self.N) for o in outs]
+                outs = [torch.empty(self.N, dtype=tdt, device=vecs[0].device) for _ in range(nouts)]
+            optr = [_check_dev(o, self.N, self.complex) for o in outs]
             sptr = _stream_ptr(stream)
         kind = (_lib.MEM_HOST_ASYNC if host_async else MEM_HOST) if host else MEM_DEVICE
         req = _lib.make_request(m, ells, n_scales, tau, tol, force_s, force_q, kind)

@@ -40,6 +40,25 @@ __device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, doub
       : "d"(a), "d"(b));
 }
 
+// Complex tensors are interleaved (re, im) doubles; for modes μ ≥ 2 the GEMM
+// row index is m = c + 2l (c = 0 re, 1 im) and a complex μ-mode product is
+// X ×_μ Mr + J(X ×_μ Mi) with J(t)_re = −t_im, J(t)_im = t_re.  The partner
+// rows 2l, 2l+1 sit in lanes lane, lane^4 of the DMMA fragment (row = 8·mi +
+// lane/4 + tile offset, tile offsets even), so J is one shuffle per element.
+template <int MI, int NI>
+__device__ __forceinline__ void complex_swap(double (&acc)[MI][NI][2], int lane) {
+  const bool im_row = ((lane >> 2) & 1) != 0;
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double partner = __shfl_xor_sync(0xffffffffu, acc[mi][ni][e], 4);
+        acc[mi][ni][e] = im_row ? partner : -partner;
+      }
+}
+
 // Peer-memory store of the slab-sharded epilogue (phiks_internal.h, Remap).
 __device__ __forceinline__ void remote_store(const Remap& rm, const OutSpec& os, int64_t rowb, int j, double v) {
   const int k = j / rm.cb;
@@ -239,6 +258,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
       const int64_t m0 = (tile / tilesN) * BM;
       const int j0 = static_cast<int>(tile % tilesN) * BN;
       const TermSpec& term = p.terms[done.t];
+      if (term.cswap) complex_swap<MI, NI>(acc, lane);
       for (int o = term.out0; o < term.out0 + term.nout; ++o) {
         const OutSpec& os = p.outs[o];
         double* dst = os.dst;
@@ -538,6 +558,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
 
       // ---- fused linear epilogue ----
       const TermSpec& term = p.terms[t];
+      if (term.cswap) complex_swap<MI, NI>(acc, lane);
       for (int o = term.out0; o < term.out0 + term.nout; ++o) {
         const OutSpec& os = p.outs[o];
         double* dst = os.dst;
@@ -915,6 +936,28 @@ cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, dou
   for (int i = 0; i < nvec; ++i) vl.v[i] = vecs[i];
   sumsq_pass1<<<dim3(kSumsqBlocks, nvec), 256, 0, st>>>(vl, count, scratch);
   sumsq_pass2<<<nvec, 256, 0, st>>>(scratch, norms2);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Real and imaginary parts of a complex n×n matrix from its interleaved real
+// form R (2n×2n column-major, R[(c+2j) + (c'+2k)·2n] = [[Mr, −Mi], [Mi, Mr]]_{cc'}(j,k)).
+__global__ void complex_parts_kernel(const double* R, int n, double* Mr, double* Mi) {
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nn;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = i % n, k = i / n;
+    const int64_t col = 2 * k * (2 * static_cast<int64_t>(n));
+    Mr[i] = R[2 * j + col];
+    Mi[i] = R[2 * j + 1 + col];
+  }
+}
+
+cudaError_t launch_complex_parts(const double* R, int n, double* Mr, double* Mi, cudaStream_t st) {
+  const int64_t nn = static_cast<int64_t>(n) * n;
+  int64_t blocks = (nn + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  complex_parts_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(R, n, Mr, Mi);
   return cudaGetLastError();
 }
 

@@ -71,7 +71,9 @@ struct PlanKey {
 struct phiks_ctx {
   int d = 0;
   int n[PHIKS_MAX_D] = {0};
-  int64_t N = 0;
+  int64_t N = 0;   // doubles per tensor (2·Nc for complex handles)
+  int64_t Nc = 0;  // elements per tensor
+  bool cplx = false;  // complex factors and tensors (interleaved re, im)
   std::vector<Factor> factors;
   int fac_of_mode[PHIKS_MAX_D] = {0};
   void* ws_own = nullptr;
@@ -255,6 +257,7 @@ struct Exec {
     const double* M;
     int group;
     std::vector<Out> outs;
+    int cswap = 0;  // complex: J applied to the accumulator (TermSpec::cswap)
   };
   void mode_launch(int64_t L, int n, int64_t R, const std::vector<LaunchTerm>& terms, const Remap* rm = nullptr) {
     if (!ok() || terms.empty()) return;
@@ -304,6 +307,7 @@ struct Exec {
           TermSpec& ts = p.terms[tt++];
           ts.in = t.in;
           ts.M = t.M;
+          ts.cswap = t.cswap;
           ts.out0 = oo;
           ts.nout = static_cast<int>(t.outs.size());
           for (const Out& o : t.outs) {
@@ -606,7 +610,7 @@ struct Exec {
 
   // every batch of run_job: sharded handles always split
   void batch(const std::vector<TuckerItem>& items, bool split_it) {
-    if (h->sharded() || split_it)
+    if (h->sharded() || h->cplx || split_it)
       tucker_batch_split(items);
     else
       tucker_batch(items);
@@ -625,12 +629,16 @@ struct Exec {
       while (scr[0].size() < nscr) scr[0].push_back(ar->alloc_doubles(N));
     if (d >= 3)
       while (scr[1].size() < nscr) scr[1].push_back(ar->alloc_doubles(N));
+    // complex tensors (interleaved): mode 1 contracts the merged (re/im, i_1)
+    // index with the 2n×2n real form of the matrix; every other mode is two real
+    // products on the (2·L, n, R) view, Mr then J(·Mi) accumulated (same group)
+    const bool cx = h->cplx;
     for (size_t c0 = 0; c0 < items.size() && ok(); c0 += chunk) {
       const size_t c1 = std::min(items.size(), c0 + chunk);
       int64_t L = 1;
       for (int mu = 0; mu < d; ++mu) {
         const int n = h->n[mu];
-        const int64_t R = N / (L * n);
+        const int64_t R = h->Nc / (L * n);
         std::vector<LaunchTerm> terms;
         for (size_t b = c0; b < c1; ++b) {
           const TuckerItem& it = items[b];
@@ -646,16 +654,46 @@ struct Exec {
             if (it.in_scale != 1.0)
               for (Out& o : t.outs) o.beta *= it.in_scale;
           }
-          terms.push_back(std::move(t));
+          if (cx && mu > 0) {
+            const auto parts = complex_parts(it.mats[mu], n);
+            LaunchTerm ti = t;
+            t.M = parts.first;
+            ti.M = parts.second;
+            ti.cswap = 1;
+            for (Out& o : ti.outs) {  // += β·J(acc_i): sole-source outputs only (split batches)
+              o.srcs.assign(1, Src{o.dst, 1.0});
+            }
+            terms.push_back(std::move(t));
+            terms.push_back(std::move(ti));
+          } else {
+            terms.push_back(std::move(t));
+          }
         }
-        mode_launch(L, n, R, terms);
+        if (cx && mu == 0)
+          mode_launch(1, 2 * n, R, terms);
+        else
+          mode_launch(cx ? 2 * L : L, n, R, terms);
         L *= n;
       }
       int64_t nsum = 0;
       for (int mu = 0; mu < d; ++mu) nsum += h->n[mu];
       tucker_ops += static_cast<int64_t>(c1 - c0);
-      mu_flops += static_cast<double>(c1 - c0) * 2.0 * static_cast<double>(N) * static_cast<double>(nsum);
+      mu_flops += static_cast<double>(c1 - c0) * (cx ? 8.0 : 2.0) * static_cast<double>(h->Nc) *
+                  static_cast<double>(nsum);
     }
+  }
+
+  // (Mr, Mi) of a complex exponential held in its 2n×2n real form, extracted
+  // once per matrix and apply (complex handles)
+  std::map<const double*, std::pair<const double*, const double*>> cparts;
+  std::pair<const double*, const double*> complex_parts(const double* Rm, int n) {
+    auto itp = cparts.find(Rm);
+    if (itp != cparts.end()) return itp->second;
+    double* mr = ar->alloc_doubles(static_cast<int64_t>(n) * n);
+    double* mi = ar->alloc_doubles(static_cast<int64_t>(n) * n);
+    emit("complex_parts", [Rm, n, mr, mi](cudaStream_t s) { return launch_complex_parts(Rm, n, mr, mi, s); });
+    cparts[Rm] = {mr, mi};
+    return {mr, mi};
   }
 
   // out_b = A_b · B_b (+ epilogue) for n×n matrices: mode-1 product of the
@@ -1080,7 +1118,28 @@ extern "C" {
 const char* phiks_last_error(void) { return g_err.c_str(); }
 const char* phiks_version(void) { return "phiks-b200 0.1.0 (sm_100a, fp64 DMMA)"; }
 
-phiks_status phiks_create(int d, const int* n, const double* const* A_host, phiks_handle* out) {
+}  // extern "C"
+
+namespace {
+
+// Real form of a complex n×n column-major matrix given as interleaved (re, im)
+// doubles: the 2n×2n matrix acting on interleaved vectors,
+// R[(c+2j) + (c'+2k)·2n] = [[Ar, −Ai], [Ai, Ar]]_{cc'}(j, k).
+std::vector<double> realify(int n, const double* Az) {
+  const size_t m = 2 * static_cast<size_t>(n);
+  std::vector<double> R(m * m);
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j) {
+      const double ar = Az[2 * (j + static_cast<size_t>(k) * n)], ai = Az[2 * (j + static_cast<size_t>(k) * n) + 1];
+      R[(2 * j) + (2 * k) * m] = ar;
+      R[(2 * j + 1) + (2 * k) * m] = ai;
+      R[(2 * j) + (2 * k + 1) * m] = -ai;
+      R[(2 * j + 1) + (2 * k + 1) * m] = ar;
+    }
+  return R;
+}
+
+phiks_status create_impl(int d, const int* n, const double* const* A_host, bool cplx, phiks_handle* out) {
   if (!out || !n || !A_host) return fail(PHIKS_ERR_ARG, "null argument");
   *out = nullptr;
   if (d < 1 || d > PHIKS_MAX_D) return fail(PHIKS_ERR_ARG, "d out of range");
@@ -1088,7 +1147,8 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PHIKS_ERR_CUDA, "no CUDA device");
   auto* h = new phiks_ctx();
   h->d = d;
-  h->N = 1;
+  h->cplx = cplx;
+  h->Nc = 1;
   for (int mu = 0; mu < d; ++mu) {
     if (n[mu] < 1 || n[mu] > PHIKS_MAX_N || !A_host[mu]) {
       delete h;
@@ -1096,8 +1156,10 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
     }
     h->n[mu] = n[mu];
     h->gn[mu] = n[mu];
-    h->N *= n[mu];
+    h->Nc *= n[mu];
   }
+  h->N = cplx ? 2 * h->Nc : h->Nc;
+  const int per = cplx ? 2 : 1;  // doubles per matrix entry
   // dedupe bitwise-identical factors
   std::vector<int> rep;
   for (int mu = 0; mu < d; ++mu) {
@@ -1105,25 +1167,32 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
     for (size_t f = 0; f < rep.size(); ++f) {
       const int m2 = rep[f];
       if (n[m2] == n[mu] &&
-          std::memcmp(A_host[m2], A_host[mu], sizeof(double) * static_cast<size_t>(n[mu]) * n[mu]) == 0) {
+          std::memcmp(A_host[m2], A_host[mu], sizeof(double) * per * static_cast<size_t>(n[mu]) * n[mu]) == 0) {
         found = static_cast<int>(f);
         break;
       }
     }
     if (found < 0) {
       Factor F;
-      F.n = n[mu];
+      // complex factors are stored (and exponentiated) in their 2n×2n real form:
+      // exp of the real form is the real form of exp (an algebra homomorphism)
+      std::vector<double> Rz;
+      const double* A = A_host[mu];
+      if (cplx) {
+        Rz = realify(n[mu], A_host[mu]);
+        A = Rz.data();
+      }
+      F.n = per * n[mu];
       const size_t bytes = sizeof(double) * static_cast<size_t>(F.n) * F.n;
       if (cudaMalloc(&F.dA, bytes) != cudaSuccess) {
         phiks_destroy(h);
         return fail(PHIKS_ERR_NOMEM, "cudaMalloc A");
       }
-      if (cudaMemcpy(F.dA, A_host[mu], bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+      if (cudaMemcpy(F.dA, A, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaFree(F.dA);
         phiks_destroy(h);
         return fail(PHIKS_ERR_CUDA, "copy A");
       }
-      const double* A = A_host[mu];
       double nrm = 0.0;
       for (int j = 0; j < F.n; ++j) {
         double c = 0.0;
@@ -1131,7 +1200,7 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
         nrm = std::max(nrm, c);
       }
       F.norm1 = nrm;
-      F.fr = plan::factor_range(F.n, A);
+      F.fr = cplx ? plan::factor_range_complex(n[mu], A_host[mu]) : plan::factor_range(F.n, A);
       h->factors.push_back(F);
       rep.push_back(mu);
       found = static_cast<int>(h->factors.size()) - 1;
@@ -1144,6 +1213,18 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
   }
   *out = h;
   return PHIKS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+phiks_status phiks_create(int d, const int* n, const double* const* A_host, phiks_handle* out) {
+  return create_impl(d, n, A_host, false, out);
+}
+
+phiks_status phiks_create_complex(int d, const int* n, const double* const* A_host, phiks_handle* out) {
+  return create_impl(d, n, A_host, true, out);
 }
 
 phiks_status phiks_destroy(phiks_handle h) {
@@ -1211,14 +1292,15 @@ phiks_status make_plan(phiks_handle h, const phiks_request* req, int p, const st
     return PHIKS_OK;
   }
   plan::Rect rect{};
-  double cr = 0.0, hr = 0.0, hi = 0.0;
+  double cr = 0.0, ci = 0.0, hr = 0.0, hi = 0.0;
   for (int mu = 0; mu < h->d; ++mu) {
     const auto& fr = h->factors[h->fac_of_mode[mu]].fr;
     cr += req->tau * fr.sigma;
+    ci += req->tau * fr.sigma_im;
     hr += req->tau * fr.hnorm;
     hi += req->tau * fr.snorm;
   }
-  rect.center = std::complex<double>(cr, 0.0);
+  rect.center = std::complex<double>(cr, ci);
   rect.hr = hr;
   rect.hi = hi;
   if (p == 0) {
@@ -1757,6 +1839,7 @@ phiks_status phiks_expm(int n, const double* A, double c, double* E, double* scr
   h.d = 1;
   h.n[0] = n;
   h.N = n;
+  h.Nc = n;
   Factor F;
   F.n = n;
   F.dA = const_cast<double*>(A);
@@ -1796,8 +1879,8 @@ phiks_status phiks_expm(int n, const double* A, double c, double* E, double* scr
   return PHIKS_OK;
 }
 
-phiks_status phiks_plan_host(int d, const int* n, const double* const* A_host, const phiks_request* req,
-                             const double* vec_norms, phiks_plan_info* out) {
+static phiks_status plan_host_impl(int d, const int* n, const double* const* A_host, bool cplx,
+                                   const phiks_request* req, const double* vec_norms, phiks_plan_info* out) {
   if (!n || !A_host || !req || !out || d < 1 || d > PHIKS_MAX_D) return fail(PHIKS_ERR_ARG, "bad argument");
   phiks_ctx h;  // host-only context: factor ranges, no device buffers
   h.d = d;
@@ -1807,13 +1890,24 @@ phiks_status phiks_plan_host(int d, const int* n, const double* const* A_host, c
     h.n[mu] = n[mu];
     h.gn[mu] = n[mu];
     h.N *= n[mu];
+    h.Nc = h.N;
     Factor F;
     F.n = n[mu];
-    F.fr = plan::factor_range(F.n, A_host[mu]);
+    F.fr = cplx ? plan::factor_range_complex(F.n, A_host[mu]) : plan::factor_range(F.n, A_host[mu]);
     h.factors.push_back(F);
     h.fac_of_mode[mu] = mu;
   }
   return phiks_plan(&h, req, vec_norms, out);
+}
+
+phiks_status phiks_plan_host(int d, const int* n, const double* const* A_host, const phiks_request* req,
+                             const double* vec_norms, phiks_plan_info* out) {
+  return plan_host_impl(d, n, A_host, false, req, vec_norms, out);
+}
+
+phiks_status phiks_plan_host_complex(int d, const int* n, const double* const* A_host, const phiks_request* req,
+                                     const double* vec_norms, phiks_plan_info* out) {
+  return plan_host_impl(d, n, A_host, true, req, vec_norms, out);
 }
 
 phiks_status phiks_select_plan(int mode, double center_re, double center_im, double hr, double hi, int p,
@@ -1868,6 +1962,7 @@ phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_ho
   if (world > 1) {
     h->n[d - 1] = n[d - 1] / world;
     h->N /= world;
+    h->Nc /= world;
     h->sym_slot = (static_cast<size_t>(h->N) * sizeof(double) + 255) & ~size_t(255);
     h->sym_bytes = kCtrlBytes + 2 * kShardChunk * h->sym_slot;
     if (cudaMalloc(reinterpret_cast<void**>(&h->sym), h->sym_bytes) != cudaSuccess) {

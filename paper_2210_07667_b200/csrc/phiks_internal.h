@@ -43,6 +43,7 @@ struct TermSpec {
   const double* M;  // n×n column-major, element (j,k) at j + k*n
   int out0;
   int nout;
+  int cswap;        // complex tensors: apply J (re ← −im, im ← re) to the accumulator first
 };
 
 struct GroupSpec {
@@ -114,6 +115,8 @@ cudaError_t launch_multi_combine(const MultiCombineParams& p, cudaStream_t st);
 cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, double* scratch,
                          double* norms2, cudaStream_t st);
 cudaError_t launch_set_identity(double* E, int n, double diag, cudaStream_t st);
+// Mr, Mi (n×n) from the interleaved real form R (2n×2n) of a complex matrix
+cudaError_t launch_complex_parts(const double* R, int n, double* Mr, double* Mi, cudaStream_t st);
 
 // Cross-rank barrier of a slab-sharded handle (one CTA): e = ++*epoch, writes e
 // into slot [rank] of every peer's flag array (st.release.sys over NVLink), then

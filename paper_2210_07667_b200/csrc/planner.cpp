@@ -269,6 +269,51 @@ FactorRange factor_range(int n, const double* A) {
   return fr;
 }
 
+FactorRange factor_range_complex(int n, const double* Az) {
+  FactorRange fr{};
+  double tr_re = 0.0, tr_im = 0.0;
+  for (int i = 0; i < n; ++i) {
+    tr_re += Az[2 * (i + static_cast<size_t>(i) * n)];
+    tr_im += Az[2 * (i + static_cast<size_t>(i) * n) + 1];
+  }
+  fr.sigma = tr_re / n;
+  fr.sigma_im = tr_im / n;
+  // B = A − σI; H = (B + B^H)/2 (Hermitian), S = (B − B^H)/2 (skew-Hermitian).
+  // A Hermitian X = Xr + iXi has the real symmetric form [[Xr, −Xi], [Xi, Xr]]
+  // with the same eigenvalues (each twice); ‖S‖₂ = ‖iS‖₂, iS = −Si + i·Sr.
+  const size_t m = 2 * static_cast<size_t>(n);
+  std::vector<double> RH(m * m), RS(m * m);
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j) {
+      const size_t jk = j + static_cast<size_t>(k) * n, kj = k + static_cast<size_t>(j) * n;
+      double br = Az[2 * jk], bi = Az[2 * jk + 1];
+      double cr = Az[2 * kj], ci = Az[2 * kj + 1];  // B_kj
+      if (j == k) {
+        br -= fr.sigma;
+        bi -= fr.sigma_im;
+        cr -= fr.sigma;
+        ci -= fr.sigma_im;
+      }
+      const double hr = 0.5 * (br + cr), hi = 0.5 * (bi - ci);  // H_jk = (B_jk + conj(B_kj))/2
+      const double sr = 0.5 * (br - cr), si = 0.5 * (bi + ci);  // S_jk = (B_jk − conj(B_kj))/2
+      const double xr = -si, xi = sr;                           // (iS)_jk
+      RH[j + k * m] = hr;
+      RH[(j + n) + (k + n) * m] = hr;
+      RH[(j + n) + k * m] = hi;
+      RH[j + (k + n) * m] = -hi;
+      RS[j + k * m] = xr;
+      RS[(j + n) + (k + n) * m] = xr;
+      RS[(j + n) + k * m] = xi;
+      RS[j + (k + n) * m] = -xi;
+    }
+  std::vector<double> d, e;
+  tridiagonalize(static_cast<int>(m), RH, d, e);
+  fr.hnorm = tridiag_abs_max(d, e);
+  tridiagonalize(static_cast<int>(m), RS, d, e);
+  fr.snorm = tridiag_abs_max(d, e);
+  return fr;
+}
+
 int tucker_count(int mode, int s, int s_hat, int q, int p) {
   return mode == kSame ? (q + s * p + s_hat) : (q * p + s * p + s_hat);
 }

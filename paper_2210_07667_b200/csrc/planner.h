@@ -15,11 +15,15 @@ void gll_rule(int q, std::vector<double>& theta, std::vector<double>& w);
 // (reading R1): σ = trace(A)/n, ||H||_2 and ||S||_2 of the Hermitian and
 // skew-Hermitian parts of A − σI.
 struct FactorRange {
-  double sigma;   // real trace shift
-  double hnorm;   // ||(B + B^T)/2||_2
-  double snorm;   // ||(B − B^T)/2||_2
+  double sigma;   // trace shift tr(A)/n (real part)
+  double hnorm;   // ||(B + B^H)/2||_2
+  double snorm;   // ||(B − B^H)/2||_2
+  double sigma_im = 0.0;  // imaginary part of the trace shift (complex A)
 };
 FactorRange factor_range(int n, const double* A);
+// complex A (interleaved re, im, column-major): ‖H‖₂ and ‖S‖₂ through the real
+// symmetric 2n×2n forms of the Hermitian matrices H and iS
+FactorRange factor_range_complex(int n, const double* Az);
 
 // Ξ = center + [−hr, hr] + i[−hi, hi]
 struct Rect {

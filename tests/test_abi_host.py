@@ -106,3 +106,44 @@ def test_cpp_planner_random_factors_match_oracle():
         ora = O.plan_for(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, pb.n_scales)
         got = _plan_host(pb)
         assert (got.s, got.q) == (ora.s, ora.q)
+
+
+def _plan_host_complex(dims, A, mode, ells, n_scales, tau, norms=None, tol=0.0):
+    lib = _lib.load()
+    n = (ctypes.c_int * len(dims))(*dims)
+    Az = [np.asfortranarray(a.astype(np.complex128)) for a in A]
+    req = _lib.make_request(0 if mode == "same" else 1, ells, n_scales, tau, tol)
+    arr = (ctypes.c_double * max(len(norms or []), 1))(*(norms or [0.0]))
+    info = _lib.PlanInfo()
+    _lib.check(lib.phiks_plan_host_complex(len(dims), n, _lib.ptr_array([a.ctypes.data for a in Az]),
+                                           ctypes.byref(req), arr if norms else None, ctypes.byref(info)),
+               "phiks_plan_host_complex")
+    return info
+
+
+@pytest.mark.parametrize("n,d", [(8, 2), (10, 3), (12, 2)])
+def test_cpp_complex_range_matches_oracle_plan(n, d):
+    # the complex validation operator (1+i)/100·Δ of PAPER.md §4.1: the library's
+    # complex numerical-range rectangle gives the oracle's plan
+    A = (1 + 1j) / 100 * W.fd_dxx_dirichlet(n)
+    dims = (n,) * d
+    V = W.random_tensor(dims, seed=3, complex_=True)
+    for mode, ells in (("same", (0, 1, 2, 3)), ("lincomb", (0, 1, 2))):
+        vs = [V] if mode == "same" else [W.random_tensor(dims, seed=5 + k, complex_=True) for k in ells]
+        ora = O.plan_for([A] * d, 1.0, mode, ells, vs, 1)
+        norms = None
+        if mode == "lincomb":
+            norms = [float(np.linalg.norm(W.as_flat(v))) for v in vs[1:]]
+        got = _plan_host_complex(dims, [A] * d, mode, ells, 1, 1.0, norms)
+        assert (got.s, got.q) == (ora.s, ora.q), (mode, got.s, got.q, ora)
+
+
+def test_cpp_complex_range_random_factors():
+    rng = np.random.default_rng(11)
+    for c in range(4):
+        dims = tuple(int(x) for x in rng.integers(3, 8, size=2))
+        fac = W.random_factors(dims, seed=700 + c, scale=float(rng.uniform(1.0, 20.0)), complex_=True)
+        V = W.random_tensor(dims, seed=c, complex_=True)
+        ora = O.plan_for(fac, 1.0, "same", (1, 2), [V], 1)
+        got = _plan_host_complex(dims, fac, "same", (1, 2), 1, 1.0)
+        assert (got.s, got.q) == (ora.s, ora.q)
