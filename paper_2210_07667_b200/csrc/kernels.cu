@@ -419,7 +419,8 @@ struct TmaGeom {
   static_assert((A_ELEMS * 8) % 128 == 0 && (B_ELEMS * 8) % 128 == 0, "128B-aligned stage tiles");
 };
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool KMAJ, bool REMOTE = false>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool KMAJ, bool REMOTE = false,
+          bool CPLX = false>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
     mode_product_tma_kernel(const __grid_constant__ ModeParams p, const __grid_constant__ TmaMaps tm) {
   constexpr int NWARPS = WARPS_M * WARPS_N;
@@ -558,7 +559,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
 
       // ---- fused linear epilogue ----
       const TermSpec& term = p.terms[t];
-      if (term.cswap) complex_swap<MI, NI>(acc, lane);
+      if (CPLX && term.cswap) complex_swap<MI, NI>(acc, lane);
       for (int o = term.out0; o < term.out0 + term.nout; ++o) {
         const OutSpec& os = p.outs[o];
         double* dst = os.dst;
@@ -677,7 +678,8 @@ static bool encode(CUtensorMap* m, const double* ptr, int rank, const cuuint64_t
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool REMOTE = false>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int MINB, bool REMOTE = false,
+          bool CPLX = false>
 static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   const bool kmaj = p.L == 1;
   const int n = p.n;
@@ -719,7 +721,7 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   if (kmaj) {
     using Gm = TmaGeom<BM, BN, BK, 1>;
     constexpr size_t smem = static_cast<size_t>(STAGES) * Gm::STAGE_ELEMS * 8 + 2 * STAGES * 8;
-    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, true, REMOTE>;
+    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, true, REMOTE, CPLX>;
     if (!attr[1]) {
       *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (*err != cudaSuccess) return true;
@@ -735,7 +737,7 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   } else {
     using Gm = TmaGeom<BM, BN, BK, 0>;
     constexpr size_t smem = static_cast<size_t>(STAGES) * Gm::STAGE_ELEMS * 8 + 2 * STAGES * 8;
-    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, false, REMOTE>;
+    auto k = mode_product_tma_kernel<BM, BN, BK, WARPS_M, WARPS_N, STAGES, MINB, false, REMOTE, CPLX>;
     if (!attr[0]) {
       *err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (*err != cudaSuccess) return true;
@@ -774,7 +776,18 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
     if (launch_tma<64, 128, 16, 2, 2, 4, 2, true>(p, st, &err)) return err;
     return launch_cfg<64, 64, 16, 2, 2, 4, 3>(p, st);
   }
-  if (p.n > 64 && var != 1) {
+  bool cswap = false;
+  for (int g = 0; g < p.ngroups; ++g)
+    for (int t = p.groups[g].t0; t < p.groups[g].t1; ++t) cswap |= p.terms[t].cswap != 0;
+  if (cswap) {  // complex modes μ ≥ 2: the J-swap instantiation (real launches keep the lean one)
+    if (p.n > 64) {
+      cudaError_t err = cudaSuccess;
+      const int64_t units = ((Mtot + 63) / 64) * ((p.n + 127) / 128) * p.ngroups;
+      const bool done = units >= 148 * 2 ? launch_tma<64, 128, 16, 2, 2, 4, 2, false, true>(p, st, &err)
+                                         : launch_tma<64, 64, 16, 2, 2, 4, 3, false, true>(p, st, &err);
+      if (done) return err;
+    }
+  } else if (p.n > 64 && var != 1) {
     cudaError_t err = cudaSuccess;
     bool done = false;
     if (var == 10) {
