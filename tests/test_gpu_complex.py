@@ -109,3 +109,17 @@ def test_complex_real_factors_agree_with_real_handle():
         b = b.cpu().numpy()
         assert np.abs(a.imag).max() == 0.0
         assert rel2(a.real, b) <= 1e-13
+
+
+def test_complex_validation_operator_d6():
+    # PAPER.md Table 1's d = 6 columns (n = 8): six-way complex tensors
+    n, d = 8, 6
+    A = (1 + 1j) / 100 * W.fd_dxx_dirichlet(n)
+    h = 1.0 / (n + 1)
+    x = np.arange(1, n + 1) * h
+    f = x * (1 - x)
+    V = 4096 * (1 + 1j) * f
+    for _ in range(d - 1):
+        V = np.multiply.outer(V, f)
+    pb = W.Problem("validation_d6", (n,) * d, [A] * d, 1.0, "same", (0, 1, 2, 3), [V], 1)
+    run_and_compare(pb)
