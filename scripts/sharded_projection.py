@@ -1,0 +1,55 @@
+"""Projection (NOT a measurement) of the slab-sharded configs[3] step at P
+GPUs from one GPU: phiks_apply_ranks_serial runs the P ranks' launches back to
+back on one GPU (same kernels, same peer-store epilogues, writing into the
+other ranks' regions in local HBM instead of over NVLink), so its time / P
+is the per-rank kernel time; the projection adds nothing for barriers or
+NVLink latency.  Used only for DESIGN.md's scaling discussion."""
+import json, os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2210_07667_b200 import PhiKS, ShardedPhiKS, apply_ranks_serial  # noqa: E402
+from paper_2210_07667_b200 import workloads as W  # noqa: E402
+from paper_2210_07667_b200.sharding import split_slabs  # noqa: E402
+
+wl = W.config(3)
+res = []
+for P in (1, 2, 4, 8):
+    hs, ins, outs = [], [], []
+    for pb in wl.problems:
+        x = W.as_flat(pb.vs[0])
+        if P == 1:
+            op = PhiKS(pb.A)
+            hs.append([op])
+        else:
+            ranks = [ShardedPhiKS(pb.A, r, P, connect=None) for r in range(P)]
+            ShardedPhiKS.connect_local(ranks)
+            hs.append(ranks)
+        ins.append([[torch.from_numpy(np.ascontiguousarray(s)).cuda()] for s in split_slabs(x, P)])
+        outs.append([[torch.empty(x.size // P, dtype=torch.float64, device="cuda") for _ in pb.ells]
+                     for _ in range(P)])
+
+    def step():
+        for pb, h, i, o in zip(wl.problems, hs, ins, outs):
+            if P == 1:
+                h[0].apply(pb.tau, pb.ells, i[0], outs=o[0])
+            else:
+                apply_ranks_serial(h, pb.tau, pb.ells, i, outs=o)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 5
+    res.append({"P": P, "serial_ms": round(t, 3), "per_rank_ms": round(t / P, 3)})
+    print(json.dumps(res[-1]), flush=True)
+    del hs, ins, outs
+    torch.cuda.empty_cache()
+t1 = res[0]["per_rank_ms"]
+for r in res:
+    r["projected_efficiency"] = round(t1 / (r["P"] * r["per_rank_ms"]), 3)
+print(json.dumps(res))
