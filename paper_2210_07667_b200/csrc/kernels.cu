@@ -566,28 +566,63 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
         const double beta = os.beta;
         const bool vec_ok = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
         if (REMOTE) {  // slab-sharded: stores into the owner rank's region
+          const Remap& rm = p.remap;
+          const int jb = T.j0 + wn0 + 2 * lt;
+          if ((rm.cb & 1) == 0) {
+            // columns (j, j+1) share their owner: resolve owner and column base once per
+            // 8-column group, then every row is one add
+            double* colp[NI];
 #pragma unroll
-          for (int mi = 0; mi < MI; ++mi) {
-            const int64_t rl = wm0 + mi * 8 + lg;
-            int64_t l, r;
-            if (KMAJ) {
-              l = 0;
-              r = T.r + rl;
-              if (r >= R) continue;
-            } else {
-              l = T.l0 + rl;
-              r = T.r;
-              if (l >= L) continue;
+            for (int ni = 0; ni < NI; ++ni) {
+              const int j = jb + ni * 8;
+              const int k = j < n ? j / rm.cb : 0;
+              colp[ni] = reinterpret_cast<double*>(rm.base[k] + reinterpret_cast<uintptr_t>(os.dst)) + rm.roff +
+                         rm.colstride * static_cast<int64_t>(j - k * rm.cb);
             }
-            const int64_t rowb = l + p.remap.rstride * r + p.remap.roff;
-            const int jb = T.j0 + wn0 + 2 * lt;
 #pragma unroll
-            for (int ni = 0; ni < NI; ++ni)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int j = jb + ni * 8 + e;
-                if (j < n) remote_store(p.remap, os, rowb, j, beta * acc[mi][ni][e]);
+            for (int mi = 0; mi < MI; ++mi) {
+              const int64_t rl = wm0 + mi * 8 + lg;
+              int64_t l, r;
+              if (KMAJ) {
+                l = 0;
+                r = T.r + rl;
+                if (r >= R) continue;
+              } else {
+                l = T.l0 + rl;
+                r = T.r;
+                if (l >= L) continue;
               }
+              const int64_t rowb = l + rm.rstride * r;
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni) {
+                const int j = jb + ni * 8;
+                if (j < n) colp[ni][rowb] = beta * acc[mi][ni][0];
+                if (j + 1 < n) colp[ni][rowb + rm.colstride] = beta * acc[mi][ni][1];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi) {
+              const int64_t rl = wm0 + mi * 8 + lg;
+              int64_t l, r;
+              if (KMAJ) {
+                l = 0;
+                r = T.r + rl;
+                if (r >= R) continue;
+              } else {
+                l = T.l0 + rl;
+                r = T.r;
+                if (l >= L) continue;
+              }
+              const int64_t rowb = l + rm.rstride * r + rm.roff;
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int j = jb + ni * 8 + e;
+                  if (j < n) remote_store(rm, os, rowb, j, beta * acc[mi][ni][e]);
+                }
+            }
           }
           continue;
         }

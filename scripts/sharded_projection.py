@@ -14,7 +14,7 @@ from paper_2210_07667_b200.sharding import split_slabs  # noqa: E402
 
 wl = W.config(3)
 res = []
-for P in (1, 2, 4, 8):
+for P in [int(x) for x in os.environ.get("PS", "1,2,4,8").split(",")]:
     hs, ins, outs = [], [], []
     for pb in wl.problems:
         x = W.as_flat(pb.vs[0])
@@ -49,7 +49,7 @@ for P in (1, 2, 4, 8):
     print(json.dumps(res[-1]), flush=True)
     del hs, ins, outs
     torch.cuda.empty_cache()
-t1 = res[0]["per_rank_ms"]
+t1 = res[0]["per_rank_ms"] * res[0]["P"]
 for r in res:
     r["projected_efficiency"] = round(t1 / (r["P"] * r["per_rank_ms"]), 3)
 print(json.dumps(res))
