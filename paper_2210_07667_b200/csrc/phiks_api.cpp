@@ -111,6 +111,12 @@ struct phiks_ctx {
   // host-memory applies: copy streams and their ordering events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_h2d = nullptr, ev_d2h = nullptr, ev_cdone = nullptr, ev_ready = nullptr;
+  // the exponential stage (stage A) of an apply runs on s_pre, ordered only
+  // after the previous apply of this handle (ev_cdone), so it overlaps the
+  // tail of whatever else is queued on the apply stream (another handle's
+  // Tucker work); the stream waits on ev_pre before the first Tucker batch
+  cudaStream_t s_pre = nullptr;
+  cudaEvent_t ev_pre = nullptr;
   bool sharded() const { return world > 1; }
 };
 
@@ -1239,6 +1245,8 @@ phiks_status phiks_destroy(phiks_handle h) {
     if (e) cudaEventDestroy(e);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
   if (h->s_cap) cudaStreamDestroy(h->s_cap);
+  if (h->s_pre) cudaStreamDestroy(h->s_pre);
+  if (h->ev_pre) cudaEventDestroy(h->ev_pre);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
   if (h->sym) cudaFree(h->sym);
@@ -1535,7 +1543,9 @@ struct ApplyRun {
     return PHIKS_OK;
   }
 
+  bool own_ws = false;
   phiks_status workspace(void* workspace, size_t ws_bytes, size_t need, char** base) {
+    own_ws = workspace == nullptr;
     if (workspace) {
       if (ws_bytes < need) {
         h->stats.workspace_bytes = need;
@@ -1570,16 +1580,39 @@ struct ApplyRun {
     ex.rec = rec;
     bind(false);
     if (host_mem && rec) return fail(PHIKS_ERR_ARG, "recorded applies take device memory");
+    // (never recorded yet: waiting on it is a no-op)
+    if (!h->ev_cdone) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_cdone, cudaEventDisableTiming));
+    // stage A on the handle's pre stream: only with the library's own workspace
+    // (a caller workspace may be in use on the stream until this apply starts),
+    // not while capturing a graph, not for recorded (emulated-rank) applies
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(cs, &cap));
+    const bool pre = !rec && own_ws && cap == cudaStreamCaptureStatusNone;
+    if (pre) {
+      if (!h->s_pre) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->s_pre, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&h->ev_pre, cudaEventDisableTiming));
+      }
+      CUDA_TRY(cudaStreamWaitEvent(h->s_pre, h->ev_cdone, 0));  // previous apply no longer reads the workspace
+      ex.st = h->s_pre;
+    }
+    ex.on_inputs = [this, pre]() {
+      if (pre) {
+        ex.check(cudaEventRecord(h->ev_pre, h->s_pre), "record pre");
+        ex.st = cs;
+        ex.check(cudaStreamWaitEvent(cs, h->ev_pre, 0), "wait pre");
+      }
+      if (host_mem) ex.check(cudaStreamWaitEvent(cs, h->ev_h2d, 0), "wait h2d");
+    };
     if (host_mem) {
       // copies on the handle's own streams: H2D overlaps stage A, the copy-out of
       // an output overlaps the rest of the job (and the next apply)
       if (!h->s_in) {
         CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&h->ev_h2d, &h->ev_d2h, &h->ev_cdone, &h->ev_ready})
+        for (cudaEvent_t* e : {&h->ev_h2d, &h->ev_d2h, &h->ev_ready})
           CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         CUDA_TRY(cudaEventRecord(h->ev_d2h, h->s_out));
-        CUDA_TRY(cudaEventRecord(h->ev_cdone, cs));
       }
       CUDA_TRY(cudaStreamWaitEvent(h->s_in, h->ev_cdone, 0));  // previous apply is done with the staging
       for (size_t i = 0; i < dv.size(); ++i)
@@ -1587,10 +1620,10 @@ struct ApplyRun {
       CUDA_TRY(cudaEventRecord(h->ev_h2d, h->s_in));
       CUDA_TRY(cudaStreamWaitEvent(cs, h->ev_d2h, 0));  // previous apply's copy-out has drained
       copied.assign(nouts, false);
-      ex.on_inputs = [this]() { ex.check(cudaStreamWaitEvent(cs, h->ev_h2d, 0), "wait h2d"); };
       ex.on_outputs = [this](const std::vector<double*>& ready) { copy_out(ready); };
     }
     run_job(ex, jb);
+    ex.st = cs;
     if (!ex.ok()) return ex.status;
     if (host_mem) {
       std::vector<double*> rest;
@@ -1599,8 +1632,8 @@ struct ApplyRun {
       copy_out(rest);
       if (!ex.ok()) return ex.status;
       CUDA_TRY(cudaEventRecord(h->ev_d2h, h->s_out));
-      CUDA_TRY(cudaEventRecord(h->ev_cdone, cs));
     }
+    if (!rec && cap == cudaStreamCaptureStatusNone) CUDA_TRY(cudaEventRecord(h->ev_cdone, cs));
     return PHIKS_OK;
   }
   std::vector<bool> copied;
@@ -1726,6 +1759,8 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
       ++h->graph_replays;
     }
     CUDA_TRY(cudaGraphLaunch(exec, cs));
+    if (!h->ev_cdone) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_cdone, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(h->ev_cdone, cs));  // orders the next apply's stage A after this replay
     run.finish_stats(need);
     return PHIKS_OK;
   }
