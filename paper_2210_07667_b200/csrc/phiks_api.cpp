@@ -1715,7 +1715,10 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
     const char* e = getenv("PHIKS_GRAPHS");
     return !(e && atoi(e) == 0);
   }();
-  if (graphs_on && !run.host_mem && !h->profiling) {
+  // graphs pay off where launch overhead matters (small tensors); large applies
+  // keep direct launches so their exponential stage overlaps on the side stream
+  const bool small_apply = h->N <= (int64_t(1) << 22);
+  if (graphs_on && small_apply && !run.host_mem && !h->profiling) {
     const cudaStream_t cs = run.cs;
     // key: everything the recorded launches depend on
     std::vector<uint64_t> key;

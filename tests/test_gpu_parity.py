@@ -228,3 +228,36 @@ def test_errors_are_loud():
         op.apply(-1.0, (1,), [v])           # tau <= 0
     with pytest.raises(PhiksError):
         op.apply(1.0, (7,), [v])            # order above PHIKS_MAX_P
+
+
+def test_back_to_back_applies_keep_their_exponentials():
+    # the exponential stage runs on a side stream; a second apply with another τ
+    # must not overwrite the first apply's exponentials while its Tucker
+    # launches still read them (no sync in between), and two handles interleave
+    pb = W.config(3, small=True).problems[0]
+    big = [W.fd_dxx_neumann(160) * 1e-3] * 3           # above the graph threshold: side-stream path
+    v = torch.from_numpy(np.ascontiguousarray(W.random_tensor((160,) * 3, seed=2).reshape(-1, order="F"))).to(DEV)
+    op = PhiKS(big)
+    ref = []
+    for tau in (0.5, 2.0):
+        ref.append([o.cpu().numpy() for o in op.apply(tau, (0, 1, 2), [v])])
+        torch.cuda.synchronize()
+    outs = [op.apply(tau, (0, 1, 2), [v]) for tau in (0.5, 2.0, 0.5)]
+    torch.cuda.synchronize()
+    for got, exp in zip(outs, [ref[0], ref[1], ref[0]]):
+        for a, b in zip(got, exp):
+            assert np.array_equal(a.cpu().numpy(), b)
+    # two handles interleaved on one stream
+    op2 = PhiKS([W.fd_dxx_neumann(160) * 2e-3] * 3)
+    r2 = [o.cpu().numpy() for o in op2.apply(1.0, (0, 1, 2), [v])]
+    torch.cuda.synchronize()
+    seq = []
+    for _ in range(3):
+        seq.append(op.apply(0.5, (0, 1, 2), [v]))
+        seq.append(op2.apply(1.0, (0, 1, 2), [v]))
+    torch.cuda.synchronize()
+    for k, got in enumerate(seq):
+        exp = ref[0] if k % 2 == 0 else r2
+        for a, b in zip(got, exp):
+            assert np.array_equal(a.cpu().numpy(), b)
+    del pb
