@@ -690,16 +690,14 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const EncodeTiledFn fn = [] {  // thread-safe one-time lookup
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(f);
-  }
+      return reinterpret_cast<EncodeTiledFn>(f);
+    return static_cast<EncodeTiledFn>(nullptr);
+  }();
   return fn;
 }
 
@@ -724,7 +722,7 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   if (p.L * p.R > (int64_t(1) << 31) * 8) return false;
   int nterms = 0;
   for (int g = 0; g < p.ngroups; ++g) nterms = p.groups[g].t1 > nterms ? p.groups[g].t1 : nterms;
-  static TmaMaps maps;  // host staging (launch copies the parameter block)
+  TmaMaps maps;  // per call (12 KB on the host stack): distinct handles may launch from different threads
   for (int t = 0; t < nterms; ++t) {
     if ((reinterpret_cast<uintptr_t>(p.terms[t].in) | reinterpret_cast<uintptr_t>(p.terms[t].M)) & 15) return false;
   }
