@@ -261,3 +261,17 @@ def test_back_to_back_applies_keep_their_exponentials():
         for a, b in zip(got, exp):
             assert np.array_equal(a.cpu().numpy(), b)
     del pb
+
+
+def test_order_eight_tensor():
+    # d = PHIKS_MAX_D = 8, both modes
+    dims = (3, 2, 4, 2, 3, 2, 2, 3)
+    fac = W.random_factors(dims, seed=88, scale=2.0)
+    V = W.random_tensor(dims, seed=8)
+    pb = W.Problem("d8_same", dims, fac, 0.7, "same", (0, 1, 2), [V], 2)
+    op, ref, outs = _run(pb, force=False)
+    _compare(pb, ref, outs, 2)
+    vs = [W.random_tensor(dims, seed=20 + k) for k in range(3)]
+    pb = W.Problem("d8_lincomb", dims, fac, 0.7, "lincomb", (0, 1, 2), vs, 1)
+    op, ref, outs = _run(pb, force=False)
+    _compare(pb, ref, outs, 1)
