@@ -275,3 +275,38 @@ def test_order_eight_tensor():
     pb = W.Problem("d8_lincomb", dims, fac, 0.7, "lincomb", (0, 1, 2), vs, 1)
     op, ref, outs = _run(pb, force=False)
     _compare(pb, ref, outs, 1)
+
+
+def test_api_error_paths():
+    import ctypes
+    from paper_2210_07667_b200 import PhiksError, ShardedPhiKS, _lib
+    pb = W.config(2, small=True).problems[0]
+    op = PhiKS(pb.A)
+    v = dev(pb.vs[0])
+    # caller workspace too small
+    with pytest.raises(PhiksError) as ei:
+        op.apply(pb.tau, pb.ells, [v], n_scales=pb.n_scales,
+                 workspace=torch.empty(16, dtype=torch.float64, device=DEV))
+    assert ei.value.code == 5  # PHIKS_ERR_WORKSPACE
+    # wrong vector count / size / dtype
+    with pytest.raises(PhiksError):
+        op.apply(pb.tau, pb.ells, [v, v], n_scales=pb.n_scales)
+    with pytest.raises(ValueError):
+        op.apply(pb.tau, pb.ells, [v[:-1].contiguous()], n_scales=pb.n_scales)
+    with pytest.raises(TypeError):
+        op.apply(pb.tau, pb.ells, [v.float()], n_scales=pb.n_scales)
+    # bad mem_kind through the raw ABI
+    req = _lib.make_request(0, pb.ells, 1, pb.tau, mem_kind=7)
+    arr = _lib.ptr_array([v.data_ptr()])
+    outs = [torch.empty_like(v) for _ in pb.ells]
+    code = _lib.load().phiks_apply(op._h, ctypes.byref(req), 1, arr, _lib.ptr_array([o.data_ptr() for o in outs]),
+                                   None, 0, 0)
+    assert code == 1
+    # a sharded handle refuses to apply before its peers are attached
+    sh = ShardedPhiKS(pb.A, 0, 2, connect=None)
+    with pytest.raises(PhiksError):
+        sh.apply(pb.tau, pb.ells, [v[: v.numel() // 2].contiguous()], n_scales=pb.n_scales)
+    sh.close()
+    # n_scales forcing s below ŝ-1
+    with pytest.raises(PhiksError):
+        op.apply(pb.tau, pb.ells, [v], n_scales=3, force_s=0, force_q=4)
