@@ -1,0 +1,386 @@
+// The job of one apply as kernel launches: the exponential stage and the
+// quadrature / squaring / exp-action Tucker batches (see host.h).
+#include "host.h"
+
+namespace phiks {
+namespace host {
+
+void expm_batch(Exec& ex, double tau, std::vector<ExpReq>& reqs) {
+  phiks_ctx* h = ex.h;
+  const int nf = static_cast<int>(h->factors.size());
+  std::vector<char> used(nf, 0);
+  for (auto& r : reqs) used[r.f] = 1;
+  // per-factor powers
+  std::vector<double*> X1(nf, nullptr), X2(nf), X3(nf), X4(nf);
+  std::map<int, double*> Ident;
+  for (int f = 0; f < nf; ++f) {
+    if (!used[f]) continue;
+    const int n = h->factors[f].n;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    X1[f] = ex.ar->alloc_doubles(nn);
+    X2[f] = ex.ar->alloc_doubles(nn);
+    X3[f] = ex.ar->alloc_doubles(nn);
+    X4[f] = ex.ar->alloc_doubles(nn);
+    if (!Ident.count(n)) {
+      Ident[n] = ex.ar->alloc_doubles(nn);
+      double* I = Ident[n];
+      ex.emit("set_identity", [I, n](cudaStream_t s) { return launch_set_identity(I, n, 1.0, s); });
+    }
+  }
+  // distinct n values
+  std::vector<int> ns;
+  for (int f = 0; f < nf; ++f)
+    if (used[f] && std::find(ns.begin(), ns.end(), h->factors[f].n) == ns.end()) ns.push_back(h->factors[f].n);
+  for (int n : ns) {
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    std::vector<Out> sc;
+    for (int f = 0; f < nf; ++f)
+      if (used[f] && h->factors[f].n == n) sc.push_back(Out{X1[f], 0.0, {Src{h->factors[f].dA, tau}}});
+    ex.combine(nn, sc);
+    std::vector<Exec::LaunchTerm> t2, t3, t4;
+    for (int f = 0; f < nf; ++f)
+      if (used[f] && h->factors[f].n == n) t2.push_back({X1[f], X1[f], f, {Out{X2[f], 1.0, {}}}});
+    ex.gemm_batch(n, t2);
+    for (int f = 0; f < nf; ++f)
+      if (used[f] && h->factors[f].n == n) {
+        t3.push_back({X1[f], X2[f], f, {Out{X3[f], 1.0, {}}}});   // X2·X1
+        t4.push_back({X2[f], X2[f], f, {Out{X4[f], 1.0, {}}}});   // X2·X2
+      }
+    for (auto& t : t4) t3.push_back(t);
+    for (size_t i = 0; i < t3.size(); ++i) t3[i].group = static_cast<int>(i);
+    ex.gemm_batch(n, t3);
+  }
+  // per request: scaling, Horner in X4, squarings
+  struct St {
+    double a;
+    int sigma;
+    double* buf[2];
+    int cur;
+  };
+  std::vector<St> sts(reqs.size());
+  int max_sigma = 0;
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    const Factor& F = h->factors[reqs[i].f];
+    const double nrm = std::fabs(reqs[i].c) * tau * F.norm1;
+    int sigma = 0;
+    if (nrm > 0.5) sigma = static_cast<int>(std::ceil(std::log2(nrm / 0.5)));
+    sts[i].sigma = sigma;
+    sts[i].a = reqs[i].c / std::ldexp(1.0, sigma);
+    const int64_t nn = static_cast<int64_t>(F.n) * F.n;
+    sts[i].buf[0] = ex.ar->alloc_doubles(nn);
+    sts[i].buf[1] = ex.ar->alloc_doubles(nn);
+    sts[i].cur = 0;
+    max_sigma = std::max(max_sigma, sigma);
+  }
+  auto coefs = [](double a, int base) {  // B_m coefficients a^r/(base+r)!, r = 0..3 (base = 4m)
+    std::vector<double> c(4);
+    for (int r = 0; r < 4; ++r) c[r] = std::pow(a, r) / factorial(base + r);
+    return c;
+  };
+  for (int n : ns) {
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    // H = Y4/16! + B3 = a^4/16! X4 + B3
+    std::vector<Out> h0;
+    for (size_t i = 0; i < reqs.size(); ++i) {
+      const int f = reqs[i].f;
+      if (h->factors[f].n != n) continue;
+      const double a = sts[i].a;
+      auto c = coefs(a, 12);
+      h0.push_back(Out{sts[i].buf[0], 0.0,
+                       {Src{X4[f], std::pow(a, 4) / factorial(16)}, Src{Ident[n], c[0]}, Src{X1[f], c[1]},
+                        Src{X2[f], c[2]}, Src{X3[f], c[3]}}});
+    }
+    ex.combine(nn, h0);
+    // three Horner GEMMs: H <- a^4 X4 H + B_m, m = 2, 1, 0
+    for (int m = 2; m >= 0; --m) {
+      std::vector<Exec::LaunchTerm> tl;
+      for (size_t i = 0; i < reqs.size(); ++i) {
+        const int f = reqs[i].f;
+        if (h->factors[f].n != n) continue;
+        const double a = sts[i].a;
+        auto c = coefs(a, 4 * m);
+        St& s = sts[i];
+        tl.push_back({s.buf[s.cur], X4[f], static_cast<int>(tl.size()),
+                      {Out{s.buf[s.cur ^ 1], std::pow(a, 4),
+                           {Src{Ident[n], c[0]}, Src{X1[f], c[1]}, Src{X2[f], c[2]}, Src{X3[f], c[3]}}}}});
+        s.cur ^= 1;
+      }
+      ex.gemm_batch(n, tl);
+    }
+    // σ squarings
+    for (int k = 0; k < max_sigma; ++k) {
+      std::vector<Exec::LaunchTerm> tl;
+      for (size_t i = 0; i < reqs.size(); ++i) {
+        const int f = reqs[i].f;
+        St& s = sts[i];
+        if (h->factors[f].n != n || s.sigma <= k) continue;
+        tl.push_back({s.buf[s.cur], s.buf[s.cur], static_cast<int>(tl.size()), {Out{s.buf[s.cur ^ 1], 1.0, {}}}});
+        s.cur ^= 1;
+      }
+      if (!tl.empty()) ex.gemm_batch(n, tl);
+    }
+  }
+  for (size_t i = 0; i < reqs.size(); ++i) reqs[i].result = sts[i].buf[sts[i].cur];
+}
+
+// ---------------------------------------------------------------------------
+// The whole φ-action (stages A-D) on device pointers.
+// vin[ℓ] (ℓ = 0..p) device input tensors or nullptr; out_same[ℓ][j] / out_lin[j]
+// device output tensors or nullptr (not requested).
+// ---------------------------------------------------------------------------
+void run_job(Exec& ex, const Job& jb) {
+  phiks_ctx* h = ex.h;
+  const int d = h->d;
+  const int p = jb.p, s = jb.s, q = jb.q;
+  const int64_t N = h->N;
+  const int nf = static_cast<int>(h->factors.size());
+  const bool same = jb.mode == PHIKS_MODE_SAME_VECTOR;
+
+  // ---- which level matrices exp(τA/2^j) are needed ----
+  bool want_phi0 = false;
+  if (same) {
+    for (int j = 0; j < jb.n_scales; ++j) want_phi0 |= jb.out_same[0][j] != nullptr;
+  } else {
+    want_phi0 = jb.vin[0] != nullptr;
+  }
+  int jmin = s;
+  if (p >= 1) jmin = std::min(jmin, 1);
+  if (want_phi0) jmin = 0;
+  if (p >= 1 && s == 0) jmin = 0;
+
+  std::vector<double> theta, w;
+  if (p >= 1) plan::gll_rule(q, theta, w);
+
+  // ---- Stage A ----
+  std::vector<ExpReq> reqs;
+  // node exponentials (θ_i ≠ 1): c_i = (1 − θ_i)/2^s; node 0 (θ = 0) gives exp(τA/2^s)
+  const int n_nodes = (p >= 1) ? q - 1 : 0;
+  for (int i = 0; i < n_nodes; ++i)
+    for (int f = 0; f < nf; ++f) reqs.push_back({f, (1.0 - theta[i]) / std::ldexp(1.0, s)});
+  if (p == 0)
+    for (int f = 0; f < nf; ++f) reqs.push_back({f, 1.0 / std::ldexp(1.0, s)});
+  expm_batch(ex, jb.tau, reqs);
+  if (!ex.ok()) return;
+  // nodeE[i][f]
+  std::vector<std::vector<const double*>> nodeE(n_nodes, std::vector<const double*>(nf));
+  for (int i = 0; i < n_nodes; ++i)
+    for (int f = 0; f < nf; ++f) nodeE[i][f] = reqs[static_cast<size_t>(i) * nf + f].result;
+  // level matrices Es[j][f], j = jmin..s
+  std::vector<std::vector<double*>> Es(s + 1, std::vector<double*>(nf, nullptr));
+  for (int f = 0; f < nf; ++f)
+    Es[s][f] = (p >= 1) ? const_cast<double*>(nodeE[0][f]) : reqs[f].result;
+  for (int j = s; j > jmin; --j) {
+    std::map<int, std::vector<Exec::LaunchTerm>> byn;
+    for (int f = 0; f < nf; ++f) {
+      const int n = h->factors[f].n;
+      Es[j - 1][f] = ex.ar->alloc_doubles(static_cast<int64_t>(n) * n);
+      auto& v = byn[n];
+      v.push_back({Es[j][f], Es[j][f], static_cast<int>(v.size()), {Out{Es[j - 1][f], 1.0, {}}}});
+    }
+    for (auto& kv : byn) ex.gemm_batch(kv.first, kv.second);
+  }
+  auto mats_for = [&](const std::vector<double*>& perf, const double** mats) {
+    for (int mu = 0; mu < d; ++mu) mats[mu] = perf[h->fac_of_mode[mu]];
+  };
+  auto node_mats = [&](int i, const double** mats) {
+    for (int mu = 0; mu < d; ++mu) mats[mu] = nodeE[i][h->fac_of_mode[mu]];
+  };
+
+  // inputs staged from host memory are needed from here on (stage A overlaps their copy)
+  if (ex.on_inputs) ex.on_inputs();
+
+  // ---- Stage D (same vector): exp(τK/2^j)v needs only the level matrices and
+  // reads the same v as the quadrature, so with p ≥ 1 it joins the quadrature
+  // batch (one launch per mode for both); a host-memory apply copies it out
+  // while the squaring runs ----
+  std::vector<TuckerItem> d_items;
+  std::vector<double*> d_ready;
+  if (same) {
+    for (int j = 0; j < jb.n_scales; ++j) {
+      if (!jb.out_same[0][j]) continue;
+      TuckerItem it;
+      it.in = jb.vin[0];
+      mats_for(Es[j], it.mats);
+      it.group = 1000 + j;
+      it.outs.push_back(Out{jb.out_same[0][j], 1.0, {}});
+      d_items.push_back(it);
+      d_ready.push_back(jb.out_same[0][j]);
+    }
+    if (p == 0) {
+      ex.batch(d_items, false);
+      if (!ex.ok()) return;
+      if (ex.on_outputs && !d_ready.empty()) ex.on_outputs(d_ready);
+      d_items.clear();
+      d_ready.clear();
+    }
+  }
+
+  // ---- state buffers ----
+  // state[j][ℓ] for the scale j (ℓ = 1..p)
+  std::vector<std::vector<double*>> state(s + 1, std::vector<double*>(p + 1, nullptr));
+  std::vector<double*> pool[2];
+  auto ws_state = [&](int j, int ell) -> double* {
+    auto& pl = pool[j % 2];
+    while (static_cast<int>(pl.size()) <= ell) pl.push_back(nullptr);
+    if (!pl[ell]) pl[ell] = ex.ar->alloc_doubles(N);
+    return pl[ell];
+  };
+  for (int j = 0; j <= s; ++j)
+    for (int ell = 1; ell <= p; ++ell) {
+      double* u = (same && j < jb.n_scales) ? jb.out_same[ell][j] : nullptr;
+      state[j][ell] = u ? u : ws_state(j, ell);
+    }
+
+  if (p >= 1) {
+    // ---- Stage B: quadrature at scale s ----
+    const double wq = w[q - 1];  // θ_q = 1 term: exp(0) = I, no Tucker operator (l.948-952)
+    std::vector<TuckerItem> items;
+    if (same) {
+      for (int i = 0; i < n_nodes; ++i) {
+        TuckerItem it;
+        it.in = jb.vin[0];
+        node_mats(i, it.mats);
+        it.group = 0;
+        for (int ell = 1; ell <= p; ++ell) {
+          Out o;
+          o.dst = state[s][ell];
+          o.beta = w[i] * std::pow(theta[i], ell - 1) / factorial(ell - 1);
+          if (i == 0)
+            o.srcs.push_back(Src{jb.vin[0], wq / factorial(ell - 1)});
+          else
+            o.srcs.push_back(Src{o.dst, 1.0});
+          it.outs.push_back(o);
+        }
+        items.push_back(it);
+      }
+    } else {
+      // Ψ_ℓ^{(s)} = Σ_i w_i E_i x_iℓ,  x_iℓ = Σ_{k=1}^ℓ θ_i^{ℓ−k}/(ℓ−k)! v_{p+1−k}/2^{(ℓ−k+1)s}
+      auto xcoef = [&](double th, int ell, int k) {
+        return std::pow(th, ell - k) / factorial(ell - k) / std::ldexp(1.0, (ell - k + 1) * s);
+      };
+      std::vector<Out> prep;
+      std::vector<std::vector<TuckerItem>> per_ell(p + 1);
+      for (int ell = 1; ell <= p; ++ell) {
+        bool first = true;
+        for (int i = 0; i < n_nodes; ++i) {
+          std::vector<Src> comb;
+          for (int k = 1; k <= ell; ++k) {
+            const double* v = jb.vin[p + 1 - k];
+            const double c = xcoef(theta[i], ell, k);
+            if (v && c != 0.0) comb.push_back(Src{v, c});
+          }
+          if (comb.empty()) continue;
+          TuckerItem it;
+          node_mats(i, it.mats);
+          it.group = ell;
+          if (comb.size() == 1) {
+            it.in = comb[0].ptr;
+            it.in_scale = comb[0].coef;
+          } else {
+            double* x = ex.ar->alloc_doubles(N);
+            prep.push_back(Out{x, 0.0, comb});
+            it.in = x;
+          }
+          Out o;
+          o.dst = state[s][ell];
+          o.beta = w[i];
+          if (first) {
+            for (int k = 1; k <= ell; ++k) {
+              const double* v = jb.vin[p + 1 - k];
+              if (v) o.srcs.push_back(Src{v, wq * xcoef(1.0, ell, k)});
+            }
+          } else {
+            o.srcs.push_back(Src{o.dst, 1.0});
+          }
+          it.outs.push_back(o);
+          first = false;
+          per_ell[ell].push_back(it);
+        }
+        if (first) {  // no node contributed: Ψ_ℓ = w_q x_qℓ
+          Out o{state[s][ell], 0.0, {}};
+          for (int k = 1; k <= ell; ++k) {
+            const double* v = jb.vin[p + 1 - k];
+            if (v) o.srcs.push_back(Src{v, wq * xcoef(1.0, ell, k)});
+          }
+          prep.push_back(o);
+          if (ell == p && s < jb.n_scales && jb.out_lin[s]) {
+            o.dst = jb.out_lin[s];
+            prep.push_back(o);
+          }
+        }
+      }
+      ex.combine(N, prep);
+      for (int ell = 1; ell <= p; ++ell)
+        for (auto& it : per_ell[ell]) items.push_back(it);
+      if (s < jb.n_scales && jb.out_lin[s]) {
+        // scale s output = Ψ_p^{(s)} (+ exp term later): mirror the Ψ_p accumulation
+        for (auto& it : items)
+          if (it.group == p) {
+            Out o = it.outs[0];
+            o.dst = jb.out_lin[s];
+            for (auto& sr : o.srcs)
+              if (sr.ptr == state[s][p]) sr.ptr = jb.out_lin[s];
+            it.outs.push_back(o);
+          }
+      }
+    }
+    for (auto& it : d_items) items.push_back(it);
+    ex.batch(items, ex.split >= 1);
+    if (!ex.ok()) return;
+    if (ex.on_outputs && !d_ready.empty()) ex.on_outputs(d_ready);
+    if (!ex.ok()) return;
+
+    // ---- Stage C: squaring, j = s..1 ----
+    for (int j = s; j >= 1; --j) {
+      std::vector<TuckerItem> sq;
+      for (int ell = p; ell >= 1; --ell) {
+        TuckerItem it;
+        it.in = state[j][ell];
+        mats_for(Es[j], it.mats);
+        it.group = ell;
+        Out o;
+        o.dst = state[j - 1][ell];
+        if (same) {
+          const double sc = std::ldexp(1.0, -ell);
+          o.beta = sc;
+          for (int k = 1; k <= ell; ++k) o.srcs.push_back(Src{state[j][k], sc / factorial(ell - k)});
+        } else {
+          o.beta = 1.0;
+          for (int k = 1; k <= ell; ++k)
+            o.srcs.push_back(Src{state[j][k], 1.0 / (factorial(ell - k) * std::ldexp(1.0, (ell - k) * j))});
+        }
+        it.outs.push_back(o);
+        if (!same && ell == p && (j - 1) < jb.n_scales && jb.out_lin[j - 1]) {
+          Out o2 = o;
+          o2.dst = jb.out_lin[j - 1];
+          it.outs.push_back(o2);
+        }
+        sq.push_back(it);
+      }
+      ex.batch(sq, ex.split >= 2);
+      if (!ex.ok()) return;
+    }
+  }
+
+  // ---- Stage D (linear combination): exp(τK/2^j)v_0 added to the result ----
+  std::vector<TuckerItem> ex_items;
+  if (!same) {
+    for (int j = 0; j < jb.n_scales; ++j) {
+      if (!jb.out_lin[j]) continue;
+      if (jb.vin[0]) {
+        TuckerItem it;
+        it.in = jb.vin[0];
+        mats_for(Es[j], it.mats);
+        it.group = j;
+        Out o{jb.out_lin[j], 1.0, {}};
+        if (p >= 1) o.srcs.push_back(Src{jb.out_lin[j], 1.0});
+        it.outs.push_back(o);
+        ex_items.push_back(it);
+      }
+    }
+  }
+  ex.batch(ex_items, false);
+}
+
+}  // namespace host
+}  // namespace phiks
