@@ -15,7 +15,7 @@ import pytest
 torch = pytest.importorskip("torch")
 
 pytestmark = pytest.mark.gpu
-CTRL = 4096  # first pooled tensor of the region (phiks_api.cpp kCtrlBytes)
+CTRL = 4096  # first pooled tensor of the region (csrc/host.h kCtrlBytes)
 
 
 def _cudart():
