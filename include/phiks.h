@@ -49,6 +49,7 @@ typedef enum {
 #define PHIKS_MAX_P 6       /* highest φ order ℓ                                     */
 #define PHIKS_MAX_SCALES 16 /* output time scales ŝ                                  */
 #define PHIKS_MAX_N 4096    /* largest n_μ                                           */
+#define PHIKS_MAX_BLOCKS 4  /* diagonal blocks of K̂ per handle (phiks_create_blocks)   */
 
 typedef enum {
   /* φ_ℓ(τK/2^j) v for every ℓ in `ells`, j = 0..n_scales-1, one vector v
@@ -110,6 +111,8 @@ typedef struct {
   double mode_product_flops;      /* algorithmic flops of those launches (2·rows·n²) */
   int64_t expm_launches;          /* small-GEMM launches of the exponential stage   */
   double expm_ms;                 /* sum of their event-measured durations (ms)     */
+  int nblocks;                    /* diagonal blocks of the handle                  */
+  phiks_plan_info block_plan[PHIKS_MAX_BLOCKS]; /* plan of each block, last apply   */
 } phiks_stats;
 
 /* Create a handle for K = A_d ⊕ … ⊕ A_1.
@@ -124,6 +127,18 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
 /* Block until the last apply on h (its kernels and host copies) has finished;
    reports a cross-rank barrier timeout of a sharded handle as PHIKS_ERR_CUDA. */
 phiks_status phiks_wait(phiks_handle h);
+
+/* Block-diagonal K̂ = diag(K_1, …, K_nb), K_b = A_{b,d} ⊕ … ⊕ A_{b,1} (PAPER.md
+   §4.4: one Kronecker sum per species of a reaction–diffusion system), all
+   blocks with the dims n[0..d-1]; A_host[b*d + μ] is block b's factor A_{b,μ}
+   (1 ≤ nblocks ≤ PHIKS_MAX_BLOCKS).  phiks_apply then takes the vectors of
+   every block, block-major (same vector: vecs[b]; lincomb: vecs[b*n_ells + i])
+   and writes every block's outputs block-major (outs[b*per_block + k], per_block
+   as for one block).  Each block gets its own §3.3 plan; the blocks share the
+   exponential stage and their Tucker operators run in the same launches
+   (phase by phase).  phiks_stats.block_plan holds the per-block plans. */
+phiks_status phiks_create_blocks(int nblocks, int d, const int* n, const double* const* A_host,
+                                 phiks_handle* out);
 
 /* Complex K (§4.1 validates PHIKS on the complex operator
    (1+i)/100·Δ): as phiks_create, but A_host[μ] points to an n[μ]×n[μ]
@@ -255,6 +270,10 @@ phiks_status phiks_select_plan(int mode, double center_re, double center_im, dou
    phiks_get_stats / host-memory applies). */
 phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_host, int rank, int world,
                                   phiks_handle* out);
+
+/* Sharded handle of a block-diagonal K̂ (phiks_create_blocks × phiks_create_sharded). */
+phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const double* const* A_host, int rank,
+                                         int world, phiks_handle* out);
 
 /* rank, world, local slab size in doubles, bytes of the symmetric region
    (any output pointer may be NULL). */

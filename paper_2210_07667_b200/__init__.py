@@ -55,15 +55,24 @@ def version() -> str:
 class PhiKS:
     """Handle on K = A_d ⊕ … ⊕ A_1 (phiks_create / phiks_destroy)."""
 
-    def __init__(self, factors: Sequence[np.ndarray], rank: int = 0, world: int = 1):
+    def __init__(self, factors: Sequence, rank: int = 0, world: int = 1):
+        """factors: [A_1, …, A_d] for K = A_d ⊕ … ⊕ A_1, or a list of such lists
+        for a block-diagonal K̂ = diag(K_1, …, K_nb) (§4.4; every block
+        with the same dims; vectors and outputs are then given block-major)."""
         lib = _lib.load()
-        self.d = len(factors)
-        self.dims = tuple(int(np.asarray(a).shape[0]) for a in factors)
+        blocks = [list(f) for f in factors] if (len(factors) and not hasattr(factors[0], "shape")
+                                                 and isinstance(factors[0], (list, tuple))) else [list(factors)]
+        self.nblocks = len(blocks)
+        self.d = len(blocks[0])
+        self.dims = tuple(int(np.asarray(a).shape[0]) for a in blocks[0])
         self.rank, self.world = int(rank), int(world)
         # complex factors (PAPER.md §4.1's validation operator is complex): complex128 throughout
-        self.complex = any(np.iscomplexobj(a) for a in factors)
+        self.complex = any(np.iscomplexobj(a) for blk in blocks for a in blk)
         dt = np.complex128 if self.complex else np.float64
-        self._A = [np.asfortranarray(np.asarray(a, dtype=dt)) for a in factors]
+        self._A = [np.asfortranarray(np.asarray(a, dtype=dt)) for blk in blocks for a in blk]
+        for blk in blocks:
+            if len(blk) != self.d or tuple(int(np.asarray(a).shape[0]) for a in blk) != self.dims:
+                raise ValueError("every block needs the same dims")
         for a in self._A:
             if a.ndim != 2 or a.shape[0] != a.shape[1]:
                 raise ValueError("factor matrices must be square")
@@ -71,14 +80,14 @@ class PhiKS:
         a_arr = _lib.ptr_array([a.ctypes.data for a in self._A])
         h = ctypes.c_void_p()
         if self.complex:
-            if self.world != 1:
-                raise ValueError("complex factors are not supported on sharded handles")
+            if self.world != 1 or self.nblocks != 1:
+                raise ValueError("complex factors: one block, not sharded")
             _lib.check(lib.phiks_create_complex(self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create_complex")
         elif self.world == 1:
-            _lib.check(lib.phiks_create(self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create")
+            _lib.check(lib.phiks_create_blocks(self.nblocks, self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create")
         else:
-            _lib.check(lib.phiks_create_sharded(self.d, n_arr, a_arr, self.rank, self.world, ctypes.byref(h)),
-                       "phiks_create_sharded")
+            _lib.check(lib.phiks_create_sharded_blocks(self.nblocks, self.d, n_arr, a_arr, self.rank, self.world,
+                                                       ctypes.byref(h)), "phiks_create_sharded")
         self._h = h
         # N: elements of the tensors apply() takes (the local slab when sharded)
         self.N = int(np.prod(self.dims)) // self.world
@@ -126,7 +135,7 @@ class PhiKS:
         lib = _lib.load()
         m = self._mode(mode)
         host = isinstance(vecs[0], np.ndarray)
-        nouts = len(ells) * n_scales if m == MODE_SAME_VECTOR else n_scales
+        nouts = self.nblocks * (len(ells) * n_scales if m == MODE_SAME_VECTOR else n_scales)
         dt = np.complex128 if self.complex else np.float64
         if host:
             vecs = [np.ascontiguousarray(np.asarray(v, dtype=dt).reshape(-1, order="F")) for v in vecs]
@@ -165,7 +174,8 @@ class PhiKS:
                 "workspace_bytes": st.workspace_bytes, "total_kernel_launches": st.total_kernel_launches,
                 "mode_product_launches": st.mode_product_launches, "mode_product_ms": st.mode_product_ms,
                 "mode_product_flops": st.mode_product_flops, "expm_launches": st.expm_launches,
-                "expm_ms": st.expm_ms}
+                "expm_ms": st.expm_ms,
+                "block_plans": [(st.block_plan[b].s, st.block_plan[b].q) for b in range(max(st.nblocks, 1))]}
 
     def set_profiling(self, on: bool = True):
         _lib.check(_lib.load().phiks_set_profiling(self._h, 1 if on else 0), "phiks_set_profiling")

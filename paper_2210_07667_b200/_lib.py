@@ -16,7 +16,7 @@ MODE_LINCOMB = 1
 MEM_DEVICE = 0
 MEM_HOST = 1
 MEM_HOST_ASYNC = 2
-MAX_D, MAX_P, MAX_SCALES, MAX_N = 8, 6, 16, 4096
+MAX_D, MAX_P, MAX_SCALES, MAX_N, MAX_BLOCKS = 8, 6, 16, 4096, 4
 IPC_HANDLE_BYTES = 64
 MAX_RANKS = 8
 
@@ -47,7 +47,7 @@ class Stats(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_size_t), ("total_kernel_launches", ctypes.c_int64),
                 ("mode_product_launches", ctypes.c_int64), ("mode_product_ms", ctypes.c_double),
                 ("mode_product_flops", ctypes.c_double), ("expm_launches", ctypes.c_int64),
-                ("expm_ms", ctypes.c_double)]
+                ("expm_ms", ctypes.c_double), ("nblocks", ctypes.c_int), ("block_plan", PlanInfo * 4)]
 
 
 _lib = None
@@ -77,6 +77,8 @@ def load() -> ctypes.CDLL:
     lib.phiks_select_plan.argtypes = [i, d, d, d, d, i, P(d), d, i, i, i, P(PlanInfo)]
     lib.phiks_set_profiling.argtypes = [vp, i]
     lib.phiks_create_sharded.argtypes = [i, P(i), P(vp), i, i, P(vp)]
+    lib.phiks_create_blocks.argtypes = [i, i, P(i), P(vp), P(vp)]
+    lib.phiks_create_sharded_blocks.argtypes = [i, i, P(i), P(vp), i, i, P(vp)]
     lib.phiks_shard_info.argtypes = [vp, P(i), P(i), P(ctypes.c_int64), P(ctypes.c_size_t)]
     lib.phiks_shard_ipc_handle.argtypes = [vp, vp]
     lib.phiks_shard_open_peers.argtypes = [vp, vp]
@@ -94,7 +96,8 @@ def load() -> ctypes.CDLL:
                  "phiks_get_stats", "phiks_mode_product", "phiks_tucker", "phiks_expm",
                  "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan", "phiks_set_profiling",
                  "phiks_create_sharded", "phiks_shard_info", "phiks_shard_ipc_handle", "phiks_shard_open_peers",
-                 "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_shard_layout", "phiks_wait", "phiks_shard_peer_base", "phiks_create_complex", "phiks_plan_host_complex"):
+                 "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_shard_layout", "phiks_wait", "phiks_shard_peer_base", "phiks_create_complex", "phiks_plan_host_complex", "phiks_create_blocks",
+                 "phiks_create_sharded_blocks"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -66,8 +66,10 @@ struct PlanKey {
   int mode, p, n_scales;
   double tau, tol;
   std::vector<double> norms;
+  int block;
   bool operator<(const PlanKey& o) const {
-    return std::tie(mode, p, n_scales, tau, tol, norms) < std::tie(o.mode, o.p, o.n_scales, o.tau, o.tol, o.norms);
+    return std::tie(mode, p, n_scales, tau, tol, norms, block) <
+           std::tie(o.mode, o.p, o.n_scales, o.tau, o.tol, o.norms, o.block);
   }
 };
 }  // namespace host
@@ -83,7 +85,10 @@ struct phiks_ctx {
   int64_t Nc = 0;  // elements per tensor
   bool cplx = false;  // complex factors and tensors (interleaved re, im)
   std::vector<Factor> factors;
-  int fac_of_mode[PHIKS_MAX_D] = {0};
+  // block-diagonal K̂ = diag(K_1, …, K_nb) (§4.4): every block has
+  // the dims n[] and its own factors; fac_of_block[b][μ] indexes `factors`
+  int nblocks = 1;
+  int fac_of_block[kMaxBlocks][PHIKS_MAX_D] = {{0}};
   void* ws_own = nullptr;
   size_t ws_own_bytes = 0;
   double* h_pinned = nullptr;  // pinned host scratch (norms)
@@ -137,7 +142,7 @@ constexpr size_t kCtrlFlags = 0;                                   // uint64 fla
 constexpr size_t kCtrlErr = kMaxRanks * sizeof(uint64_t);          // int err
 constexpr size_t kCtrlEpoch = 128;                                 // uint64 barrier count
 constexpr size_t kCtrlNorms = 256;                                 // double norms[2][kMaxRanks][kMaxVecs]
-constexpr size_t kCtrlNormsBuf = kMaxRanks * kMaxVecs * sizeof(double);
+constexpr size_t kCtrlNormsBuf = kMaxRanks * kMaxBlocks * kMaxVecs * sizeof(double);
 constexpr size_t kCtrlBytes = 4096;
 static_assert(kCtrlNorms + 2 * kCtrlNormsBuf <= kCtrlBytes, "control block layout");
 static_assert(kCtrlErr + sizeof(int) <= kCtrlEpoch && kCtrlEpoch + 8 <= kCtrlNorms, "control block layout");
@@ -743,17 +748,19 @@ struct Job {
   int n_scales;
   double tau;
   int s, q;
+  int block = 0;  // which factor set (fac_of_block) the job's Kronecker sum uses
   const double* vin[kMaxVecs] = {nullptr};
   double* out_same[kMaxVecs][PHIKS_MAX_SCALES] = {{nullptr}};
   double* out_lin[PHIKS_MAX_SCALES] = {nullptr};
 };
 
-void run_job(Exec& ex, const Job& jb);
+// the jobs of all blocks of one apply, their Tucker batches merged phase by phase
+void run_jobs(Exec& ex, const std::vector<Job>& jobs);
 
 // defined in phiks_api.cpp
 phiks_status validate(phiks_handle h, const phiks_request* req, int& p);
 phiks_status make_plan(phiks_handle h, const phiks_request* req, int p, const std::vector<double>& norms,
-                       plan::Plan& out);
+                       plan::Plan& out, int block = 0);
 phiks_status check_barrier_flag(phiks_handle h);
 
 // One apply on one handle, split into phases so that several emulated ranks
@@ -762,6 +769,7 @@ struct ApplyRun {
   phiks_handle h = nullptr;
   const phiks_request* req = nullptr;
   int p = 0, n_vecs = 0, nouts = 0;
+  int nb = 1, vpb = 1, opb = 1;  // blocks; vectors and outputs per block (block-major arrays)
   bool same = true, host_mem = false, host_async = false, size_only = false;
   const double* const* vecs = nullptr;
   double* const* outs = nullptr;
@@ -770,14 +778,14 @@ struct ApplyRun {
   size_t tbytes = 0;
   Arena ar;
   Exec ex{};
-  Job jb{};
+  std::vector<Job> jobs;
   std::vector<double*> dv, dout;
-  plan::Plan pl;
+  std::vector<plan::Plan> pls;
   int split = 2;
   // lincomb norms
   bool need_norms = false;
-  std::vector<int> which;        // index into vecs of v_1..v_p present
-  double* nscratch = nullptr;    // device: 1024*kMaxVecs partials + kMaxVecs norms²
+  std::vector<std::pair<int, int>> which;  // (block, index into the block's vectors) of v_1..v_p present
+  double* nscratch = nullptr;    // device: 1024*kMaxVecs partials + the norms²
   std::vector<double*> ntmp;     // host-memory inputs staged for the norms
   int norm_launches = 0;
   size_t norm_off = kCtrlNorms;  // this apply's norm-slot buffer in the control block
@@ -793,9 +801,12 @@ struct ApplyRun {
     outs = outs_;
     size_only = size_only_;
     same = req->mode == PHIKS_MODE_SAME_VECTOR;
-    nouts = same ? req->n_ells * req->n_scales : req->n_scales;
+    nb = h->nblocks;
+    vpb = same ? 1 : req->n_ells;
+    opb = same ? req->n_ells * req->n_scales : req->n_scales;
+    nouts = nb * opb;
     if (!size_only) {
-      if (same ? n_vecs != 1 : n_vecs != req->n_ells) return fail(PHIKS_ERR_ARG, "n_vecs");
+      if (n_vecs != nb * vpb) return fail(PHIKS_ERR_ARG, "n_vecs");
       if (!vecs || !outs) return fail(PHIKS_ERR_ARG, "null vecs/outs");
       for (int i = 0; i < n_vecs; ++i)
         if (!vecs[i]) return fail(PHIKS_ERR_ARG, "null vector");
@@ -815,47 +826,58 @@ struct ApplyRun {
       return e ? atoi(e) : 2;
     }();
     split = split_mode;
-    jb.mode = req->mode;
-    jb.p = p;
-    jb.n_scales = req->n_scales;
-    jb.tau = req->tau;
-    if (size_only) dv.assign(same ? 1 : req->n_ells, nullptr);
-    else dv.assign(n_vecs > 0 ? n_vecs : 0, nullptr);
+    jobs.assign(nb, Job{});
+    for (int b = 0; b < nb; ++b) {
+      jobs[b].mode = req->mode;
+      jobs[b].p = p;
+      jobs[b].n_scales = req->n_scales;
+      jobs[b].tau = req->tau;
+      jobs[b].block = b;
+    }
+    pls.assign(nb, plan::Plan{});
+    dv.assign(nb * vpb, nullptr);
     dout.assign(nouts, nullptr);
     need_norms = !same && p >= 1 && req->force_s < 0 && !size_only;
     return PHIKS_OK;
   }
 
-  // ---- lincomb plan input: ||v_ℓ||₂ (deterministic GPU reduction; sharded:
-  // local sums of squares scattered to every rank, summed in rank order) ----
+  // ---- lincomb plan input: ||v_ℓ||₂ of every block (deterministic GPU
+  // reduction; sharded: local sums of squares scattered to every rank, summed
+  // in rank order) ----
   phiks_status norms_enqueue(bool do_barrier) {
     if (!need_norms) return PHIKS_OK;
     std::vector<const double*> vv;
-    for (int ell = 1; ell <= p; ++ell)
-      for (int i = 0; i < req->n_ells; ++i)
-        if (req->ells[i] == ell) which.push_back(i);
+    for (int b = 0; b < nb; ++b)
+      for (int ell = 1; ell <= p; ++ell)
+        for (int i = 0; i < req->n_ells; ++i)
+          if (req->ells[i] == ell) which.emplace_back(b, i);
     if (which.empty()) return PHIKS_OK;
-    const size_t sbytes = sizeof(double) * (1024 * kMaxVecs + kMaxVecs);
+    const int nv = static_cast<int>(which.size());
+    const size_t sbytes = sizeof(double) * (1024 * kMaxVecs + nv);
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&nscratch), sbytes, cs));
-    for (size_t k = 0; k < which.size(); ++k) {
+    for (const auto& bi : which) {
+      const double* src = vecs[bi.first * vpb + bi.second];
       if (host_mem) {
         double* t = nullptr;
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&t), tbytes, cs));
-        CUDA_TRY(cudaMemcpyAsync(t, vecs[which[k]], tbytes, cudaMemcpyHostToDevice, cs));
+        CUDA_TRY(cudaMemcpyAsync(t, src, tbytes, cudaMemcpyHostToDevice, cs));
         ntmp.push_back(t);
         vv.push_back(t);
       } else {
-        vv.push_back(vecs[which[k]]);
+        vv.push_back(src);
       }
     }
-    CUDA_TRY(launch_sumsq(vv.data(), static_cast<int>(vv.size()), N, nscratch, nscratch + 1024 * kMaxVecs, cs));
-    norm_launches = 2;
+    for (int k0 = 0; k0 < nv; k0 += kMaxVecs) {
+      const int cnt = std::min(kMaxVecs, nv - k0);
+      CUDA_TRY(launch_sumsq(vv.data() + k0, cnt, N, nscratch, nscratch + 1024 * kMaxVecs + k0, cs));
+      norm_launches += 2;
+    }
     if (h->sharded()) {
       norm_off = kCtrlNorms + (h->norm_phase++ & 1) * kCtrlNormsBuf;
       ScatterParams sp{};
       sp.rank = h->rank;
       sp.world = h->world;
-      sp.cnt = static_cast<int>(which.size());
+      sp.cnt = nv;
       sp.src = nscratch + 1024 * kMaxVecs;
       for (int k = 0; k < h->world; ++k) sp.dst[k] = reinterpret_cast<double*>(h->peer[k] + norm_off);
       CUDA_TRY(launch_scatter_small(sp, cs));
@@ -870,16 +892,17 @@ struct ApplyRun {
     }
     return PHIKS_OK;
   }
-  // read back (synchronises the stream) and plan; `ctrl` = the control block
-  // holding the gathered partial sums (sharded) — any rank's, they are equal
+  // read back (synchronises the stream) and plan every block; `ctrl` = the
+  // control block holding the gathered partial sums (sharded) — any rank's
   phiks_status norms_finish(const char* ctrl) {
-    std::vector<double> norms(p, 0.0);
+    std::vector<std::vector<double>> norms(nb, std::vector<double>(p, 0.0));
     if (!which.empty()) {
       const int nv = static_cast<int>(which.size());
       const int W = h->sharded() ? h->world : 1;
+      std::vector<double> host(static_cast<size_t>(nv) * W);
       const double* srcp = h->sharded() ? reinterpret_cast<const double*>(ctrl + norm_off)
                                         : nscratch + 1024 * kMaxVecs;
-      CUDA_TRY(cudaMemcpyAsync(h->h_pinned, srcp, sizeof(double) * nv * W, cudaMemcpyDeviceToHost, cs));
+      CUDA_TRY(cudaMemcpyAsync(host.data(), srcp, sizeof(double) * nv * W, cudaMemcpyDeviceToHost, cs));
       for (double* t : ntmp) CUDA_TRY(cudaFreeAsync(t, cs));
       ntmp.clear();
       CUDA_TRY(cudaFreeAsync(nscratch, cs));
@@ -887,23 +910,33 @@ struct ApplyRun {
       CUDA_TRY(cudaStreamSynchronize(cs));
       for (int k = 0; k < nv; ++k) {
         double s2 = 0.0;
-        for (int r = 0; r < W; ++r) s2 += h->h_pinned[r * nv + k];
-        norms[req->ells[which[k]] - 1] = std::sqrt(s2);
+        for (int r = 0; r < W; ++r) s2 += host[static_cast<size_t>(r) * nv + k];
+        norms[which[k].first][req->ells[which[k].second] - 1] = std::sqrt(s2);
       }
     }
-    return make_plan(h, req, p, norms, pl);
+    for (int b = 0; b < nb; ++b) {
+      phiks_status st = make_plan(h, req, p, norms[b], pls[b], b);
+      if (st != PHIKS_OK) return st;
+    }
+    return PHIKS_OK;
   }
 
   phiks_status plan_direct(const phiks_plan_info* forced) {
     if (forced) {
-      pl.s = forced->s;
-      pl.q = forced->q;
-      pl.ok = true;
+      for (auto& pl : pls) {
+        pl.s = forced->s;
+        pl.q = forced->q;
+        pl.ok = true;
+      }
       return PHIKS_OK;
     }
     if (!same && p >= 1 && req->force_s < 0 && size_only) return fail(PHIKS_ERR_ARG, "lincomb sizing needs a plan");
     std::vector<double> norms;
-    return make_plan(h, req, p, norms, pl);
+    for (int b = 0; b < nb; ++b) {
+      phiks_status st = make_plan(h, req, p, norms, pls[b], b);
+      if (st != PHIKS_OK) return st;
+    }
+    return PHIKS_OK;
   }
 
   void bind(bool measure) {
@@ -915,25 +948,32 @@ struct ApplyRun {
     auto fake = [](int k) { return reinterpret_cast<double*>(static_cast<uintptr_t>(0x7f0000000000ULL) + 4096ULL * k); };
     for (int i = 0; i < static_cast<int>(dv.size()); ++i)
       dv[i] = host_mem ? ar.alloc_doubles(N) : (size_only ? fake(i) : const_cast<double*>(vecs[i]));
-    for (int i = 0; i < nouts; ++i) dout[i] = host_mem ? ar.alloc_doubles(N) : (size_only ? fake(64 + i) : outs[i]);
-    for (int i = 0; i < kMaxVecs; ++i) jb.vin[i] = nullptr;
-    if (same) {
-      jb.vin[0] = dv.empty() ? nullptr : dv[0];
-      for (int j = 0; j < req->n_scales; ++j)
-        for (int i = 0; i < req->n_ells; ++i) jb.out_same[req->ells[i]][j] = dout[j * req->n_ells + i];
-    } else {
-      for (int i = 0; i < req->n_ells; ++i) jb.vin[req->ells[i]] = dv.empty() ? nullptr : dv[i];
-      for (int j = 0; j < req->n_scales; ++j) jb.out_lin[j] = dout[j];
+    for (int i = 0; i < nouts; ++i) dout[i] = host_mem ? ar.alloc_doubles(N) : (size_only ? fake(256 + i) : outs[i]);
+    for (int b = 0; b < nb; ++b) {
+      Job& jb = jobs[b];
+      for (int i = 0; i < kMaxVecs; ++i) jb.vin[i] = nullptr;
+      const double* const* bv = dv.data() + b * vpb;
+      double* const* bo = dout.data() + b * opb;
+      if (same) {
+        jb.vin[0] = bv[0];
+        for (int j = 0; j < req->n_scales; ++j)
+          for (int i = 0; i < req->n_ells; ++i) jb.out_same[req->ells[i]][j] = bo[j * req->n_ells + i];
+      } else {
+        for (int i = 0; i < req->n_ells; ++i) jb.vin[req->ells[i]] = bv[i];
+        for (int j = 0; j < req->n_scales; ++j) jb.out_lin[j] = bo[j];
+      }
     }
   }
 
   phiks_status measure(size_t* need) {
-    jb.s = pl.s;
-    jb.q = pl.q;
+    for (int b = 0; b < nb; ++b) {
+      jobs[b].s = pls[b].s;
+      jobs[b].q = pls[b].q;
+    }
     ex = Exec{h, cs, true, &ar};
     ex.split = split;
     bind(true);
-    run_job(ex, jb);
+    run_jobs(ex, jobs);
     if (!ex.ok()) return ex.status;
     *need = ar.off;
     return PHIKS_OK;
@@ -1018,7 +1058,7 @@ struct ApplyRun {
       copied.assign(nouts, false);
       ex.on_outputs = [this](const std::vector<double*>& ready) { copy_out(ready); };
     }
-    run_job(ex, jb);
+    run_jobs(ex, jobs);
     ex.st = cs;
     if (!ex.ok()) return ex.status;
     if (host_mem) {
@@ -1047,9 +1087,19 @@ struct ApplyRun {
 
   void finish_stats(size_t need) {
     phiks_stats& S = h->stats;
-    S.plan.s = pl.s;
-    S.plan.q = pl.q;
-    S.plan.T_formula = plan::tucker_count(req->mode, pl.s, req->n_scales, pl.q, p);
+    S.plan.s = pls[0].s;
+    S.plan.q = pls[0].q;
+    S.plan.T_formula = plan::tucker_count(req->mode, pls[0].s, req->n_scales, pls[0].q, p);
+    S.nblocks = nb;
+    for (int b = 0; b < kMaxBlocks; ++b) {
+      S.block_plan[b] = phiks_plan_info{};
+      if (b < nb) {
+        S.block_plan[b].s = pls[b].s;
+        S.block_plan[b].q = pls[b].q;
+        S.block_plan[b].T_formula = plan::tucker_count(req->mode, pls[b].s, req->n_scales, pls[b].q, p);
+        S.block_plan[b].T_executed = -1;
+      }
+    }
     S.plan.T_executed = static_cast<int>(ex.tucker_ops);
     S.kernel_launches = ex.launches + norm_launches;
     S.tucker_ops = ex.tucker_ops;

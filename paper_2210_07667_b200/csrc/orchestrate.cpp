@@ -128,62 +128,101 @@ void expm_batch(Exec& ex, double tau, std::vector<ExpReq>& reqs) {
 // vin[ℓ] (ℓ = 0..p) device input tensors or nullptr; out_same[ℓ][j] / out_lin[j]
 // device output tensors or nullptr (not requested).
 // ---------------------------------------------------------------------------
-void run_job(Exec& ex, const Job& jb) {
+// All blocks' jobs of one apply (one job per diagonal block of K̂, PAPER.md
+// §4.4; a single job for an ordinary handle).  Each job follows PAPER.md §3
+// with its own plan (s_b, q_b); their exponential requests form one stage A
+// and their Tucker operators are merged phase by phase into the same batches
+// (quadrature, then squaring level j for every job with s_b ≥ j, then the
+// exp-action terms), so the blocks share launches.
+void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
   phiks_ctx* h = ex.h;
   const int d = h->d;
-  const int p = jb.p, s = jb.s, q = jb.q;
   const int64_t N = h->N;
+  const int nj = static_cast<int>(jobs.size());
+  if (nj == 0) return;
+  const int p = jobs[0].p;
+  const bool same = jobs[0].mode == PHIKS_MODE_SAME_VECTOR;
+  const double tau = jobs[0].tau;
+
+  struct JS {
+    const Job* jb;
+    int s, q, jmin, n_nodes, gbase;
+    std::vector<double> theta, w;
+    std::vector<int> facs;  // distinct factor indices of the block
+    size_t req0;            // first stage-A request of this job
+    std::vector<std::vector<const double*>> nodeE;  // [i][f]
+    std::vector<std::vector<double*>> Es;           // [j][f]
+    std::vector<std::vector<double*>> state;        // [j][ℓ]
+    std::vector<double*> pool[2];
+  };
   const int nf = static_cast<int>(h->factors.size());
-  const bool same = jb.mode == PHIKS_MODE_SAME_VECTOR;
-
-  // ---- which level matrices exp(τA/2^j) are needed ----
-  bool want_phi0 = false;
-  if (same) {
-    for (int j = 0; j < jb.n_scales; ++j) want_phi0 |= jb.out_same[0][j] != nullptr;
-  } else {
-    want_phi0 = jb.vin[0] != nullptr;
-  }
-  int jmin = s;
-  if (p >= 1) jmin = std::min(jmin, 1);
-  if (want_phi0) jmin = 0;
-  if (p >= 1 && s == 0) jmin = 0;
-
-  std::vector<double> theta, w;
-  if (p >= 1) plan::gll_rule(q, theta, w);
-
-  // ---- Stage A ----
+  std::vector<JS> js(nj);
   std::vector<ExpReq> reqs;
-  // node exponentials (θ_i ≠ 1): c_i = (1 − θ_i)/2^s; node 0 (θ = 0) gives exp(τA/2^s)
-  const int n_nodes = (p >= 1) ? q - 1 : 0;
-  for (int i = 0; i < n_nodes; ++i)
-    for (int f = 0; f < nf; ++f) reqs.push_back({f, (1.0 - theta[i]) / std::ldexp(1.0, s)});
-  if (p == 0)
-    for (int f = 0; f < nf; ++f) reqs.push_back({f, 1.0 / std::ldexp(1.0, s)});
-  expm_batch(ex, jb.tau, reqs);
+  for (int b = 0; b < nj; ++b) {
+    JS& J = js[b];
+    const Job& jb = jobs[b];
+    J.jb = &jb;
+    J.s = jb.s;
+    J.q = jb.q;
+    J.gbase = 10000 * b;  // epilogue groups of different jobs never merge
+    // ---- which level matrices exp(τA/2^j) are needed ----
+    bool want_phi0 = false;
+    if (same) {
+      for (int j = 0; j < jb.n_scales; ++j) want_phi0 |= jb.out_same[0][j] != nullptr;
+    } else {
+      want_phi0 = jb.vin[0] != nullptr;
+    }
+    J.jmin = J.s;
+    if (p >= 1) J.jmin = std::min(J.jmin, 1);
+    if (want_phi0) J.jmin = 0;
+    if (p >= 1 && J.s == 0) J.jmin = 0;
+    if (p >= 1) plan::gll_rule(J.q, J.theta, J.w);
+    J.n_nodes = (p >= 1) ? J.q - 1 : 0;
+    for (int mu = 0; mu < d; ++mu) {
+      const int f = h->fac_of_block[jb.block][mu];
+      if (std::find(J.facs.begin(), J.facs.end(), f) == J.facs.end()) J.facs.push_back(f);
+    }
+    // ---- Stage A requests: node exponentials (θ_i ≠ 1): c_i = (1 − θ_i)/2^s;
+    // node 0 (θ = 0) gives exp(τA/2^s) ----
+    J.req0 = reqs.size();
+    for (int i = 0; i < J.n_nodes; ++i)
+      for (int f : J.facs) reqs.push_back({f, (1.0 - J.theta[i]) / std::ldexp(1.0, J.s)});
+    if (p == 0)
+      for (int f : J.facs) reqs.push_back({f, 1.0 / std::ldexp(1.0, J.s)});
+  }
+  expm_batch(ex, tau, reqs);
   if (!ex.ok()) return;
-  // nodeE[i][f]
-  std::vector<std::vector<const double*>> nodeE(n_nodes, std::vector<const double*>(nf));
-  for (int i = 0; i < n_nodes; ++i)
-    for (int f = 0; f < nf; ++f) nodeE[i][f] = reqs[static_cast<size_t>(i) * nf + f].result;
-  // level matrices Es[j][f], j = jmin..s
-  std::vector<std::vector<double*>> Es(s + 1, std::vector<double*>(nf, nullptr));
-  for (int f = 0; f < nf; ++f)
-    Es[s][f] = (p >= 1) ? const_cast<double*>(nodeE[0][f]) : reqs[f].result;
-  for (int j = s; j > jmin; --j) {
+  int max_lev = 0;
+  for (JS& J : js) {
+    const size_t nfb = J.facs.size();
+    J.nodeE.assign(J.n_nodes, std::vector<const double*>(nf, nullptr));
+    for (int i = 0; i < J.n_nodes; ++i)
+      for (size_t k = 0; k < nfb; ++k) J.nodeE[i][J.facs[k]] = reqs[J.req0 + i * nfb + k].result;
+    J.Es.assign(J.s + 1, std::vector<double*>(nf, nullptr));
+    for (size_t k = 0; k < nfb; ++k)
+      J.Es[J.s][J.facs[k]] = (p >= 1) ? const_cast<double*>(J.nodeE[0][J.facs[k]]) : reqs[J.req0 + k].result;
+    max_lev = std::max(max_lev, J.s - J.jmin);
+  }
+  // level matrices Es[j] = Es[j+1]², j = s_b−1..jmin_b: the k-th squaring of every job in one batch
+  for (int k = 0; k < max_lev; ++k) {
     std::map<int, std::vector<Exec::LaunchTerm>> byn;
-    for (int f = 0; f < nf; ++f) {
-      const int n = h->factors[f].n;
-      Es[j - 1][f] = ex.ar->alloc_doubles(static_cast<int64_t>(n) * n);
-      auto& v = byn[n];
-      v.push_back({Es[j][f], Es[j][f], static_cast<int>(v.size()), {Out{Es[j - 1][f], 1.0, {}}}});
+    for (JS& J : js) {
+      const int j = J.s - k;
+      if (j <= J.jmin) continue;
+      for (int f : J.facs) {
+        const int n = h->factors[f].n;
+        J.Es[j - 1][f] = ex.ar->alloc_doubles(static_cast<int64_t>(n) * n);
+        auto& v = byn[n];
+        v.push_back({J.Es[j][f], J.Es[j][f], static_cast<int>(v.size()), {Out{J.Es[j - 1][f], 1.0, {}}}});
+      }
     }
     for (auto& kv : byn) ex.gemm_batch(kv.first, kv.second);
   }
-  auto mats_for = [&](const std::vector<double*>& perf, const double** mats) {
-    for (int mu = 0; mu < d; ++mu) mats[mu] = perf[h->fac_of_mode[mu]];
+  auto mats_for = [&](const JS& J, const std::vector<double*>& perf, const double** mats) {
+    for (int mu = 0; mu < d; ++mu) mats[mu] = perf[h->fac_of_block[J.jb->block][mu]];
   };
-  auto node_mats = [&](int i, const double** mats) {
-    for (int mu = 0; mu < d; ++mu) mats[mu] = nodeE[i][h->fac_of_mode[mu]];
+  auto node_mats = [&](const JS& J, int i, const double** mats) {
+    for (int mu = 0; mu < d; ++mu) mats[mu] = J.nodeE[i][h->fac_of_block[J.jb->block][mu]];
   };
 
   // inputs staged from host memory are needed from here on (stage A overlaps their copy)
@@ -196,15 +235,18 @@ void run_job(Exec& ex, const Job& jb) {
   std::vector<TuckerItem> d_items;
   std::vector<double*> d_ready;
   if (same) {
-    for (int j = 0; j < jb.n_scales; ++j) {
-      if (!jb.out_same[0][j]) continue;
-      TuckerItem it;
-      it.in = jb.vin[0];
-      mats_for(Es[j], it.mats);
-      it.group = 1000 + j;
-      it.outs.push_back(Out{jb.out_same[0][j], 1.0, {}});
-      d_items.push_back(it);
-      d_ready.push_back(jb.out_same[0][j]);
+    for (JS& J : js) {
+      const Job& jb = *J.jb;
+      for (int j = 0; j < jb.n_scales; ++j) {
+        if (!jb.out_same[0][j]) continue;
+        TuckerItem it;
+        it.in = jb.vin[0];
+        mats_for(J, J.Es[j], it.mats);
+        it.group = J.gbase + 1000 + j;
+        it.outs.push_back(Out{jb.out_same[0][j], 1.0, {}});
+        d_items.push_back(it);
+        d_ready.push_back(jb.out_same[0][j]);
+      }
     }
     if (p == 0) {
       ex.batch(d_items, false);
@@ -215,147 +257,164 @@ void run_job(Exec& ex, const Job& jb) {
     }
   }
 
-  // ---- state buffers ----
-  // state[j][ℓ] for the scale j (ℓ = 1..p)
-  std::vector<std::vector<double*>> state(s + 1, std::vector<double*>(p + 1, nullptr));
-  std::vector<double*> pool[2];
-  auto ws_state = [&](int j, int ell) -> double* {
-    auto& pl = pool[j % 2];
-    while (static_cast<int>(pl.size()) <= ell) pl.push_back(nullptr);
-    if (!pl[ell]) pl[ell] = ex.ar->alloc_doubles(N);
-    return pl[ell];
-  };
-  for (int j = 0; j <= s; ++j)
-    for (int ell = 1; ell <= p; ++ell) {
-      double* u = (same && j < jb.n_scales) ? jb.out_same[ell][j] : nullptr;
-      state[j][ell] = u ? u : ws_state(j, ell);
-    }
+  // ---- state buffers: state[j][ℓ] for the scale j (ℓ = 1..p) ----
+  for (JS& J : js) {
+    const Job& jb = *J.jb;
+    J.state.assign(J.s + 1, std::vector<double*>(p + 1, nullptr));
+    for (int j = 0; j <= J.s; ++j)
+      for (int ell = 1; ell <= p; ++ell) {
+        double* u = (same && j < jb.n_scales) ? jb.out_same[ell][j] : nullptr;
+        if (!u) {
+          auto& pl = J.pool[j % 2];
+          while (static_cast<int>(pl.size()) <= ell) pl.push_back(nullptr);
+          if (!pl[ell]) pl[ell] = ex.ar->alloc_doubles(N);
+          u = pl[ell];
+        }
+        J.state[j][ell] = u;
+      }
+  }
 
   if (p >= 1) {
-    // ---- Stage B: quadrature at scale s ----
-    const double wq = w[q - 1];  // θ_q = 1 term: exp(0) = I, no Tucker operator (l.948-952)
+    // ---- Stage B: quadrature at scale s_b, every job in one batch ----
     std::vector<TuckerItem> items;
-    if (same) {
-      for (int i = 0; i < n_nodes; ++i) {
-        TuckerItem it;
-        it.in = jb.vin[0];
-        node_mats(i, it.mats);
-        it.group = 0;
-        for (int ell = 1; ell <= p; ++ell) {
-          Out o;
-          o.dst = state[s][ell];
-          o.beta = w[i] * std::pow(theta[i], ell - 1) / factorial(ell - 1);
-          if (i == 0)
-            o.srcs.push_back(Src{jb.vin[0], wq / factorial(ell - 1)});
-          else
-            o.srcs.push_back(Src{o.dst, 1.0});
-          it.outs.push_back(o);
-        }
-        items.push_back(it);
-      }
-    } else {
-      // Ψ_ℓ^{(s)} = Σ_i w_i E_i x_iℓ,  x_iℓ = Σ_{k=1}^ℓ θ_i^{ℓ−k}/(ℓ−k)! v_{p+1−k}/2^{(ℓ−k+1)s}
-      auto xcoef = [&](double th, int ell, int k) {
-        return std::pow(th, ell - k) / factorial(ell - k) / std::ldexp(1.0, (ell - k + 1) * s);
-      };
-      std::vector<Out> prep;
-      std::vector<std::vector<TuckerItem>> per_ell(p + 1);
-      for (int ell = 1; ell <= p; ++ell) {
-        bool first = true;
-        for (int i = 0; i < n_nodes; ++i) {
-          std::vector<Src> comb;
-          for (int k = 1; k <= ell; ++k) {
-            const double* v = jb.vin[p + 1 - k];
-            const double c = xcoef(theta[i], ell, k);
-            if (v && c != 0.0) comb.push_back(Src{v, c});
-          }
-          if (comb.empty()) continue;
+    std::vector<Out> prep;
+    for (JS& J : js) {
+      const Job& jb = *J.jb;
+      const int s = J.s, q = J.q;
+      const std::vector<double>& theta = J.theta;
+      const std::vector<double>& w = J.w;
+      const double wq = w[q - 1];  // θ_q = 1 term: exp(0) = I, no Tucker operator (l.948-952)
+      auto& state = J.state;
+      if (same) {
+        for (int i = 0; i < J.n_nodes; ++i) {
           TuckerItem it;
-          node_mats(i, it.mats);
-          it.group = ell;
-          if (comb.size() == 1) {
-            it.in = comb[0].ptr;
-            it.in_scale = comb[0].coef;
-          } else {
-            double* x = ex.ar->alloc_doubles(N);
-            prep.push_back(Out{x, 0.0, comb});
-            it.in = x;
+          it.in = jb.vin[0];
+          node_mats(J, i, it.mats);
+          it.group = J.gbase;
+          for (int ell = 1; ell <= p; ++ell) {
+            Out o;
+            o.dst = state[s][ell];
+            o.beta = w[i] * std::pow(theta[i], ell - 1) / factorial(ell - 1);
+            if (i == 0)
+              o.srcs.push_back(Src{jb.vin[0], wq / factorial(ell - 1)});
+            else
+              o.srcs.push_back(Src{o.dst, 1.0});
+            it.outs.push_back(o);
           }
-          Out o;
-          o.dst = state[s][ell];
-          o.beta = w[i];
-          if (first) {
+          items.push_back(it);
+        }
+      } else {
+        // Ψ_ℓ^{(s)} = Σ_i w_i E_i x_iℓ,  x_iℓ = Σ_{k=1}^ℓ θ_i^{ℓ−k}/(ℓ−k)! v_{p+1−k}/2^{(ℓ−k+1)s}
+        auto xcoef = [&](double th, int ell, int k) {
+          return std::pow(th, ell - k) / factorial(ell - k) / std::ldexp(1.0, (ell - k + 1) * s);
+        };
+        std::vector<std::vector<TuckerItem>> per_ell(p + 1);
+        std::vector<TuckerItem> jitems;
+        for (int ell = 1; ell <= p; ++ell) {
+          bool first = true;
+          for (int i = 0; i < J.n_nodes; ++i) {
+            std::vector<Src> comb;
+            for (int k = 1; k <= ell; ++k) {
+              const double* v = jb.vin[p + 1 - k];
+              const double c = xcoef(theta[i], ell, k);
+              if (v && c != 0.0) comb.push_back(Src{v, c});
+            }
+            if (comb.empty()) continue;
+            TuckerItem it;
+            node_mats(J, i, it.mats);
+            it.group = J.gbase + ell;
+            if (comb.size() == 1) {
+              it.in = comb[0].ptr;
+              it.in_scale = comb[0].coef;
+            } else {
+              double* x = ex.ar->alloc_doubles(N);
+              prep.push_back(Out{x, 0.0, comb});
+              it.in = x;
+            }
+            Out o;
+            o.dst = state[s][ell];
+            o.beta = w[i];
+            if (first) {
+              for (int k = 1; k <= ell; ++k) {
+                const double* v = jb.vin[p + 1 - k];
+                if (v) o.srcs.push_back(Src{v, wq * xcoef(1.0, ell, k)});
+              }
+            } else {
+              o.srcs.push_back(Src{o.dst, 1.0});
+            }
+            it.outs.push_back(o);
+            first = false;
+            per_ell[ell].push_back(it);
+          }
+          if (first) {  // no node contributed: Ψ_ℓ = w_q x_qℓ
+            Out o{state[s][ell], 0.0, {}};
             for (int k = 1; k <= ell; ++k) {
               const double* v = jb.vin[p + 1 - k];
               if (v) o.srcs.push_back(Src{v, wq * xcoef(1.0, ell, k)});
             }
-          } else {
-            o.srcs.push_back(Src{o.dst, 1.0});
-          }
-          it.outs.push_back(o);
-          first = false;
-          per_ell[ell].push_back(it);
-        }
-        if (first) {  // no node contributed: Ψ_ℓ = w_q x_qℓ
-          Out o{state[s][ell], 0.0, {}};
-          for (int k = 1; k <= ell; ++k) {
-            const double* v = jb.vin[p + 1 - k];
-            if (v) o.srcs.push_back(Src{v, wq * xcoef(1.0, ell, k)});
-          }
-          prep.push_back(o);
-          if (ell == p && s < jb.n_scales && jb.out_lin[s]) {
-            o.dst = jb.out_lin[s];
             prep.push_back(o);
+            if (ell == p && s < jb.n_scales && jb.out_lin[s]) {
+              o.dst = jb.out_lin[s];
+              prep.push_back(o);
+            }
           }
         }
-      }
-      ex.combine(N, prep);
-      for (int ell = 1; ell <= p; ++ell)
-        for (auto& it : per_ell[ell]) items.push_back(it);
-      if (s < jb.n_scales && jb.out_lin[s]) {
-        // scale s output = Ψ_p^{(s)} (+ exp term later): mirror the Ψ_p accumulation
-        for (auto& it : items)
-          if (it.group == p) {
-            Out o = it.outs[0];
-            o.dst = jb.out_lin[s];
-            for (auto& sr : o.srcs)
-              if (sr.ptr == state[s][p]) sr.ptr = jb.out_lin[s];
-            it.outs.push_back(o);
-          }
+        for (int ell = 1; ell <= p; ++ell)
+          for (auto& it : per_ell[ell]) jitems.push_back(it);
+        if (s < jb.n_scales && jb.out_lin[s]) {
+          // scale s output = Ψ_p^{(s)} (+ exp term later): mirror the Ψ_p accumulation
+          for (auto& it : jitems)
+            if (it.group == J.gbase + p) {
+              Out o = it.outs[0];
+              o.dst = jb.out_lin[s];
+              for (auto& sr : o.srcs)
+                if (sr.ptr == state[s][p]) sr.ptr = jb.out_lin[s];
+              it.outs.push_back(o);
+            }
+        }
+        for (auto& it : jitems) items.push_back(it);
       }
     }
+    ex.combine(N, prep);
     for (auto& it : d_items) items.push_back(it);
     ex.batch(items, ex.split >= 1);
     if (!ex.ok()) return;
     if (ex.on_outputs && !d_ready.empty()) ex.on_outputs(d_ready);
     if (!ex.ok()) return;
 
-    // ---- Stage C: squaring, j = s..1 ----
-    for (int j = s; j >= 1; --j) {
+    // ---- Stage C: squaring, level j for every job with s_b ≥ j ----
+    int max_s = 0;
+    for (const JS& J : js) max_s = std::max(max_s, J.s);
+    for (int j = max_s; j >= 1; --j) {
       std::vector<TuckerItem> sq;
-      for (int ell = p; ell >= 1; --ell) {
-        TuckerItem it;
-        it.in = state[j][ell];
-        mats_for(Es[j], it.mats);
-        it.group = ell;
-        Out o;
-        o.dst = state[j - 1][ell];
-        if (same) {
-          const double sc = std::ldexp(1.0, -ell);
-          o.beta = sc;
-          for (int k = 1; k <= ell; ++k) o.srcs.push_back(Src{state[j][k], sc / factorial(ell - k)});
-        } else {
-          o.beta = 1.0;
-          for (int k = 1; k <= ell; ++k)
-            o.srcs.push_back(Src{state[j][k], 1.0 / (factorial(ell - k) * std::ldexp(1.0, (ell - k) * j))});
+      for (JS& J : js) {
+        if (J.s < j) continue;
+        const Job& jb = *J.jb;
+        auto& state = J.state;
+        for (int ell = p; ell >= 1; --ell) {
+          TuckerItem it;
+          it.in = state[j][ell];
+          mats_for(J, J.Es[j], it.mats);
+          it.group = J.gbase + ell;
+          Out o;
+          o.dst = state[j - 1][ell];
+          if (same) {
+            const double sc = std::ldexp(1.0, -ell);
+            o.beta = sc;
+            for (int k = 1; k <= ell; ++k) o.srcs.push_back(Src{state[j][k], sc / factorial(ell - k)});
+          } else {
+            o.beta = 1.0;
+            for (int k = 1; k <= ell; ++k)
+              o.srcs.push_back(Src{state[j][k], 1.0 / (factorial(ell - k) * std::ldexp(1.0, (ell - k) * j))});
+          }
+          it.outs.push_back(o);
+          if (!same && ell == p && (j - 1) < jb.n_scales && jb.out_lin[j - 1]) {
+            Out o2 = o;
+            o2.dst = jb.out_lin[j - 1];
+            it.outs.push_back(o2);
+          }
+          sq.push_back(it);
         }
-        it.outs.push_back(o);
-        if (!same && ell == p && (j - 1) < jb.n_scales && jb.out_lin[j - 1]) {
-          Out o2 = o;
-          o2.dst = jb.out_lin[j - 1];
-          it.outs.push_back(o2);
-        }
-        sq.push_back(it);
       }
       ex.batch(sq, ex.split >= 2);
       if (!ex.ok()) return;
@@ -365,17 +424,20 @@ void run_job(Exec& ex, const Job& jb) {
   // ---- Stage D (linear combination): exp(τK/2^j)v_0 added to the result ----
   std::vector<TuckerItem> ex_items;
   if (!same) {
-    for (int j = 0; j < jb.n_scales; ++j) {
-      if (!jb.out_lin[j]) continue;
-      if (jb.vin[0]) {
-        TuckerItem it;
-        it.in = jb.vin[0];
-        mats_for(Es[j], it.mats);
-        it.group = j;
-        Out o{jb.out_lin[j], 1.0, {}};
-        if (p >= 1) o.srcs.push_back(Src{jb.out_lin[j], 1.0});
-        it.outs.push_back(o);
-        ex_items.push_back(it);
+    for (JS& J : js) {
+      const Job& jb = *J.jb;
+      for (int j = 0; j < jb.n_scales; ++j) {
+        if (!jb.out_lin[j]) continue;
+        if (jb.vin[0]) {
+          TuckerItem it;
+          it.in = jb.vin[0];
+          mats_for(J, J.Es[j], it.mats);
+          it.group = J.gbase + j;
+          Out o{jb.out_lin[j], 1.0, {}};
+          if (p >= 1) o.srcs.push_back(Src{jb.out_lin[j], 1.0});
+          it.outs.push_back(o);
+          ex_items.push_back(it);
+        }
       }
     }
   }

@@ -33,15 +33,20 @@ std::vector<double> realify(int n, const double* Az) {
   return R;
 }
 
-phiks_status create_impl(int d, const int* n, const double* const* A_host, bool cplx, phiks_handle* out) {
+phiks_status create_impl(int d, const int* n, const double* const* A_host, bool cplx, phiks_handle* out,
+                         int nblocks = 1) {
   if (!out || !n || !A_host) return fail(PHIKS_ERR_ARG, "null argument");
   *out = nullptr;
   if (d < 1 || d > PHIKS_MAX_D) return fail(PHIKS_ERR_ARG, "d out of range");
+  if (nblocks < 1 || nblocks > kMaxBlocks) return fail(PHIKS_ERR_ARG, "nblocks out of range");
+  for (int k = 0; k < nblocks * d; ++k)
+    if (!A_host[k]) return fail(PHIKS_ERR_ARG, "null A");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PHIKS_ERR_CUDA, "no CUDA device");
   auto* h = new phiks_ctx();
   h->d = d;
   h->cplx = cplx;
+  h->nblocks = nblocks;
   h->Nc = 1;
   for (int mu = 0; mu < d; ++mu) {
     if (n[mu] < 1 || n[mu] > PHIKS_MAX_N || !A_host[mu]) {
@@ -54,14 +59,16 @@ phiks_status create_impl(int d, const int* n, const double* const* A_host, bool 
   }
   h->N = cplx ? 2 * h->Nc : h->Nc;
   const int per = cplx ? 2 : 1;  // doubles per matrix entry
-  // dedupe bitwise-identical factors
-  std::vector<int> rep;
-  for (int mu = 0; mu < d; ++mu) {
+  // dedupe bitwise-identical factors (across modes and blocks)
+  std::vector<int> rep;  // A_host index of each distinct factor
+  for (int bm = 0; bm < nblocks * d; ++bm) {
+    const int mu = bm % d;
+    const double* Ah = A_host[bm];
     int found = -1;
     for (size_t f = 0; f < rep.size(); ++f) {
       const int m2 = rep[f];
-      if (n[m2] == n[mu] &&
-          std::memcmp(A_host[m2], A_host[mu], sizeof(double) * per * static_cast<size_t>(n[mu]) * n[mu]) == 0) {
+      if (n[m2 % d] == n[mu] &&
+          std::memcmp(A_host[m2], Ah, sizeof(double) * per * static_cast<size_t>(n[mu]) * n[mu]) == 0) {
         found = static_cast<int>(f);
         break;
       }
@@ -71,9 +78,9 @@ phiks_status create_impl(int d, const int* n, const double* const* A_host, bool 
       // complex factors are stored (and exponentiated) in their 2n×2n real form:
       // exp of the real form is the real form of exp (an algebra homomorphism)
       std::vector<double> Rz;
-      const double* A = A_host[mu];
+      const double* A = Ah;
       if (cplx) {
-        Rz = realify(n[mu], A_host[mu]);
+        Rz = realify(n[mu], Ah);
         A = Rz.data();
       }
       F.n = per * n[mu];
@@ -94,12 +101,12 @@ phiks_status create_impl(int d, const int* n, const double* const* A_host, bool 
         nrm = std::max(nrm, c);
       }
       F.norm1 = nrm;
-      F.fr = cplx ? plan::factor_range_complex(n[mu], A_host[mu]) : plan::factor_range(F.n, A);
+      F.fr = cplx ? plan::factor_range_complex(n[mu], Ah) : plan::factor_range(F.n, A);
       h->factors.push_back(F);
-      rep.push_back(mu);
+      rep.push_back(bm);
       found = static_cast<int>(h->factors.size()) - 1;
     }
-    h->fac_of_mode[mu] = found;
+    h->fac_of_block[bm / d][mu] = found;
   }
   if (cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned), 64 * sizeof(double)) != cudaSuccess) {
     phiks_destroy(h);
@@ -119,6 +126,10 @@ phiks_status phiks_create(int d, const int* n, const double* const* A_host, phik
 
 phiks_status phiks_create_complex(int d, const int* n, const double* const* A_host, phiks_handle* out) {
   return create_impl(d, n, A_host, true, out);
+}
+
+phiks_status phiks_create_blocks(int nblocks, int d, const int* n, const double* const* A_host, phiks_handle* out) {
+  return create_impl(d, n, A_host, false, out, nblocks);
 }
 
 phiks_status phiks_destroy(phiks_handle h) {
@@ -173,7 +184,7 @@ phiks_status validate(phiks_handle h, const phiks_request* req, int& p) {
 }
 
 phiks_status make_plan(phiks_handle h, const phiks_request* req, int p, const std::vector<double>& norms,
-                       plan::Plan& out) {
+                       plan::Plan& out, int block) {
   const int s_min = req->n_scales - 1;
   if (req->force_s >= 0) {
     out.s = req->force_s;
@@ -183,7 +194,7 @@ phiks_status make_plan(phiks_handle h, const phiks_request* req, int p, const st
     return PHIKS_OK;
   }
   const double tol = req->tol > 0 ? req->tol : std::ldexp(1.0, -53);
-  PlanKey key{req->mode, p, req->n_scales, req->tau, tol, norms};
+  PlanKey key{req->mode, p, req->n_scales, req->tau, tol, norms, block};
   auto it = h->plan_cache.find(key);
   if (it != h->plan_cache.end()) {
     out = it->second;
@@ -192,7 +203,7 @@ phiks_status make_plan(phiks_handle h, const phiks_request* req, int p, const st
   plan::Rect rect{};
   double cr = 0.0, ci = 0.0, hr = 0.0, hi = 0.0;
   for (int mu = 0; mu < h->d; ++mu) {
-    const auto& fr = h->factors[h->fac_of_mode[mu]].fr;
+    const auto& fr = h->factors[h->fac_of_block[block][mu]].fr;
     cr += req->tau * fr.sigma;
     ci += req->tau * fr.sigma_im;
     hr += req->tau * fr.hnorm;
@@ -322,8 +333,8 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
       return u;
     };
     key.insert(key.end(), {static_cast<uint64_t>(req->mode), static_cast<uint64_t>(req->n_scales), bits(req->tau),
-                           bits(req->tol), static_cast<uint64_t>(run.pl.s), static_cast<uint64_t>(run.pl.q),
-                           static_cast<uint64_t>(run.split), reinterpret_cast<uint64_t>(base), need});
+                           bits(req->tol), static_cast<uint64_t>(run.split), reinterpret_cast<uint64_t>(base), need});
+    for (const auto& pl : run.pls) key.insert(key.end(), {static_cast<uint64_t>(pl.s), static_cast<uint64_t>(pl.q)});
     for (int i = 0; i < req->n_ells; ++i) key.push_back(static_cast<uint64_t>(req->ells[i]));
     for (int i = 0; i < n_vecs; ++i) key.push_back(reinterpret_cast<uint64_t>(vecs[i]));
     for (int i = 0; i < run.nouts; ++i) key.push_back(reinterpret_cast<uint64_t>(outs[i]));
@@ -527,7 +538,7 @@ static phiks_status plan_host_impl(int d, const int* n, const double* const* A_h
     F.n = n[mu];
     F.fr = cplx ? plan::factor_range_complex(F.n, A_host[mu]) : plan::factor_range(F.n, A_host[mu]);
     h.factors.push_back(F);
-    h.fac_of_mode[mu] = mu;
+    h.fac_of_block[0][mu] = mu;
   }
   return phiks_plan(&h, req, vec_norms, out);
 }

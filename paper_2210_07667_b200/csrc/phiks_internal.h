@@ -55,6 +55,7 @@ constexpr int kMaxTerms = 48;   // also the TMA descriptor count per launch
 constexpr int kMaxOuts = 128;
 constexpr int kMaxSrcs = 224;
 constexpr int kMaxRanks = 8;    // slab-sharded handles: ranks of one NVSwitch box
+constexpr int kMaxBlocks = PHIKS_MAX_BLOCKS;  // diagonal blocks of K̂ per handle
 
 // Remote (peer-memory) epilogue of the slab-sharded Tucker operator: when
 // world > 0 every output of the launch is written to the symmetric region of

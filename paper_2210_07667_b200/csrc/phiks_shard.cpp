@@ -8,6 +8,11 @@ extern "C" {
 // ===========================================================================
 phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_host, int rank, int world,
                                   phiks_handle* out) {
+  return phiks_create_sharded_blocks(1, d, n, A_host, rank, world, out);
+}
+
+phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const double* const* A_host, int rank,
+                                         int world, phiks_handle* out) {
   if (!out || !n) return fail(PHIKS_ERR_ARG, "null argument");
   *out = nullptr;
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return fail(PHIKS_ERR_ARG, "rank/world");
@@ -17,7 +22,7 @@ phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_ho
       return fail(PHIKS_ERR_ARG, "n_d and n_{d-1} must be divisible by world");
   }
   phiks_handle h = nullptr;
-  phiks_status st = phiks_create(d, n, A_host, &h);
+  phiks_status st = phiks_create_blocks(nblocks, d, n, A_host, &h);
   if (st != PHIKS_OK) return st;
   h->rank = rank;
   h->world = world;
@@ -117,7 +122,7 @@ phiks_status phiks_apply_ranks_serial(const phiks_handle* hs, int world, const p
     if (req->mem_kind != PHIKS_MEM_DEVICE) return fail(PHIKS_ERR_ARG, "ranks_serial takes device memory");
   }
   const bool same = req->mode == PHIKS_MODE_SAME_VECTOR;
-  const int nouts = same ? req->n_ells * req->n_scales : req->n_scales;
+  const int nouts = hs[0]->nblocks * (same ? req->n_ells * req->n_scales : req->n_scales);
   std::vector<ApplyRun> runs(world);
   for (int k = 0; k < world; ++k) {
     phiks_status st = runs[k].init(hs[k], req, n_vecs, vecs + static_cast<size_t>(k) * n_vecs,

@@ -119,7 +119,7 @@ def apply_ranks_serial(ranks: Sequence[ShardedPhiKS], tau: float, ells: Sequence
     from . import PhiKS, _check_dev, _stream_ptr
     world = len(ranks)
     m = PhiKS._mode(mode)
-    nouts = len(ells) * n_scales if m == _lib.MODE_SAME_VECTOR else n_scales
+    nouts = ranks[0].op.nblocks * (len(ells) * n_scales if m == _lib.MODE_SAME_VECTOR else n_scales)
     N = ranks[0].N
     if outs is None:
         outs = [[torch.empty(N, dtype=torch.float64, device=vecs[k][0].device) for _ in range(nouts)]
