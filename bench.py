@@ -179,33 +179,38 @@ def b200_arm(args):
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
 
-    # ---- workload: configs[3]; N > 1 slab-shards every tensor along mode 3 ----
+    # ---- workload: configs[3], the block-diagonal K̂ = diag(K_u, K_v) of the two
+    # species in ONE handle (phiks_create_blocks, §4.4: per-species plans,
+    # shared launches); N > 1 slab-shards every tensor along mode 3 ----
     wl = W.config(3)
-    ops, vins, outs, host_in, host_out = [], [], [], [], []
+    pb0 = wl.problems[0]
+    assert all((pb.tau, pb.ells, pb.mode, pb.n_scales) == (pb0.tau, pb0.ells, pb0.mode, pb0.n_scales)
+               for pb in wl.problems)
+    blocks = [pb.A for pb in wl.problems]
+    op = ShardedPhiKS(blocks, rank, world) if world > 1 else PhiKS(blocks)
+    ops = [op]
+    vins, host_in = [], []
     for pb in wl.problems:
-        op = ShardedPhiKS(pb.A, rank, world) if world > 1 else PhiKS(pb.A)
-        ops.append(op)
         x = W.as_flat(pb.vs[0])
         if world > 1:
             x = np.ascontiguousarray(split_slabs(x, world)[rank])
         vins.append(torch.from_numpy(x.copy()).to(dev))
-        outs.append([torch.empty_like(vins[-1]) for _ in pb.ells])
         hi = torch.empty(x.size, dtype=torch.float64, pin_memory=True)
         hi.numpy()[:] = x
         host_in.append(hi)
-        host_out.append([torch.empty(x.size, dtype=torch.float64, pin_memory=True) for _ in pb.ells])
+    nloc = vins[0].numel()
+    outs = [torch.empty_like(vins[0]) for _ in range(len(wl.problems) * len(pb0.ells))]
+    host_out = [torch.empty(nloc, dtype=torch.float64, pin_memory=True) for _ in outs]
 
     def step():
-        for op, pb, v, o in zip(ops, wl.problems, vins, outs):
-            op.apply(pb.tau, pb.ells, [v], mode=pb.mode, n_scales=pb.n_scales, outs=o, stream=stream)
+        op.apply(pb0.tau, pb0.ells, vins, mode=pb0.mode, n_scales=pb0.n_scales, outs=outs, stream=stream)
 
     def step_host():
         # public API with pinned host buffers: H2D of the step's inputs and D2H of every
         # output inside the library's apply (PHIKS_MEM_HOST_ASYNC: copies on its own
-        # streams, overlapping the other species' compute)
-        for op, pb, v, o in zip(ops, wl.problems, host_in, host_out):
-            op.apply(pb.tau, pb.ells, [v.numpy()], mode=pb.mode, n_scales=pb.n_scales, outs=[t.numpy() for t in o],
-                     host_async=True)
+        # streams; the exp-action outputs leave while the rest of the step runs)
+        op.apply(pb0.tau, pb0.ells, [v.numpy() for v in host_in], mode=pb0.mode, n_scales=pb0.n_scales,
+                 outs=[t.numpy() for t in host_out], host_async=True)
 
     # ---- measured FP64 tensor-core peak (DMMA microbenchmark) ----
     sink = torch.empty(148 * 4 * 256, dtype=torch.float64, device=dev)
@@ -224,8 +229,9 @@ def b200_arm(args):
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
-    flops_step = sum(op.stats()["mu_mode_flops"] for op in ops)
-    plans = [{"s": op.stats()["s"], "q": op.stats()["q"], "T_executed": op.stats()["T_executed"]} for op in ops]
+    flops_step = sum(o.stats()["mu_mode_flops"] for o in ops)
+    plans = [{"species": b, "s": s, "q": q} for b, (s, q) in enumerate(op.stats()["block_plans"])]
+    plans.append({"T_executed_total": op.stats()["tucker_ops"]})
 
     # ---- timed region (device-resident inputs) ----
     for op in ops:
@@ -267,7 +273,7 @@ def b200_arm(args):
         for op in ops:
             op.wait()
         torch.cuda.synchronize()
-        k = max(1, min(args.steps, 5))
+        k = max(1, args.steps)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
@@ -281,10 +287,9 @@ def b200_arm(args):
             tt = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
-        N = int(np.prod(wl.problems[0].dims)) // world
         e2e = {"value": flops_step * world * k / te / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": sum(8 * N for _ in wl.problems),
-               "d2h_bytes_per_step": sum(8 * N * len(pb.ells) for pb in wl.problems),
+               "h2d_bytes_per_step": sum(8 * t.numel() for t in host_in),
+               "d2h_bytes_per_step": sum(8 * t.numel() for t in host_out),
                "ms_per_step": te / k * 1e3, "timing": "host wall clock around k steps of C-ABI applies with pinned host buffers (PHIKS_MEM_HOST_ASYNC) and the final wait"}
 
     # ---- CPU baseline: the oracle, rank 0, N = 1 only ----
@@ -315,7 +320,7 @@ def b200_arm(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD,
+            "config": {"workload": WORKLOAD, "handle": "one block-diagonal handle (2 blocks = species)",
                        "parallelism": f"slab{world} (mode-3 slabs, transposition fused into peer stores)"
                        if world > 1 else "single",
                        "l2": "inputs larger than L2 (134 MB per vector > 126 MB L2)", "plans": plans,

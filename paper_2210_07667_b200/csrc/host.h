@@ -123,7 +123,13 @@ struct phiks_ctx {
   int64_t graph_replays = 0;
   // host-memory applies: copy streams and their ordering events
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t ev_h2d = nullptr, ev_d2h = nullptr, ev_cdone = nullptr, ev_ready = nullptr;
+  // the library-owned workspace is two halves used by alternate applies
+  // (ws_parity): an apply's stage A and host copies may run ahead of the previous
+  // apply, ordered only after the apply before it (same half): ev_cdone[half]
+  // = compute done, ev_d2h[half] = copy-out done
+  int ws_parity = 0;
+  cudaEvent_t ev_h2d = nullptr, ev_ready = nullptr;
+  cudaEvent_t ev_d2h[2] = {nullptr, nullptr}, ev_cdone[2] = {nullptr, nullptr};
   // the exponential stage (stage A) of an apply runs on s_pre, ordered only
   // after the previous apply of this handle (ev_cdone), so it overlaps the
   // tail of whatever else is queued on the apply stream (another handle's
@@ -980,6 +986,7 @@ struct ApplyRun {
   }
 
   bool own_ws = false;
+  int half = 0;
   phiks_status workspace(void* workspace, size_t ws_bytes, size_t need, char** base) {
     own_ws = workspace == nullptr;
     if (workspace) {
@@ -990,20 +997,22 @@ struct ApplyRun {
       *base = static_cast<char*>(workspace);
       return PHIKS_OK;
     }
-    if (h->ws_own_bytes < need) {
+    const size_t halfb = ((need > 0 ? need : 256) + 4095) & ~size_t(4095);
+    if (h->ws_own_bytes < 2 * halfb) {
       for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);  // they reference the old workspace
       h->graphs.clear();
       if (h->ws_own) {
-        CUDA_TRY(cudaStreamSynchronize(cs));
+        CUDA_TRY(cudaDeviceSynchronize());  // both halves may be in use on the handle's streams
         CUDA_TRY(cudaFree(h->ws_own));
         h->ws_own = nullptr;
         h->ws_own_bytes = 0;
       }
-      if (cudaMalloc(&h->ws_own, need > 0 ? need : 256) != cudaSuccess)
-        return fail(PHIKS_ERR_NOMEM, "workspace cudaMalloc");
-      h->ws_own_bytes = need > 0 ? need : 256;
+      if (cudaMalloc(&h->ws_own, 2 * halfb) != cudaSuccess) return fail(PHIKS_ERR_NOMEM, "workspace cudaMalloc");
+      h->ws_own_bytes = 2 * halfb;
     }
-    *base = static_cast<char*>(h->ws_own);
+    half = h->ws_parity;
+    h->ws_parity ^= 1;
+    *base = static_cast<char*>(h->ws_own) + half * (h->ws_own_bytes / 2);
     return PHIKS_OK;
   }
 
@@ -1017,7 +1026,8 @@ struct ApplyRun {
     bind(false);
     if (host_mem && rec) return fail(PHIKS_ERR_ARG, "recorded applies take device memory");
     // (never recorded yet: waiting on it is a no-op)
-    if (!h->ev_cdone) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_cdone, cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k)
+      if (!h->ev_cdone[k]) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_cdone[k], cudaEventDisableTiming));
     // stage A on the handle's pre stream: only with the library's own workspace
     // (a caller workspace may be in use on the stream until this apply starts),
     // not while capturing a graph, not for recorded (emulated-rank) applies
@@ -1029,7 +1039,8 @@ struct ApplyRun {
         CUDA_TRY(cudaStreamCreateWithFlags(&h->s_pre, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&h->ev_pre, cudaEventDisableTiming));
       }
-      CUDA_TRY(cudaStreamWaitEvent(h->s_pre, h->ev_cdone, 0));  // previous apply no longer reads the workspace
+      // the apply before the previous one (same workspace half) no longer reads it
+      CUDA_TRY(cudaStreamWaitEvent(h->s_pre, h->ev_cdone[half], 0));
       ex.st = h->s_pre;
     }
     ex.on_inputs = [this, pre]() {
@@ -1046,15 +1057,14 @@ struct ApplyRun {
       if (!h->s_in) {
         CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&h->ev_h2d, &h->ev_d2h, &h->ev_ready})
+        for (cudaEvent_t* e : {&h->ev_h2d, &h->ev_d2h[0], &h->ev_d2h[1], &h->ev_ready})
           CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventRecord(h->ev_d2h, h->s_out));
       }
-      CUDA_TRY(cudaStreamWaitEvent(h->s_in, h->ev_cdone, 0));  // previous apply is done with the staging
+      CUDA_TRY(cudaStreamWaitEvent(h->s_in, h->ev_cdone[half], 0));  // staging half no longer read
       for (size_t i = 0; i < dv.size(); ++i)
         CUDA_TRY(cudaMemcpyAsync(dv[i], vecs[i], tbytes, cudaMemcpyHostToDevice, h->s_in));
       CUDA_TRY(cudaEventRecord(h->ev_h2d, h->s_in));
-      CUDA_TRY(cudaStreamWaitEvent(cs, h->ev_d2h, 0));  // previous apply's copy-out has drained
+      CUDA_TRY(cudaStreamWaitEvent(cs, h->ev_d2h[half], 0));  // copy-out of this staging half has drained
       copied.assign(nouts, false);
       ex.on_outputs = [this](const std::vector<double*>& ready) { copy_out(ready); };
     }
@@ -1067,9 +1077,9 @@ struct ApplyRun {
         if (!copied[i]) rest.push_back(dout[i]);
       copy_out(rest);
       if (!ex.ok()) return ex.status;
-      CUDA_TRY(cudaEventRecord(h->ev_d2h, h->s_out));
+      CUDA_TRY(cudaEventRecord(h->ev_d2h[half], h->s_out));
     }
-    if (!rec && cap == cudaStreamCaptureStatusNone) CUDA_TRY(cudaEventRecord(h->ev_cdone, cs));
+    if (!rec && cap == cudaStreamCaptureStatusNone) CUDA_TRY(cudaEventRecord(h->ev_cdone[half], cs));
     return PHIKS_OK;
   }
   std::vector<bool> copied;

@@ -140,7 +140,7 @@ phiks_status phiks_destroy(phiks_handle h) {
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
   for (int k = 0; k < kMaxRanks; ++k)
     if (h->peer_ipc[k] && h->peer[k]) cudaIpcCloseMemHandle(h->peer[k]);
-  for (cudaEvent_t e : {h->ev_h2d, h->ev_d2h, h->ev_cdone, h->ev_ready})
+  for (cudaEvent_t e : {h->ev_h2d, h->ev_d2h[0], h->ev_d2h[1], h->ev_cdone[0], h->ev_cdone[1], h->ev_ready})
     if (e) cudaEventDestroy(e);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
   if (h->s_cap) cudaStreamDestroy(h->s_cap);
@@ -367,15 +367,16 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
       ++h->graph_replays;
     }
     CUDA_TRY(cudaGraphLaunch(exec, cs));
-    if (!h->ev_cdone) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_cdone, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(h->ev_cdone, cs));  // orders the next apply's stage A after this replay
+    for (int k = 0; k < 2; ++k)
+      if (!h->ev_cdone[k]) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_cdone[k], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(h->ev_cdone[run.half], cs));  // orders later side-stream work after this replay
     run.finish_stats(need);
     return PHIKS_OK;
   }
   st = run.execute(base, need, nullptr);
   if (st != PHIKS_OK) return st;
   if (run.host_mem && !run.host_async) {
-    CUDA_TRY(cudaEventSynchronize(h->ev_d2h));
+    CUDA_TRY(cudaEventSynchronize(h->ev_d2h[run.half]));
     CUDA_TRY(cudaStreamSynchronize(run.cs));
     st = check_barrier_flag(h);
     if (st != PHIKS_OK) return st;

@@ -194,8 +194,10 @@ phiks_status phiks_shard_layout(int d, const int* n, int rank, int world, int st
 
 phiks_status phiks_wait(phiks_handle h) {
   if (!h) return fail(PHIKS_ERR_ARG, "null handle");
-  if (h->ev_d2h) CUDA_TRY(cudaEventSynchronize(h->ev_d2h));
-  if (h->ev_cdone) CUDA_TRY(cudaEventSynchronize(h->ev_cdone));
+  for (int k = 0; k < 2; ++k) {
+    if (h->ev_d2h[k]) CUDA_TRY(cudaEventSynchronize(h->ev_d2h[k]));
+    if (h->ev_cdone[k]) CUDA_TRY(cudaEventSynchronize(h->ev_cdone[k]));
+  }
   return check_barrier_flag(h);
 }
 

@@ -13,28 +13,25 @@ from paper_2210_07667_b200 import workloads as W  # noqa: E402
 from paper_2210_07667_b200.sharding import split_slabs  # noqa: E402
 
 wl = W.config(3)
+pb0 = wl.problems[0]
+blocks = [pb.A for pb in wl.problems]
 res = []
 for P in [int(x) for x in os.environ.get("PS", "1,2,4,8").split(",")]:
-    hs, ins, outs = [], [], []
-    for pb in wl.problems:
-        x = W.as_flat(pb.vs[0])
-        if P == 1:
-            op = PhiKS(pb.A)
-            hs.append([op])
-        else:
-            ranks = [ShardedPhiKS(pb.A, r, P, connect=None) for r in range(P)]
-            ShardedPhiKS.connect_local(ranks)
-            hs.append(ranks)
-        ins.append([[torch.from_numpy(np.ascontiguousarray(s)).cuda()] for s in split_slabs(x, P)])
-        outs.append([[torch.empty(x.size // P, dtype=torch.float64, device="cuda") for _ in pb.ells]
-                     for _ in range(P)])
+    xs = [W.as_flat(pb.vs[0]) for pb in wl.problems]
+    if P == 1:
+        ranks = [PhiKS(blocks)]
+    else:
+        ranks = [ShardedPhiKS(blocks, r, P, connect=None) for r in range(P)]
+        ShardedPhiKS.connect_local(ranks)
+    ins = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, P)[r])).cuda() for x in xs] for r in range(P)]
+    outs = [[torch.empty(xs[0].size // P, dtype=torch.float64, device="cuda")
+             for _ in range(len(wl.problems) * len(pb0.ells))] for _ in range(P)]
 
     def step():
-        for pb, h, i, o in zip(wl.problems, hs, ins, outs):
-            if P == 1:
-                h[0].apply(pb.tau, pb.ells, i[0], outs=o[0])
-            else:
-                apply_ranks_serial(h, pb.tau, pb.ells, i, outs=o)
+        if P == 1:
+            ranks[0].apply(pb0.tau, pb0.ells, ins[0], outs=outs[0])
+        else:
+            apply_ranks_serial(ranks, pb0.tau, pb0.ells, ins, outs=outs)
     for _ in range(3):
         step()
     torch.cuda.synchronize()
@@ -47,7 +44,7 @@ for P in [int(x) for x in os.environ.get("PS", "1,2,4,8").split(",")]:
     t = e0.elapsed_time(e1) / 5
     res.append({"P": P, "serial_ms": round(t, 3), "per_rank_ms": round(t / P, 3)})
     print(json.dumps(res[-1]), flush=True)
-    del hs, ins, outs
+    del ranks, ins, outs
     torch.cuda.empty_cache()
 t1 = res[0]["per_rank_ms"] * res[0]["P"]
 for r in res:
