@@ -543,13 +543,45 @@ struct Exec {
         dsts.push_back(dptr);
         rows.push_back(row);
       }
-      for (auto& row : rows)
-        for (auto& t : row)
-          if (std::find(srcs.begin(), srcs.end(), t.first) == srcs.end()) srcs.push_back(t.first);
-      std::vector<std::vector<double>> coef(dsts.size(), std::vector<double>(srcs.size(), 0.0));
-      for (size_t o = 0; o < dsts.size(); ++o)
-        for (auto& t : rows[o]) coef[o][std::find(srcs.begin(), srcs.end(), t.first) - srcs.begin()] += t.second;
-      mcombine(N, srcs, dsts, coef);
+      // independent groups of outputs (no shared source or destination, e.g. the
+      // blocks of a block-diagonal handle) stream separately: each reads only its
+      // own sources
+      std::vector<int> comp(dsts.size());
+      for (size_t o = 0; o < dsts.size(); ++o) comp[o] = static_cast<int>(o);
+      std::function<int(int)> root = [&](int x) { return comp[x] == x ? x : comp[x] = root(comp[x]); };
+      std::map<const double*, int> owner;  // pointer -> an output touching it
+      for (size_t o = 0; o < dsts.size(); ++o) {
+        auto touch = [&](const double* ptr) {
+          auto it = owner.find(ptr);
+          if (it == owner.end())
+            owner[ptr] = static_cast<int>(o);
+          else
+            comp[root(static_cast<int>(o))] = root(it->second);
+        };
+        touch(dsts[o]);
+        for (auto& t : rows[o]) touch(t.first);
+      }
+      std::vector<int> done(dsts.size(), 0);
+      for (size_t o0 = 0; o0 < dsts.size(); ++o0) {
+        const int r0 = root(static_cast<int>(o0));
+        if (done[r0]) continue;
+        done[r0] = 1;
+        std::vector<size_t> members;
+        for (size_t o = 0; o < dsts.size(); ++o)
+          if (root(static_cast<int>(o)) == r0) members.push_back(o);
+        for (size_t o : members)
+          for (auto& t : rows[o])
+            if (std::find(srcs.begin(), srcs.end(), t.first) == srcs.end()) srcs.push_back(t.first);
+        std::vector<double*> cd;
+        std::vector<std::vector<double>> coef(members.size(), std::vector<double>(srcs.size(), 0.0));
+        for (size_t m = 0; m < members.size(); ++m) {
+          cd.push_back(dsts[members[m]]);
+          for (auto& t : rows[members[m]])
+            coef[m][std::find(srcs.begin(), srcs.end(), t.first) - srcs.begin()] += t.second;
+        }
+        mcombine(N, srcs, cd, coef);
+        srcs.clear();
+      }
     }
   }
 

@@ -1,9 +1,11 @@
-"""ncu target in the bench configuration: configs[3] species 0 (256^3,
-phi_0..phi_2 same-vector), one warm apply then one profiled apply.  Each
-apply launches 9 TMA mode-product kernels (quadrature batch, squaring batch,
-exp action; 3 modes each):
+"""ncu target in the bench configuration: configs[3], both species in one
+block-diagonal handle (256^3, phi_0..phi_2 same-vector), one warm apply then
+one profiled apply.  Each apply launches 6 Tucker mode-product kernels of the
+64x128 instantiation (merged quadrature+exp-action batch of both species, then
+the merged squaring batch; 3 modes each):
 
-  ncu --set full -k regex:mode_product_tma -s 9 -c 9 python scripts/profile_bench.py
+  ncu --set full --kernel-name-base demangled -k "regex:mode_product_tma_kernel<64, 128" \
+      -s 6 -c 6 python scripts/profile_bench.py
 """
 import os
 import sys
@@ -15,12 +17,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2210_07667_b200 import PhiKS  # noqa: E402
 from paper_2210_07667_b200 import workloads as W  # noqa: E402
 
-pb = W.config(3).problems[0]
-op = PhiKS(pb.A)
-v = torch.from_numpy(np.ascontiguousarray(W.as_flat(pb.vs[0]))).cuda()
-outs = [torch.empty_like(v) for _ in pb.ells]
+wl = W.config(3)
+pb = wl.problems[0]
+op = PhiKS([p.A for p in wl.problems])
+vs = [torch.from_numpy(np.ascontiguousarray(W.as_flat(p.vs[0]))).cuda() for p in wl.problems]
+outs = [torch.empty_like(vs[0]) for _ in range(len(wl.problems) * len(pb.ells))]
 for _ in range(2):
-    op.apply(pb.tau, pb.ells, [v], mode=pb.mode, n_scales=pb.n_scales, outs=outs)
+    op.apply(pb.tau, pb.ells, vs, mode=pb.mode, n_scales=pb.n_scales, outs=outs)
 torch.cuda.synchronize()
 st = op.stats()
-print("ok", st["s"], st["q"], st["tucker_ops"], st["kernel_launches"])
+print("ok", st["block_plans"], st["tucker_ops"], st["kernel_launches"])
