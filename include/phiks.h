@@ -238,13 +238,14 @@ phiks_status phiks_select_plan(int mode, double center_re, double center_im, dou
  * outermost mode, with modes 1..d-1 contracted locally and the mode-d product
  * done through an all-to-all transpose").
  *
- * Rank r of P owns the contiguous slab i_d ∈ [r·n_d/P, (r+1)·n_d/P) of every
- * tensor: N/P doubles, column-major with dims (n_1, …, n_{d-1}, n_d/P) — i.e.
- * elements [r·N/P, (r+1)·N/P) of the global column-major array.  Each Tucker
+ * Rank r of P owns the contiguous slab i_d ∈ [o_r, o_r + c_r) of every tensor
+ * (block distribution: c_r = n_d/P, plus one for r < n_d mod P; o_r the sum of
+ * the previous counts): column-major with dims (n_1, …, n_{d-1}, c_r), i.e.
+ * elements [M·o_r, M·(o_r + c_r)) of the global column-major array, M = N/n_d.  Each Tucker
  * operator (Eq. (4); the μ-mode products commute, l.252-270) runs
  * modes 1..d-2 on the slab, then the mode-(d-1) product whose epilogue stores
  * every output column straight into the peer rank that owns it in the
- * transposed layout (slab of mode d-1, dims (n_1..n_{d-2}, n_{d-1}/P, n_d)),
+ * transposed layout (slab of mode d-1, dims (n_1..n_{d-2}, c'_k, n_d)),
  * a device-side barrier, the mode-d product there (local), whose epilogue
  * stores back into the slab layout on the owner, and a second barrier: the
  * all-to-all transposition is fused into the producing kernels' stores over
@@ -258,8 +259,10 @@ phiks_status phiks_select_plan(int mode, double center_re, double center_im, dou
 
 /* Create rank `rank` of a `world`-way slab-sharded handle for the GLOBAL
    dims n[0..d-1] and factors A_host (every rank passes the same factors).
-   world = 1 gives an ordinary handle.  world > 1 needs d ≥ 2,
-   world ≤ 8 and n[d-1], n[d-2] divisible by world (PHIKS_ERR_ARG otherwise).
+   world = 1 gives an ordinary handle.  world > 1 needs d ≥ 2, world ≤ 8 and
+   n[d-1], n[d-2] ≥ world (PHIKS_ERR_ARG otherwise); the slabs are block-
+   distributed (rank r owns n_d/world indices, one more for r < n_d mod world),
+   so the local slab sizes may differ between ranks (phiks_shard_info).
    Before the first apply the peers must be attached with
    phiks_shard_open_peers (one process per GPU) or phiks_shard_set_peer_bases
    (one process).  phiks_apply on the handle then takes and returns local
@@ -310,6 +313,13 @@ phiks_status phiks_shard_set_peer_bases(phiks_handle h, void* const* bases);
    k = j / cb at element offset l + rstride·r + roff + colstride·(j − k·cb)
    of the destination tensor.  The library's own launches use exactly this. */
 phiks_status phiks_shard_layout(int d, const int* n, int rank, int world, int stage, int64_t* out7);
+
+/* General geometry, also for ragged slabs (n_d or n_{d-1} not divisible by
+   world; the first n mod world ranks own one more index).  out: 4 + 3·world
+   values {L, n, R, colstride, kstart[world], kstride[world], kroff[world]};
+   output element (l, j, r) goes to rank k = owner(j) (block distribution of
+   the n columns) at offset l + kstride[k]·r + kroff[k] + colstride·(j − kstart[k]). */
+phiks_status phiks_shard_layout_ex(int d, const int* n, int rank, int world, int stage, int64_t* out);
 
 /* Emulation of `world` ranks on ONE GPU (tests): hs[k] is rank k (all in this
    process, peers set with phiks_shard_set_peer_bases).  Runs every rank's

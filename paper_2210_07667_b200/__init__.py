@@ -90,7 +90,11 @@ class PhiKS:
                                                        ctypes.byref(h)), "phiks_create_sharded")
         self._h = h
         # N: elements of the tensors apply() takes (the local slab when sharded)
-        self.N = int(np.prod(self.dims)) // self.world
+        self.N = int(np.prod(self.dims))
+        if self.world > 1:
+            cnt = ctypes.c_int64()
+            _lib.check(lib.phiks_shard_info(self._h, None, None, ctypes.byref(cnt), None), "phiks_shard_info")
+            self.N = int(cnt.value)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

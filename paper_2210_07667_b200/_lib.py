@@ -90,6 +90,7 @@ def load() -> ctypes.CDLL:
     lib.phiks_plan_host_complex.argtypes = [i, P(i), P(vp), P(Request), P(d), P(PlanInfo)]
     lib.phiks_shard_peer_base.argtypes = [vp, i, P(vp)]
     lib.phiks_shard_layout.argtypes = [i, P(i), i, i, i, P(ctypes.c_int64)]
+    lib.phiks_shard_layout_ex.argtypes = [i, P(i), i, i, i, P(ctypes.c_int64)]
     lib.phiks_last_error.restype = ctypes.c_char_p
     lib.phiks_version.restype = ctypes.c_char_p
     for name in ("phiks_create", "phiks_destroy", "phiks_plan", "phiks_apply", "phiks_workspace_size",
@@ -97,7 +98,7 @@ def load() -> ctypes.CDLL:
                  "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan", "phiks_set_profiling",
                  "phiks_create_sharded", "phiks_shard_info", "phiks_shard_ipc_handle", "phiks_shard_open_peers",
                  "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_shard_layout", "phiks_wait", "phiks_shard_peer_base", "phiks_create_complex", "phiks_plan_host_complex", "phiks_create_blocks",
-                 "phiks_create_sharded_blocks"):
+                 "phiks_create_sharded_blocks", "phiks_shard_layout_ex"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

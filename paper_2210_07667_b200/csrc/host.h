@@ -172,25 +172,53 @@ struct Arena {
   }
 };
 
+// Block distribution of n indices over P ranks: the first n mod P ranks own
+// one more.  Used for the slabs of mode d (layout S_d) and of mode d-1 (S_{d-1}).
+inline int64_t blk_cnt(int64_t n, int P, int k) { return n / P + (k < n % P ? 1 : 0); }
+inline int64_t blk_start(int64_t n, int P, int k) { return k * (n / P) + std::min<int64_t>(k, n % P); }
+
 // Geometry of the two peer-store launches of a slab-sharded Tucker operator
 // (DESIGN.md §0(e)).  gn: global dims.  stage 0: the mode-(d-1) product on the
-// slab (layout S_d) storing into layout S_{d-1}; stage 1: the mode-d product
-// on layout S_{d-1} storing back into S_d.  Output element (l, j, r) of the
-// (L, n, R) launch goes to rank k = j / cb at offset
-//   l + rstride·r + roff + colstride·(j − k·cb).
+// slab (layout S_d, dims (n_1..n_{d-2}, n_{d-1}, cd_r)) storing into layout
+// S_{d-1} (dims (n_1..n_{d-2}, cb_k, n_d)) of the owner k of each output column;
+// stage 1: the mode-d product on layout S_{d-1} storing back into S_d.  Element
+// (l, j, r) of the (L, n, R) launch goes to rank k = owner(j) (block
+// distribution of the n columns) at offset
+//   l + kstride[k]·r + kroff[k] + colstride·(j − kstart[k]).
 struct ShardStage {
-  int64_t L, n, R, cb, rstride, roff, colstride;
+  int64_t L, n, R, colstride;
+  int world;
+  int64_t kstart[kMaxRanks], kstride[kMaxRanks], kroff[kMaxRanks];
+  bool uniform;
 };
 inline ShardStage shard_stage(int d, const int* gn, int rank, int world, int stage) {
   int64_t L0 = 1;
   for (int mu = 0; mu + 2 < d; ++mu) L0 *= gn[mu];
   const int64_t na = gn[d - 2], nd = gn[d - 1];
-  const int64_t cb = na / world, cd = nd / world;
   ShardStage s{};
+  s.world = world;
+  s.uniform = (na % world == 0) && (nd % world == 0);
   if (stage == 0) {
-    s = ShardStage{L0, na, cd, cb, L0 * cb, L0 * cb * rank * cd, L0};
+    s.L = L0;
+    s.n = na;
+    s.R = blk_cnt(nd, world, rank);
+    s.colstride = L0;
+    for (int k = 0; k < world; ++k) {
+      const int64_t cbk = blk_cnt(na, world, k);
+      s.kstart[k] = blk_start(na, world, k);
+      s.kstride[k] = L0 * cbk;
+      s.kroff[k] = L0 * cbk * blk_start(nd, world, rank);
+    }
   } else {
-    s = ShardStage{L0 * cb, nd, 1, cd, 0, L0 * cb * rank, L0 * na};
+    s.L = L0 * blk_cnt(na, world, rank);
+    s.n = nd;
+    s.R = 1;
+    s.colstride = L0 * na;
+    for (int k = 0; k < world; ++k) {
+      s.kstart[k] = blk_start(nd, world, k);
+      s.kstride[k] = 0;
+      s.kroff[k] = L0 * blk_start(na, world, rank);
+    }
   }
   return s;
 }
@@ -625,11 +653,16 @@ struct Exec {
     auto remap_of = [&](const ShardStage& s) {
       Remap r{};
       r.world = P;
-      r.cb = static_cast<int>(s.cb);
-      r.rstride = s.rstride;
-      r.roff = s.roff;
+      r.cq = static_cast<int>(s.n / P);
+      r.crem = static_cast<int>(s.n % P);
+      r.uniform = s.uniform ? 1 : 0;
       r.colstride = s.colstride;
-      for (int k = 0; k < P; ++k) r.base[k] = h->peer[k];
+      for (int k = 0; k < P; ++k) {
+        r.kstart[k] = static_cast<int>(s.kstart[k]);
+        r.kstride[k] = s.kstride[k];
+        r.kroff[k] = s.kroff[k];
+        r.base[k] = h->peer[k];
+      }
       return r;
     };
     const Remap ra = remap_of(s0), rb = remap_of(s1);

@@ -60,10 +60,16 @@ __device__ __forceinline__ void complex_swap(double (&acc)[MI][NI][2], int lane)
 }
 
 // Peer-memory store of the slab-sharded epilogue (phiks_internal.h, Remap).
-__device__ __forceinline__ void remote_store(const Remap& rm, const OutSpec& os, int64_t rowb, int j, double v) {
-  const int k = j / rm.cb;
+__device__ __forceinline__ int remap_owner(const Remap& rm, int j) {
+  const int big = (rm.cq + 1) * rm.crem;
+  return j < big ? j / (rm.cq + 1) : rm.crem + (j - big) / rm.cq;
+}
+// element (l, j, r): rowl = l (+ nothing else), r = the R index
+__device__ __forceinline__ void remote_store(const Remap& rm, const OutSpec& os, int64_t l, int64_t r, int j,
+                                             double v) {
+  const int k = remap_owner(rm, j);
   double* base = reinterpret_cast<double*>(rm.base[k] + reinterpret_cast<uintptr_t>(os.dst));
-  base[rowb + rm.colstride * static_cast<int64_t>(j - k * rm.cb)] = v;
+  base[l + rm.kstride[k] * r + rm.kroff[k] + rm.colstride * static_cast<int64_t>(j - rm.kstart[k])] = v;
 }
 
 }  // namespace
@@ -269,14 +275,13 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
             const int64_t m = m0 + wm0 + mi * 8 + lg;
             if (m >= Mtot) continue;
             const int64_t l = KMAJ ? 0 : m % L, r = KMAJ ? m : m / L;
-            const int64_t rowb = l + p.remap.rstride * r + p.remap.roff;
             const int jb = j0 + wn0 + 2 * lt;
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int j = jb + ni * 8 + e;
-                if (j < n) remote_store(p.remap, os, rowb, j, beta * acc[mi][ni][e]);
+                if (j < n) remote_store(p.remap, os, l, r, j, beta * acc[mi][ni][e]);
               }
           }
           continue;
@@ -568,16 +573,16 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
         if (REMOTE) {  // slab-sharded: stores into the owner rank's region
           const Remap& rm = p.remap;
           const int jb = T.j0 + wn0 + 2 * lt;
-          if ((rm.cb & 1) == 0) {
+          if (rm.uniform && (rm.cq & 1) == 0) {
             // columns (j, j+1) share their owner: resolve owner and column base once per
             // 8-column group, then every row is one add
             double* colp[NI];
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) {
               const int j = jb + ni * 8;
-              const int k = j < n ? j / rm.cb : 0;
-              colp[ni] = reinterpret_cast<double*>(rm.base[k] + reinterpret_cast<uintptr_t>(os.dst)) + rm.roff +
-                         rm.colstride * static_cast<int64_t>(j - k * rm.cb);
+              const int k = j < n ? j / rm.cq : 0;
+              colp[ni] = reinterpret_cast<double*>(rm.base[k] + reinterpret_cast<uintptr_t>(os.dst)) + rm.kroff[0] +
+                         rm.colstride * static_cast<int64_t>(j - rm.kstart[k]);
             }
 #pragma unroll
             for (int mi = 0; mi < MI; ++mi) {
@@ -592,7 +597,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
                 r = T.r;
                 if (l >= L) continue;
               }
-              const int64_t rowb = l + rm.rstride * r;
+              const int64_t rowb = l + rm.kstride[0] * r;
 #pragma unroll
               for (int ni = 0; ni < NI; ++ni) {
                 const int j = jb + ni * 8;
@@ -614,13 +619,12 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32, MINB)
                 r = T.r;
                 if (l >= L) continue;
               }
-              const int64_t rowb = l + rm.rstride * r + rm.roff;
 #pragma unroll
               for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                   const int j = jb + ni * 8 + e;
-                  if (j < n) remote_store(rm, os, rowb, j, beta * acc[mi][ni][e]);
+                  if (j < n) remote_store(rm, os, l, r, j, beta * acc[mi][ni][e]);
                 }
             }
           }

@@ -59,16 +59,21 @@ constexpr int kMaxBlocks = PHIKS_MAX_BLOCKS;  // diagonal blocks of K̂ per hand
 
 // Remote (peer-memory) epilogue of the slab-sharded Tucker operator: when
 // world > 0 every output of the launch is written to the symmetric region of
-// the rank that owns its column j of the μ-mode product,
-//     k = j / cb,   dst = base[k] + (size_t)OutSpec::dst (a byte offset)
-//                        + l + rstride·r + roff + colstride·(j − k·cb),
+// the rank that owns its column j of the μ-mode product.  Columns are block-
+// distributed: the first crem ranks own cq+1 columns, the others cq, so
+//     k = j < (cq+1)·crem ? j/(cq+1) : crem + (j − (cq+1)·crem)/cq,
+//     dst = base[k] + (size_t)OutSpec::dst (a byte offset)
+//           + l + kstride[k]·r + kroff[k] + colstride·(j − kstart[k]),
 // (l, j, r) the (L, n, R) coordinates of the element.  This folds the
 // slab↔slab transposition of the mode-d product into the
 // stores of the producing mode product.  Remote outputs carry no sources.
 struct Remap {
-  int world;  // 0: local outputs (OutSpec::dst is a pointer)
-  int cb;     // columns per destination rank
-  int64_t rstride, roff, colstride;
+  int world;    // 0: local outputs (OutSpec::dst is a pointer)
+  int cq, crem; // block distribution of the n columns over the ranks
+  int uniform;  // crem == 0 and every kstride / kroff equal (hoisted fast path)
+  int64_t colstride;
+  int kstart[kMaxRanks];
+  int64_t kstride[kMaxRanks], kroff[kMaxRanks];
   char* base[kMaxRanks];
 };
 

@@ -18,8 +18,7 @@ phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return fail(PHIKS_ERR_ARG, "rank/world");
   if (world > 1) {
     if (d < 2) return fail(PHIKS_ERR_ARG, "sharding needs d >= 2");
-    if (n[d - 1] % world != 0 || n[d - 2] % world != 0)
-      return fail(PHIKS_ERR_ARG, "n_d and n_{d-1} must be divisible by world");
+    if (n[d - 1] < world || n[d - 2] < world) return fail(PHIKS_ERR_ARG, "n_d and n_{d-1} must be >= world");
   }
   phiks_handle h = nullptr;
   phiks_status st = phiks_create_blocks(nblocks, d, n, A_host, &h);
@@ -27,10 +26,17 @@ phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const
   h->rank = rank;
   h->world = world;
   if (world > 1) {
-    h->n[d - 1] = n[d - 1] / world;
-    h->N /= world;
-    h->Nc /= world;
-    h->sym_slot = (static_cast<size_t>(h->N) * sizeof(double) + 255) & ~size_t(255);
+    // slabs of mode d (layout S_d) and of mode d-1 (S_{d-1}), block-distributed
+    int64_t L0 = 1;
+    for (int mu = 0; mu + 2 < d; ++mu) L0 *= n[mu];
+    const int64_t na = n[d - 2], nd = n[d - 1];
+    h->n[d - 1] = static_cast<int>(blk_cnt(nd, world, rank));
+    h->Nc = L0 * na * h->n[d - 1];
+    h->N = h->Nc;
+    int64_t slot = 0;  // the largest local tensor of either layout on any rank
+    for (int k = 0; k < world; ++k)
+      slot = std::max({slot, L0 * na * blk_cnt(nd, world, k), L0 * blk_cnt(na, world, k) * nd});
+    h->sym_slot = (static_cast<size_t>(slot) * sizeof(double) + 255) & ~size_t(255);
     h->sym_bytes = kCtrlBytes + 2 * kShardChunk * h->sym_slot;
     if (cudaMalloc(reinterpret_cast<void**>(&h->sym), h->sym_bytes) != cudaSuccess) {
       phiks_destroy(h);
@@ -184,10 +190,29 @@ phiks_status phiks_shard_layout(int d, const int* n, int rank, int world, int st
   if (!n || !out7 || d < 2 || d > PHIKS_MAX_D || world < 1 || world > kMaxRanks || rank < 0 || rank >= world ||
       (stage != 0 && stage != 1))
     return fail(PHIKS_ERR_ARG, "bad argument");
-  if (n[d - 1] % world != 0 || n[d - 2] % world != 0) return fail(PHIKS_ERR_ARG, "dims not divisible by world");
+  if (n[d - 1] % world != 0 || n[d - 2] % world != 0)
+    return fail(PHIKS_ERR_ARG, "dims not divisible by world (use phiks_shard_layout_ex)");
   const ShardStage s = shard_stage(d, n, rank, world, stage);
-  const int64_t v[7] = {s.L, s.n, s.R, s.cb, s.rstride, s.roff, s.colstride};
+  const int64_t cb = s.n / world;
+  const int64_t v[7] = {s.L, s.n, s.R, cb, s.kstride[0], s.kroff[0], s.colstride};
   for (int i = 0; i < 7; ++i) out7[i] = v[i];
+  return PHIKS_OK;
+}
+
+phiks_status phiks_shard_layout_ex(int d, const int* n, int rank, int world, int stage, int64_t* out) {
+  if (!n || !out || d < 2 || d > PHIKS_MAX_D || world < 1 || world > kMaxRanks || rank < 0 || rank >= world ||
+      (stage != 0 && stage != 1) || n[d - 1] < world || n[d - 2] < world)
+    return fail(PHIKS_ERR_ARG, "bad argument");
+  const ShardStage s = shard_stage(d, n, rank, world, stage);
+  out[0] = s.L;
+  out[1] = s.n;
+  out[2] = s.R;
+  out[3] = s.colstride;
+  for (int k = 0; k < world; ++k) {
+    out[4 + k] = s.kstart[k];
+    out[4 + world + k] = s.kstride[k];
+    out[4 + 2 * world + k] = s.kroff[k];
+  }
   return PHIKS_OK;
 }
 

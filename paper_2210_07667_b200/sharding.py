@@ -19,18 +19,31 @@ import numpy as np
 from . import _lib
 
 
-def slab_bounds(N: int, world: int, rank: int):
-    """[lo, hi) of rank's slab in the flat column-major array (N % world == 0)."""
-    if N % world:
-        raise ValueError("N must be divisible by world")
-    c = N // world
-    return rank * c, (rank + 1) * c
+def block_range(n: int, world: int, rank: int):
+    """[start, start+count) of rank's share of n indices: n // world each, one
+    more for the first n % world ranks (the library's distribution)."""
+    q, rem = divmod(n, world)
+    start = rank * q + min(rank, rem)
+    return start, start + q + (1 if rank < rem else 0)
 
 
-def split_slabs(x, world: int) -> list:
+def slab_bounds(N: int, world: int, rank: int, dims=None):
+    """[lo, hi) of rank's slab in the flat column-major array: the block of the
+    outermost mode (dims[-1]) it owns.  Without dims, N % world == 0 is required."""
+    if dims is None:
+        if N % world:
+            raise ValueError("N must be divisible by world (pass dims for ragged slabs)")
+        c = N // world
+        return rank * c, (rank + 1) * c
+    M = N // int(dims[-1])
+    a, b = block_range(int(dims[-1]), world, rank)
+    return M * a, M * b
+
+
+def split_slabs(x, world: int, dims=None) -> list:
     """Views of the world slabs of a flat global tensor (numpy or torch)."""
     N = x.shape[0] if hasattr(x, "shape") else len(x)
-    return [x[slice(*slab_bounds(N, world, r))] for r in range(world)]
+    return [x[slice(*slab_bounds(N, world, r, dims))] for r in range(world)]
 
 
 def _PhiKS():
@@ -49,7 +62,7 @@ class ShardedPhiKS:
                  group=None):
         self.op = _PhiKS()(factors, rank=rank, world=world)
         self.rank, self.world = rank, world
-        self.N = self.op.N
+        self.N = self.op.N  # this rank's slab (ragged slabs differ between ranks)
         self.dims = self.op.dims
         if connect == "dist" and world > 1:
             self.connect_dist(group)
@@ -120,12 +133,11 @@ def apply_ranks_serial(ranks: Sequence[ShardedPhiKS], tau: float, ells: Sequence
     world = len(ranks)
     m = PhiKS._mode(mode)
     nouts = ranks[0].op.nblocks * (len(ells) * n_scales if m == _lib.MODE_SAME_VECTOR else n_scales)
-    N = ranks[0].N
     if outs is None:
-        outs = [[torch.empty(N, dtype=torch.float64, device=vecs[k][0].device) for _ in range(nouts)]
+        outs = [[torch.empty(ranks[k].N, dtype=torch.float64, device=vecs[k][0].device) for _ in range(nouts)]
                 for k in range(world)]
-    vptr = [_check_dev(v, N) for k in range(world) for v in vecs[k]]
-    optr = [_check_dev(o, N) for k in range(world) for o in outs[k]]
+    vptr = [_check_dev(v, ranks[k].N) for k in range(world) for v in vecs[k]]
+    optr = [_check_dev(o, ranks[k].N) for k in range(world) for o in outs[k]]
     req = _lib.make_request(m, ells, n_scales, tau, tol)
     hs = (ctypes.c_void_p * world)(*[r.op._h.value for r in ranks])
     _lib.check(_lib.load().phiks_apply_ranks_serial(hs, world, ctypes.byref(req), len(vecs[0]),

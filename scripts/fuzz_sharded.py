@@ -17,8 +17,12 @@ for c in range(count):
     P = int(rng.choice([2, 4, 8]))
     d = int(rng.integers(2, 5))
     dims = [int(x) for x in rng.integers(2, 40 if d <= 3 else 12, size=d)]
-    dims[-1] = P * int(rng.integers(1, 40 if d <= 3 else 6))
-    dims[-2] = P * int(rng.integers(1, 40 if d <= 3 else 6))
+    if os.environ.get("RAGGED"):
+        dims[-1] = P + int(rng.integers(0, 60 if d <= 3 else 12))
+        dims[-2] = P + int(rng.integers(0, 60 if d <= 3 else 12))
+    else:
+        dims[-1] = P * int(rng.integers(1, 40 if d <= 3 else 6))
+        dims[-2] = P * int(rng.integers(1, 40 if d <= 3 else 6))
     dims = tuple(dims)
     fac = W.random_factors(dims, seed=2000 + c, scale=float(rng.uniform(0.2, 20.0)))
     mode = "same" if rng.integers(0, 2) == 0 else "lincomb"
@@ -32,7 +36,8 @@ for c in range(count):
         single = PhiKS(fac).apply(tau, ells, [torch.from_numpy(v.copy()).cuda() for v in vs], mode=mode, n_scales=ns)
         ranks = [ShardedPhiKS(fac, r, P, connect=None) for r in range(P)]
         ShardedPhiKS.connect_local(ranks)
-        vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(v, P)[r])).cuda() for v in vs] for r in range(P)]
+        vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(v, P, dims)[r])).cuda() for v in vs]
+                for r in range(P)]
         outs = apply_ranks_serial(ranks, tau, ells, vecs, mode=mode, n_scales=ns)
         torch.cuda.synchronize()
         e = 0.0

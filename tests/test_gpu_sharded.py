@@ -126,3 +126,33 @@ def test_sharded_world1_is_plain_handle():
     single, _ = run_single(pb)
     for a, b in zip(outs, single):
         assert np.array_equal(a, b)
+
+
+def run_sharded_ragged(pb, world):
+    ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
+    ShardedPhiKS.connect_local(ranks)
+    flat = [W.as_flat(v) for v in pb.vs]
+    vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, world, pb.dims)[r])).to(DEV) for x in flat]
+            for r in range(world)]
+    outs = apply_ranks_serial(ranks, pb.tau, pb.ells, vecs, mode=pb.mode, n_scales=pb.n_scales)
+    torch.cuda.synchronize()
+    gathered = [torch.cat([outs[r][i] for r in range(world)]).cpu().numpy() for i in range(len(outs[0]))]
+    for r in ranks:
+        r.close()
+    return gathered
+
+
+@pytest.mark.parametrize("dims,world,mode", [((6, 10, 7), 3, "same"), ((5, 9, 11), 4, "lincomb"),
+                                             ((4, 13, 10), 8, "same"), ((30, 25), 6, "lincomb"),
+                                             ((3, 4, 9, 9), 2, "same"), ((40, 130, 70), 8, "same")])
+def test_sharded_ragged_slabs(dims, world, mode):
+    # P does not divide n_d and/or n_{d-1}: block-distributed slabs of different sizes
+    fac = W.random_factors(dims, seed=sum(dims) + world, scale=4.0)
+    ells = (0, 1, 2)
+    vs = [W.random_tensor(dims, seed=7 + k) for k in range(1 if mode == "same" else 3)]
+    pb = W.Problem(f"ragged_{dims}_{world}", dims, fac, 0.6, mode, ells, vs, 2)
+    outs = run_sharded_ragged(pb, world)
+    compare_oracle(pb, outs, 2)
+    single, _ = run_single(pb)
+    for a, b in zip(outs, single):
+        assert rel2(a, b) <= 1e-15

@@ -116,7 +116,7 @@ def test_create_sharded_rejects_bad_arguments():
     ptrs = _lib.ptr_array([A.ctypes.data] * 3)
     h = ctypes.c_void_p()
     n3 = (ctypes.c_int * 3)(8, 8, 8)
-    n_bad = (ctypes.c_int * 3)(8, 6, 8)   # n_{d-1} = 6 not divisible by 4
+    n_bad = (ctypes.c_int * 3)(8, 3, 8)   # n_{d-1} = 3 < world = 4
     n1 = (ctypes.c_int * 1)(8)
     assert lib.phiks_create_sharded(3, n3, ptrs, 0, 9, ctypes.byref(h)) == 1   # world > 8
     assert lib.phiks_create_sharded(3, n3, ptrs, 2, 2, ctypes.byref(h)) == 1   # rank >= world
@@ -191,3 +191,82 @@ def test_sharded_tucker_gloo_world2():
     for rank, full, nrm in res:
         np.testing.assert_allclose(full, ref, rtol=1e-13, atol=1e-13)
         assert abs(nrm - np.linalg.norm(x)) <= 1e-13 * np.linalg.norm(x)
+
+
+# ---------------------------------------------------------------------------
+# ragged slabs (P not dividing n_d or n_{d-1}): phiks_shard_layout_ex
+# ---------------------------------------------------------------------------
+from paper_2210_07667_b200.sharding import block_range  # noqa: E402
+
+
+def layout_ex(dims, rank, world, stage):
+    lib = _lib.load()
+    out = (ctypes.c_int64 * (4 + 3 * world))()
+    n = (ctypes.c_int * len(dims))(*dims)
+    _lib.check(lib.phiks_shard_layout_ex(len(dims), n, rank, world, stage, out), "phiks_shard_layout_ex")
+    v = list(out)
+    return {"L": v[0], "n": v[1], "R": v[2], "colstride": v[3], "kstart": v[4:4 + world],
+            "kstride": v[4 + world:4 + 2 * world], "kroff": v[4 + 2 * world:4 + 3 * world]}
+
+
+def owner(j, n, world):
+    return next(k for k in range(world) if j < block_range(n, world, k)[1])
+
+
+def peer_store_ex(Y, lay, world):
+    L, n, R = Y.shape
+    l, j, r = np.meshgrid(np.arange(L), np.arange(n), np.arange(R), indexing="ij")
+    k = np.vectorize(lambda jj: owner(jj, n, world))(j)
+    ks = np.asarray(lay["kstart"])[k]
+    kst = np.asarray(lay["kstride"])[k]
+    kro = np.asarray(lay["kroff"])[k]
+    off = l + kst * r + kro + lay["colstride"] * (j - ks)
+    return [(off[k == q], Y[k == q]) for q in range(world)]
+
+
+def simulate_ragged(dims, mats, x, world):
+    d = len(dims)
+    L0 = int(np.prod(dims[:-2]))
+    na, nd = dims[-2], dims[-1]
+    slabs = []
+    for r, s in enumerate(split_slabs(x, world, dims)):
+        ld = list(dims)
+        a, b = block_range(nd, world, r)
+        ld[-1] = b - a
+        T = W.from_flat(s.copy(), ld)
+        for mu in range(d - 2):
+            T = O.mu_mode_product(T, mats[mu], mu)
+        slabs.append(W.as_flat(T))
+    sizes = [[L0 * (block_range(na, world, k)[1] - block_range(na, world, k)[0]) * nd for k in range(world)],
+             [L0 * na * (block_range(nd, world, k)[1] - block_range(nd, world, k)[0]) for k in range(world)]]
+    for stage in (0, 1):
+        recv = [np.full(sizes[stage][k], np.nan) for k in range(world)]
+        for r in range(world):
+            lay = layout_ex(dims, r, world, stage)
+            Y = local_mode_product(slabs[r], lay["L"], lay["n"], lay["R"], mats[d - 2 + stage])
+            for q, (off, val) in enumerate(peer_store_ex(Y, lay, world)):
+                assert np.all(np.isnan(recv[q][off])), "two stores hit one element"
+                recv[q][off] = val
+        assert not any(np.isnan(v).any() for v in recv), "an element received no store"
+        slabs = recv
+    return np.concatenate(slabs)
+
+
+@pytest.mark.parametrize("dims,world", [((5, 7, 10), 3), ((6, 9), 4), ((3, 10, 9), 8), ((2, 3, 5, 9), 2),
+                                        ((4, 8, 8), 4)])
+def test_ragged_sharded_tucker_simulation_equals_oracle(dims, world):
+    mats = W.random_factors(dims, seed=17, scale=1.0)
+    x = W.as_flat(W.random_tensor(dims, seed=4))
+    got = simulate_ragged(dims, mats, x, world)
+    ref = W.as_flat(O.tucker(W.from_flat(x, dims), mats))
+    np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13)
+
+
+def test_layout_ex_matches_uniform_layout():
+    dims, world = (5, 8, 16), 4
+    for stage in (0, 1):
+        for r in range(world):
+            a, b = layout(dims, r, world, stage), layout_ex(dims, r, world, stage)
+            assert (a["L"], a["n"], a["R"], a["colstride"]) == (b["L"], b["n"], b["R"], b["colstride"])
+            assert all(s == a["rstride"] for s in b["kstride"]) and all(o == a["roff"] for o in b["kroff"])
+            assert b["kstart"] == [k * a["cb"] for k in range(world)]
