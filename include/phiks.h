@@ -278,7 +278,13 @@ phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_ho
 phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const double* const* A_host, int rank,
                                          int world, phiks_handle* out);
 
-/* rank, world, local slab size in doubles, bytes of the symmetric region
+/* Sharded handle of a complex K (phiks_create_complex × phiks_create_sharded):
+   the complex μ-mode products run locally and the two transposition stages
+   move their results with peer-store copies (real view (2, n_1, …, n_d)). */
+phiks_status phiks_create_sharded_complex(int d, const int* n, const double* const* A_host, int rank, int world,
+                                          phiks_handle* out);
+
+/* rank, world, local slab size in elements, bytes of the symmetric region
    (any output pointer may be NULL). */
 phiks_status phiks_shard_info(phiks_handle h, int* rank, int* world, int64_t* local_count,
                               size_t* sym_bytes);

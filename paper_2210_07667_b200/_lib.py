@@ -79,6 +79,7 @@ def load() -> ctypes.CDLL:
     lib.phiks_create_sharded.argtypes = [i, P(i), P(vp), i, i, P(vp)]
     lib.phiks_create_blocks.argtypes = [i, i, P(i), P(vp), P(vp)]
     lib.phiks_create_sharded_blocks.argtypes = [i, i, P(i), P(vp), i, i, P(vp)]
+    lib.phiks_create_sharded_complex.argtypes = [i, P(i), P(vp), i, i, P(vp)]
     lib.phiks_shard_info.argtypes = [vp, P(i), P(i), P(ctypes.c_int64), P(ctypes.c_size_t)]
     lib.phiks_shard_ipc_handle.argtypes = [vp, vp]
     lib.phiks_shard_open_peers.argtypes = [vp, vp]
@@ -98,7 +99,8 @@ def load() -> ctypes.CDLL:
                  "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan", "phiks_set_profiling",
                  "phiks_create_sharded", "phiks_shard_info", "phiks_shard_ipc_handle", "phiks_shard_open_peers",
                  "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_shard_layout", "phiks_wait", "phiks_shard_peer_base", "phiks_create_complex", "phiks_plan_host_complex", "phiks_create_blocks",
-                 "phiks_create_sharded_blocks", "phiks_shard_layout_ex"):
+                 "phiks_create_sharded_blocks", "phiks_shard_layout_ex",
+                 "phiks_create_sharded_complex"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

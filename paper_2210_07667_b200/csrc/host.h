@@ -624,8 +624,132 @@ struct Exec {
   double* symY(int i) const {
     return reinterpret_cast<double*>(h->sym + kCtrlBytes + (kShardChunk + i) * h->sym_slot);
   }
+  // complex sharded handles: every product local (two accumulating real terms
+  // for modes μ ≥ 2, the 2n×2n real form for μ = 1), the two transposition stages
+  // as peer-store copies with the geometry of the real view (2, n_1, …, n_d)
+  void tucker_raw_sharded_complex(const std::vector<TuckerItem>& items) {
+    const int d = h->d, P = h->world, rk = h->rank;
+    const size_t nb = items.size();
+    const int64_t slotd = static_cast<int64_t>(h->sym_slot / sizeof(double));
+    auto& scr = scr_pool;
+    while (scr[0].size() < nb) scr[0].push_back(ar->alloc_doubles(slotd));
+    while (scr[1].size() < nb) scr[1].push_back(ar->alloc_doubles(slotd));
+    int gv[PHIKS_MAX_D + 1];
+    gv[0] = 2;
+    for (int mu = 0; mu < d; ++mu) gv[mu + 1] = h->gn[mu];
+    // one complex μ-mode product on the local layout whose dims are dims[0..d-1]
+    auto cproduct = [&](int mu, const int* dims, std::vector<const double*> in, std::vector<double*> out,
+                        std::vector<const double*> mats) {
+      int64_t Lc = 1, Nc = 1;
+      for (int k = 0; k < d; ++k) Nc *= dims[k];
+      for (int k = 0; k < mu; ++k) Lc *= dims[k];
+      const int n = dims[mu];
+      const int64_t R = Nc / (Lc * n);
+      std::vector<LaunchTerm> terms;
+      for (size_t b = 0; b < nb; ++b) {
+        LaunchTerm t;
+        t.in = in[b];
+        t.group = static_cast<int>(b);
+        t.outs.push_back(Out{out[b], 1.0, {}});
+        if (mu == 0) {
+          t.M = mats[b];
+          terms.push_back(std::move(t));
+        } else {
+          const auto parts = complex_parts(mats[b], n);
+          LaunchTerm ti = t;
+          t.M = parts.first;
+          ti.M = parts.second;
+          ti.cswap = 1;
+          for (Out& o : ti.outs) o.srcs.assign(1, Src{o.dst, 1.0});
+          terms.push_back(std::move(t));
+          terms.push_back(std::move(ti));
+        }
+      }
+      if (mu == 0)
+        mode_launch(1, 2 * n, R, terms);
+      else
+        mode_launch(2 * Lc, n, R, terms);
+    };
+    auto remap_copy = [&](const ShardStage& s, const double* src, size_t dst_off) {
+      Remap r{};
+      r.world = P;
+      r.cq = static_cast<int>(s.n / P);
+      r.crem = static_cast<int>(s.n % P);
+      r.uniform = s.uniform ? 1 : 0;
+      r.colstride = s.colstride;
+      for (int k = 0; k < P; ++k) {
+        r.kstart[k] = static_cast<int>(s.kstart[k]);
+        r.kstride[k] = s.kstride[k];
+        r.kroff[k] = s.kroff[k];
+        r.base[k] = h->peer[k];
+      }
+      const int64_t L = s.L, R = s.R;
+      const int n = static_cast<int>(s.n);
+      emit("remap_copy", [src, L, n, R, dst_off, r](cudaStream_t st2) {
+        return launch_remap_copy(src, L, n, R, dst_off, r, st2);
+      });
+    };
+    // local dims of layout S_d
+    int dimsS[PHIKS_MAX_D];
+    for (int k = 0; k < d; ++k) dimsS[k] = h->n[k];
+    std::vector<const double*> cur(nb);
+    for (size_t b = 0; b < nb; ++b) cur[b] = items[b].in;
+    int ping = 0;
+    for (int mu = 0; mu + 2 < d; ++mu) {
+      std::vector<double*> outv(nb);
+      std::vector<const double*> mats(nb);
+      for (size_t b = 0; b < nb; ++b) {
+        outv[b] = scr[ping][b];
+        mats[b] = items[b].mats[mu];
+      }
+      cproduct(mu, dimsS, cur, outv, mats);
+      for (size_t b = 0; b < nb; ++b) cur[b] = outv[b];
+      ping ^= 1;
+    }
+    // stage 0: mode d-1 locally, then to the owners' T pools (layout S_{d-1})
+    {
+      std::vector<double*> outv(nb);
+      std::vector<const double*> mats(nb);
+      for (size_t b = 0; b < nb; ++b) {
+        outv[b] = scr[ping][b];
+        mats[b] = items[b].mats[d - 2];
+      }
+      cproduct(d - 2, dimsS, cur, outv, mats);
+      const ShardStage s0 = shard_stage(d + 1, gv, rk, P, 0);
+      for (size_t b = 0; b < nb; ++b) remap_copy(s0, outv[b], kCtrlBytes + b * h->sym_slot);
+      ping ^= 1;
+    }
+    barrier();
+    // stage 1: mode d locally on the transposed slab, then back to layout S_d
+    {
+      int dimsT[PHIKS_MAX_D];
+      for (int k = 0; k < d; ++k) dimsT[k] = h->gn[k];
+      dimsT[d - 2] = static_cast<int>(blk_cnt(h->gn[d - 2], P, rk));
+      std::vector<const double*> in(nb);
+      std::vector<double*> outv(nb);
+      std::vector<const double*> mats(nb);
+      for (size_t b = 0; b < nb; ++b) {
+        in[b] = symT(static_cast<int>(b));
+        outv[b] = scr[ping][b];
+        mats[b] = items[b].mats[d - 1];
+      }
+      cproduct(d - 1, dimsT, in, outv, mats);
+      const ShardStage s1 = shard_stage(d + 1, gv, rk, P, 1);
+      for (size_t b = 0; b < nb; ++b) remap_copy(s1, outv[b], kCtrlBytes + (kShardChunk + b) * h->sym_slot);
+    }
+    barrier();
+    int64_t nsum = 0;
+    for (int mu = 0; mu < d; ++mu) nsum += h->gn[mu];
+    tucker_ops += static_cast<int64_t>(nb);
+    mu_flops += static_cast<double>(nb) * 8.0 * static_cast<double>(h->Nc) * static_cast<double>(nsum);
+  }
+
   void tucker_raw_sharded(const std::vector<TuckerItem>& items) {
     if (!ok() || items.empty()) return;
+    if (h->cplx) {
+      tucker_raw_sharded_complex(items);
+      return;
+    }
     const int d = h->d, P = h->world, rk = h->rank;
     const int64_t N = h->N;
     const size_t nb = items.size();

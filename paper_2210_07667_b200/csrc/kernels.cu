@@ -990,6 +990,37 @@ cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, dou
 }
 
 // ---------------------------------------------------------------------------
+// Peer-store copy of a local (L, n, R) tensor with the Remap of a sharded stage
+// (complex sharded handles: the complex μ-mode product is two accumulating real
+// products, computed locally, then moved to the owners by this kernel).
+__global__ void remap_copy_kernel(const double* __restrict__ src, int64_t L, int n, int64_t R, size_t dst_off,
+                                  const __grid_constant__ Remap rm) {
+  const int64_t total = L * n * R;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t l = e % L;
+    const int64_t t = e / L;
+    const int j = static_cast<int>(t % n);
+    const int64_t r = t / n;
+    const int k = remap_owner(rm, j);
+    double* base = reinterpret_cast<double*>(rm.base[k] + dst_off);
+    base[l + rm.kstride[k] * r + rm.kroff[k] + rm.colstride * static_cast<int64_t>(j - rm.kstart[k])] = src[e];
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+cudaError_t launch_remap_copy(const double* src, int64_t L, int n, int64_t R, size_t dst_off, const Remap& rm,
+                              cudaStream_t st) {
+  const int64_t total = L * n * R;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) return cudaSuccess;
+  remap_copy_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(src, L, n, R, dst_off, rm);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Real and imaginary parts of a complex n×n matrix from its interleaved real
 // form R (2n×2n column-major, R[(c+2j) + (c'+2k)·2n] = [[Mr, −Mi], [Mi, Mr]]_{cc'}(j,k)).
 __global__ void complex_parts_kernel(const double* R, int n, double* Mr, double* Mi) {

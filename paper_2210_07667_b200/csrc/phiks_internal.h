@@ -121,6 +121,9 @@ cudaError_t launch_multi_combine(const MultiCombineParams& p, cudaStream_t st);
 cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, double* scratch,
                          double* norms2, cudaStream_t st);
 cudaError_t launch_set_identity(double* E, int n, double diag, cudaStream_t st);
+// dst(owner, offset) = src(l, j, r) for a local (L, n, R) tensor under a Remap
+cudaError_t launch_remap_copy(const double* src, int64_t L, int n, int64_t R, size_t dst_off, const Remap& rm,
+                              cudaStream_t st);
 // Mr, Mi (n×n) from the interleaved real form R (2n×2n) of a complex matrix
 cudaError_t launch_complex_parts(const double* R, int n, double* Mr, double* Mi, cudaStream_t st);
 

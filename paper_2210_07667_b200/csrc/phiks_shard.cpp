@@ -11,8 +11,27 @@ phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_ho
   return phiks_create_sharded_blocks(1, d, n, A_host, rank, world, out);
 }
 
+}  // extern "C"
+
+static phiks_status create_sharded_impl(int nblocks, int d, const int* n, const double* const* A_host, int rank,
+                                        int world, bool cplx, phiks_handle* out);
+
+extern "C" {
+
 phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const double* const* A_host, int rank,
                                          int world, phiks_handle* out) {
+  return create_sharded_impl(nblocks, d, n, A_host, rank, world, false, out);
+}
+
+phiks_status phiks_create_sharded_complex(int d, const int* n, const double* const* A_host, int rank, int world,
+                                          phiks_handle* out) {
+  return create_sharded_impl(1, d, n, A_host, rank, world, true, out);
+}
+
+}  // extern "C"
+
+static phiks_status create_sharded_impl(int nblocks, int d, const int* n, const double* const* A_host, int rank,
+                                        int world, bool cplx, phiks_handle* out) {
   if (!out || !n) return fail(PHIKS_ERR_ARG, "null argument");
   *out = nullptr;
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return fail(PHIKS_ERR_ARG, "rank/world");
@@ -21,7 +40,7 @@ phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const
     if (n[d - 1] < world || n[d - 2] < world) return fail(PHIKS_ERR_ARG, "n_d and n_{d-1} must be >= world");
   }
   phiks_handle h = nullptr;
-  phiks_status st = phiks_create_blocks(nblocks, d, n, A_host, &h);
+  phiks_status st = cplx ? phiks_create_complex(d, n, A_host, &h) : phiks_create_blocks(nblocks, d, n, A_host, &h);
   if (st != PHIKS_OK) return st;
   h->rank = rank;
   h->world = world;
@@ -32,10 +51,11 @@ phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const
     const int64_t na = n[d - 2], nd = n[d - 1];
     h->n[d - 1] = static_cast<int>(blk_cnt(nd, world, rank));
     h->Nc = L0 * na * h->n[d - 1];
-    h->N = h->Nc;
-    int64_t slot = 0;  // the largest local tensor of either layout on any rank
+    h->N = cplx ? 2 * h->Nc : h->Nc;
+    int64_t slot = 0;  // the largest local tensor of either layout on any rank (in doubles)
     for (int k = 0; k < world; ++k)
       slot = std::max({slot, L0 * na * blk_cnt(nd, world, k), L0 * blk_cnt(na, world, k) * nd});
+    if (cplx) slot *= 2;
     h->sym_slot = (static_cast<size_t>(slot) * sizeof(double) + 255) & ~size_t(255);
     h->sym_bytes = kCtrlBytes + 2 * kShardChunk * h->sym_slot;
     if (cudaMalloc(reinterpret_cast<void**>(&h->sym), h->sym_bytes) != cudaSuccess) {
@@ -54,11 +74,13 @@ phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const
   return PHIKS_OK;
 }
 
+extern "C" {
+
 phiks_status phiks_shard_info(phiks_handle h, int* rank, int* world, int64_t* local_count, size_t* sym_bytes) {
   if (!h) return fail(PHIKS_ERR_ARG, "null handle");
   if (rank) *rank = h->rank;
   if (world) *world = h->world;
-  if (local_count) *local_count = h->N;
+  if (local_count) *local_count = h->Nc;
   if (sym_bytes) *sym_bytes = h->sym_bytes;
   return PHIKS_OK;
 }

@@ -133,11 +133,13 @@ def apply_ranks_serial(ranks: Sequence[ShardedPhiKS], tau: float, ells: Sequence
     world = len(ranks)
     m = PhiKS._mode(mode)
     nouts = ranks[0].op.nblocks * (len(ells) * n_scales if m == _lib.MODE_SAME_VECTOR else n_scales)
+    cplx = ranks[0].op.complex
+    dt = torch.complex128 if cplx else torch.float64
     if outs is None:
-        outs = [[torch.empty(ranks[k].N, dtype=torch.float64, device=vecs[k][0].device) for _ in range(nouts)]
+        outs = [[torch.empty(ranks[k].N, dtype=dt, device=vecs[k][0].device) for _ in range(nouts)]
                 for k in range(world)]
-    vptr = [_check_dev(v, ranks[k].N) for k in range(world) for v in vecs[k]]
-    optr = [_check_dev(o, ranks[k].N) for k in range(world) for o in outs[k]]
+    vptr = [_check_dev(v, ranks[k].N, cplx) for k in range(world) for v in vecs[k]]
+    optr = [_check_dev(o, ranks[k].N, cplx) for k in range(world) for o in outs[k]]
     req = _lib.make_request(m, ells, n_scales, tau, tol)
     hs = (ctypes.c_void_p * world)(*[r.op._h.value for r in ranks])
     _lib.check(_lib.load().phiks_apply_ranks_serial(hs, world, ctypes.byref(req), len(vecs[0]),

@@ -156,3 +156,28 @@ def test_sharded_ragged_slabs(dims, world, mode):
     single, _ = run_single(pb)
     for a, b in zip(outs, single):
         assert rel2(a, b) <= 1e-15
+
+
+@pytest.mark.parametrize("dims,world,mode", [((6, 8, 8), 2, "same"), ((5, 9, 7), 3, "lincomb"), ((12, 10), 4, "same"),
+                                             ((3, 4, 5, 8), 4, "lincomb"), ((70, 66, 40), 8, "same")])
+def test_sharded_complex(dims, world, mode):
+    fac = W.random_factors(dims, seed=sum(dims), scale=3.0, complex_=True)
+    ells = (0, 1, 2)
+    vs = [W.random_tensor(dims, seed=11 + k, complex_=True) for k in range(1 if mode == "same" else 3)]
+    pb = W.Problem(f"cplx_shard_{dims}_{world}", dims, fac, 0.7, mode, ells, vs, 2)
+    ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
+    ShardedPhiKS.connect_local(ranks)
+    flat = [W.as_flat(v) for v in pb.vs]
+    vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, world, dims)[r])).to(DEV) for x in flat]
+            for r in range(world)]
+    outs = apply_ranks_serial(ranks, pb.tau, pb.ells, vecs, mode=pb.mode, n_scales=pb.n_scales)
+    torch.cuda.synchronize()
+    gathered = [torch.cat([outs[r][i] for r in range(world)]).cpu().numpy() for i in range(len(outs[0]))]
+    for r in ranks:
+        r.close()
+    compare_oracle(pb, gathered, 2)
+    single = PhiKS(pb.A).apply(pb.tau, pb.ells, [torch.from_numpy(np.ascontiguousarray(x)).to(DEV) for x in flat],
+                               mode=pb.mode, n_scales=2)
+    torch.cuda.synchronize()
+    for a, b in zip(gathered, single):
+        assert rel2(a, b.cpu().numpy()) <= 1e-15
