@@ -140,6 +140,10 @@ phiks_status phiks_wait(phiks_handle h);
 phiks_status phiks_create_blocks(int nblocks, int d, const int* n, const double* const* A_host,
                                  phiks_handle* out);
 
+/* phiks_create_blocks with complex factors (interleaved, as phiks_create_complex). */
+phiks_status phiks_create_blocks_complex(int nblocks, int d, const int* n, const double* const* A_host,
+                                         phiks_handle* out);
+
 /* Complex K (§4.1 validates PHIKS on the complex operator
    (1+i)/100·Δ): as phiks_create, but A_host[μ] points to an n[μ]×n[μ]
    column-major complex matrix stored as interleaved (re, im) doubles
@@ -283,6 +287,10 @@ phiks_status phiks_create_sharded_blocks(int nblocks, int d, const int* n, const
    move their results with peer-store copies (real view (2, n_1, …, n_d)). */
 phiks_status phiks_create_sharded_complex(int d, const int* n, const double* const* A_host, int rank, int world,
                                           phiks_handle* out);
+
+/* Sharded block-diagonal handle with complex factors. */
+phiks_status phiks_create_sharded_blocks_complex(int nblocks, int d, const int* n, const double* const* A_host,
+                                                 int rank, int world, phiks_handle* out);
 
 /* rank, world, local slab size in elements, bytes of the symmetric region
    (any output pointer may be NULL). */

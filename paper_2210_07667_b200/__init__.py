@@ -80,13 +80,13 @@ class PhiKS:
         a_arr = _lib.ptr_array([a.ctypes.data for a in self._A])
         h = ctypes.c_void_p()
         if self.complex:
-            if self.nblocks != 1:
-                raise ValueError("complex factors: one block")
             if self.world == 1:
-                _lib.check(lib.phiks_create_complex(self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create_complex")
+                _lib.check(lib.phiks_create_blocks_complex(self.nblocks, self.d, n_arr, a_arr, ctypes.byref(h)),
+                           "phiks_create_complex")
             else:
-                _lib.check(lib.phiks_create_sharded_complex(self.d, n_arr, a_arr, self.rank, self.world,
-                                                            ctypes.byref(h)), "phiks_create_sharded_complex")
+                _lib.check(lib.phiks_create_sharded_blocks_complex(self.nblocks, self.d, n_arr, a_arr, self.rank,
+                                                                   self.world, ctypes.byref(h)),
+                           "phiks_create_sharded_complex")
         elif self.world == 1:
             _lib.check(lib.phiks_create_blocks(self.nblocks, self.d, n_arr, a_arr, ctypes.byref(h)), "phiks_create")
         else:

@@ -80,6 +80,8 @@ def load() -> ctypes.CDLL:
     lib.phiks_create_blocks.argtypes = [i, i, P(i), P(vp), P(vp)]
     lib.phiks_create_sharded_blocks.argtypes = [i, i, P(i), P(vp), i, i, P(vp)]
     lib.phiks_create_sharded_complex.argtypes = [i, P(i), P(vp), i, i, P(vp)]
+    lib.phiks_create_blocks_complex.argtypes = [i, i, P(i), P(vp), P(vp)]
+    lib.phiks_create_sharded_blocks_complex.argtypes = [i, i, P(i), P(vp), i, i, P(vp)]
     lib.phiks_shard_info.argtypes = [vp, P(i), P(i), P(ctypes.c_int64), P(ctypes.c_size_t)]
     lib.phiks_shard_ipc_handle.argtypes = [vp, vp]
     lib.phiks_shard_open_peers.argtypes = [vp, vp]
@@ -100,7 +102,8 @@ def load() -> ctypes.CDLL:
                  "phiks_create_sharded", "phiks_shard_info", "phiks_shard_ipc_handle", "phiks_shard_open_peers",
                  "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_shard_layout", "phiks_wait", "phiks_shard_peer_base", "phiks_create_complex", "phiks_plan_host_complex", "phiks_create_blocks",
                  "phiks_create_sharded_blocks", "phiks_shard_layout_ex",
-                 "phiks_create_sharded_complex"):
+                 "phiks_create_sharded_complex", "phiks_create_blocks_complex",
+                 "phiks_create_sharded_blocks_complex"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

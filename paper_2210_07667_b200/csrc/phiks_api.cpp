@@ -132,6 +132,11 @@ phiks_status phiks_create_blocks(int nblocks, int d, const int* n, const double*
   return create_impl(d, n, A_host, false, out, nblocks);
 }
 
+phiks_status phiks_create_blocks_complex(int nblocks, int d, const int* n, const double* const* A_host,
+                                         phiks_handle* out) {
+  return create_impl(d, n, A_host, true, out, nblocks);
+}
+
 phiks_status phiks_destroy(phiks_handle h) {
   if (!h) return PHIKS_OK;
   for (auto& F : h->factors)

@@ -28,6 +28,11 @@ phiks_status phiks_create_sharded_complex(int d, const int* n, const double* con
   return create_sharded_impl(1, d, n, A_host, rank, world, true, out);
 }
 
+phiks_status phiks_create_sharded_blocks_complex(int nblocks, int d, const int* n, const double* const* A_host,
+                                                 int rank, int world, phiks_handle* out) {
+  return create_sharded_impl(nblocks, d, n, A_host, rank, world, true, out);
+}
+
 }  // extern "C"
 
 static phiks_status create_sharded_impl(int nblocks, int d, const int* n, const double* const* A_host, int rank,
@@ -40,7 +45,8 @@ static phiks_status create_sharded_impl(int nblocks, int d, const int* n, const 
     if (n[d - 1] < world || n[d - 2] < world) return fail(PHIKS_ERR_ARG, "n_d and n_{d-1} must be >= world");
   }
   phiks_handle h = nullptr;
-  phiks_status st = cplx ? phiks_create_complex(d, n, A_host, &h) : phiks_create_blocks(nblocks, d, n, A_host, &h);
+  phiks_status st = cplx ? phiks_create_blocks_complex(nblocks, d, n, A_host, &h)
+                         : phiks_create_blocks(nblocks, d, n, A_host, &h);
   if (st != PHIKS_OK) return st;
   h->rank = rank;
   h->world = world;

@@ -94,3 +94,36 @@ def test_blocks_sharded_emulated():
         assert rel2(got, single[k].cpu().numpy()) <= 1e-15, k
     for r in ranks:
         r.close()
+
+
+def test_blocks_complex():
+    # complex factors in a block-diagonal handle (phiks_create_blocks_complex)
+    dims = (14, 9, 6)
+    pbs = []
+    for b, scale in enumerate((1.0, 12.0)):
+        fac = W.random_factors(dims, seed=300 + b, scale=scale, complex_=True)
+        vs = [W.random_tensor(dims, seed=310 + 3 * b + k, complex_=True) for k in range(3)]
+        pbs.append(W.Problem(f"cblk{b}", dims, fac, 0.7, "lincomb", (0, 1, 2), vs, 2))
+    op = check_blocks(pbs)
+    assert op.complex
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_blocks_complex_sharded_emulated(world):
+    dims = (7, 11, 10)
+    pbs = [W.Problem(f"cb{b}", dims, W.random_factors(dims, seed=320 + b, scale=4.0, complex_=True), 0.5, "same",
+                     (0, 1, 3), [W.random_tensor(dims, seed=330 + b, complex_=True)], 2) for b in range(2)]
+    ranks = [ShardedPhiKS([pb.A for pb in pbs], r, world, connect=None) for r in range(world)]
+    ShardedPhiKS.connect_local(ranks)
+    slabs = [split_slabs(W.as_flat(pb.vs[0]), world, dims) for pb in pbs]
+    vecs = [[torch.from_numpy(np.ascontiguousarray(slabs[b][r])).to(DEV) for b in range(len(pbs))]
+            for r in range(world)]
+    outs = apply_ranks_serial(ranks, 0.5, (0, 1, 3), vecs, mode="same", n_scales=2)
+    torch.cuda.synchronize()
+    single = PhiKS([pb.A for pb in pbs]).apply(0.5, (0, 1, 3), [dev(pb.vs[0]) for pb in pbs], n_scales=2)
+    torch.cuda.synchronize()
+    for k in range(len(single)):
+        got = torch.cat([outs[r][k] for r in range(world)]).cpu().numpy()
+        assert rel2(got, single[k].cpu().numpy()) <= 1e-15, k
+    for r in ranks:
+        r.close()
