@@ -200,6 +200,21 @@ phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out);
 phiks_status phiks_mode_product(int d, const int* n, int mu, int batch, const double* const* in,
                                 const double* const* M, double* const* out, void* stream);
 
+/* The μ-mode product of phiks_mode_product on the int8 tensor cores
+   (tcgen05.mma kind::i8): every mode-μ fiber of in[b] and every
+   row of M[b] is written exactly in `slices` (6 or 7) balanced base-256
+   digits scaled by a power of two, and the digit products with s + t < S are
+   accumulated exactly in int32; with 7 digits each operand keeps 55 bits and
+   the error bound is that of an fp64 dot product (§3.1 Eq. (13) is
+   the product computed).  n_μ ≤ 256.  `workspace` is device memory of at
+   least phiks_mode_product_i8_workspace bytes (owned by the caller, reused
+   across calls on the same stream); errors as phiks_mode_product,
+   PHIKS_ERR_ARG for unsupported sizes or digit counts. */
+phiks_status phiks_mode_product_i8_workspace(int d, const int* n, int mu, int slices, int batch, size_t* bytes);
+phiks_status phiks_mode_product_i8(int d, const int* n, int mu, int slices, int batch, const double* const* in,
+                                   const double* const* M, double* const* out, void* workspace, size_t ws_bytes,
+                                   void* stream);
+
 /* Tucker operator (Eq. (4)): out = in ×_1 M_0 ×_2 M_1 … ×_d M_{d-1},
    device pointers; scratch: 2*N doubles of device memory (NULL if d == 1). */
 phiks_status phiks_tucker(int d, const int* n, const double* in, const double* const* M,

@@ -206,6 +206,26 @@ def mode_product(dims: Sequence[int], mu: int, ins: Sequence, Ms: Sequence, outs
                "phiks_mode_product")
 
 
+def mode_product_i8(dims: Sequence[int], mu: int, ins: Sequence, Ms: Sequence, outs: Sequence, slices: int = 8,
+                    workspace=None, stream=None):
+    """mode_product on the int8 tensor cores (exact 7-bit slicing)."""
+    lib = _lib.load()
+    torch = _torch()
+    N = int(np.prod(dims))
+    n_arr = (ctypes.c_int * len(dims))(*dims)
+    need = ctypes.c_size_t(0)
+    _lib.check(lib.phiks_mode_product_i8_workspace(len(dims), n_arr, int(mu), int(slices), len(ins),
+                                                   ctypes.byref(need)), "phiks_mode_product_i8_workspace")
+    if workspace is None or workspace.numel() < need.value:
+        workspace = torch.empty(max(need.value, 1), dtype=torch.uint8, device=ins[0].device)
+    _lib.check(lib.phiks_mode_product_i8(len(dims), n_arr, int(mu), int(slices), len(ins),
+                                         _lib.ptr_array([_check_dev(t, N) for t in ins]),
+                                         _lib.ptr_array([_check_dev(M) for M in Ms]),
+                                         _lib.ptr_array([_check_dev(t, N) for t in outs]), workspace.data_ptr(),
+                                         workspace.numel(), _stream_ptr(stream)), "phiks_mode_product_i8")
+    return workspace
+
+
 def tucker(dims: Sequence[int], x, Ms: Sequence, out, scratch=None, stream=None):
     lib = _lib.load()
     torch = _torch()

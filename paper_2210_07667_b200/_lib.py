@@ -89,6 +89,8 @@ def load() -> ctypes.CDLL:
     lib.phiks_shard_set_peer_bases.argtypes = [vp, P(vp)]
     lib.phiks_apply_ranks_serial.argtypes = [P(vp), i, P(Request), i, P(vp), P(vp), vp]
     lib.phiks_wait.argtypes = [vp]
+    lib.phiks_mode_product_i8_workspace.argtypes = [i, P(i), i, i, i, P(ctypes.c_size_t)]
+    lib.phiks_mode_product_i8.argtypes = [i, P(i), i, i, i, P(vp), P(vp), P(vp), vp, ctypes.c_size_t, vp]
     lib.phiks_create_complex.argtypes = [i, P(i), P(vp), P(vp)]
     lib.phiks_plan_host_complex.argtypes = [i, P(i), P(vp), P(Request), P(d), P(PlanInfo)]
     lib.phiks_shard_peer_base.argtypes = [vp, i, P(vp)]
@@ -103,7 +105,8 @@ def load() -> ctypes.CDLL:
                  "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_shard_layout", "phiks_wait", "phiks_shard_peer_base", "phiks_create_complex", "phiks_plan_host_complex", "phiks_create_blocks",
                  "phiks_create_sharded_blocks", "phiks_shard_layout_ex",
                  "phiks_create_sharded_complex", "phiks_create_blocks_complex",
-                 "phiks_create_sharded_blocks_complex"):
+                 "phiks_create_sharded_blocks_complex",
+                 "phiks_mode_product_i8_workspace", "phiks_mode_product_i8"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

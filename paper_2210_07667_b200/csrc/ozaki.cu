@@ -1,0 +1,596 @@
+// fp64 μ-mode products on the int8 tensor cores (tcgen05.mma kind::i8).
+//
+// DESIGN.md §4c.  The μ-mode product Y = X ×_μ E (§3.1, Eq. (13))
+// contracts every mode-μ fiber x_c (c = l + L·r of the (L, n, R) view) with the
+// rows e_j of E.  Each fiber and each row is written exactly (up to a
+// truncation below 2^{ex-8S+1}) in S balanced base-256 digits, an error-free
+// splitting in the manner of Ozaki:
+//     x_c = 2^{ex_c-7} Σ_{s=0..S-1} 256^{-s} a_{c,s},   e_j = 2^{ee_j-7} Σ_t 256^{-t} b_{j,t},
+// a, b ∈ [-128, 127]^n integer vectors (|x| < 2^{ex-1} for the whole fiber).
+// Then
+//     y_{c,j} = 2^{ex_c+ee_j-14} Σ_{g=0..S-1} 256^{-g} D_g,   D_g = Σ_{s+t=g} a_{c,s}·b_{j,t},
+// keeping the pairs with s + t < S (the dropped ones are below the
+// representation error).  Every D_g is an exact int32 sum (|D_g| ≤ S·n·2^14
+// < 2^31 for n ≤ 256) accumulated by tcgen05.mma kind::i8 in TMEM, one
+// accumulator per diagonal g; the epilogue combines them in fp64 (Horner in
+// 2^-8) and applies the power-of-two scales.  With S = 7 each operand carries
+// 55 bits relative to twice its fiber / row maximum, so the error is bounded
+// like that of an fp64 dot product, |Δy| ≲ n·2^-52·max|e_j|·max|x_c|.
+//
+// Kernels: split_x (fibers → K-major int8 digits [slot][s][c][k] + 2^{ex_c}),
+// split_e (rows of E → [slot][t][j][k] + 2^{ee_j}), and a persistent
+// warp-specialised GEMM: each CTA owns one 64-row tile of E (its digits stay
+// resident in shared memory) and walks 128-fiber tiles; TMA (SWIZZLE_32B, 4-D
+// maps over (k, row, digit, slot)) streams one digit of one 32-wide k-block per
+// stage; one elected thread issues, per stage s, a_s × [b_0 | … | b_{S-1-s}]
+// as MMAs of N = 64(S-s) ≤ 256 whose column range is exactly the diagonal
+// accumulators s … S-1 (diagonal g at TMEM columns [64g, 64g+64)); 8 epilogue
+// warps drain TMEM while the next tile's MMAs run.
+#include <cuda.h>
+
+#include "phiks_internal.h"
+
+namespace phiks {
+
+namespace {
+
+constexpr int kOzBM = 128;  // fibers per tile (UMMA M, TMEM lanes)
+constexpr int kOzBN = 64;   // rows of E per tile (UMMA N)
+constexpr int kOzBK = 32;   // k per stage (bytes: one SWIZZLE_32B row, one UMMA K)
+constexpr int kOzStages = 4;
+
+__device__ __forceinline__ unsigned oz_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// ---- exact splitting into S balanced base-256 digits ----
+// |v| < 2^{ex-1}: F = trunc(|v|·2^{8S-1-ex}) < 2^{8S-2} (exact integer ops on
+// the fp64 fields); G = ±F + 0x80…80 has bytes d_i + 128, d_i the balanced
+// digits of ±F; digit s (most significant first) = byte S-1-s of G ^ 0x80…80
+template <int S>
+__device__ __forceinline__ uint64_t oz_digits(double v, int ex) {
+  const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
+  const int e = static_cast<int>((bits >> 52) & 0x7FF);
+  uint64_t m = bits & ((uint64_t(1) << 52) - 1);
+  int E = -1074;
+  if (e != 0) {
+    m |= uint64_t(1) << 52;
+    E = e - 1075;
+  }
+  const int sh = E - ex + 8 * S - 1;
+  const uint64_t F = sh >= 0 ? (m << sh) : (sh > -64 ? (m >> -sh) : 0);
+  constexpr uint64_t C = 0x8080808080808080ull >> (64 - 8 * S);
+  const uint64_t G = ((bits >> 63) ? (0 - F) : F) + C;
+  return G ^ C;
+}
+template <int S>
+__device__ __forceinline__ void split4(const double (&v)[4], int ex, uint32_t (&pk)[S]) {
+  uint64_t h[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) h[q] = oz_digits<S>(v[q], ex);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int i = S - 1 - s;  // byte of the digit
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = static_cast<uint32_t>(h[q] >> (8 * (i & 4)));
+    const uint32_t sel = (i & 3) | (((i & 3) + 4) << 4);
+    const uint32_t x01 = __byte_perm(w[0], w[1], sel), x23 = __byte_perm(w[2], w[3], sel);
+    pk[s] = __byte_perm(x01, x23, 0x5410);
+  }
+}
+
+__device__ __forceinline__ double warp_max(double m) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return m;
+}
+
+// exponent with |v| < 2^{ex-1} for every |v| ≤ m (m > 0 finite)
+__device__ __forceinline__ int slice_exponent(double m) { return m > 0.0 ? ilogb(m) + 2 : 0; }
+
+// ---- split_x: 32 fibers per CTA (256 threads), staged through shared memory ----
+template <int S>
+__global__ void __launch_bounds__(256) oz_split_x_kernel(const OzakiParams p) {
+  extern __shared__ double tile[];  // [32][P], P = n | 1
+  const int slot = blockIdx.y;
+  const double* X = p.x[slot];
+  const int64_t L = p.L, C = p.L * p.R;
+  const int n = p.n, P = n | 1, Kp = p.Kp;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nf = static_cast<int>(C - c0 < 32 ? C - c0 : 32);
+  if (L == 1) {  // the 32 fibers are one contiguous block of 32·n doubles
+    const double* src = X + c0 * n;
+    const int total = nf * n;
+    for (int i = tid; i < total; i += 256) {
+      const int f = i / n, k = i - f * n;
+      tile[f * P + k] = __ldg(src + i);
+    }
+  } else {  // lane → fiber (consecutive l are contiguous), warps over k
+    const int64_t c = c0 + lane;
+    if (lane < nf) {
+      const int64_t l = c % L, r = c / L;
+      const double* src = X + l + L * n * r;
+      for (int k = warp; k < n; k += 8) tile[lane * P + k] = __ldg(src + L * k);
+    }
+  }
+  __syncthreads();
+  int8_t* xs = p.xs + static_cast<int64_t>(slot) * S * C * Kp;
+  for (int f = warp; f < nf; f += 8) {
+    const int64_t c = c0 + f;
+    double m = 0.0;
+    bool bad = false;
+    for (int k = lane; k < n; k += 32) {
+      const double v = tile[f * P + k];
+      m = fmax(m, fabs(v));
+      bad |= !isfinite(v);
+    }
+    m = warp_max(m);
+    bad = __any_sync(0xffffffffu, bad);
+    const int ex = bad ? 0 : slice_exponent(m);
+    for (int k0 = 4 * lane; k0 < Kp; k0 += 128) {
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = (k0 + q < n && !bad) ? tile[f * P + k0 + q] : 0.0;
+      uint32_t pk[S];
+      split4<S>(v, ex, pk);
+#pragma unroll
+      for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(xs + (s * C + c) * Kp + k0) = pk[s];
+    }
+    if (lane == 0) p.xsc[static_cast<int64_t>(slot) * C + c] = bad ? __longlong_as_double(0x7ff8000000000000ll)
+                                                                  : scalbn(1.0, ex);
+  }
+}
+
+// ---- split_e: one warp per row j of E (column-major, E[j + k·n]) ----
+template <int S>
+__global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
+  const int slot = blockIdx.y;
+  const double* E = p.e[slot];
+  const int n = p.n, Kp = p.Kp;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (j >= n) return;
+  double m = 0.0;
+  bool bad = false;
+  for (int k = lane; k < n; k += 32) {
+    const double v = E[j + static_cast<int64_t>(k) * n];
+    m = fmax(m, fabs(v));
+    bad |= !isfinite(v);
+  }
+  m = warp_max(m);
+  bad = __any_sync(0xffffffffu, bad);
+  const int ex = bad ? 0 : slice_exponent(m);
+  int8_t* es = p.es + static_cast<int64_t>(slot) * S * n * Kp;
+  for (int k0 = 4 * lane; k0 < Kp; k0 += 128) {
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = (k0 + q < n && !bad) ? E[j + static_cast<int64_t>(k0 + q) * n] : 0.0;
+    uint32_t pk[S];
+    split4<S>(v, ex, pk);
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      *reinterpret_cast<uint32_t*>(es + (static_cast<int64_t>(s) * n + j) * Kp + k0) = pk[s];
+  }
+  if (lane == 0) p.esc[static_cast<int64_t>(slot) * n + j] = bad ? __longlong_as_double(0x7ff8000000000000ll)
+                                                               : scalbn(1.0, ex);
+}
+
+// ---- tcgen05 / TMA / mbarrier helpers ----
+__device__ __forceinline__ void oz_mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(oz_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void oz_mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(oz_smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void oz_mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "OZ_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra OZ_WAIT_%=;\n"
+      "}\n" ::"r"(oz_smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void oz_tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                               uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(oz_smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(oz_smem_u32(bar))
+      : "memory");
+}
+// K-major SWIZZLE_32B operand: rows of 32 bytes, 8-row atoms of 256 bytes
+__device__ __forceinline__ uint64_t oz_desc_sw32(const void* p) {
+  const uint32_t a = oz_smem_u32(p);
+  uint64_t d = static_cast<uint64_t>((a >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;          // leading byte offset (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(256 >> 4) << 32;   // stride byte offset: 8 rows × 32 B
+  d |= static_cast<uint64_t>(1) << 46;          // descriptor version (sm_100)
+  d |= static_cast<uint64_t>(6) << 61;          // SWIZZLE_32B
+  return d;
+}
+// kind::i8 instruction descriptor: D s32, A/B s8, both K-major, M = 128, N = BN
+__host__ __device__ constexpr uint32_t oz_idesc(int bn) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(bn >> 3) << 17) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void oz_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void oz_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   oz_smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void oz_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ bool oz_elect() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void oz_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(oz_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void oz_ld8(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+// exact int32 → fp64 without I2F: 1.5·2^52 + 2^31 + v has v in its low mantissa bits
+__device__ __forceinline__ double oz_i2d(uint32_t v) {
+  return __hiloint2double(0x43380000, static_cast<int>(v ^ 0x80000000u)) - 6755401588539392.0;
+}
+
+// Persistent GEMM geometry: the E-digit tile of a (term, n-tile) stays resident
+// (S × 64 rows × Kp bytes); fiber digits stream through an NST-stage ring of
+// SPS-digit units (k-block kb, digit group sg).
+template <int S>
+struct OzGeom {
+  static constexpr int SPS = 1;                                // digits per stage
+  static constexpr int A_BYTES = SPS * kOzBM * kOzBK;         // one stage
+  static constexpr int NST = 65536 / A_BYTES;
+  static constexpr int B_KB = S * kOzBN * kOzBK;              // resident E slices per k-block
+  static constexpr int B_BYTES = (kOzMaxN / kOzBK) * B_KB;    // Kp ≤ kOzMaxN
+  static constexpr int SMEM = NST * A_BYTES + B_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int EPI_WARPS = 8;                          // 2 per TMEM lane quarter (column halves)
+  static constexpr int THREADS = 64 + EPI_WARPS * 32;
+  static_assert(S * kOzBN <= 512, "TMEM holds one 64-column accumulator per diagonal");
+  static_assert(SMEM <= 232448, "shared memory");
+};
+
+// work of CTA k: n-tile nt = k % ntn, units u = q, q + Q, … over (term, m-tile),
+// term-major, so the ntn CTAs sharing q read the same fiber tiles together
+struct OzSched {
+  int ntn, nt, q, Q;
+  int64_t Mt, units;
+  __device__ OzSched(const OzakiParams& p) {
+    ntn = (p.n + kOzBN - 1) / kOzBN;
+    nt = static_cast<int>(blockIdx.x % ntn);
+    q = static_cast<int>(blockIdx.x / ntn);
+    Q = static_cast<int>(gridDim.x / ntn);
+    Mt = (p.L * p.R + kOzBM - 1) / kOzBM;
+    units = Mt * p.nterms;
+  }
+};
+
+template <int S>
+__global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
+    oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
+                   const __grid_constant__ CUtensorMap tb) {
+  using G = OzGeom<S>;
+  extern __shared__ uint8_t oz_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* bres = smem + G::NST * G::A_BYTES;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(bres + G::B_BYTES);
+  uint64_t* a_empty = a_full + G::NST;
+  uint64_t* b_full = a_empty + G::NST;
+  uint64_t* b_empty = b_full + 1;
+  uint64_t* t_full = b_empty + 1;
+  uint64_t* t_empty = t_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const OzSched sc(p);
+  if (sc.q >= sc.Q) return;  // idle CTA (grid not a multiple of the n-tile count)
+  const int nk = p.Kp / kOzBK;
+  constexpr int NSG = S / G::SPS;
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+    for (int s = 0; s < G::NST; ++s) {
+      oz_mbar_init(&a_full[s], 1);
+      oz_mbar_init(&a_empty[s], 1);
+    }
+    oz_mbar_init(b_full, 1);
+    oz_mbar_init(b_empty, 1);
+    oz_mbar_init(t_full, 1);
+    oz_mbar_init(t_empty, G::EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(oz_smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer (whole warp in lockstep, one elected lane issues) ----
+    int cur_term = -1, bgen = 0, it = 0;
+    for (int64_t u = sc.q; u < sc.units; u += sc.Q) {
+      const int term = static_cast<int>(u / sc.Mt);
+      const int mt = static_cast<int>(u % sc.Mt);
+      if (term != cur_term) {  // (re)load the resident E slices of this (term, n-tile)
+        if (bgen > 0) oz_mbar_wait(b_empty, (bgen - 1) & 1);
+        if (oz_elect()) {
+          oz_mbar_expect_tx(b_full, static_cast<unsigned>(nk * G::B_KB));
+          for (int kb = 0; kb < nk; ++kb)
+            oz_tma_load_4d(bres + kb * G::B_KB, &tb, kb * kOzBK, sc.nt * kOzBN, 0, p.terms[term].eslot, b_full);
+        }
+        __syncwarp();
+        cur_term = term;
+        ++bgen;
+      }
+      const int xs = p.terms[term].xslot;
+      for (int kb = 0; kb < nk; ++kb)
+        for (int sg = 0; sg < NSG; ++sg, ++it) {
+          const int st = it % G::NST;
+          if (it >= G::NST) oz_mbar_wait(&a_empty[st], ((it / G::NST) & 1) ^ 1);
+          if (oz_elect()) {
+            oz_mbar_expect_tx(&a_full[st], G::A_BYTES);
+            oz_tma_load_4d(smem + st * G::A_BYTES, &ta, kb * kOzBK, mt * kOzBM, sg * G::SPS, xs, &a_full[st]);
+          }
+          __syncwarp();
+        }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer (whole warp in lockstep, one elected lane issues) ----
+    // diagonal g = s + t accumulates in TMEM columns [64g, 64g + 64); descriptors
+    // advance by adding (byte offset >> 4) to their start-address field
+    const uint64_t a_desc0 = oz_desc_sw32(smem), b_desc0 = oz_desc_sw32(bres);
+    int cur_term = -1, bgen = 0, it = 0, tile = 0;
+    for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
+      const int term = static_cast<int>(u / sc.Mt);
+      if (term != cur_term) {
+        if (bgen > 0) {
+          if (oz_elect()) oz_commit(b_empty);  // the previous E tile is free once its MMAs are done
+          __syncwarp();
+        }
+        oz_mbar_wait(b_full, bgen & 1);
+        cur_term = term;
+        ++bgen;
+      }
+      if (tile > 0) oz_mbar_wait(t_empty, (tile - 1) & 1);  // epilogue drained the accumulators
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      for (int kb = 0; kb < nk; ++kb)
+        for (int sg = 0; sg < NSG; ++sg, ++it) {
+          const int st = it % G::NST;
+          oz_mbar_wait(&a_full[st], (it / G::NST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint64_t ad0 = a_desc0 + static_cast<uint64_t>((st * G::A_BYTES) >> 4);
+          const uint64_t bd0 = b_desc0 + static_cast<uint64_t>((kb * G::B_KB) >> 4);
+          if (oz_elect()) {
+#pragma unroll
+            for (int si = 0; si < G::SPS; ++si) {
+              const int s = sg * G::SPS + si;
+              const uint64_t ad = ad0 + static_cast<uint64_t>((si * kOzBM * kOzBK) >> 4);
+              const uint32_t accf = (kb > 0 || s > 0) ? 1u : 0u;
+              // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA
+              for (int c0 = 0; c0 < (S - s) * kOzBN; c0 += 256) {
+                const int nn = min(256, (S - s) * kOzBN - c0);
+                oz_mma(tmem + static_cast<uint32_t>(s * kOzBN + c0), ad,
+                       bd0 + static_cast<uint64_t>((c0 * kOzBK) >> 4), oz_idesc(nn), accf);
+              }
+            }
+            oz_commit(&a_empty[st]);
+          }
+          __syncwarp();
+        }
+      if (oz_elect()) oz_commit(t_full);
+      __syncwarp();
+    }
+  } else {
+    // ---- epilogue warps: lane quarter wq = warp % 4 (TMEM lanes 32wq..), column half ch ----
+    const int wq = warp & 3, ch = (warp - 2) >> 2;
+    const int64_t C = p.L * p.R, L = p.L;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16) + ch * 32;
+    int tile = 0;
+    for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
+      const int term_i = static_cast<int>(u / sc.Mt);
+      const int64_t mt = u % sc.Mt;
+      const OzakiTerm term = p.terms[term_i];
+      const int64_t c = mt * kOzBM + wq * 32 + lane;
+      const bool rvalid = c < C;
+      const double xsv = rvalid ? p.xsc[static_cast<int64_t>(term.xslot) * C + c] : 0.0;
+      oz_mbar_wait(t_full, tile & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      double acc[32];
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        uint32_t v[S][8];
+#pragma unroll
+        for (int g = 0; g < S; ++g) oz_ld8(tl + g * kOzBN + cb * 8, v[g]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          double a = oz_i2d(v[S - 1][q]);
+#pragma unroll
+          for (int g = S - 2; g >= 0; --g) a = fma(a, 0x1p-8, oz_i2d(v[g][q]));
+          acc[cb * 8 + q] = a;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) oz_mbar_arrive(t_empty);
+      // scale and store (overlaps the next tile's MMAs)
+      const int j0 = sc.nt * kOzBN + ch * 32;
+      const double* esc = p.esc + static_cast<int64_t>(term.eslot) * p.n + j0;
+      const int jn = p.n - j0;  // valid columns of this half
+      if (rvalid && jn > 0) {
+        const double rs = term.beta * 0x1p-14 * xsv;
+        const int64_t l = c % L, r = c / L;
+        double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
+        if (jn >= 32) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) acc[q] *= rs * __ldg(esc + q);
+          if (L == 1 && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 32; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(acc[q], acc[q + 1]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) outp[L * q] = acc[q];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (q < jn) outp[L * q] = acc[q] * (rs * __ldg(esc + q));
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+}
+
+typedef CUresult (*OzEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+OzEncodeFn oz_encode_fn() {
+  static const OzEncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<OzEncodeFn>(f);
+    return static_cast<OzEncodeFn>(nullptr);
+  }();
+  return fn;
+}
+
+// 4-D map over int8 slices [slot][slice][row][k] with a (32, rows_box, slice_box, 1) box, SWIZZLE_32B
+bool oz_encode(CUtensorMap* m, const int8_t* base, int64_t Kp, int64_t rows, int S, int slots, int rows_box,
+               int slice_box) {
+  OzEncodeFn fn = oz_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(S),
+                              static_cast<cuuint64_t>(slots)};
+  const cuuint64_t str[3] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Kp * rows),
+                             static_cast<cuuint64_t>(Kp * rows * S)};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(kOzBK), static_cast<cuuint32_t>(rows_box),
+                             static_cast<cuuint32_t>(slice_box), 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int S>
+cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e) {
+  const int64_t C = p.L * p.R;
+  if (split_x) {
+    const size_t sm = static_cast<size_t>(32) * (p.n | 1) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(oz_split_x_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           32 * (kOzMaxN | 1) * 8);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
+  }
+  if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
+  if (p.nterms == 0) return cudaGetLastError();
+  CUtensorMap ta, tb;
+  if (!oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS) ||
+      !oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S))
+    return cudaErrorInvalidValue;
+  using G = OzGeom<S>;
+  static bool gattr = false;
+  static int sms = 0;
+  if (!gattr) {
+    cudaError_t e = cudaFuncSetAttribute(oz_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    gattr = true;
+  }
+  const int ntn = (p.n + kOzBN - 1) / kOzBN;
+  const int64_t units = ((C + kOzBM - 1) / kOzBM) * p.nterms;
+  int64_t per = sms / ntn;  // CTAs per n-tile
+  if (per > units) per = units;
+  if (per < 1) per = 1;
+  oz_gemm_kernel<S><<<static_cast<unsigned>(per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, tb);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne) {
+  const int64_t C = L * R, Kp = (n + kOzBK - 1) / kOzBK * kOzBK;
+  auto al = [](size_t b) { return (b + 1023) & ~size_t(1023); };
+  return al(static_cast<size_t>(nx) * S * C * Kp) + al(static_cast<size_t>(nx) * C * 8) +
+         al(static_cast<size_t>(ne) * S * n * Kp) + al(static_cast<size_t>(ne) * n * 8);
+}
+
+void ozaki_bind_workspace(OzakiParams& p, void* ws) {
+  const int64_t C = p.L * p.R;
+  p.Kp = (p.n + kOzBK - 1) / kOzBK * kOzBK;
+  auto al = [](size_t b) { return (b + 1023) & ~size_t(1023); };
+  char* w = static_cast<char*>(ws);
+  p.xs = reinterpret_cast<int8_t*>(w);
+  w += al(static_cast<size_t>(p.nx) * p.S * C * p.Kp);
+  p.xsc = reinterpret_cast<double*>(w);
+  w += al(static_cast<size_t>(p.nx) * C * 8);
+  p.es = reinterpret_cast<int8_t*>(w);
+  w += al(static_cast<size_t>(p.ne) * p.S * p.n * p.Kp);
+  p.esc = reinterpret_cast<double*>(w);
+}
+
+bool ozaki_supported(int64_t L, int n, int64_t R, int S) {
+  const int64_t C = L * R;
+  return S >= 6 && S <= 7 && n >= 1 && n <= kOzMaxN && C >= 1 && C < (int64_t(1) << 31);
+}
+
+cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e) {
+  switch (p.S) {
+    case 6: return oz_launch<6>(p, st, split_x, split_e);
+    case 7: return oz_launch<7>(p, st, split_x, split_e);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace phiks

@@ -465,6 +465,60 @@ phiks_status phiks_mode_product(int d, const int* n, int mu, int batch, const do
   return PHIKS_OK;
 }
 
+phiks_status phiks_mode_product_i8_workspace(int d, const int* n, int mu, int slices, int batch, size_t* bytes) {
+  if (d < 1 || d > PHIKS_MAX_D || !n || mu < 0 || mu >= d || batch < 0 || !bytes) return fail(PHIKS_ERR_ARG, "bad argument");
+  int64_t L = 1, R = 1;
+  for (int k = 0; k < mu; ++k) L *= n[k];
+  for (int k = mu + 1; k < d; ++k) R *= n[k];
+  if (!ozaki_supported(L, n[mu], R, slices)) return fail(PHIKS_ERR_ARG, "int8 mode product: unsupported size or slices");
+  const int cap = std::min(std::max(batch, 1), kMaxTerms);
+  *bytes = ozaki_workspace_bytes(L, n[mu], R, slices, cap, cap);
+  return PHIKS_OK;
+}
+
+phiks_status phiks_mode_product_i8(int d, const int* n, int mu, int slices, int batch, const double* const* in,
+                                   const double* const* M, double* const* out, void* workspace, size_t ws_bytes,
+                                   void* stream) {
+  size_t need = 0;
+  phiks_status st = phiks_mode_product_i8_workspace(d, n, mu, slices, batch, &need);
+  if (st != PHIKS_OK) return st;
+  if (batch > 0 && (!in || !M || !out)) return fail(PHIKS_ERR_ARG, "bad argument");
+  if (!workspace || ws_bytes < need) return fail(PHIKS_ERR_ARG, "workspace too small");
+  int64_t L = 1, R = 1;
+  for (int k = 0; k < mu; ++k) L *= n[k];
+  for (int k = mu + 1; k < d; ++k) R *= n[k];
+  for (int i0 = 0; i0 < batch; i0 += kMaxTerms) {
+    OzakiParams* pp = new OzakiParams();
+    OzakiParams& p = *pp;
+    p.L = L;
+    p.R = R;
+    p.n = n[mu];
+    p.S = slices;
+    p.nx = p.ne = p.nterms = 0;
+    for (int i = i0; i < std::min(batch, i0 + kMaxTerms); ++i) {
+      int xs = -1, es = -1;
+      for (int k = 0; k < p.nx; ++k)
+        if (p.x[k] == in[i]) xs = k;
+      for (int k = 0; k < p.ne; ++k)
+        if (p.e[k] == M[i]) es = k;
+      if (xs < 0) {
+        xs = p.nx;
+        p.x[p.nx++] = in[i];
+      }
+      if (es < 0) {
+        es = p.ne;
+        p.e[p.ne++] = M[i];
+      }
+      p.terms[p.nterms++] = OzakiTerm{xs, es, out[i], 1.0};
+    }
+    ozaki_bind_workspace(p, workspace);
+    cudaError_t e = launch_ozaki_mode(p, static_cast<cudaStream_t>(stream));
+    delete pp;
+    if (e != cudaSuccess) return fail(PHIKS_ERR_CUDA, std::string("int8 mode product: ") + cudaGetErrorString(e));
+  }
+  return PHIKS_OK;
+}
+
 phiks_status phiks_tucker(int d, const int* n, const double* in, const double* const* M, double* out,
                           double* scratch, void* stream) {
   if (d < 1 || d > PHIKS_MAX_D || !n || !in || !M || !out || (d > 1 && !scratch))

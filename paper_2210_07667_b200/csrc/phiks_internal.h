@@ -112,6 +112,33 @@ struct MultiCombineParams {
   double coef[kMcMaxOut][kMcMaxSrc];
 };
 
+// μ-mode products on the int8 tensor cores (ozaki.cu): every
+// term t computes out_t = beta_t · (x_{xslot} ×_μ e_{eslot}) (plain outputs, no
+// sources), each fiber / row written in S balanced base-256 digits.
+constexpr int kOzMaxN = 256;      // mode size limit (resident E tile, int32 exactness)
+constexpr int kOzMaxSlices = 7;
+struct OzakiTerm {
+  int xslot, eslot;
+  double* out;
+  double beta;
+};
+struct OzakiParams {
+  int64_t L, R;
+  int n, Kp, S;
+  int nx, ne, nterms;
+  const double* x[kMaxTerms];  // distinct inputs (L, n, R)
+  const double* e[kMaxTerms];  // distinct matrices (n×n column-major)
+  OzakiTerm terms[kMaxTerms];
+  int8_t* xs;    // workspace (ozaki_bind_workspace): [nx][S][L·R][Kp] slices
+  double* xsc;   // [nx][L·R] fiber scales 2^ex
+  int8_t* es;    // [ne][S][n][Kp]
+  double* esc;   // [ne][n]
+};
+bool ozaki_supported(int64_t L, int n, int64_t R, int S);
+size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne);
+void ozaki_bind_workspace(OzakiParams& p, void* ws);  // sets Kp and the workspace pointers
+cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_x = true, bool split_e = true);
+
 // Kernel launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st);
 cudaError_t launch_combine(const CombineParams& p, cudaStream_t st);
