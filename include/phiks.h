@@ -113,6 +113,13 @@ typedef struct {
   double expm_ms;                 /* sum of their event-measured durations (ms)     */
   int nblocks;                    /* diagonal blocks of the handle                  */
   phiks_plan_info block_plan[PHIKS_MAX_BLOCKS]; /* plan of each block, last apply   */
+  int64_t i8_mode_launches;       /* mode-product launches of the last apply that took
+                                     the int8 tensor-core path (phiks_set_gemm_path)  */
+  int64_t i8_launches;            /* profiling: the subset of mode_product_launches  */
+  double i8_ms;                   /*   on the int8 path (digit splits + GEMM) and    */
+  double i8_flops;                /*   their time and fp64-equivalent flops          */
+  int64_t i8_gemm_launches;       /* profiling: the int8 GEMM launches alone         */
+  double i8_gemm_ms;              /*   and their time                                */
 } phiks_stats;
 
 /* Create a handle for K = A_d ⊕ … ⊕ A_1.
@@ -189,6 +196,20 @@ phiks_status phiks_workspace_size(phiks_handle h, const phiks_request* req,
    events on the apply's stream (for the roofline report); phiks_get_stats then
    waits for those events.  Off by default. */
 phiks_status phiks_set_profiling(phiks_handle h, int on);
+
+/* Path of the Tucker operators' μ-mode products:
+   PHIKS_GEMM_DMMA: the fp64 DMMA kernel for every product;
+   PHIKS_GEMM_I8: the int8 tensor-core kernel (7 balanced base-256 digits per
+     operand, exact int32 accumulation: fp64-class error) wherever it applies
+     (real handles, unsharded, n_μ ≤ 256, plain outputs), DMMA elsewhere;
+   PHIKS_GEMM_AUTO (default, or the PHIKS_GEMM environment variable "dmma" /
+     "i8" / "auto" at create): the int8 kernel for products with n_μ ≥ 128 and
+     n_μ · N ≥ 2^26, where it is faster.  Invalidates the handle's captured
+     graphs.  PHIKS_ERR_ARG for an unknown path. */
+#define PHIKS_GEMM_AUTO 0
+#define PHIKS_GEMM_DMMA 1
+#define PHIKS_GEMM_I8 2
+phiks_status phiks_set_gemm_path(phiks_handle h, int path);
 
 /* Telemetry of the last phiks_apply on this handle. */
 phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out);

@@ -183,7 +183,15 @@ class PhiKS:
                 "mode_product_launches": st.mode_product_launches, "mode_product_ms": st.mode_product_ms,
                 "mode_product_flops": st.mode_product_flops, "expm_launches": st.expm_launches,
                 "expm_ms": st.expm_ms,
-                "block_plans": [(st.block_plan[b].s, st.block_plan[b].q) for b in range(max(st.nblocks, 1))]}
+                "block_plans": [(st.block_plan[b].s, st.block_plan[b].q) for b in range(max(st.nblocks, 1))],
+                "i8_mode_launches": st.i8_mode_launches, "i8_launches": st.i8_launches, "i8_ms": st.i8_ms,
+                "i8_flops": st.i8_flops, "i8_gemm_launches": st.i8_gemm_launches, "i8_gemm_ms": st.i8_gemm_ms}
+
+    GEMM_PATHS = {"auto": 0, "dmma": 1, "i8": 2}
+
+    def set_gemm_path(self, path: str):
+        """μ-mode-product path of the Tucker launches: "auto", "dmma" or "i8"."""
+        _lib.check(_lib.load().phiks_set_gemm_path(self._h, self.GEMM_PATHS[path]), "phiks_set_gemm_path")
 
     def set_profiling(self, on: bool = True):
         _lib.check(_lib.load().phiks_set_profiling(self._h, 1 if on else 0), "phiks_set_profiling")

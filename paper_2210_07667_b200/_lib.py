@@ -47,7 +47,9 @@ class Stats(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_size_t), ("total_kernel_launches", ctypes.c_int64),
                 ("mode_product_launches", ctypes.c_int64), ("mode_product_ms", ctypes.c_double),
                 ("mode_product_flops", ctypes.c_double), ("expm_launches", ctypes.c_int64),
-                ("expm_ms", ctypes.c_double), ("nblocks", ctypes.c_int), ("block_plan", PlanInfo * 4)]
+                ("expm_ms", ctypes.c_double), ("nblocks", ctypes.c_int), ("block_plan", PlanInfo * 4),
+                ("i8_mode_launches", ctypes.c_int64), ("i8_launches", ctypes.c_int64), ("i8_ms", ctypes.c_double),
+                ("i8_flops", ctypes.c_double), ("i8_gemm_launches", ctypes.c_int64), ("i8_gemm_ms", ctypes.c_double)]
 
 
 _lib = None
@@ -89,6 +91,7 @@ def load() -> ctypes.CDLL:
     lib.phiks_shard_set_peer_bases.argtypes = [vp, P(vp)]
     lib.phiks_apply_ranks_serial.argtypes = [P(vp), i, P(Request), i, P(vp), P(vp), vp]
     lib.phiks_wait.argtypes = [vp]
+    lib.phiks_set_gemm_path.argtypes = [vp, i]
     lib.phiks_mode_product_i8_workspace.argtypes = [i, P(i), i, i, i, P(ctypes.c_size_t)]
     lib.phiks_mode_product_i8.argtypes = [i, P(i), i, i, i, P(vp), P(vp), P(vp), vp, ctypes.c_size_t, vp]
     lib.phiks_create_complex.argtypes = [i, P(i), P(vp), P(vp)]
@@ -106,7 +109,7 @@ def load() -> ctypes.CDLL:
                  "phiks_create_sharded_blocks", "phiks_shard_layout_ex",
                  "phiks_create_sharded_complex", "phiks_create_blocks_complex",
                  "phiks_create_sharded_blocks_complex",
-                 "phiks_mode_product_i8_workspace", "phiks_mode_product_i8"):
+                 "phiks_mode_product_i8_workspace", "phiks_mode_product_i8", "phiks_set_gemm_path"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

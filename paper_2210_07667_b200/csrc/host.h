@@ -23,6 +23,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <set>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -98,7 +99,15 @@ struct phiks_ctx {
   bool profiling = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> ev_flops;
-  std::vector<char> ev_expm;  // 1: a small-GEMM launch of the exponential stage
+  std::vector<char> ev_expm;  // 1: small-GEMM launch of the exponential stage; 2: int8 (§4c) GEMM, 3: its digit splits
+  // μ-mode-product path of the Tucker launches (phiks_set_gemm_path; PHIKS_GEMM env for the default)
+  int gemm_path = default_gemm_path();
+  static int default_gemm_path() {
+    const char* e = std::getenv("PHIKS_GEMM");
+    if (e && std::strcmp(e, "dmma") == 0) return PHIKS_GEMM_DMMA;
+    if (e && std::strcmp(e, "i8") == 0) return PHIKS_GEMM_I8;
+    return PHIKS_GEMM_AUTO;
+  }
   int ev_used = 0;
   // ---- slab sharding along the outermost mode (phiks_create_sharded) ----
   // n[] holds the LOCAL dims of layout S_d (n[d-1] = gn[d-1]/world); the
@@ -305,6 +314,89 @@ struct Exec {
     check(launch_barrier(bp, st), "barrier");
   }
 
+  // ---- int8 tensor-core route of plain mode products (ozaki.cu) ----
+  int64_t i8_launches = 0;
+  double* oz_ws = nullptr;  // grown on demand, reused by every int8 launch of the apply (one stream)
+  size_t oz_ws_bytes = 0;
+  static constexpr int kOzDigits = 7;
+  template <class Terms>
+  bool ozaki_route(int64_t L, int n, int64_t R, const Terms& terms, const Remap* rm) const {
+    if (rm || in_expm || h->cplx || h->sharded() || rec || h->gemm_path == PHIKS_GEMM_DMMA) return false;
+    if (!ozaki_supported(L, n, R, kOzDigits)) return false;
+    if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 128 || L * R * n < (int64_t(1) << 26))) return false;
+    std::set<int> groups;
+    for (const auto& t : terms) {
+      if (t.cswap || t.outs.size() != 1 || !t.outs[0].srcs.empty()) return false;
+      if (!groups.insert(t.group).second) return false;
+    }
+    return true;
+  }
+  template <class Terms>
+  void ozaki_launch(int64_t L, int n, int64_t R, const Terms& terms) {
+    constexpr int kChunkX = 8;  // distinct inputs split per launch (bounds the digit workspace)
+    size_t i = 0;
+    while (i < terms.size() && ok()) {
+      auto pp = std::make_shared<OzakiParams>();
+      OzakiParams& p = *pp;
+      std::memset(&p, 0, sizeof(p));
+      p.L = L;
+      p.R = R;
+      p.n = n;
+      p.S = kOzDigits;
+      size_t j = i;
+      for (; j < terms.size() && p.nterms < kMaxTerms; ++j) {
+        int xs = -1, es = -1;
+        for (int k = 0; k < p.nx; ++k)
+          if (p.x[k] == terms[j].in) xs = k;
+        for (int k = 0; k < p.ne; ++k)
+          if (p.e[k] == terms[j].M) es = k;
+        if ((xs < 0 && p.nx == kChunkX) || (es < 0 && p.ne == kMaxTerms)) break;
+        if (xs < 0) {
+          xs = p.nx;
+          p.x[p.nx++] = terms[j].in;
+        }
+        if (es < 0) {
+          es = p.ne;
+          p.e[p.ne++] = terms[j].M;
+        }
+        p.terms[p.nterms++] = OzakiTerm{xs, es, terms[j].outs[0].dst, terms[j].outs[0].beta};
+      }
+      const size_t need = ozaki_workspace_bytes(L, n, R, p.S, p.nx, p.ne);
+      if (need > oz_ws_bytes) {
+        oz_ws = ar->alloc_doubles(static_cast<int64_t>((need + 7) / 8));
+        oz_ws_bytes = need;
+      }
+      ozaki_bind_workspace(p, oz_ws);
+      ++i8_launches;
+      // digit splits, then the GEMM (separate event pairs: kind 3 splits, kind 2 GEMM)
+      for (int phase = 0; phase < 2; ++phase) {
+        const bool prof = !measure && h->profiling && !rec;
+        if (prof) {
+          if (h->ev_used == static_cast<int>(h->ev.size())) {
+            cudaEvent_t a, b;
+            check(cudaEventCreate(&a), "cudaEventCreate");
+            check(cudaEventCreate(&b), "cudaEventCreate");
+            h->ev.emplace_back(a, b);
+            h->ev_flops.push_back(0.0);
+            h->ev_expm.push_back(0);
+          }
+          h->ev_flops[h->ev_used] =
+              phase == 0 ? 0.0 : 2.0 * static_cast<double>(L * R) * n * static_cast<double>(n) * p.nterms;
+          h->ev_expm[h->ev_used] = phase == 0 ? 3 : 2;
+          check(cudaEventRecord(h->ev[h->ev_used].first, st), "cudaEventRecord");
+        }
+        if (phase == 0) {
+          emit("digits_i8", [pp](cudaStream_t s2) { return launch_ozaki_mode(*pp, s2, true, true, false); });
+          ++launches;  // split_x + split_e
+        } else {
+          emit("mode_product_i8", [pp](cudaStream_t s2) { return launch_ozaki_mode(*pp, s2, false, false, true); });
+        }
+        if (prof) check(cudaEventRecord(h->ev[h->ev_used++].second, st), "cudaEventRecord");
+      }
+      i = j;
+    }
+  }
+
   // ---- one mode-product launch from host-side term lists ----
   struct LaunchTerm {
     const double* in;
@@ -315,6 +407,10 @@ struct Exec {
   };
   void mode_launch(int64_t L, int n, int64_t R, const std::vector<LaunchTerm>& terms, const Remap* rm = nullptr) {
     if (!ok() || terms.empty()) return;
+    if (ozaki_route(L, n, R, terms, rm)) {
+      ozaki_launch(L, n, R, terms);
+      return;
+    }
     // chunk so every launch fits ModeParams; a group's terms stay in order
     size_t i = 0;
     while (i < terms.size() && ok()) {
@@ -1302,6 +1398,7 @@ struct ApplyRun {
     S.plan.T_executed = static_cast<int>(ex.tucker_ops);
     S.kernel_launches = ex.launches + norm_launches;
     S.tucker_ops = ex.tucker_ops;
+    S.i8_mode_launches = ex.i8_launches;
     S.mu_mode_flops = ex.mu_flops;
     S.expm_flops = ex.expm_flops;
     S.workspace_bytes = need;

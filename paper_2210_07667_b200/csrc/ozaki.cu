@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(256) oz_split_x_kernel(const OzakiParams p) {
 #pragma unroll
       for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(xs + (s * C + c) * Kp + k0) = pk[s];
     }
-    if (lane == 0) p.xsc[static_cast<int64_t>(slot) * C + c] = bad ? __longlong_as_double(0x7ff8000000000000ll)
-                                                                  : scalbn(1.0, ex);
+    if (lane == 0)  // the fiber's exponent (NaN marks a non-finite fiber)
+      p.xsc[static_cast<int64_t>(slot) * C + c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
   }
 }
 
@@ -173,8 +173,7 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
     for (int s = 0; s < S; ++s)
       *reinterpret_cast<uint32_t*>(es + (static_cast<int64_t>(s) * n + j) * Kp + k0) = pk[s];
   }
-  if (lane == 0) p.esc[static_cast<int64_t>(slot) * n + j] = bad ? __longlong_as_double(0x7ff8000000000000ll)
-                                                               : scalbn(1.0, ex);
+  if (lane == 0) p.esc[static_cast<int64_t>(slot) * n + j] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
 }
 
 // ---- tcgen05 / TMA / mbarrier helpers ----
@@ -457,12 +456,18 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
       const double* esc = p.esc + static_cast<int64_t>(term.eslot) * p.n + j0;
       const int jn = p.n - j0;  // valid columns of this half
       if (rvalid && jn > 0) {
-        const double rs = term.beta * 0x1p-14 * xsv;
+        // y = scalbn(β·acc, ex_c + ee_j − 14): one rounding, the whole exponent range
         const int64_t l = c % L, r = c / L;
         double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
-        if (jn >= 32) {
+        const bool xbad = isnan(xsv);
+        const int xe = xbad ? 0 : static_cast<int>(xsv) - 14;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) acc[q] *= rs * __ldg(esc + q);
+        for (int q = 0; q < 32; ++q) {
+          const double ee = q < jn ? __ldg(esc + q) : 0.0;
+          acc[q] = (xbad || isnan(ee)) ? __longlong_as_double(0x7ff8000000000000ll)
+                                       : scalbn(acc[q] * term.beta, xe + static_cast<int>(ee));
+        }
+        if (jn >= 32) {
           if (L == 1 && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
 #pragma unroll
             for (int q = 0; q < 32; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(acc[q], acc[q + 1]);
@@ -473,7 +478,7 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
         } else {
 #pragma unroll
           for (int q = 0; q < 32; ++q)
-            if (q < jn) outp[L * q] = acc[q] * (rs * __ldg(esc + q));
+            if (q < jn) outp[L * q] = acc[q];
         }
       }
     }
@@ -518,7 +523,7 @@ bool oz_encode(CUtensorMap* m, const int8_t* base, int64_t Kp, int64_t rows, int
 }
 
 template <int S>
-cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e) {
+cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e, bool gemm) {
   const int64_t C = p.L * p.R;
   if (split_x) {
     const size_t sm = static_cast<size_t>(32) * (p.n | 1) * sizeof(double);
@@ -532,7 +537,7 @@ cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool 
     oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
   }
   if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
-  if (p.nterms == 0) return cudaGetLastError();
+  if (p.nterms == 0 || !gemm) return cudaGetLastError();
   CUtensorMap ta, tb;
   if (!oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS) ||
       !oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S))
@@ -585,10 +590,10 @@ bool ozaki_supported(int64_t L, int n, int64_t R, int S) {
   return S >= 6 && S <= 7 && n >= 1 && n <= kOzMaxN && C >= 1 && C < (int64_t(1) << 31);
 }
 
-cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e) {
+cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e, bool gemm) {
   switch (p.S) {
-    case 6: return oz_launch<6>(p, st, split_x, split_e);
-    case 7: return oz_launch<7>(p, st, split_x, split_e);
+    case 6: return oz_launch<6>(p, st, split_x, split_e, gemm);
+    case 7: return oz_launch<7>(p, st, split_x, split_e, gemm);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -413,20 +413,46 @@ phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out) {
   out->mode_product_flops = 0.0;
   out->expm_launches = 0;
   out->expm_ms = 0.0;
+  out->i8_launches = 0;
+  out->i8_ms = 0.0;
+  out->i8_flops = 0.0;
+  out->i8_gemm_launches = 0;
+  out->i8_gemm_ms = 0.0;
   if (h->profiling) {
     for (int i = 0; i < h->ev_used; ++i) {
       CUDA_TRY(cudaEventSynchronize(h->ev[i].second));
       float ms = 0.f;
       CUDA_TRY(cudaEventElapsedTime(&ms, h->ev[i].first, h->ev[i].second));
-      if (h->ev_expm[i]) {
+      if (h->ev_expm[i] == 1) {
         out->expm_ms += ms;
         ++out->expm_launches;
       } else {
         out->mode_product_ms += ms;
         out->mode_product_flops += h->ev_flops[i];
         ++out->mode_product_launches;
+        if (h->ev_expm[i] >= 2) {
+          out->i8_ms += ms;
+          out->i8_flops += h->ev_flops[i];
+          ++out->i8_launches;
+        }
+        if (h->ev_expm[i] == 2) {
+          out->i8_gemm_ms += ms;
+          ++out->i8_gemm_launches;
+        }
       }
     }
+  }
+  return PHIKS_OK;
+}
+
+phiks_status phiks_set_gemm_path(phiks_handle h, int path) {
+  if (!h) return fail(PHIKS_ERR_ARG, "null handle");
+  if (path != PHIKS_GEMM_AUTO && path != PHIKS_GEMM_DMMA && path != PHIKS_GEMM_I8)
+    return fail(PHIKS_ERR_ARG, "unknown gemm path");
+  if (h->gemm_path != path) {
+    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);  // captured with the other path
+    h->graphs.clear();
+    h->gemm_path = path;
   }
   return PHIKS_OK;
 }

@@ -130,14 +130,15 @@ struct OzakiParams {
   const double* e[kMaxTerms];  // distinct matrices (n×n column-major)
   OzakiTerm terms[kMaxTerms];
   int8_t* xs;    // workspace (ozaki_bind_workspace): [nx][S][L·R][Kp] slices
-  double* xsc;   // [nx][L·R] fiber scales 2^ex
+  double* xsc;   // [nx][L·R] fiber exponents ex (NaN: non-finite fiber)
   int8_t* es;    // [ne][S][n][Kp]
-  double* esc;   // [ne][n]
+  double* esc;   // [ne][n] row exponents
 };
 bool ozaki_supported(int64_t L, int n, int64_t R, int S);
 size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne);
 void ozaki_bind_workspace(OzakiParams& p, void* ws);  // sets Kp and the workspace pointers
-cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_x = true, bool split_e = true);
+cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_x = true, bool split_e = true,
+                              bool gemm = true);
 
 // Kernel launchers (kernels.cu).  Return cudaError_t of the launch.
 cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st);

@@ -87,7 +87,9 @@ def test_blocks_sharded_emulated():
             for r in range(world)]
     outs = apply_ranks_serial(ranks, pbs[0].tau, pbs[0].ells, vecs, mode="same")
     torch.cuda.synchronize()
-    single = PhiKS([pb.A for pb in pbs]).apply(pbs[0].tau, pbs[0].ells, [dev(pb.vs[0]) for pb in pbs])
+    sop = PhiKS([pb.A for pb in pbs])
+    sop.set_gemm_path("dmma")  # sharded handles run the DMMA kernel
+    single = sop.apply(pbs[0].tau, pbs[0].ells, [dev(pb.vs[0]) for pb in pbs])
     torch.cuda.synchronize()
     for k in range(len(single)):
         got = torch.cat([outs[r][k] for r in range(world)]).cpu().numpy()
@@ -120,7 +122,9 @@ def test_blocks_complex_sharded_emulated(world):
             for r in range(world)]
     outs = apply_ranks_serial(ranks, 0.5, (0, 1, 3), vecs, mode="same", n_scales=2)
     torch.cuda.synchronize()
-    single = PhiKS([pb.A for pb in pbs]).apply(0.5, (0, 1, 3), [dev(pb.vs[0]) for pb in pbs], n_scales=2)
+    sop = PhiKS([pb.A for pb in pbs])
+    sop.set_gemm_path("dmma")
+    single = sop.apply(0.5, (0, 1, 3), [dev(pb.vs[0]) for pb in pbs], n_scales=2)
     torch.cuda.synchronize()
     for k in range(len(single)):
         got = torch.cat([outs[r][k] for r in range(world)]).cpu().numpy()

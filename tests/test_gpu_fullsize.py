@@ -104,6 +104,7 @@ def test_config3_full_sharded8_equals_single():
     pb = W.config(3).problems[0]
     x = W.as_flat(pb.vs[0])
     op = PhiKS(pb.A)
+    op.set_gemm_path("dmma")  # the sharded handle runs the DMMA kernel: same arithmetic, bitwise equal
     single = [o.cpu().numpy() for o in op.apply(pb.tau, pb.ells, [to_dev(pb.vs[0])], n_scales=1)]
     del op
     world = 8

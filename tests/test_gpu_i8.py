@@ -1,0 +1,203 @@
+"""GPU parity of the int8 tensor-core μ-mode products:
+phiks_mode_product_i8 against numpy fp64 on ragged shapes, shared inputs and
+matrices, extreme magnitudes, zeros and non-finite values; whole φ-actions on
+the int8 path against the CPU oracle and against the DMMA path; the path
+selection (phiks_set_gemm_path) and its fallbacks."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import phiks_oracle as O  # noqa: E402
+from paper_2210_07667_b200 import PhiKS, mode_product, mode_product_i8  # noqa: E402
+from paper_2210_07667_b200 import workloads as W  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def np_mode(x, dims, mu, M):
+    X = x.reshape(dims[::-1])  # column-major flat: the last C-order axis is mode 0
+    ax = len(dims) - 1 - mu
+    return np.moveaxis(np.tensordot(M, X, axes=([1], [ax])), 0, ax).reshape(-1)
+
+
+def colmajor(M):
+    return torch.from_numpy(np.asfortranarray(M).reshape(-1, order="F").copy()).to(DEV)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def dot_bound(xs, dims, mu, M):
+    """Per-element |M|·|x| (the scale of an fp64 dot product's error bound)."""
+    return np_mode(np.abs(xs), dims, mu, np.abs(M))
+
+
+@pytest.mark.parametrize("dims,mu", [((40, 33, 17), 0), ((40, 33, 17), 1), ((40, 33, 17), 2), ((256, 9), 0),
+                                     ((7, 250), 1), ((130, 64, 5), 1), ((3, 128, 129), 2), ((33, 200, 41), 1),
+                                     ((1, 1000, 96), 2), ((129,), 0), ((5, 1, 31), 1)])
+@pytest.mark.parametrize("digits", [6, 7])
+def test_i8_mode_product_vs_numpy(dims, mu, digits):
+    rng = np.random.default_rng(hash((dims, mu, digits)) % 2 ** 32)
+    N = int(np.prod(dims))
+    n = dims[mu]
+    xs = [rng.standard_normal(N) * np.exp(rng.uniform(-4, 4, N)) for _ in range(2)]
+    Ms = [rng.standard_normal((n, n)) * np.exp(rng.uniform(-3, 3, (n, n))) for _ in range(2)]
+    xin = [torch.from_numpy(x).to(DEV) for x in xs]
+    Min = [colmajor(M) for M in Ms]
+    pairs = [(0, 0), (1, 1), (0, 1), (1, 0)]
+    outs = [torch.empty(N, dtype=torch.float64, device=DEV) for _ in pairs]
+    mode_product_i8(dims, mu, [xin[a] for a, _ in pairs], [Min[b] for _, b in pairs], outs, slices=digits)
+    torch.cuda.synchronize()
+    # error bound per element: |Δy| ≤ c·n·2^-(8S-9)·max|e_j|·max|x_c|; check the
+    # relative 2-norm and the elementwise bound against the dot-product scale
+    for o, (a, b) in zip(outs, pairs):
+        ref = np_mode(xs[a], dims, mu, Ms[b])
+        got = o.cpu().numpy()
+        e = rel(got, ref)
+        assert e <= (2e-14 if digits == 7 else 5e-12), (dims, mu, digits, e)
+        Xf = xs[a].reshape(dims[::-1])
+        ax = len(dims) - 1 - mu
+        xmax = np.max(np.abs(Xf), axis=ax, keepdims=True)  # per fiber
+        emax = np.max(np.abs(Ms[b]), axis=1)                  # per row j
+        scale = np.moveaxis(np.broadcast_to(xmax, Xf.shape), ax, 0)
+        scale = np.moveaxis(scale * emax.reshape((-1,) + (1,) * (len(dims) - 1)), 0, ax).reshape(-1)
+        bound = n * 2.0 ** (-(8 * digits - 9)) * scale
+        assert np.all(np.abs(got - ref) <= bound + 1e-300), (dims, mu, digits)
+
+
+def test_i8_mode_product_special_values():
+    dims, mu = (64, 130), 1
+    N = 64 * 130
+    n = 130
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(N)
+    X = x.reshape(130, 64)  # [k, l]
+    X[:, 3] = 0.0                      # an all-zero fiber
+    X[:, 5] *= 1e300                   # huge
+    X[:, 6] *= 1e-300                  # tiny (normal)
+    X[:, 7] = 5e-324 * rng.integers(-50, 50, 130)  # subnormal
+    X[:, 8] = 0.0
+    X[17, 8] = np.nan                  # a NaN poisons its fiber only
+    X[:, 9] = 0.0
+    X[3, 9] = np.inf
+    M = rng.standard_normal((n, n))
+    x = X.reshape(-1)
+    out = torch.empty(N, dtype=torch.float64, device=DEV)
+    mode_product_i8(dims, mu, [torch.from_numpy(x.copy()).to(DEV)], [colmajor(M)], [out], slices=7)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().reshape(130, 64)
+    with np.errstate(invalid="ignore", over="ignore"):
+        ref = np_mode(x, dims, mu, M).reshape(130, 64)
+    assert np.all(got[:, 3] == 0.0)
+    for c, f in ((5, 1e-300), (6, 1e300)):  # compare rescaled (the 2-norm of 1e300 values overflows)
+        assert rel(got[:, c] * f, ref[:, c] * f) <= 1e-14, c
+    assert rel(got[:, 7], ref[:, 7]) <= 1e-12  # subnormal inputs keep their (reduced) precision
+    assert np.all(np.isnan(got[:, 8])) and np.all(np.isnan(got[:, 9]))
+    ok = [c for c in range(64) if c not in (3, 5, 6, 7, 8, 9)]
+    assert rel(got[:, ok], ref[:, ok]) <= 1e-14
+
+
+def test_i8_matches_dmma_building_block_large():
+    dims = (256, 256, 64)
+    N = int(np.prod(dims))
+    g = torch.Generator(device=DEV).manual_seed(3)
+    x = torch.rand(N, dtype=torch.float64, device=DEV, generator=g) * 3
+    for mu in range(3):
+        n = dims[mu]
+        M = torch.randn(n * n, dtype=torch.float64, device=DEV, generator=g)
+        a = torch.empty_like(x)
+        b = torch.empty_like(x)
+        mode_product(dims, mu, [x], [M], [a])
+        mode_product_i8(dims, mu, [x], [M], [b], slices=7)
+        torch.cuda.synchronize()
+        assert float(torch.linalg.norm(a - b) / torch.linalg.norm(a)) <= 1e-14, mu
+
+
+def test_i8_rejects_unsupported():
+    x = torch.zeros(300 * 4, dtype=torch.float64, device=DEV)
+    M = torch.zeros(300 * 300, dtype=torch.float64, device=DEV)
+    with pytest.raises(RuntimeError):
+        mode_product_i8((300, 4), 0, [x], [M], [x.clone()], slices=7)
+    with pytest.raises(RuntimeError):
+        mode_product_i8((4, 4), 0, [x[:16]], [M[:16]], [x[:16].clone()], slices=8)
+
+
+def _apply(op, pb, path):
+    op.set_gemm_path(path)
+    vs = [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).to(DEV) for v in pb.vs]
+    outs = op.apply(pb.tau, pb.ells, vs, mode=pb.mode, n_scales=pb.n_scales)
+    torch.cuda.synchronize()
+    return [o.cpu().numpy() for o in outs], op.stats()
+
+
+def _oracle_outs(pb):
+    ref = O.phiks(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, n_scales=pb.n_scales)
+    if pb.mode == "same":
+        return [W.as_flat(ref.out[(ell, j)]) for j in range(pb.n_scales) for ell in pb.ells]
+    return [W.as_flat(ref.out[j]) for j in range(pb.n_scales)]
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_i8_path_apply_parity_small_configs(cfg):
+    for pb in W.config(cfg, small=True).problems:
+        if max(pb.dims) > 256:
+            continue
+        op = PhiKS(pb.A)
+        got, st = _apply(op, pb, "i8")
+        ref = _oracle_outs(pb)
+        for k, (g, r) in enumerate(zip(got, ref)):
+            assert rel(g, r) <= 1e-12, (pb.name, k, rel(g, r))
+        gd, std = _apply(op, pb, "dmma")
+        assert std["i8_mode_launches"] == 0
+        for g, r in zip(got, gd):
+            assert rel(g, r) <= 1e-13
+
+
+def test_i8_path_apply_random_problems():
+    rng = np.random.default_rng(11)
+    for c in range(6):
+        d = int(rng.integers(2, 4))
+        dims = tuple(int(x) for x in rng.integers(24, 140 if d == 3 else 256, size=d))
+        fac = W.random_factors(dims, seed=500 + c, scale=float(rng.uniform(0.5, 20.0)))
+        mode = "same" if c % 2 == 0 else "lincomb"
+        ells = (0, 1, 2) if mode == "same" else (0, 1, 2, 3)
+        vs = [W.random_tensor(dims, seed=600 + 7 * c + k) for k in range(1 if mode == "same" else len(ells))]
+        pb = W.Problem(f"i8rand{c}", dims, fac, float(rng.uniform(0.2, 1.5)), mode, ells, vs, int(rng.integers(1, 3)))
+        op = PhiKS(pb.A)
+        got, st = _apply(op, pb, "i8")
+        assert st["i8_mode_launches"] > 0, pb.name
+        for k, (g, r) in enumerate(zip(got, _oracle_outs(pb))):
+            assert rel(g, r) <= 1e-12, (pb.name, k, rel(g, r))
+
+
+def test_i8_path_blocks_handle_and_fallback():
+    # a block-diagonal handle on the int8 path; a mode with n_μ > 256 falls back to DMMA
+    dims = (300, 40)
+    pbs = []
+    for b in range(2):
+        fac = W.random_factors(dims, seed=700 + b, scale=4.0 + 6 * b)
+        pbs.append(W.Problem(f"blk{b}", dims, fac, 0.5, "same", (0, 1, 2), [W.random_tensor(dims, seed=710 + b)], 1))
+    op = PhiKS([pb.A for pb in pbs])
+    op.set_gemm_path("i8")
+    vs = [torch.from_numpy(np.ascontiguousarray(W.as_flat(pb.vs[0]))).to(DEV) for pb in pbs]
+    outs = op.apply(0.5, (0, 1, 2), vs)
+    torch.cuda.synchronize()
+    st = op.stats()
+    assert st["i8_mode_launches"] > 0  # mode 2 (n = 40) on the int8 path, mode 1 (n = 300 > 256) on DMMA
+    for b, pb in enumerate(pbs):
+        for k, r in enumerate(_oracle_outs(pb)):
+            assert rel(outs[b * 3 + k].cpu().numpy(), r) <= 1e-12
+
+
+def test_i8_path_selection_api():
+    pb = W.config(2, small=True).problems[0]
+    op = PhiKS(pb.A)
+    with pytest.raises(KeyError):
+        op.set_gemm_path("fp32")
+    _, st = _apply(op, pb, "dmma")
+    assert st["i8_mode_launches"] == 0
+    _, st = _apply(op, pb, "i8")
+    assert st["i8_mode_launches"] > 0

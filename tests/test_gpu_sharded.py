@@ -47,6 +47,7 @@ def run_sharded(pb, world, n_scales=None, force=None):
 def run_single(pb, n_scales=None):
     n_scales = pb.n_scales if n_scales is None else n_scales
     op = PhiKS(pb.A)
+    op.set_gemm_path("dmma")  # sharded handles run the DMMA kernel; compare like with like
     outs = op.apply(pb.tau, pb.ells, [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).to(DEV) for v in pb.vs],
                     mode=pb.mode, n_scales=n_scales)
     torch.cuda.synchronize()
@@ -176,8 +177,10 @@ def test_sharded_complex(dims, world, mode):
     for r in ranks:
         r.close()
     compare_oracle(pb, gathered, 2)
-    single = PhiKS(pb.A).apply(pb.tau, pb.ells, [torch.from_numpy(np.ascontiguousarray(x)).to(DEV) for x in flat],
-                               mode=pb.mode, n_scales=2)
+    sop = PhiKS(pb.A)
+    sop.set_gemm_path("dmma")
+    single = sop.apply(pb.tau, pb.ells, [torch.from_numpy(np.ascontiguousarray(x)).to(DEV) for x in flat],
+                       mode=pb.mode, n_scales=2)
     torch.cuda.synchronize()
     for a, b in zip(gathered, single):
         assert rel2(a, b.cpu().numpy()) <= 1e-15
