@@ -114,6 +114,85 @@ def load_traffic():
         return None, None
 
 
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def expm_entry(args, ex_n, ex_ms):
+    return {"launches": ex_n, "event_ms_per_step": ex_ms / max(args.steps, 1),
+            "note": "runs on the handle's side stream, overlapped with the other species' Tucker "
+                    "launches; its event time includes that sharing"}
+
+
+def dmma_roofline(args, t_local, mp_ms, mp_fl, mp_n, ex_n, ex_ms, peak_tf):
+    bpg, tsrc = load_traffic()
+    # dram bytes per launch: the committed ncu capture's bytes per algorithmic GFLOP
+    # of this kernel, times the average GFLOP of the launches timed here
+    traffic = bpg * (mp_fl / max(mp_n, 1) / 1e9) if (bpg and mp_n) else None
+    ach = mp_fl / (mp_ms / 1e3) / 1e12 if mp_ms > 0 else None
+    return {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": (ach / peak_tf) if ach else None, "traffic": traffic,
+            "kernel": "mode_product_tma_kernel (FP64 DMMA.8x8x4, TMA + mbarrier ring): the Tucker-operator launches",
+            "algorithmic_bytes_per_launch": 16.0 * (mp_fl / max(mp_n, 1)) / (2.0 * 256),
+            "peak_source": "measured in this run: phiks_fp64_peak_launch DMMA microbenchmark (max of 3)",
+            "per_launch_ms": mp_ms / max(mp_n, 1), "launches_timed": mp_n,
+            "share_of_step": (mp_ms / 1e3) / t_local if t_local > 0 else None,
+            "expm_stage": expm_entry(args, ex_n, ex_ms), "traffic_source": tsrc}
+
+
+I8_PAIRS = 28  # digit products per fp64 product: pairs (s, t) of 7 digits with s + t < 7
+
+
+def i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, g_ms, g_n, ex_n, ex_ms, dmma_peak):
+    """Roofline of the dominant kernel, the int8 digit-product GEMM (ozaki.cu): algorithmic int8
+    ops = 28 digit pairs × 2·rows·n² per fp64 product; peak = the measured bf16 dense peak of
+    MEASURED_PEAKS.json × 2 (the guide's nominal int8 : bf16 ratio), the sustained figure since the
+    kernel runs inside a long step."""
+    pk = measured_peaks()
+    bf16 = pk.get("bf16_tflops_sustained") or pk.get("bf16_tflops")
+    peak = 2.0 * bf16 if bf16 else 4500.0
+    ops = I8_PAIRS * i8_fl  # i8_flops counts 2·rows·n² per GEMM term
+    ach = ops / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
+    tr = load_i8_traffic()
+    per_launch_gflop = i8_fl / max(g_n, 1) / 1e9
+    traffic = tr["dram_bytes_per_fp64_gflop"] * per_launch_gflop if tr else None
+    # algorithmic bytes of a GEMM launch: the fiber digits (7 B per element and distinct input, once)
+    # + the fp64 outputs (8 B per element and term); elements per term = flops / (2·n), n = 256
+    elems = i8_fl / max(g_n, 1) / (2.0 * 256)
+    return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOP/s (int8)",
+            "frac": (ach / peak) if ach else None, "traffic": traffic,
+            "kernel": "oz_gemm_kernel<7> (tcgen05.mma kind::i8, TMEM accumulators, TMA SWIZZLE_32B): "
+                      "the Tucker-operator μ-mode products",
+            "algorithmic_ops_per_launch": ops / max(g_n, 1),
+            "algorithmic_bytes_per_launch_max": elems * 15.0,
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained × 2 (int8 : bf16 dense = 2, "
+                            "B200_PROFILING.md)") if bf16 else "nominal 4.5 POPS (MEASURED_PEAKS.json absent)",
+            "per_launch_ms": g_ms / max(g_n, 1), "launches_timed": g_n,
+            "share_of_step": (g_ms / 1e3) / t_local if t_local > 0 else None,
+            "fp64_equivalent": {"tflops": i8_fl / (i8_ms / 1e3) / 1e12 if i8_ms > 0 else None,
+                                "vs_measured_dmma_peak": (i8_fl / (i8_ms / 1e3) / 1e12 / dmma_peak)
+                                if i8_ms > 0 else None, "dmma_peak_tflops": dmma_peak,
+                                "note": "fp64 flops of the products over the int8 path's time (digit splits "
+                                        "+ GEMM)"},
+            "digit_splits": {"ms_per_step": (i8_ms - g_ms) / max(args.steps, 1)},
+            "tucker_launches": {"ms_per_step": mp_ms / max(args.steps, 1), "launches": mp_n},
+            "expm_stage": expm_entry(args, ex_n, ex_ms),
+            "traffic_source": tr.get("source") if tr else None}
+
+
+def load_i8_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_summary_i8.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 def run_oracle_sample(problems):
     """The oracle (as it stands) on a bounded sample; returns (flops, seconds)."""
@@ -257,6 +336,10 @@ def b200_arm(args):
     mp_n = sum(s["mode_product_launches"] for s in st)
     ex_ms = sum(s["expm_ms"] for s in st)
     ex_n = sum(s["expm_launches"] for s in st)
+    i8_ms = sum(s["i8_ms"] for s in st)
+    i8_fl = sum(s["i8_flops"] for s in st)
+    i8_gemm_ms = sum(s["i8_gemm_ms"] for s in st)
+    i8_gemm_n = sum(s["i8_gemm_launches"] for s in st)
     for op in ops:
         op.set_profiling(False)
     t = t_local
@@ -299,27 +382,19 @@ def b200_arm(args):
         cpu = {"value": f / tc / 1e9, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
                "sample": "the full step (both species, 256^3) once, numpy/OpenBLAS fp64", "seconds": tc}
 
-    bpg, tsrc = load_traffic()
-    # dram bytes per launch: the committed ncu capture's bytes per algorithmic GFLOP
-    # of this kernel, times the average GFLOP of the launches timed here
-    traffic = bpg * (mp_fl / max(mp_n, 1) / 1e9) if (bpg and mp_n) else None
-    ach = mp_fl / (mp_ms / 1e3) / 1e12 if mp_ms > 0 else None
-    roof = {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
-            "frac": (ach / peak_tf) if ach else None, "traffic": traffic,
-            "kernel": "mode_product_tma_kernel (FP64 DMMA.8x8x4, TMA + mbarrier ring): the Tucker-operator launches",
-            "algorithmic_bytes_per_launch": 16.0 * (mp_fl / max(mp_n, 1)) / (2.0 * 256),
-            "peak_source": "measured in this run: phiks_fp64_peak_launch DMMA microbenchmark (max of 3)",
-            "per_launch_ms": mp_ms / max(mp_n, 1), "launches_timed": mp_n,
-            "share_of_step": (mp_ms / 1e3) / t_local if t_local > 0 else None,
-            "expm_stage": {"launches": ex_n, "event_ms_per_step": ex_ms / max(args.steps, 1),
-                           "note": "runs on the handle's side stream, overlapped with the other species' Tucker "
-                                   "launches; its event time includes that sharing"},
-            "traffic_source": tsrc}
+    if i8_gemm_n:
+        roof = i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, i8_gemm_ms, i8_gemm_n, ex_n, ex_ms,
+                           peak_tf)
+    else:
+        roof = dmma_roofline(args, t_local, mp_ms, mp_fl, mp_n, ex_n, ex_ms, peak_tf)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "compute": ("μ-mode products as exact int8 digit products on the tcgen05 tensor cores (7 balanced "
+                        "base-256 digits per fp64 operand, int32 accumulation, fp64 splits and epilogue: "
+                        "DESIGN.md §4c)") if i8_gemm_n else "fp64 DMMA tensor cores",
             "config": {"workload": WORKLOAD, "handle": "one block-diagonal handle (2 blocks = species)",
                        "parallelism": f"slab{world} (mode-3 slabs, transposition fused into peer stores)"
                        if world > 1 else "single",

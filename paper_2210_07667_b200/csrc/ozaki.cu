@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(256) oz_split_x_kernel(const OzakiParams p) {
     if (lane < nf) {
       const int64_t l = c % L, r = c / L;
       const double* src = X + l + L * n * r;
+#pragma unroll 8
       for (int k = warp; k < n; k += 8) tile[lane * P + k] = __ldg(src + L * k);
     }
   }
@@ -141,6 +142,45 @@ __global__ void __launch_bounds__(256) oz_split_x_kernel(const OzakiParams p) {
     if (lane == 0)  // the fiber's exponent (NaN marks a non-finite fiber)
       p.xsc[static_cast<int64_t>(slot) * C + c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
   }
+}
+
+// ---- split_x, contiguous fibers (L = 1): one warp per fiber, values in registers ----
+template <int S>
+__global__ void __launch_bounds__(256) oz_split_x_contig_kernel(const OzakiParams p) {
+  const int slot = blockIdx.y;
+  const int64_t C = p.R;
+  const int n = p.n, Kp = p.Kp;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (c >= C) return;
+  const double* src = p.x[slot] + c * n;
+  double v[kOzMaxN / 128][4];
+  double m = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < kOzMaxN / 128; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 128 * i + 4 * lane + q;
+      v[i][q] = k < n ? __ldg(src + k) : 0.0;
+      m = fmax(m, fabs(v[i][q]));
+      bad |= !isfinite(v[i][q]);
+    }
+  m = warp_max(m);
+  bad = __any_sync(0xffffffffu, bad);
+  const int ex = bad ? 0 : slice_exponent(m);
+  int8_t* xs = p.xs + static_cast<int64_t>(slot) * S * C * Kp;
+#pragma unroll
+  for (int i = 0; i < kOzMaxN / 128; ++i) {
+    const int k0 = 128 * i + 4 * lane;
+    if (k0 < Kp) {
+      uint32_t pk[S];
+      split4<S>(v[i], ex, pk);
+#pragma unroll
+      for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(xs + (s * C + c) * Kp + k0) = pk[s];
+    }
+  }
+  if (lane == 0) p.xsc[static_cast<int64_t>(slot) * C + c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
 }
 
 // ---- split_e: one warp per row j of E (column-major, E[j + k·n]) ----
@@ -173,7 +213,8 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
     for (int s = 0; s < S; ++s)
       *reinterpret_cast<uint32_t*>(es + (static_cast<int64_t>(s) * n + j) * Kp + k0) = pk[s];
   }
-  if (lane == 0) p.esc[static_cast<int64_t>(slot) * n + j] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
+  if (lane == 0)  // the row's scale 2^{ee-30} (the GEMM epilogue's 2^-30: 2^-14 of the digit scaling, 2^-16 of its sums)
+    p.esc[static_cast<int64_t>(slot) * n + j] = bad ? __longlong_as_double(0x7ff8000000000000ll) : scalbn(1.0, ex - 30);
 }
 
 // ---- tcgen05 / TMA / mbarrier helpers ----
@@ -265,6 +306,10 @@ __device__ __forceinline__ void oz_ld8(uint32_t taddr, uint32_t* v) {
 // exact int32 → fp64 without I2F: 1.5·2^52 + 2^31 + v has v in its low mantissa bits
 __device__ __forceinline__ double oz_i2d(uint32_t v) {
   return __hiloint2double(0x43380000, static_cast<int>(v ^ 0x80000000u)) - 6755401588539392.0;
+}
+// exact int64 → fp64 for |v| < 2^51: the bits of 1.5·2^52 + v
+__device__ __forceinline__ double oz_l2d(long long v) {
+  return __longlong_as_double(v + 0x4338000000000000ll) - 6755399441055744.0;
 }
 
 // Persistent GEMM geometry: the E-digit tile of a (term, n-tile) stays resident
@@ -433,6 +478,8 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
       const double xsv = rvalid ? p.xsc[static_cast<int64_t>(term.xslot) * C + c] : 0.0;
       oz_mbar_wait(t_full, tile & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      // drain: per column, 2^16 Σ_g 256^{-g} D_g from three exact int64 partial sums
+      // (D_0·2^16 + D_1·2^8 + D_2, D_3·2^16 + D_4·2^8 + D_5, D_6; each < 2^42) and two fp64 fmas
       double acc[32];
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) {
@@ -442,10 +489,13 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          double a = oz_i2d(v[S - 1][q]);
-#pragma unroll
-          for (int g = S - 2; g >= 0; --g) a = fma(a, 0x1p-8, oz_i2d(v[g][q]));
-          acc[cb * 8 + q] = a;
+          const long long ta = static_cast<long long>(static_cast<int>(v[0][q])) * 65536 +
+                               static_cast<long long>(static_cast<int>(v[1][q])) * 256 + static_cast<int>(v[2][q]);
+          const long long tb = static_cast<long long>(static_cast<int>(v[3][q])) * 65536 +
+                               static_cast<long long>(static_cast<int>(v[4][q])) * 256 + static_cast<int>(v[5][q]);
+          double y = oz_l2d(tb);
+          if (S == 7) y = fma(oz_i2d(v[S - 1][q]), 0x1p-8, y);
+          acc[cb * 8 + q] = fma(y, 0x1p-24, oz_l2d(ta));
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -456,17 +506,16 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
       const double* esc = p.esc + static_cast<int64_t>(term.eslot) * p.n + j0;
       const int jn = p.n - j0;  // valid columns of this half
       if (rvalid && jn > 0) {
-        // y = scalbn(β·acc, ex_c + ee_j − 14): one rounding, the whole exponent range
+        // y = (acc · 2^{ee_j − 30}) · (β·2^{ex_c}): the power-of-two product first (no intermediate overflow)
         const int64_t l = c % L, r = c / L;
         double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
-        const bool xbad = isnan(xsv);
-        const int xe = xbad ? 0 : static_cast<int>(xsv) - 14;
+        const int xe = isnan(xsv) ? 0 : static_cast<int>(xsv);
+        const double rb = isnan(xsv) ? xsv
+                          : (xe >= -1022 && xe <= 1023)
+                              ? term.beta * __longlong_as_double(static_cast<long long>(xe + 1023) << 52)
+                              : scalbn(term.beta, xe);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const double ee = q < jn ? __ldg(esc + q) : 0.0;
-          acc[q] = (xbad || isnan(ee)) ? __longlong_as_double(0x7ff8000000000000ll)
-                                       : scalbn(acc[q] * term.beta, xe + static_cast<int>(ee));
-        }
+        for (int q = 0; q < 32; ++q) acc[q] = (acc[q] * (q < jn ? __ldg(esc + q) : 0.0)) * rb;  // exact, then rounded
         if (jn >= 32) {
           if (L == 1 && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
 #pragma unroll
@@ -534,7 +583,10 @@ cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool 
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
+    if (p.L == 1)
+      oz_split_x_contig_kernel<S><<<dim3(static_cast<unsigned>((C + 7) / 8), p.nx), 256, 0, st>>>(p);
+    else
+      oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
   }
   if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
   if (p.nterms == 0 || !gemm) return cudaGetLastError();
