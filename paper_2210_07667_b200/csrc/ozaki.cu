@@ -44,30 +44,38 @@ __device__ __forceinline__ unsigned oz_smem_u32(const void* p) {
 }
 
 // ---- exact splitting into S balanced base-256 digits ----
-// |v| < 2^{ex-1}: F = trunc(|v|·2^{8S-1-ex}) < 2^{8S-2} (exact integer ops on
-// the fp64 fields); G = ±F + 0x80…80 has bytes d_i + 128, d_i the balanced
-// digits of ±F; digit s (most significant first) = byte S-1-s of G ^ 0x80…80
+// |v| < 2^{ex-1}: F = trunc(v·2^{8S-1-ex}) (an exact power-of-two scaling and one
+// fp64 → int64 conversion), |F| < 2^{8S-2}; G = F + 0x80…80 has bytes d_i + 128,
+// d_i the balanced digits of F; digit s (most significant first) = byte S-1-s
+// of G ^ 0x80…80.  The scaling is split in two factors when 2^{8S-1-ex}
+// overflows (fibers of subnormal magnitude).
+struct OzScale {
+  double a, b;
+  bool two;
+};
 template <int S>
-__device__ __forceinline__ uint64_t oz_digits(double v, int ex) {
-  const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
-  const int e = static_cast<int>((bits >> 52) & 0x7FF);
-  uint64_t m = bits & ((uint64_t(1) << 52) - 1);
-  int E = -1074;
-  if (e != 0) {
-    m |= uint64_t(1) << 52;
-    E = e - 1075;
-  }
-  const int sh = E - ex + 8 * S - 1;
-  const uint64_t F = sh >= 0 ? (m << sh) : (sh > -64 ? (m >> -sh) : 0);
+__device__ __forceinline__ OzScale oz_scale(int ex) {
+  const int k = 8 * S - 1 - ex;
+  OzScale sc;
+  sc.two = k > 1000;
+  sc.a = __longlong_as_double(static_cast<long long>((sc.two ? 1000 : k) + 1023) << 52);
+  sc.b = __longlong_as_double(static_cast<long long>((sc.two ? k - 1000 : 0) + 1023) << 52);
+  return sc;
+}
+template <int S>
+__device__ __forceinline__ uint64_t oz_digits(double v, const OzScale& sc) {
+  double t = v * sc.a;
+  if (sc.two) t *= sc.b;
+  const long long F = __double2ll_rz(t);
   constexpr uint64_t C = 0x8080808080808080ull >> (64 - 8 * S);
-  const uint64_t G = ((bits >> 63) ? (0 - F) : F) + C;
-  return G ^ C;
+  return (static_cast<uint64_t>(F) + C) ^ C;
 }
 template <int S>
 __device__ __forceinline__ void split4(const double (&v)[4], int ex, uint32_t (&pk)[S]) {
+  const OzScale sc = oz_scale<S>(ex);
   uint64_t h[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) h[q] = oz_digits<S>(v[q], ex);
+  for (int q = 0; q < 4; ++q) h[q] = oz_digits<S>(v[q], sc);
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int i = S - 1 - s;  // byte of the digit
@@ -310,6 +318,121 @@ __device__ __forceinline__ double oz_i2d(uint32_t v) {
 // exact int64 → fp64 for |v| < 2^51: the bits of 1.5·2^52 + v
 __device__ __forceinline__ double oz_l2d(long long v) {
   return __longlong_as_double(v + 0x4338000000000000ll) - 6755399441055744.0;
+}
+
+// ---- split_x, strided fibers (L % 32 == 0): persistent, TMA double buffer ----
+// A tile is 32 consecutive fibers (l0..l0+31, r) × all n k, loaded by one TMA
+// box (32, n, 1) of the (L, n, R) tensor into smem [k][32]; warp w takes
+// k ∈ [32w, 32w+32) of every fiber (lane = fiber): partial maxima meet in smem,
+// then each thread writes its 32 digits per slice as two 16-byte stores.
+struct OzXMaps {
+  CUtensorMap m[8];
+};
+constexpr int kOzSplitSlots = 8;
+
+template <int S>
+__global__ void __launch_bounds__(512, 1)
+    oz_split_x_tma_kernel(const OzakiParams p, const __grid_constant__ OzXMaps maps,
+                          const __grid_constant__ CUtensorMap dmap, int slot0, int nslots) {
+  extern __shared__ __align__(1024) double oz_sx_raw[];
+  double* buf = oz_sx_raw;  // indexed from the shared array itself: the compiler keeps LDS
+  const int n = p.n, Kp = p.Kp;
+  const int64_t L = p.L, C = p.L * p.R;
+  const int tile_elems = 32 * n;
+  double* red = oz_sx_raw + 2 * 32 * kOzMaxN + S * 2 * 4096 / 8;  // [16][32] partial maxima
+  int* redbad = reinterpret_cast<int*>(red + 16 * 32);             // [16][32]
+  uint64_t* full = reinterpret_cast<uint64_t*>(redbad + 16 * 32);
+  // digit staging: per digit s and 128-byte k-half h, a SWIZZLE_128B image of the
+  // 32 fibers × 128 bytes box (16-byte chunk q of row r at q ^ (r & 7)), written
+  // conflict-free and stored by TMA (which undoes the swizzle)
+  uint8_t* stage = reinterpret_cast<uint8_t*>(oz_sx_raw) + 2 * 32 * kOzMaxN * 8;  // 1 KB aligned
+  const int nh = Kp > 128 ? 2 : 1;  // k-halves (Kp ≤ 256)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntc = C / 32;
+  const int64_t total = ntc * nslots;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < nslots && b < kOzSplitSlots; ++b)
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.m[b])) : "memory");
+    oz_mbar_init(&full[0], 1);
+    oz_mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t it, int b) {
+    const int sl = static_cast<int>(it / ntc);
+    const int64_t c0 = (it % ntc) * 32;
+    oz_mbar_expect_tx(&full[b], static_cast<unsigned>(tile_elems * 8));
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(oz_smem_u32(buf + b * tile_elems)),
+        "l"(reinterpret_cast<uint64_t>(&maps.m[sl])), "r"(static_cast<int>(c0 % L)), "r"(0),
+        "r"(static_cast<int>(c0 / L)), "r"(oz_smem_u32(&full[b]))
+        : "memory");
+  };
+  if (threadIdx.x == 0 && blockIdx.x < total) issue(blockIdx.x, 0);
+  int i = 0;
+  for (int64_t it = blockIdx.x; it < total; it += gridDim.x, ++i) {
+    const int b = i & 1;
+    if (threadIdx.x == 0 && it + gridDim.x < total) issue(it + gridDim.x, b ^ 1);  // buffer b^1 is free
+    oz_mbar_wait(&full[b], (i >> 1) & 1);
+    const double* t = buf + b * tile_elems;
+    const int sl = slot0 + static_cast<int>(it / ntc);
+    const int64_t c = (it % ntc) * 32 + lane;
+    const int k0 = 16 * warp;
+    double m = 0.0;
+    int bad = 0;
+#pragma unroll 8
+    for (int k = k0; k < k0 + 16 && k < n; ++k) {
+      const double v = t[k * 32 + lane];
+      m = fmax(m, fabs(v));
+      bad |= !isfinite(v);
+    }
+    red[warp * 32 + lane] = m;
+    redbad[warp * 32 + lane] = bad;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < 16; ++w) {
+      m = fmax(m, red[w * 32 + lane]);
+      bad |= redbad[w * 32 + lane];
+    }
+    const int ex = bad ? 0 : slice_exponent(m);
+    if (k0 < Kp) {
+      uint32_t pk[4][S];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = k0 + 4 * g + q;
+          v[q] = (k < n && !bad) ? t[k * 32 + lane] : 0.0;
+        }
+        split4<S>(v, ex, pk[g]);
+      }
+      const int h = k0 >> 7, q = (k0 & 127) >> 4;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        *reinterpret_cast<uint4*>(stage + ((s * 2 + h) * 32 + lane) * 128 + ((q ^ (lane & 7)) << 4)) =
+            make_uint4(pk[0][s], pk[1][s], pk[2][s], pk[3][s]);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // staging visible to the TMA store
+    if (warp == 0)
+      p.xsc[static_cast<int64_t>(sl) * C + c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
+    __syncthreads();  // staging complete; every warp is done with buffer b and the partial maxima
+    if (threadIdx.x == 0) {
+      const int64_t c0 = (it % ntc) * 32;
+      for (int s = 0; s < S; ++s)
+        for (int h = 0; h < nh; ++h)
+          asm volatile(
+              "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n" ::"l"(
+                  reinterpret_cast<uint64_t>(&dmap)),
+              "r"(h * 128), "r"(static_cast<int>(c0)), "r"(s), "r"(sl), "r"(oz_smem_u32(stage + (s * 2 + h) * 4096))
+              : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // staging read out before reuse
+    }
+    __syncthreads();  // staging free for the next tile
+  }
 }
 
 // Persistent GEMM geometry: the E-digit tile of a (term, n-tile) stays resident
@@ -571,6 +694,40 @@ bool oz_encode(CUtensorMap* m, const int8_t* base, int64_t Kp, int64_t rows, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D map over an fp64 (L, n, R) tensor with a (32, n, 1) box (split_x tiles)
+bool oz_encode_x(CUtensorMap* m, const double* base, int64_t L, int n, int64_t R) {
+  OzEncodeFn fn = oz_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(R)};
+  const cuuint64_t str[2] = {static_cast<cuuint64_t>(L) * 8, static_cast<cuuint64_t>(L) * n * 8};
+  const cuuint32_t box[3] = {32, static_cast<cuuint32_t>(n), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 4-D map over the digit array [slot][digit][fiber][k] with a (128, 32, 1, 1) box, SWIZZLE_128B (split_x stores)
+bool oz_encode_digits(CUtensorMap* m, const int8_t* base, int64_t Kp, int64_t rows, int S, int slots) {
+  OzEncodeFn fn = oz_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(S),
+                              static_cast<cuuint64_t>(slots)};
+  const cuuint64_t str[3] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Kp * rows),
+                             static_cast<cuuint64_t>(Kp * rows * S)};
+  const cuuint32_t box[4] = {128, 32, 1, 1};  // Kp ≥ 128 (the last k-half is clipped by the tensor bounds)
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool oz_split_tma_ok(const OzakiParams& p) {
+  for (int b = 0; b < p.nx; ++b)
+    if (reinterpret_cast<uintptr_t>(p.x[b]) & 15) return false;
+  return p.R < (int64_t(1) << 31) && p.L < (int64_t(1) << 31);
+}
+
 template <int S>
 cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e, bool gemm) {
   const int64_t C = p.L * p.R;
@@ -583,10 +740,35 @@ cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool 
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    if (p.L == 1)
+    if (p.L == 1) {
       oz_split_x_contig_kernel<S><<<dim3(static_cast<unsigned>((C + 7) / 8), p.nx), 256, 0, st>>>(p);
-    else
+    } else if (p.L % 32 == 0 && p.n <= 256 && p.Kp >= 128 && oz_split_tma_ok(p)) {
+      static bool tattr = false;
+      static int sms = 0;
+      const int smem = 2 * 32 * kOzMaxN * 8 + S * 2 * 4096 + 16 * 32 * 8 + 16 * 32 * 4 + 64;
+      if (!tattr) {
+        cudaError_t e = cudaFuncSetAttribute(oz_split_x_tma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        tattr = true;
+      }
+      for (int s0 = 0; s0 < p.nx; s0 += kOzSplitSlots) {
+        const int ns = p.nx - s0 < kOzSplitSlots ? p.nx - s0 : kOzSplitSlots;
+        OzXMaps maps;
+        for (int b = 0; b < ns; ++b)
+          if (!oz_encode_x(&maps.m[b], p.x[s0 + b], p.L, p.n, p.R)) return cudaErrorInvalidValue;
+        CUtensorMap dmap;
+        if (!oz_encode_digits(&dmap, p.xs, p.Kp, C, S, p.nx)) return cudaErrorInvalidValue;
+        const int64_t total = (C / 32) * ns;
+        const int grid = static_cast<int>(total < sms ? total : sms);
+        oz_split_x_tma_kernel<S><<<grid, 512, smem, st>>>(p, maps, dmap, s0, ns);
+      }
+    } else {
       oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
+    }
   }
   if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
   if (p.nterms == 0 || !gemm) return cudaGetLastError();
