@@ -36,7 +36,8 @@ namespace {
 
 constexpr int kOzBM = 128;  // fibers per tile (UMMA M, TMEM lanes)
 constexpr int kOzBN = 64;   // rows of E per tile (UMMA N)
-constexpr int kOzBK = 32;   // k per stage (bytes: one SWIZZLE_32B row, one UMMA K)
+constexpr int kOzBK = 128;  // k per stage (bytes: one SWIZZLE_128B row = 4 UMMA K-steps of 32)
+constexpr int kOzUK = 32;   // k per UMMA (int8)
 constexpr int kOzStages = 4;
 
 __device__ __forceinline__ unsigned oz_smem_u32(const void* p) {
@@ -252,14 +253,16 @@ __device__ __forceinline__ void oz_tma_load_4d(void* dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(oz_smem_u32(bar))
       : "memory");
 }
-// K-major SWIZZLE_32B operand: rows of 32 bytes, 8-row atoms of 256 bytes
-__device__ __forceinline__ uint64_t oz_desc_sw32(const void* p) {
+// K-major SWIZZLE_128B operand: rows of 128 bytes, 8-row atoms of 1 KB (1 KB
+// aligned); the k-th 32-byte UMMA slice of a row starts 32k bytes further
+// (start address + 2k: the swizzle is applied to the absolute address)
+__device__ __forceinline__ uint64_t oz_desc_sw128(const void* p) {
   const uint32_t a = oz_smem_u32(p);
   uint64_t d = static_cast<uint64_t>((a >> 4) & 0x3FFFu);
   d |= static_cast<uint64_t>(1) << 16;          // leading byte offset (unused for swizzled K-major)
-  d |= static_cast<uint64_t>(256 >> 4) << 32;   // stride byte offset: 8 rows × 32 B
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;  // stride byte offset: 8 rows × 128 B
   d |= static_cast<uint64_t>(1) << 46;          // descriptor version (sm_100)
-  d |= static_cast<uint64_t>(6) << 61;          // SWIZZLE_32B
+  d |= static_cast<uint64_t>(2) << 61;          // SWIZZLE_128B
   return d;
 }
 // kind::i8 instruction descriptor: D s32, A/B s8, both K-major, M = 128, N = BN
@@ -442,7 +445,7 @@ template <int S>
 struct OzGeom {
   static constexpr int SPS = 1;                                // digits per stage
   static constexpr int A_BYTES = SPS * kOzBM * kOzBK;         // one stage
-  static constexpr int NST = 65536 / A_BYTES;
+  static constexpr int NST = 4;                                // 64 KB ring
   static constexpr int B_KB = S * kOzBN * kOzBK;              // resident E slices per k-block
   static constexpr int B_BYTES = (kOzMaxN / kOzBK) * B_KB;    // Kp ≤ kOzMaxN
   static constexpr int SMEM = NST * A_BYTES + B_BYTES + 1024 /*align*/ + 512 /*barriers*/;
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
     // ---- MMA issuer (whole warp in lockstep, one elected lane issues) ----
     // diagonal g = s + t accumulates in TMEM columns [64g, 64g + 64); descriptors
     // advance by adding (byte offset >> 4) to their start-address field
-    const uint64_t a_desc0 = oz_desc_sw32(smem), b_desc0 = oz_desc_sw32(bres);
+    const uint64_t a_desc0 = oz_desc_sw128(smem), b_desc0 = oz_desc_sw128(bres);
     int cur_term = -1, bgen = 0, it = 0, tile = 0;
     for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
       const int term = static_cast<int>(u / sc.Mt);
@@ -571,12 +574,16 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
             for (int si = 0; si < G::SPS; ++si) {
               const int s = sg * G::SPS + si;
               const uint64_t ad = ad0 + static_cast<uint64_t>((si * kOzBM * kOzBK) >> 4);
-              const uint32_t accf = (kb > 0 || s > 0) ? 1u : 0u;
-              // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA
-              for (int c0 = 0; c0 < (S - s) * kOzBN; c0 += 256) {
-                const int nn = min(256, (S - s) * kOzBN - c0);
-                oz_mma(tmem + static_cast<uint32_t>(s * kOzBN + c0), ad,
-                       bd0 + static_cast<uint64_t>((c0 * kOzBK) >> 4), oz_idesc(nn), accf);
+#pragma unroll
+              for (int kk = 0; kk < kOzBK / kOzUK; ++kk) {
+                const uint32_t accf = (kb > 0 || s > 0 || kk > 0) ? 1u : 0u;
+                // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA
+                for (int c0 = 0; c0 < (S - s) * kOzBN; c0 += 256) {
+                  const int nn = min(256, (S - s) * kOzBN - c0);
+                  oz_mma(tmem + static_cast<uint32_t>(s * kOzBN + c0), ad + static_cast<uint64_t>(kk * 2),
+                         bd0 + static_cast<uint64_t>((c0 * kOzBK) >> 4) + static_cast<uint64_t>(kk * 2),
+                         oz_idesc(nn), accf);
+                }
               }
             }
             oz_commit(&a_empty[st]);
@@ -677,7 +684,7 @@ OzEncodeFn oz_encode_fn() {
   return fn;
 }
 
-// 4-D map over int8 slices [slot][slice][row][k] with a (32, rows_box, slice_box, 1) box, SWIZZLE_32B
+// 4-D map over int8 digits [slot][digit][row][k] with a (128, rows_box, digit_box, 1) box, SWIZZLE_128B
 bool oz_encode(CUtensorMap* m, const int8_t* base, int64_t Kp, int64_t rows, int S, int slots, int rows_box,
                int slice_box) {
   OzEncodeFn fn = oz_encode_fn();
@@ -690,7 +697,7 @@ bool oz_encode(CUtensorMap* m, const int8_t* base, int64_t Kp, int64_t rows, int
                              static_cast<cuuint32_t>(slice_box), 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, str, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -4,7 +4,8 @@ one profiled apply.  Each apply launches 6 Tucker mode-product kernels of the
 64x128 instantiation (merged quadrature+exp-action batch of both species, then
 the merged squaring batch; 3 modes each):
 
-  ncu --set full --kernel-name-base demangled -k "regex:mode_product_tma_kernel<64, 128" \
+  ncu --set full --kernel-name-base demangled -k "regex:mode_product_tma_kernel<64, 128" \  (PHIKS_GEMM=dmma)
+  ncu --set full -k regex:oz_gemm -s 10 -c 10 python scripts/profile_bench.py  (int8 path, default) \
       -s 6 -c 6 python scripts/profile_bench.py
 """
 import os
