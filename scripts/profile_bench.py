@@ -1,12 +1,15 @@
 """ncu target in the bench configuration: configs[3], both species in one
 block-diagonal handle (256^3, phi_0..phi_2 same-vector), one warm apply then
-one profiled apply.  Each apply launches 6 Tucker mode-product kernels of the
-64x128 instantiation (merged quadrature+exp-action batch of both species, then
-the merged squaring batch; 3 modes each):
+one profiled apply.  On the default (int8) path an apply launches 10 int8
+GEMMs (oz_gemm_kernel: merged quadrature+exp-action batch of both species and
+the merged squaring batch, 3 modes each, inputs split in chunks of 8):
 
-  ncu --set full --kernel-name-base demangled -k "regex:mode_product_tma_kernel<64, 128" \  (PHIKS_GEMM=dmma)
-  ncu --set full -k regex:oz_gemm -s 10 -c 10 python scripts/profile_bench.py  (int8 path, default) \
-      -s 6 -c 6 python scripts/profile_bench.py
+  ncu --set full -k regex:oz_gemm -s 10 -c 10 python scripts/profile_bench.py
+
+with PHIKS_GEMM=dmma, 6 DMMA launches of the 64x128 instantiation:
+
+  PHIKS_GEMM=dmma ncu --set full --kernel-name-base demangled \
+      -k "regex:tma_kernel<.int.64, .int.128" -s 6 -c 6 python scripts/profile_bench.py
 """
 import os
 import sys
