@@ -203,7 +203,7 @@ phiks_status phiks_set_profiling(phiks_handle h, int on);
      operand, exact int32 accumulation: fp64-class error) wherever it applies
      (real handles, unsharded, n_μ ≤ 256, plain outputs), DMMA elsewhere;
    PHIKS_GEMM_AUTO (default, or the PHIKS_GEMM environment variable "dmma" /
-     "i8" / "auto" at create): the int8 kernel for products with n_μ ≥ 128 on
+     "i8" / "auto" at create): the int8 kernel for products with n_μ ≥ 192 on
      tensors of N ≥ 2^20 elements, where it is faster.  Invalidates the handle's captured
      graphs.  PHIKS_ERR_ARG for an unknown path. */
 #define PHIKS_GEMM_AUTO 0
