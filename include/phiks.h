@@ -120,6 +120,10 @@ typedef struct {
   double i8_flops;                /*   their time and fp64-equivalent flops          */
   int64_t i8_gemm_launches;       /* profiling: the int8 GEMM launches alone         */
   double i8_gemm_ms;              /*   and their time                                */
+  int64_t i8_chained_ops;         /* Tucker operators of the last apply whose modes ran
+                                     chained on the int8 path (no fp64 intermediates:
+                                     each product writes the next mode's digits,
+                                     DESIGN.md §4d; PHIKS_CHAIN=0 disables)          */
 } phiks_stats;
 
 /* Create a handle for K = A_d ⊕ … ⊕ A_1.

@@ -185,7 +185,8 @@ class PhiKS:
                 "expm_ms": st.expm_ms,
                 "block_plans": [(st.block_plan[b].s, st.block_plan[b].q) for b in range(max(st.nblocks, 1))],
                 "i8_mode_launches": st.i8_mode_launches, "i8_launches": st.i8_launches, "i8_ms": st.i8_ms,
-                "i8_flops": st.i8_flops, "i8_gemm_launches": st.i8_gemm_launches, "i8_gemm_ms": st.i8_gemm_ms}
+                "i8_flops": st.i8_flops, "i8_gemm_launches": st.i8_gemm_launches, "i8_gemm_ms": st.i8_gemm_ms,
+                "i8_chained_ops": st.i8_chained_ops}
 
     GEMM_PATHS = {"auto": 0, "dmma": 1, "i8": 2}
 

@@ -316,6 +316,7 @@ struct Exec {
 
   // ---- int8 tensor-core route of plain mode products (ozaki.cu) ----
   int64_t i8_launches = 0;
+  int64_t i8_chained = 0;  // Tucker operators run as chained int8 modes
   double* oz_ws = nullptr;  // grown on demand, reused by every int8 launch of the apply (one stream)
   size_t oz_ws_bytes = 0;
   static constexpr int kOzDigits = 7;
@@ -368,34 +369,166 @@ struct Exec {
         oz_ws_bytes = need;
       }
       ozaki_bind_workspace(p, oz_ws);
-      ++i8_launches;
-      // digit splits, then the GEMM (separate event pairs: kind 3 splits, kind 2 GEMM)
-      for (int phase = 0; phase < 2; ++phase) {
-        const bool prof = !measure && h->profiling && !rec;
-        if (prof) {
-          if (h->ev_used == static_cast<int>(h->ev.size())) {
-            cudaEvent_t a, b;
-            check(cudaEventCreate(&a), "cudaEventCreate");
-            check(cudaEventCreate(&b), "cudaEventCreate");
-            h->ev.emplace_back(a, b);
-            h->ev_flops.push_back(0.0);
-            h->ev_expm.push_back(0);
-          }
-          h->ev_flops[h->ev_used] =
-              phase == 0 ? 0.0 : 2.0 * static_cast<double>(L * R) * n * static_cast<double>(n) * p.nterms;
-          h->ev_expm[h->ev_used] = phase == 0 ? 3 : 2;
-          check(cudaEventRecord(h->ev[h->ev_used].first, st), "cudaEventRecord");
-        }
-        if (phase == 0) {
-          emit("digits_i8", [pp](cudaStream_t s2) { return launch_ozaki_mode(*pp, s2, true, true, false); });
-          ++launches;  // split_x + split_e
-        } else {
-          emit("mode_product_i8", [pp](cudaStream_t s2) { return launch_ozaki_mode(*pp, s2, false, false, true); });
-        }
-        if (prof) check(cudaEventRecord(h->ev[h->ev_used++].second, st), "cudaEventRecord");
-      }
+      oz_emit(pp, true);
       i = j;
     }
+  }
+  void oz_ws_reserve(size_t need) {
+    if (need > oz_ws_bytes) {
+      oz_ws = ar->alloc_doubles(static_cast<int64_t>((need + 7) / 8));
+      oz_ws_bytes = need;
+    }
+  }
+  // digit splits (+ chain exponents), then the GEMM (separate event pairs: kind 3 splits, kind 2 GEMM)
+  void oz_emit(const std::shared_ptr<OzakiParams>& pp, bool split_x) {
+    const OzakiParams& p = *pp;
+    ++i8_launches;
+    for (int phase = 0; phase < 2; ++phase) {
+      const bool prof = !measure && h->profiling && !rec;
+      if (prof) {
+        if (h->ev_used == static_cast<int>(h->ev.size())) {
+          cudaEvent_t a, b;
+          check(cudaEventCreate(&a), "cudaEventCreate");
+          check(cudaEventCreate(&b), "cudaEventCreate");
+          h->ev.emplace_back(a, b);
+          h->ev_flops.push_back(0.0);
+          h->ev_expm.push_back(0);
+        }
+        h->ev_flops[h->ev_used] =
+            phase == 0 ? 0.0 : 2.0 * static_cast<double>(p.L * p.R) * p.n * static_cast<double>(p.n) * p.nterms;
+        h->ev_expm[h->ev_used] = phase == 0 ? 3 : 2;
+        check(cudaEventRecord(h->ev[h->ev_used].first, st), "cudaEventRecord");
+      }
+      if (phase == 0) {
+        emit("digits_i8", [pp, split_x](cudaStream_t s2) { return launch_ozaki_mode(*pp, s2, split_x, true, false); });
+        if (split_x) ++launches;  // split_x + split_e (+ chain)
+        if (p.n_next > 0) ++launches;
+      } else {
+        emit("mode_product_i8", [pp](cudaStream_t s2) { return launch_ozaki_mode(*pp, s2, false, false, true); });
+      }
+      if (prof) check(cudaEventRecord(h->ev[h->ev_used++].second, st), "cudaEventRecord");
+    }
+  }
+
+  // ---- chained int8 Tucker operators ----
+  // Every mode of the batch on the int8 path with no fp64 intermediate: the product
+  // of mode μ < d writes the digits of mode μ+1 (fp64 layout, MN-major A operand of
+  // the next GEMM) with fiber exponents bounded before the product (oz_chain_kernel).
+  int8_t* oz_dig[2] = {nullptr, nullptr};
+  double* oz_ex[2] = {nullptr, nullptr};
+  double* oz_mx = nullptr;  // Mx of the current product (read by its own epilogue only)
+  size_t oz_chain_cap = 0;  // Tucker operators the buffers hold
+  static bool chain_env() {
+    static const bool on = [] {
+      const char* e = std::getenv("PHIKS_CHAIN");
+      return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on;
+  }
+  bool ozaki_chain_route(const std::vector<TuckerItem>& items, size_t c0, size_t c1) const {
+    if (in_expm || h->cplx || h->sharded() || rec || h->gemm_path == PHIKS_GEMM_DMMA || !chain_env()) return false;
+    const int d = h->d;
+    if (d < 2) return false;
+    const int64_t N = h->N;
+    int64_t L = 1;
+    for (int mu = 0; mu < d; ++mu) {
+      const int n = h->n[mu];
+      const int64_t R = N / (L * n);
+      if (!ozaki_supported(L, n, R, kOzDigits) || n % 16 != 0) return false;
+      if (mu > 0 && (L % 128 != 0 || L >= (int64_t(1) << 31) || R >= (int64_t(1) << 31))) return false;
+      if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 192 || N < (int64_t(1) << 20))) return false;
+      L *= n;
+    }
+    std::set<int> groups;  // last mode: one plain output per operator, distinct groups
+    for (size_t b = c0; b < c1; ++b) {
+      const TuckerItem& it = items[b];
+      if (it.outs.size() != 1 || !it.outs[0].srcs.empty()) return false;
+      if (!groups.insert(it.group).second) return false;
+    }
+    return true;
+  }
+  size_t chain_cap() const {  // digit buffers 2·cap·S·N bytes, at most ~8 GB
+    const double per = 2.0 * kOzDigits * static_cast<double>(h->N);
+    return static_cast<size_t>(std::max(1.0, std::min(24.0, std::floor(8e9 / per))));
+  }
+  void tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size_t c1) {
+    const int d = h->d, S = kOzDigits;
+    const int64_t N = h->N;
+    const int nt = static_cast<int>(c1 - c0);
+    int nmin = h->n[0];
+    for (int mu = 1; mu < d; ++mu) nmin = std::min(nmin, h->n[mu]);
+    if (oz_chain_cap < static_cast<size_t>(nt)) {
+      const size_t cap = chain_cap();
+      for (int k = 0; k < 2; ++k) {
+        oz_dig[k] = reinterpret_cast<int8_t*>(ar->alloc_doubles(static_cast<int64_t>((cap * S * N + 7) / 8)));
+        oz_ex[k] = ar->alloc_doubles(static_cast<int64_t>(cap) * (N / nmin));
+      }
+      oz_mx = ar->alloc_doubles(static_cast<int64_t>(cap) * (N / (static_cast<int64_t>(nmin) * nmin)));
+      oz_chain_cap = cap;
+    }
+    int64_t L = 1;
+    for (int mu = 0; mu < d && ok(); ++mu) {
+      const int n = h->n[mu];
+      const int64_t R = N / (L * n);
+      auto pp = std::make_shared<OzakiParams>();
+      OzakiParams& p = *pp;
+      std::memset(&p, 0, sizeof(p));
+      p.L = L;
+      p.R = R;
+      p.n = n;
+      p.S = S;
+      p.n_next = mu + 1 < d ? h->n[mu + 1] : 0;
+      const int64_t Cn = mu + 1 < d ? N / h->n[mu + 1] : 0;
+      for (int b = 0; b < nt; ++b) {
+        const TuckerItem& it = items[c0 + b];
+        int xs = b, es = -1;
+        if (mu == 0) {
+          xs = -1;
+          for (int k = 0; k < p.nx; ++k)
+            if (p.x[k] == it.in) xs = k;
+          if (xs < 0) {
+            xs = p.nx;
+            p.x[p.nx++] = it.in;
+          }
+        }
+        for (int k = 0; k < p.ne; ++k)
+          if (p.e[k] == it.mats[mu]) es = k;
+        if (es < 0) {
+          es = p.ne;
+          p.e[p.ne++] = it.mats[mu];
+        }
+        OzakiTerm t{xs, es, nullptr, 1.0, nullptr, nullptr, nullptr};
+        if (mu + 1 < d) {
+          t.dig = oz_dig[mu % 2] + static_cast<int64_t>(b) * S * N;
+          t.nex = oz_ex[mu % 2] + static_cast<int64_t>(b) * Cn;
+          t.nmx = oz_mx + static_cast<int64_t>(b) * (N / (static_cast<int64_t>(n) * h->n[mu + 1]));
+        } else {
+          t.out = it.outs[0].dst;
+          t.beta = it.outs[0].beta * it.in_scale;
+        }
+        p.terms[p.nterms++] = t;
+      }
+      const int nx_split = mu == 0 ? p.nx : 0;
+      oz_ws_reserve(ozaki_workspace_bytes(L, n, R, S, nx_split, p.ne));
+      const int nx_keep = p.nx;
+      p.nx = nx_split;
+      ozaki_bind_workspace(p, oz_ws);
+      if (mu > 0) {  // A: the previous product's digit planes and exponent bounds
+        p.nx = nt;
+        p.xs = oz_dig[(mu - 1) % 2];
+        p.xsc = oz_ex[(mu - 1) % 2];
+        p.a_mn = 1;
+      } else {
+        p.nx = nx_keep;
+      }
+      oz_emit(pp, mu == 0);
+      L *= n;
+    }
+    int64_t nsum = 0;
+    for (int mu = 0; mu < d; ++mu) nsum += h->n[mu];
+    tucker_ops += nt;
+    i8_chained += nt;
+    mu_flops += static_cast<double>(nt) * 2.0 * static_cast<double>(N) * static_cast<double>(nsum);
   }
 
   // ---- one mode-product launch from host-side term lists ----
@@ -933,6 +1066,12 @@ struct Exec {
     if (!ok() || items.empty()) return;
     const int d = h->d;
     const int64_t N = h->N;
+    if (ozaki_chain_route(items, 0, items.size())) {  // every mode on the int8 path, no fp64 intermediates
+      const size_t cap = chain_cap();
+      for (size_t s0 = 0; s0 < items.size() && ok(); s0 += cap)
+        tucker_chain_i8(items, s0, std::min(items.size(), s0 + cap));
+      return;
+    }
     // items per chunk bounded by the number of groups a non-last launch can hold
     const size_t chunk = static_cast<size_t>(kMaxGroups);
     const size_t nscr = std::min(items.size(), chunk);
@@ -1400,6 +1539,7 @@ struct ApplyRun {
     S.kernel_launches = ex.launches + norm_launches;
     S.tucker_ops = ex.tucker_ops;
     S.i8_mode_launches = ex.i8_launches;
+    S.i8_chained_ops = ex.i8_chained;
     S.mu_mode_flops = ex.mu_flops;
     S.expm_flops = ex.expm_flops;
     S.workspace_bytes = need;

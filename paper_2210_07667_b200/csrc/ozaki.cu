@@ -71,12 +71,9 @@ __device__ __forceinline__ uint64_t oz_digits(double v, const OzScale& sc) {
   constexpr uint64_t C = 0x8080808080808080ull >> (64 - 8 * S);
   return (static_cast<uint64_t>(F) + C) ^ C;
 }
+// digit s of 4 consecutive elements as one 32-bit word (element q in byte q)
 template <int S>
-__device__ __forceinline__ void split4(const double (&v)[4], int ex, uint32_t (&pk)[S]) {
-  const OzScale sc = oz_scale<S>(ex);
-  uint64_t h[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) h[q] = oz_digits<S>(v[q], sc);
+__device__ __forceinline__ void pack4(const uint64_t (&h)[4], uint32_t (&pk)[S]) {
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int i = S - 1 - s;  // byte of the digit
@@ -87,6 +84,14 @@ __device__ __forceinline__ void split4(const double (&v)[4], int ex, uint32_t (&
     const uint32_t x01 = __byte_perm(w[0], w[1], sel), x23 = __byte_perm(w[2], w[3], sel);
     pk[s] = __byte_perm(x01, x23, 0x5410);
   }
+}
+template <int S>
+__device__ __forceinline__ void split4(const double (&v)[4], int ex, uint32_t (&pk)[S]) {
+  const OzScale sc = oz_scale<S>(ex);
+  uint64_t h[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) h[q] = oz_digits<S>(v[q], sc);
+  pack4<S>(h, pk);
 }
 
 __device__ __forceinline__ double warp_max(double m) {
@@ -201,14 +206,17 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (j >= n) return;
-  double m = 0.0;
+  double m = 0.0, a1 = 0.0;
   bool bad = false;
   for (int k = lane; k < n; k += 32) {
     const double v = E[j + static_cast<int64_t>(k) * n];
     m = fmax(m, fabs(v));
+    a1 += fabs(v);
     bad |= !isfinite(v);
   }
   m = warp_max(m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a1 += __shfl_xor_sync(0xffffffffu, a1, o);
   bad = __any_sync(0xffffffffu, bad);
   const int ex = bad ? 0 : slice_exponent(m);
   int8_t* es = p.es + static_cast<int64_t>(slot) * S * n * Kp;
@@ -222,8 +230,76 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
     for (int s = 0; s < S; ++s)
       *reinterpret_cast<uint32_t*>(es + (static_cast<int64_t>(s) * n + j) * Kp + k0) = pk[s];
   }
-  if (lane == 0)  // the row's scale 2^{ee-30} (the GEMM epilogue's 2^-30: 2^-14 of the digit scaling, 2^-16 of its sums)
-    p.esc[static_cast<int64_t>(slot) * n + j] = bad ? __longlong_as_double(0x7ff8000000000000ll) : scalbn(1.0, ex - 30);
+  if (lane == 0) {  // the row's scale 2^{ee-30} (the GEMM epilogue's 2^-30: 2^-14 of the digit scaling, 2^-16 of its sums)
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    p.esc[static_cast<int64_t>(slot) * n + j] = bad ? qnan : scalbn(1.0, ex - 30);
+    // b_j with ‖e_j‖₁ < 2^{b_j} (a1 carries ≤ n·2^-53 relative rounding: margin 2^-40); the
+    // truncated digits have |ẽ| ≤ |e|, so |Σ_k ẽ_jk x̃_k| < 2^{b_j}·max|x̃| (chained modes, §4d)
+    if (p.eb) p.eb[static_cast<int64_t>(slot) * n + j] = bad ? qnan : (a1 > 0.0 ? ilogb(a1 * (1.0 + 0x1p-40)) + 1 : -1100);
+  }
+}
+
+// ---- chained Tucker modes: next-mode fiber exponents as bounds ----
+// For Y = X ×_μ E, |y(l, j, i, r')| ≤ ‖e_j‖₁·max_k |x(l, k, i, r')| < 2^{b_j + ex(l, i, r') − 1}
+// (i = i_{μ+1}), so the mode-(μ+1) fiber c' = l + L·j + L·n·r' (over i) can be split with
+// ex'(c') = b_j + max_i ex(l, i, r') before the product is computed: the product's epilogue
+// writes the next mode's digits directly.  One thread per (l, r') of a term.
+__global__ void __launch_bounds__(256) oz_chain_kernel(const OzakiParams p) {
+  __shared__ double red[8][32];
+  __shared__ double smx[32];
+  const OzakiTerm term = p.terms[blockIdx.y];
+  const int64_t L = p.L, C = p.L * p.R;
+  const int n = p.n, nn = p.n_next;
+  const int64_t M = C / nn;  // (l, r') pairs
+  const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  // Mx(l, r') = max_i ex(l, i, r') for 32 consecutive (l, r'), the warps splitting i
+  {
+    const int64_t m = m0 + lane;
+    double mx = -2000.0;
+    bool nan = false;
+    if (m < M) {
+      const int64_t l = m % L, rq = m / L;
+      const double* ex = p.xsc + static_cast<int64_t>(term.xslot) * C + l + L * nn * rq;
+      for (int i = warp; i < nn; i += 8) {
+        const double v = ex[L * i];
+        nan |= isnan(v);
+        mx = fmax(mx, v);
+      }
+    }
+    red[warp][lane] = nan ? qnan : mx;
+    __syncthreads();
+    if (warp == 0) {
+      double t = red[0][lane];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) {
+        const double u = red[w][lane];
+        t = (isnan(t) || isnan(u)) ? qnan : fmax(t, u);
+      }
+      smx[lane] = t;
+      if (m < M) term.nmx[m] = t;
+    }
+    __syncthreads();
+  }
+  // ex'(c') for c' = l + L·j + L·n·r' over the chunk's (l, r') and every j
+  const double* eb = p.eb + static_cast<int64_t>(term.eslot) * n;
+  const int cnt = static_cast<int>(M - m0 < 32 ? M - m0 : 32);
+  for (int idx = threadIdx.x; idx < 32 * n; idx += 256) {
+    int mi, j;
+    if (L == 1) {
+      mi = idx / n;
+      j = idx - mi * n;
+    } else {
+      j = idx >> 5;
+      mi = idx & 31;
+    }
+    if (mi >= cnt) continue;
+    const int64_t m = m0 + mi, l = m % L, rq = m / L;
+    // |y| < 2^1024 for finite y, and below 2^-1100 y is 0: the clamps keep the bound valid
+    const double e = __ldg(eb + j) + smx[mi];
+    term.nex[l + L * j + L * n * rq] = isnan(e) ? qnan : fmin(fmax(e, -1100.0), 1025.0);
+  }
 }
 
 // ---- tcgen05 / TMA / mbarrier helpers ----
@@ -265,9 +341,23 @@ __device__ __forceinline__ uint64_t oz_desc_sw128(const void* p) {
   d |= static_cast<uint64_t>(2) << 61;          // SWIZZLE_128B
   return d;
 }
-// kind::i8 instruction descriptor: D s32, A/B s8, both K-major, M = 128, N = BN
-__host__ __device__ constexpr uint32_t oz_idesc(int bn) {
-  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(bn >> 3) << 17) | ((128u >> 4) << 24);
+// MN-major SWIZZLE_128B operand (A of chained modes): k-rows of 128 bytes = 128
+// fibers (one MN atom: the leading byte offset is unused), 8-row groups 1 KB apart
+// (stride byte offset); the k-th 32-row UMMA slice starts 4 KB further
+__device__ __forceinline__ uint64_t oz_desc_mn_sw128(const void* p) {
+  const uint32_t a = oz_smem_u32(p);
+  uint64_t d = static_cast<uint64_t>((a >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+// kind::i8 instruction descriptor: D s32, A/B s8, B K-major, A K-major (or MN-major:
+// bit 15), M = 128, N = BN
+__host__ __device__ constexpr uint32_t oz_idesc(int bn, bool amn = false) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (amn ? (1u << 15) : 0u) | (static_cast<uint32_t>(bn >> 3) << 17) |
+         ((128u >> 4) << 24);
 }
 __device__ __forceinline__ void oz_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -470,7 +560,7 @@ struct OzSched {
   }
 };
 
-template <int S>
+template <int S, bool AMN, bool OUTD>
 __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb) {
@@ -538,7 +628,13 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
           if (it >= G::NST) oz_mbar_wait(&a_empty[st], ((it / G::NST) & 1) ^ 1);
           if (oz_elect()) {
             oz_mbar_expect_tx(&a_full[st], G::A_BYTES);
-            oz_tma_load_4d(smem + st * G::A_BYTES, &ta, kb * kOzBK, mt * kOzBM, sg * G::SPS, xs, &a_full[st]);
+            if (AMN) {  // (l, k, r, slot·S + digit) map over the fp64-layout digit planes; L % 128 == 0
+              const int64_t c0 = static_cast<int64_t>(mt) * kOzBM;
+              oz_tma_load_4d(smem + st * G::A_BYTES, &ta, static_cast<int>(c0 % p.L), kb * kOzBK,
+                             static_cast<int>(c0 / p.L), xs * S + sg * G::SPS, &a_full[st]);
+            } else {
+              oz_tma_load_4d(smem + st * G::A_BYTES, &ta, kb * kOzBK, mt * kOzBM, sg * G::SPS, xs, &a_full[st]);
+            }
           }
           __syncwarp();
         }
@@ -547,7 +643,8 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
     // ---- MMA issuer (whole warp in lockstep, one elected lane issues) ----
     // diagonal g = s + t accumulates in TMEM columns [64g, 64g + 64); descriptors
     // advance by adding (byte offset >> 4) to their start-address field
-    const uint64_t a_desc0 = oz_desc_sw128(smem), b_desc0 = oz_desc_sw128(bres);
+    const uint64_t a_desc0 = AMN ? oz_desc_mn_sw128(smem) : oz_desc_sw128(smem), b_desc0 = oz_desc_sw128(bres);
+    constexpr uint64_t a_kstep = AMN ? (kOzUK * kOzBM) >> 4 : kOzUK >> 4;  // one UMMA k-step of A
     int cur_term = -1, bgen = 0, it = 0, tile = 0;
     for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
       const int term = static_cast<int>(u / sc.Mt);
@@ -580,9 +677,9 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
                 // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA
                 for (int c0 = 0; c0 < (S - s) * kOzBN; c0 += 256) {
                   const int nn = min(256, (S - s) * kOzBN - c0);
-                  oz_mma(tmem + static_cast<uint32_t>(s * kOzBN + c0), ad + static_cast<uint64_t>(kk * 2),
+                  oz_mma(tmem + static_cast<uint32_t>(s * kOzBN + c0), ad + static_cast<uint64_t>(kk) * a_kstep,
                          bd0 + static_cast<uint64_t>((c0 * kOzBK) >> 4) + static_cast<uint64_t>(kk * 2),
-                         oz_idesc(nn), accf);
+                         oz_idesc(nn, AMN), accf);
                 }
               }
             }
@@ -605,7 +702,19 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
       const OzakiTerm term = p.terms[term_i];
       const int64_t c = mt * kOzBM + wq * 32 + lane;
       const bool rvalid = c < C;
+      const int64_t l = c % L, r = c / L;
+      // per-tile operands issued before the accumulator wait: the fiber exponent, the
+      // 32 column scales of this half (lane q holds column j0 + q, broadcast by shuffles)
+      // and, for chained modes, the row-norm exponents b_j and the fiber's Mx
       const double xsv = rvalid ? p.xsc[static_cast<int64_t>(term.xslot) * C + c] : 0.0;
+      const int j0 = sc.nt * kOzBN + ch * 32;
+      const int jn = p.n - j0;  // valid columns of this half
+      const double esc_l = lane < jn ? __ldg(p.esc + static_cast<int64_t>(term.eslot) * p.n + j0 + lane) : 0.0;
+      double eb_l = 0.0, mx = 0.0;
+      if (OUTD) {
+        eb_l = lane < jn ? __ldg(p.eb + static_cast<int64_t>(term.eslot) * p.n + j0 + lane) : 0.0;
+        mx = rvalid ? term.nmx[l + L * (r / p.n_next)] : 0.0;
+      }
       oz_mbar_wait(t_full, tile & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       // drain: per column, 2^16 Σ_g 256^{-g} D_g from three exact int64 partial sums
@@ -632,20 +741,84 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
       __syncwarp();
       if (lane == 0) oz_mbar_arrive(t_empty);
       // scale and store (overlaps the next tile's MMAs)
-      const int j0 = sc.nt * kOzBN + ch * 32;
-      const double* esc = p.esc + static_cast<int64_t>(term.eslot) * p.n + j0;
-      const int jn = p.n - j0;  // valid columns of this half
-      if (rvalid && jn > 0) {
-        // y = (acc · 2^{ee_j − 30}) · (β·2^{ex_c}): the power-of-two product first (no intermediate overflow)
-        const int64_t l = c % L, r = c / L;
-        double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
-        const int xe = isnan(xsv) ? 0 : static_cast<int>(xsv);
-        const double rb = isnan(xsv) ? xsv
-                          : (xe >= -1022 && xe <= 1023)
-                              ? term.beta * __longlong_as_double(static_cast<long long>(xe + 1023) << 52)
-                              : scalbn(term.beta, xe);
+      // y = (acc · 2^{ee_j − 30}) · (β·2^{ex_c}): the power-of-two product first (no intermediate overflow)
+      const int xe = isnan(xsv) ? 0 : static_cast<int>(xsv);
+      const double rb = isnan(xsv) ? xsv
+                        : (xe >= -1022 && xe <= 1023)
+                            ? term.beta * __longlong_as_double(static_cast<long long>(xe + 1023) << 52)
+                            : scalbn(term.beta, xe);
+      if (OUTD) {
+        // the next mode's digits of y: fiber c' = l + L·j + L·n·r' of mode μ+1
+        // (r = i + n'·r') has exponent e = clamp(b_j + Mx(l, r')) (NaN marks a non-finite fiber),
+        // exactly as oz_chain_kernel tabulates it; y·2^{8S-1-e} = acc·2^{(ee_j-30) + ex_c + 8S-1-e}
+        // is one exact power-of-two scaling of the accumulator (β = 1 on chained modes), so the
+        // digits take one DMUL and one F2I per element; digit s of element (l, j, r) goes to
+        // dig[s·N + l + L·(j + n·r)]
+        const int64_t N = C * p.n;
+        if (term.beta != 1.0)
 #pragma unroll
-        for (int q = 0; q < 32; ++q) acc[q] = (acc[q] * (q < jn ? __ldg(esc + q) : 0.0)) * rb;  // exact, then rounded
+          for (int q = 0; q < 32; ++q) acc[q] *= term.beta;
+        // column pair (b_j, ee_j - 30) packed in 16-bit halves, INT_MIN for a non-finite row of E
+        const int cp_l = (isnan(esc_l) || isnan(eb_l))
+                             ? INT_MIN
+                             : ((static_cast<int>(eb_l) + 0x4000) << 16) | (ilogb(esc_l) + 0x4000);
+        const bool rbad = isnan(xsv) || isnan(mx);
+        const int rk = rbad ? 0 : xe + 8 * S - 1, mxi = rbad ? 0 : static_cast<int>(mx);
+        // F = trunc(acc·2^k) read off the bits of acc with integer shifts (no FP64-pipe
+        // conversion): acc is 0 or a normal number (|acc| ≥ 2^-32), |F| < 2^55 by the bound
+        auto digits = [&](int q) -> uint64_t {
+          const int cpq = __shfl_sync(0xffffffffu, cp_l, q);
+          const int e = min(max(((cpq >> 16) - 0x4000) + mxi, -1100), 1025);
+          const int k = ((cpq & 0xffff) - 0x4000) + rk - e;
+          const long long bits = __double_as_longlong(acc[q]);
+          const int E = static_cast<int>((bits >> 52) & 0x7ff);
+          const int sh = E - (1023 + 52) + k;  // F_abs = m·2^sh
+          const uint64_t m = (static_cast<uint64_t>(bits) & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+          uint64_t fa = sh >= 0 ? (m << min(sh, 63)) : (sh > -64 ? (m >> -sh) : 0ull);
+          fa = E == 0 ? 0ull : fa;
+          const uint64_t F = bits < 0 ? (0ull - fa) : fa;
+          constexpr uint64_t Cc = 0x8080808080808080ull >> (64 - 8 * S);
+          return (rbad || cpq == INT_MIN) ? 0ull : (F + Cc) ^ Cc;
+        };
+        int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
+        const bool st_ok = rvalid && jn > 0;
+        if (L == 1 && jn >= 32) {  // 32 consecutive bytes of each digit plane: two 16-byte stores
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t pk[4][S];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const uint64_t h4[4] = {digits(16 * h2 + 4 * g), digits(16 * h2 + 4 * g + 1), digits(16 * h2 + 4 * g + 2),
+                                      digits(16 * h2 + 4 * g + 3)};
+              pack4<S>(h4, pk[g]);
+            }
+            if (st_ok) {
+#pragma unroll
+              for (int sd = 0; sd < S; ++sd)
+                *reinterpret_cast<uint4*>(dg + sd * N + 16 * h2) =
+                    make_uint4(pk[0][sd], pk[1][sd], pk[2][sd], pk[3][sd]);
+            }
+          }
+        } else {  // lanes hold consecutive l: each (digit, column) store is 32 consecutive bytes per warp
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const uint64_t hv = digits(q);  // every lane takes part in the shuffles
+            if (st_ok && q < jn) {
+              int8_t* ps = dg + L * q;
+#pragma unroll
+              for (int sd = 0; sd < S; ++sd) {
+                *ps = static_cast<int8_t>(hv >> (8 * (S - 1 - sd)));
+                ps += N;
+              }
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] = (acc[q] * __shfl_sync(0xffffffffu, esc_l, q)) * rb;  // exact, then rounded
+      }
+      if (!OUTD && rvalid && jn > 0) {
+        double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
         if (jn >= 32) {
           if (L == 1 && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
 #pragma unroll
@@ -729,10 +902,50 @@ bool oz_encode_digits(CUtensorMap* m, const int8_t* base, int64_t Kp, int64_t ro
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 4-D map over digit planes in the fp64 layout, (l, k, r, plane) with a (128, 128, 1, 1)
+// box, SWIZZLE_128B: the MN-major A tiles of chained modes (L % 128 == 0)
+bool oz_encode_mn(CUtensorMap* m, const int8_t* base, int64_t L, int n, int64_t R, int planes) {
+  OzEncodeFn fn = oz_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(R),
+                              static_cast<cuuint64_t>(planes)};
+  const cuuint64_t str[3] = {static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(L) * n,
+                             static_cast<cuuint64_t>(L) * n * static_cast<cuuint64_t>(R)};
+  const cuuint32_t box[4] = {128, static_cast<cuuint32_t>(kOzBK), 1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(base), dims, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool oz_split_tma_ok(const OzakiParams& p) {
   for (int b = 0; b < p.nx; ++b)
     if (reinterpret_cast<uintptr_t>(p.x[b]) & 15) return false;
   return p.R < (int64_t(1) << 31) && p.L < (int64_t(1) << 31);
+}
+
+template <int S, bool AMN, bool OUTD>
+cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
+  using G = OzGeom<S>;
+  static bool gattr = false;
+  static int sms = 0;
+  if (!gattr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(oz_gemm_kernel<S, AMN, OUTD>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    gattr = true;
+  }
+  const int64_t C = p.L * p.R;
+  const int ntn = (p.n + kOzBN - 1) / kOzBN;
+  const int64_t units = ((C + kOzBM - 1) / kOzBM) * p.nterms;
+  int64_t per = sms / ntn;  // CTAs per n-tile
+  if (per > units) per = units;
+  if (per < 1) per = 1;
+  oz_gemm_kernel<S, AMN, OUTD><<<static_cast<unsigned>(per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, tb);
+  return cudaGetLastError();
 }
 
 template <int S>
@@ -778,29 +991,21 @@ cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool 
     }
   }
   if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
+  if (split_e && p.n_next > 0 && p.nterms > 0) {  // next-mode exponent bounds (chained modes)
+    const int64_t m = C / p.n_next;
+    oz_chain_kernel<<<dim3(static_cast<unsigned>((m + 31) / 32), p.nterms), 256, 0, st>>>(p);
+  }
   if (p.nterms == 0 || !gemm) return cudaGetLastError();
   CUtensorMap ta, tb;
-  if (!oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS) ||
-      !oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S))
-    return cudaErrorInvalidValue;
-  using G = OzGeom<S>;
-  static bool gattr = false;
-  static int sms = 0;
-  if (!gattr) {
-    cudaError_t e = cudaFuncSetAttribute(oz_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    gattr = true;
+  const bool amap = p.a_mn ? oz_encode_mn(&ta, p.xs, p.L, p.n, p.R, S * p.nx)
+                           : oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS);
+  if (!amap || !oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S)) return cudaErrorInvalidValue;
+  if (p.a_mn) {
+    if (p.n_next > 0) return oz_gemm_go<S, true, true>(p, st, ta, tb);
+    return oz_gemm_go<S, true, false>(p, st, ta, tb);
   }
-  const int ntn = (p.n + kOzBN - 1) / kOzBN;
-  const int64_t units = ((C + kOzBM - 1) / kOzBM) * p.nterms;
-  int64_t per = sms / ntn;  // CTAs per n-tile
-  if (per > units) per = units;
-  if (per < 1) per = 1;
-  oz_gemm_kernel<S><<<static_cast<unsigned>(per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, tb);
-  return cudaGetLastError();
+  if (p.n_next > 0) return oz_gemm_go<S, false, true>(p, st, ta, tb);
+  return oz_gemm_go<S, false, false>(p, st, ta, tb);
 }
 
 }  // namespace
@@ -809,7 +1014,7 @@ size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne)
   const int64_t C = L * R, Kp = (n + kOzBK - 1) / kOzBK * kOzBK;
   auto al = [](size_t b) { return (b + 1023) & ~size_t(1023); };
   return al(static_cast<size_t>(nx) * S * C * Kp) + al(static_cast<size_t>(nx) * C * 8) +
-         al(static_cast<size_t>(ne) * S * n * Kp) + al(static_cast<size_t>(ne) * n * 8);
+         al(static_cast<size_t>(ne) * S * n * Kp) + 2 * al(static_cast<size_t>(ne) * n * 8);
 }
 
 void ozaki_bind_workspace(OzakiParams& p, void* ws) {
@@ -824,6 +1029,8 @@ void ozaki_bind_workspace(OzakiParams& p, void* ws) {
   p.es = reinterpret_cast<int8_t*>(w);
   w += al(static_cast<size_t>(p.ne) * p.S * p.n * p.Kp);
   p.esc = reinterpret_cast<double*>(w);
+  w += al(static_cast<size_t>(p.ne) * p.n * 8);
+  p.eb = reinterpret_cast<double*>(w);
 }
 
 bool ozaki_supported(int64_t L, int n, int64_t R, int S) {

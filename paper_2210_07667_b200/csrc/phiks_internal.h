@@ -121,6 +121,13 @@ struct OzakiTerm {
   int xslot, eslot;
   double* out;
   double beta;
+  // chained Tucker modes: with dig set, the epilogue writes the
+  // NEXT mode's digits instead of out: digit s of output element i at
+  // dig[s·L·n·R + i] (the fp64 layout, one byte plane per digit), each next-mode
+  // fiber scaled by its exponent nex[c'] (bound from the chain kernel)
+  int8_t* dig;
+  double* nex;
+  double* nmx;  // chained: Mx(l, r') = max_i ex(l, i, r') of the input fibers (oz_chain_kernel)
 };
 struct OzakiParams {
   int64_t L, R;
@@ -133,6 +140,9 @@ struct OzakiParams {
   double* xsc;   // [nx][L·R] fiber exponents ex (NaN: non-finite fiber)
   int8_t* es;    // [ne][S][n][Kp]
   double* esc;   // [ne][n] row exponents
+  double* eb;    // [ne][n] exponents b_j with ‖e_j‖₁ < 2^{b_j} (chained modes)
+  int a_mn;      // 1: xs holds [nx][S][L·n·R] digit planes in the fp64 layout (MN-major A, L % 128 == 0)
+  int n_next;    // chained: n_{μ+1} (0: plain fp64 outputs)
 };
 bool ozaki_supported(int64_t L, int n, int64_t R, int S);
 size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne);

@@ -201,3 +201,64 @@ def test_i8_path_selection_api():
     assert st["i8_mode_launches"] == 0
     _, st = _apply(op, pb, "i8")
     assert st["i8_mode_launches"] > 0
+
+
+# ---- chained modes: every mode on the int8 path, each product
+# writing the next mode's digits with exponents bounded before the product ----
+CHAIN_SHAPES = [(128, 96), (128, 48, 32), (256, 16, 64), (128, 16, 16, 16)]
+
+
+@pytest.mark.parametrize("dims", CHAIN_SHAPES)
+@pytest.mark.parametrize("mode", ["same", "lincomb"])
+def test_i8_chain_apply_parity(dims, mode):
+    seed = 800 + sum(dims) + (0 if mode == "same" else 1)
+    rng = np.random.default_rng(seed)
+    fac = W.random_factors(dims, seed=seed, scale=float(rng.uniform(1.0, 12.0)))
+    ells = (0, 1, 2) if mode == "same" else (0, 1, 2, 3)
+    vs = [W.random_tensor(dims, seed=seed + 10 + k) for k in range(1 if mode == "same" else len(ells))]
+    pb = W.Problem(f"chain{dims}{mode}", dims, fac, float(rng.uniform(0.3, 1.2)), mode, ells, vs, 2)
+    op = PhiKS(pb.A)
+    got, st = _apply(op, pb, "i8")
+    # every quadrature / squaring batch is chained; lincomb's exp(τK/2^j)v_0 terms (one per
+    # scale, several outputs per operator) keep the per-mode path
+    assert st["i8_chained_ops"] >= st["tucker_ops"] - (0 if mode == "same" else pb.n_scales) > 0, st
+    for k, (g, r) in enumerate(zip(got, _oracle_outs(pb))):
+        assert rel(g, r) <= 1e-12, (pb.name, k, rel(g, r))
+
+
+def test_i8_chain_fd_operators_and_power_of_two_scaling():
+    # Neumann / Dirichlet-ADR factors (rows of exp(τA) sum to ~1: tight exponent bounds);
+    # φ-actions are linear in v, and scaling v by 2^k shifts every digit exponent by k, so
+    # the chained path returns exactly 2^k times the unscaled result
+    dims = (128, 64, 32)
+    A = [0.7 * W.fd_dxx_neumann(dims[0]), W.fd_dxx_dirichlet(dims[1]) + 3.0 * W.fd_dx_dirichlet(dims[1]),
+         0.2 * W.fd_dxx_neumann(dims[2])]
+    v = W.uniform_tensor(dims, 0.0, 3.0, seed=901)
+    pb = W.Problem("chainfd", dims, A, 2e-3, "same", (0, 1, 2), [v], 2)
+    op = PhiKS(pb.A)
+    got, st = _apply(op, pb, "i8")
+    assert st["i8_chained_ops"] == st["tucker_ops"]
+    for k, (g, r) in enumerate(zip(got, _oracle_outs(pb))):
+        assert rel(g, r) <= 1e-12, (k, rel(g, r))
+    for e in (-1000, 600):
+        pbs = W.Problem("chainfd_s", dims, A, 2e-3, "same", (0, 1, 2), [np.ldexp(v, e)], 2)
+        gs, _ = _apply(op, pbs, "i8")
+        for g0, g1 in zip(got, gs):
+            assert np.array_equal(np.ldexp(g0, e), g1), e
+
+
+def test_i8_chain_zero_and_nonfinite_inputs():
+    dims = (128, 32, 16)
+    fac = W.random_factors(dims, seed=950, scale=3.0)
+    op = PhiKS(fac)
+    z = np.zeros(dims)
+    got, st = _apply(op, W.Problem("z", dims, fac, 0.5, "same", (0, 1), [z], 1), "i8")
+    assert st["i8_chained_ops"] > 0
+    for g in got:
+        assert not np.any(g)
+    v = W.random_tensor(dims, seed=951)
+    v[tuple(k // 3 for k in v.shape)] = np.nan
+    got, _ = _apply(op, W.Problem("nan", dims, fac, 0.5, "same", (0, 1), [v], 1), "i8")
+    # a dense Tucker operator spreads the NaN to every output (as fp64 arithmetic does)
+    for g in got:
+        assert np.all(np.isnan(g))
