@@ -165,7 +165,7 @@ def i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, g_ms, g_n, ex_n
     elems = i8_fl / max(g_n, 1) / (2.0 * 256)
     return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOP/s (int8)",
             "frac": (ach / peak) if ach else None, "traffic": traffic,
-            "kernel": "oz_gemm_kernel<7> (tcgen05.mma kind::i8, TMEM accumulators, TMA SWIZZLE_32B): "
+            "kernel": "oz_gemm_kernel<7, AMN, OUTD> (tcgen05.mma kind::i8, TMEM accumulators, TMA SWIZZLE_128B, chained modes: DESIGN.md §4d): "
                       "the Tucker-operator μ-mode products",
             "algorithmic_ops_per_launch": ops / max(g_n, 1),
             "algorithmic_bytes_per_launch_max": elems * 15.0,
@@ -176,7 +176,7 @@ def i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, g_ms, g_n, ex_n
             "fp64_equivalent": {"tflops": i8_fl / (i8_ms / 1e3) / 1e12 if i8_ms > 0 else None,
                                 "vs_measured_dmma_peak": (i8_fl / (i8_ms / 1e3) / 1e12 / dmma_peak)
                                 if i8_ms > 0 else None, "dmma_peak_tflops": dmma_peak,
-                                "note": "fp64 flops of the products over the int8 path's time (digit splits "
+                                "note": "fp64 flops of the products over the int8 path's time (splits of the inputs, chain exponent bounds "
                                         "+ GEMM)"},
             "digit_splits": {"ms_per_step": (i8_ms - g_ms) / max(args.steps, 1)},
             "tucker_launches": {"ms_per_step": mp_ms / max(args.steps, 1), "launches": mp_n},
