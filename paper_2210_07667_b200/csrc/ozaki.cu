@@ -28,6 +28,9 @@
 // warps drain TMEM while the next tile's MMAs run.
 #include <cuda.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "phiks_internal.h"
 
 namespace phiks {
@@ -235,7 +238,14 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
     p.esc[static_cast<int64_t>(slot) * n + j] = bad ? qnan : scalbn(1.0, ex - 30);
     // b_j with ‖e_j‖₁ < 2^{b_j} (a1 carries ≤ n·2^-53 relative rounding: margin 2^-40); the
     // truncated digits have |ẽ| ≤ |e|, so |Σ_k ẽ_jk x̃_k| < 2^{b_j}·max|x̃| (chained modes, §4d)
-    if (p.eb) p.eb[static_cast<int64_t>(slot) * n + j] = bad ? qnan : (a1 > 0.0 ? ilogb(a1 * (1.0 + 0x1p-40)) + 1 : -1100);
+    const int b = a1 > 0.0 ? ilogb(a1 * (1.0 + 0x1p-40)) + 1 : -1100;
+    if (p.eb) p.eb[static_cast<int64_t>(slot) * n + j] = bad ? qnan : b;
+    if (p.ecol) {
+      p.ecol[static_cast<int64_t>(slot) * n + j] = bad ? INT_MIN : (ex - 30) - b;
+      if (bad) atomicOr(p.eext + 2 * p.ne + slot, 1);
+      atomicMin(p.eext + slot, b);
+      atomicMax(p.eext + p.ne + slot, b);
+    }
   }
 }
 
@@ -528,6 +538,190 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
+// One output tile of the epilogue (both GEMM kernels): fiber c (TMEM lane), columns
+// j0 .. j0+31 of term term_i; waits for the accumulators (t_full, phase), drains them,
+// releases TMEM through release(), then scales and stores (fp64 or the next mode's digits).
+template <int S, bool OUTD, class Release>
+__device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_i, int64_t c, int j0, uint32_t tl,
+                                             uint64_t* t_full, unsigned phase, Release release) {
+  const int lane = threadIdx.x & 31;
+  const int64_t C = p.L * p.R, L = p.L;
+  const OzakiTerm term = p.terms[term_i];
+  const bool rvalid = c < C;
+  const int64_t l = c % L, r = c / L;
+  // per-tile operands issued before the accumulator wait: the fiber exponent, the
+  // 32 column scales of this half (lane q holds column j0 + q, broadcast by shuffles)
+  // and, for chained modes, the row-norm exponents b_j and the fiber's Mx
+  const double xsv = rvalid ? p.xsc[static_cast<int64_t>(term.xslot) * C + c] : 0.0;
+  const int jn = p.n - j0;  // valid columns of this half
+  const double esc_l = lane < jn ? __ldg(p.esc + static_cast<int64_t>(term.eslot) * p.n + j0 + lane) : 0.0;
+  double eb_l = 0.0, mx = 0.0;
+  int colk[OUTD ? 32 : 1];
+  bool ebad = false;
+  int emin = 0, emax = 0;
+  if (OUTD) {
+    eb_l = lane < jn ? __ldg(p.eb + static_cast<int64_t>(term.eslot) * p.n + j0 + lane) : 0.0;
+    mx = rvalid ? term.nmx[l + L * (r / p.n_next)] : 0.0;
+    const int* ec = p.ecol + static_cast<int64_t>(term.eslot) * p.n + j0;
+    if (jn >= 32) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int4 v4 = __ldg(reinterpret_cast<const int4*>(ec) + i);
+        colk[4 * i] = v4.x;
+        colk[4 * i + 1] = v4.y;
+        colk[4 * i + 2] = v4.z;
+        colk[4 * i + 3] = v4.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) colk[q] = q < jn ? __ldg(ec + q) : 0;
+    }
+    emin = __ldg(p.eext + term.eslot);
+    emax = __ldg(p.eext + p.ne + term.eslot);
+    ebad = __ldg(p.eext + 2 * p.ne + term.eslot) != 0;
+  }
+  oz_mbar_wait(t_full, phase);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // drain: per column, 2^16 Σ_g 256^{-g} D_g from three exact int64 partial sums
+  // (D_0·2^16 + D_1·2^8 + D_2, D_3·2^16 + D_4·2^8 + D_5, D_6; each < 2^42) and two fp64 fmas
+  double acc[32];
+#pragma unroll
+  for (int cb = 0; cb < 4; ++cb) {
+    uint32_t v[S][8];
+#pragma unroll
+    for (int g = 0; g < S; ++g) oz_ld8(tl + g * kOzBN + cb * 8, v[g]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const long long ta = static_cast<long long>(static_cast<int>(v[0][q])) * 65536 +
+                           static_cast<long long>(static_cast<int>(v[1][q])) * 256 + static_cast<int>(v[2][q]);
+      const long long tb = static_cast<long long>(static_cast<int>(v[3][q])) * 65536 +
+                           static_cast<long long>(static_cast<int>(v[4][q])) * 256 + static_cast<int>(v[5][q]);
+      double y = oz_l2d(tb);
+      if (S == 7) y = fma(oz_i2d(v[S - 1][q]), 0x1p-8, y);
+      acc[cb * 8 + q] = fma(y, 0x1p-24, oz_l2d(ta));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncwarp();
+  release();
+
+  // scale and store (overlaps the next tile's MMAs)
+  // y = (acc · 2^{ee_j − 30}) · (β·2^{ex_c}): the power-of-two product first (no intermediate overflow)
+  const int xe = isnan(xsv) ? 0 : static_cast<int>(xsv);
+  const double rb = isnan(xsv) ? xsv
+                    : (xe >= -1022 && xe <= 1023)
+                        ? term.beta * __longlong_as_double(static_cast<long long>(xe + 1023) << 52)
+                        : scalbn(term.beta, xe);
+  if (OUTD) {
+    // the next mode's digits of y: fiber c' = l + L·j + L·n·r' of mode μ+1
+    // (r = i + n'·r') has exponent e = clamp(b_j + Mx(l, r')) (NaN marks a non-finite fiber),
+    // exactly as oz_chain_kernel tabulates it; y·2^{8S-1-e} = acc·2^{(ee_j-30) + ex_c + 8S-1-e}
+    // is one exact power-of-two scaling of the accumulator (β = 1 on chained modes), so the
+    // digits take one DMUL and one F2I per element; digit s of element (l, j, r) goes to
+    // dig[s·N + l + L·(j + n·r)]
+    const int64_t N = C * p.n;
+    if (term.beta != 1.0)
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q] *= term.beta;
+    // column pair (b_j, ee_j - 30) packed in 16-bit halves, INT_MIN for a non-finite row of E
+    const int cp_l = (isnan(esc_l) || isnan(eb_l))
+                         ? INT_MIN
+                         : ((static_cast<int>(eb_l) + 0x4000) << 16) | (ilogb(esc_l) + 0x4000);
+    const bool rbad = isnan(xsv) || isnan(mx);
+    const int rk = rbad ? 0 : xe + 8 * S - 1, mxi = rbad ? 0 : static_cast<int>(mx);
+    // F = trunc(acc·2^k) read off the bits of acc with integer shifts (no FP64-pipe
+    // conversion): acc is 0 or a normal number (|acc| ≥ 2^-32), |F| < 2^55 by the bound, so
+    // F = (m·4) >> (1077 − E − k) with m the 53-bit significand and E the biased exponent
+    // (acc = 0 has E = 0 and shifts out entirely)
+    constexpr uint64_t Cc = 0x8080808080808080ull >> (64 - 8 * S);
+    auto digit_bits = [&](double a, int k) -> uint64_t {
+      const long long bits = __double_as_longlong(a);
+      const int E = static_cast<int>(static_cast<uint64_t>(bits) >> 52) & 0x7ff;
+      const int rs = max(1077 - E - k, 0);
+      const uint64_t m4 = ((static_cast<uint64_t>(bits) & 0xFFFFFFFFFFFFFull) | (1ull << 52)) << 2;
+      const uint64_t fa = rs < 64 ? (m4 >> rs) : 0ull;
+      const uint64_t sg = static_cast<uint64_t>(bits >> 63);
+      return (((fa ^ sg) - sg) + Cc) ^ Cc;
+    };
+    // fast path (warp-uniform): every row of E finite and no clamp of e = b_j + Mx, so
+    // k = ((ee_j − 30) − b_j) + (ex_c + 8S − 1 − Mx) = colk[q] + rowk: one add per element
+    const bool fast = __all_sync(0xffffffffu, !rbad && !ebad && emin + mxi >= -1100 && emax + mxi <= 1025);
+    const int rowk = rk - mxi;
+    auto digits = [&](int q) -> uint64_t {
+      if (fast) return digit_bits(acc[q], colk[q] + rowk);
+      const int cpq = __shfl_sync(0xffffffffu, cp_l, q);
+      const int e = min(max(((cpq >> 16) - 0x4000) + mxi, -1100), 1025);
+      const int k = ((cpq & 0xffff) - 0x4000) + rk - e;
+      const uint64_t h = digit_bits(acc[q], k);
+      return (rbad || cpq == INT_MIN) ? 0ull : h;
+    };
+    const bool st_ok = rvalid && jn > 0;
+    if (L == 1) {  // 32 consecutive bytes of each digit plane per thread: two 16-byte stores
+      int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        uint32_t pk[4][S];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const uint64_t h4[4] = {digits(16 * h2 + 4 * g), digits(16 * h2 + 4 * g + 1), digits(16 * h2 + 4 * g + 2),
+                                  digits(16 * h2 + 4 * g + 3)};
+          pack4<S>(h4, pk[g]);
+        }
+        if (st_ok && jn >= 32) {
+#pragma unroll
+          for (int sd = 0; sd < S; ++sd)
+            *reinterpret_cast<uint4*>(dg + sd * N + 16 * h2) = make_uint4(pk[0][sd], pk[1][sd], pk[2][sd], pk[3][sd]);
+        } else if (st_ok) {
+#pragma unroll
+          for (int sd = 0; sd < S; ++sd)
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (16 * h2 + q < jn) dg[sd * N + 16 * h2 + q] = static_cast<int8_t>(pk[q >> 2][sd] >> (8 * (q & 3)));
+        }
+      }
+    } else {
+      // lanes hold consecutive l (L % 128 == 0): per 4 columns, the 4×4 byte blocks of each
+      // lane quad are transposed by two shuffle rounds, so lane i of a quad stores the
+      // 4 consecutive rows of column q0 + i as one 32-bit word
+      const int qi = lane & 3;
+      const uint32_t sel1 = (qi & 1) ? 0x3715u : 0x6240u, sel2 = (qi & 2) ? 0x3276u : 0x5410u;
+      int8_t* dq = term.dig + (l - qi) + L * (j0 + qi + static_cast<int64_t>(p.n) * r);
+#pragma unroll
+      for (int q0 = 0; q0 < 32; q0 += 4) {
+        const uint64_t h4[4] = {digits(q0), digits(q0 + 1), digits(q0 + 2), digits(q0 + 3)};
+        uint32_t pk[S];
+        pack4<S>(h4, pk);
+#pragma unroll
+        for (int sd = 0; sd < S; ++sd) {
+          const uint32_t t1 = __byte_perm(pk[sd], __shfl_xor_sync(0xffffffffu, pk[sd], 1), sel1);
+          const uint32_t t2 = __byte_perm(t1, __shfl_xor_sync(0xffffffffu, t1, 2), sel2);
+          if (st_ok && q0 + qi < jn) *reinterpret_cast<uint32_t*>(dq + sd * N + L * q0) = t2;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q] = (acc[q] * __shfl_sync(0xffffffffu, esc_l, q)) * rb;  // exact, then rounded
+  }
+  if (!OUTD && rvalid && jn > 0) {
+    double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
+    if (jn >= 32) {
+      if (L == 1 && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < 32; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(acc[q], acc[q + 1]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) outp[L * q] = acc[q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < jn) outp[L * q] = acc[q];
+    }
+  }
+}
+
 // Persistent GEMM geometry: the E-digit tile of a (term, n-tile) stays resident
 // (S × 64 rows × Kp bytes); fiber digits stream through an NST-stage ring of
 // SPS-digit units (k-block kb, digit group sg).
@@ -535,7 +729,7 @@ template <int S>
 struct OzGeom {
   static constexpr int SPS = 1;                                // digits per stage
   static constexpr int A_BYTES = SPS * kOzBM * kOzBK;         // one stage
-  static constexpr int NST = 4;                                // 64 KB ring
+  static constexpr int NST = 6;                                // 96 KB ring (L2 latency cover for the short digit stages)
   static constexpr int B_KB = S * kOzBN * kOzBK;              // resident E slices per k-block
   static constexpr int B_BYTES = (kOzMaxN / kOzBK) * B_KB;    // Kp ≤ kOzMaxN
   static constexpr int SMEM = NST * A_BYTES + B_BYTES + 1024 /*align*/ + 512 /*barriers*/;
@@ -657,188 +851,309 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
         cur_term = term;
         ++bgen;
       }
-      if (tile > 0) oz_mbar_wait(t_empty, (tile - 1) & 1);  // epilogue drained the accumulators
+      if (tile > 0 && !(p.dbg & 1)) oz_mbar_wait(t_empty, (tile - 1) & 1);  // epilogue drained the accumulators
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      for (int kb = 0; kb < nk; ++kb)
-        for (int sg = 0; sg < NSG; ++sg, ++it) {
+      // fully unrolled over the digits: every MMA's column offset, N and instruction
+      // descriptor are compile-time constants (the issue loop is a few uniform adds per MMA)
+      for (int kb = 0; kb < nk; ++kb) {
+        const uint64_t bd0 = b_desc0 + static_cast<uint64_t>((kb * G::B_KB) >> 4);
+#pragma unroll
+        for (int s = 0; s < S; ++s, ++it) {
           const int st = it % G::NST;
           oz_mbar_wait(&a_full[st], (it / G::NST) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           const uint64_t ad0 = a_desc0 + static_cast<uint64_t>((st * G::A_BYTES) >> 4);
-          const uint64_t bd0 = b_desc0 + static_cast<uint64_t>((kb * G::B_KB) >> 4);
           if (oz_elect()) {
 #pragma unroll
-            for (int si = 0; si < G::SPS; ++si) {
-              const int s = sg * G::SPS + si;
-              const uint64_t ad = ad0 + static_cast<uint64_t>((si * kOzBM * kOzBK) >> 4);
+            for (int kk = 0; kk < kOzBK / kOzUK; ++kk) {
+              const uint32_t accf = (kb > 0 || s > 0 || kk > 0) ? 1u : 0u;
+              // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA
 #pragma unroll
-              for (int kk = 0; kk < kOzBK / kOzUK; ++kk) {
-                const uint32_t accf = (kb > 0 || s > 0 || kk > 0) ? 1u : 0u;
-                // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA
-                for (int c0 = 0; c0 < (S - s) * kOzBN; c0 += 256) {
-                  const int nn = min(256, (S - s) * kOzBN - c0);
-                  oz_mma(tmem + static_cast<uint32_t>(s * kOzBN + c0), ad + static_cast<uint64_t>(kk) * a_kstep,
-                         bd0 + static_cast<uint64_t>((c0 * kOzBK) >> 4) + static_cast<uint64_t>(kk * 2),
-                         oz_idesc(nn, AMN), accf);
-                }
+              for (int c0 = 0; c0 < (S - s) * kOzBN; c0 += 256) {
+                const int nn = (S - s) * kOzBN - c0 < 256 ? (S - s) * kOzBN - c0 : 256;
+                oz_mma(tmem + static_cast<uint32_t>(s * kOzBN + c0), ad0 + static_cast<uint64_t>(kk) * a_kstep,
+                       bd0 + static_cast<uint64_t>((c0 * kOzBK) >> 4) + static_cast<uint64_t>(kk * 2),
+                       oz_idesc(nn, AMN), accf);
               }
             }
             oz_commit(&a_empty[st]);
           }
           __syncwarp();
         }
+      }
       if (oz_elect()) oz_commit(t_full);
       __syncwarp();
     }
   } else {
     // ---- epilogue warps: lane quarter wq = warp % 4 (TMEM lanes 32wq..), column half ch ----
     const int wq = warp & 3, ch = (warp - 2) >> 2;
-    const int64_t C = p.L * p.R, L = p.L;
     const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16) + ch * 32;
     int tile = 0;
     for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
       const int term_i = static_cast<int>(u / sc.Mt);
       const int64_t mt = u % sc.Mt;
-      const OzakiTerm term = p.terms[term_i];
-      const int64_t c = mt * kOzBM + wq * 32 + lane;
-      const bool rvalid = c < C;
-      const int64_t l = c % L, r = c / L;
-      // per-tile operands issued before the accumulator wait: the fiber exponent, the
-      // 32 column scales of this half (lane q holds column j0 + q, broadcast by shuffles)
-      // and, for chained modes, the row-norm exponents b_j and the fiber's Mx
-      const double xsv = rvalid ? p.xsc[static_cast<int64_t>(term.xslot) * C + c] : 0.0;
-      const int j0 = sc.nt * kOzBN + ch * 32;
-      const int jn = p.n - j0;  // valid columns of this half
-      const double esc_l = lane < jn ? __ldg(p.esc + static_cast<int64_t>(term.eslot) * p.n + j0 + lane) : 0.0;
-      double eb_l = 0.0, mx = 0.0;
-      if (OUTD) {
-        eb_l = lane < jn ? __ldg(p.eb + static_cast<int64_t>(term.eslot) * p.n + j0 + lane) : 0.0;
-        mx = rvalid ? term.nmx[l + L * (r / p.n_next)] : 0.0;
-      }
-      oz_mbar_wait(t_full, tile & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      // drain: per column, 2^16 Σ_g 256^{-g} D_g from three exact int64 partial sums
-      // (D_0·2^16 + D_1·2^8 + D_2, D_3·2^16 + D_4·2^8 + D_5, D_6; each < 2^42) and two fp64 fmas
-      double acc[32];
-#pragma unroll
-      for (int cb = 0; cb < 4; ++cb) {
-        uint32_t v[S][8];
-#pragma unroll
-        for (int g = 0; g < S; ++g) oz_ld8(tl + g * kOzBN + cb * 8, v[g]);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const long long ta = static_cast<long long>(static_cast<int>(v[0][q])) * 65536 +
-                               static_cast<long long>(static_cast<int>(v[1][q])) * 256 + static_cast<int>(v[2][q]);
-          const long long tb = static_cast<long long>(static_cast<int>(v[3][q])) * 65536 +
-                               static_cast<long long>(static_cast<int>(v[4][q])) * 256 + static_cast<int>(v[5][q]);
-          double y = oz_l2d(tb);
-          if (S == 7) y = fma(oz_i2d(v[S - 1][q]), 0x1p-8, y);
-          acc[cb * 8 + q] = fma(y, 0x1p-24, oz_l2d(ta));
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) oz_mbar_arrive(t_empty);
-      // scale and store (overlaps the next tile's MMAs)
-      // y = (acc · 2^{ee_j − 30}) · (β·2^{ex_c}): the power-of-two product first (no intermediate overflow)
-      const int xe = isnan(xsv) ? 0 : static_cast<int>(xsv);
-      const double rb = isnan(xsv) ? xsv
-                        : (xe >= -1022 && xe <= 1023)
-                            ? term.beta * __longlong_as_double(static_cast<long long>(xe + 1023) << 52)
-                            : scalbn(term.beta, xe);
-      if (OUTD) {
-        // the next mode's digits of y: fiber c' = l + L·j + L·n·r' of mode μ+1
-        // (r = i + n'·r') has exponent e = clamp(b_j + Mx(l, r')) (NaN marks a non-finite fiber),
-        // exactly as oz_chain_kernel tabulates it; y·2^{8S-1-e} = acc·2^{(ee_j-30) + ex_c + 8S-1-e}
-        // is one exact power-of-two scaling of the accumulator (β = 1 on chained modes), so the
-        // digits take one DMUL and one F2I per element; digit s of element (l, j, r) goes to
-        // dig[s·N + l + L·(j + n·r)]
-        const int64_t N = C * p.n;
-        if (term.beta != 1.0)
-#pragma unroll
-          for (int q = 0; q < 32; ++q) acc[q] *= term.beta;
-        // column pair (b_j, ee_j - 30) packed in 16-bit halves, INT_MIN for a non-finite row of E
-        const int cp_l = (isnan(esc_l) || isnan(eb_l))
-                             ? INT_MIN
-                             : ((static_cast<int>(eb_l) + 0x4000) << 16) | (ilogb(esc_l) + 0x4000);
-        const bool rbad = isnan(xsv) || isnan(mx);
-        const int rk = rbad ? 0 : xe + 8 * S - 1, mxi = rbad ? 0 : static_cast<int>(mx);
-        // F = trunc(acc·2^k) read off the bits of acc with integer shifts (no FP64-pipe
-        // conversion): acc is 0 or a normal number (|acc| ≥ 2^-32), |F| < 2^55 by the bound
-        auto digits = [&](int q) -> uint64_t {
-          const int cpq = __shfl_sync(0xffffffffu, cp_l, q);
-          const int e = min(max(((cpq >> 16) - 0x4000) + mxi, -1100), 1025);
-          const int k = ((cpq & 0xffff) - 0x4000) + rk - e;
-          const long long bits = __double_as_longlong(acc[q]);
-          const int E = static_cast<int>((bits >> 52) & 0x7ff);
-          const int sh = E - (1023 + 52) + k;  // F_abs = m·2^sh
-          const uint64_t m = (static_cast<uint64_t>(bits) & 0xFFFFFFFFFFFFFull) | (1ull << 52);
-          uint64_t fa = sh >= 0 ? (m << min(sh, 63)) : (sh > -64 ? (m >> -sh) : 0ull);
-          fa = E == 0 ? 0ull : fa;
-          const uint64_t F = bits < 0 ? (0ull - fa) : fa;
-          constexpr uint64_t Cc = 0x8080808080808080ull >> (64 - 8 * S);
-          return (rbad || cpq == INT_MIN) ? 0ull : (F + Cc) ^ Cc;
-        };
-        int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
-        const bool st_ok = rvalid && jn > 0;
-        if (L == 1 && jn >= 32) {  // 32 consecutive bytes of each digit plane: two 16-byte stores
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            uint32_t pk[4][S];
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const uint64_t h4[4] = {digits(16 * h2 + 4 * g), digits(16 * h2 + 4 * g + 1), digits(16 * h2 + 4 * g + 2),
-                                      digits(16 * h2 + 4 * g + 3)};
-              pack4<S>(h4, pk[g]);
-            }
-            if (st_ok) {
-#pragma unroll
-              for (int sd = 0; sd < S; ++sd)
-                *reinterpret_cast<uint4*>(dg + sd * N + 16 * h2) =
-                    make_uint4(pk[0][sd], pk[1][sd], pk[2][sd], pk[3][sd]);
-            }
-          }
-        } else {  // lanes hold consecutive l: each (digit, column) store is 32 consecutive bytes per warp
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const uint64_t hv = digits(q);  // every lane takes part in the shuffles
-            if (st_ok && q < jn) {
-              int8_t* ps = dg + L * q;
-#pragma unroll
-              for (int sd = 0; sd < S; ++sd) {
-                *ps = static_cast<int8_t>(hv >> (8 * (S - 1 - sd)));
-                ps += N;
-              }
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) acc[q] = (acc[q] * __shfl_sync(0xffffffffu, esc_l, q)) * rb;  // exact, then rounded
-      }
-      if (!OUTD && rvalid && jn > 0) {
-        double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
-        if (jn >= 32) {
-          if (L == 1 && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
-#pragma unroll
-            for (int q = 0; q < 32; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(acc[q], acc[q + 1]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) outp[L * q] = acc[q];
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (q < jn) outp[L * q] = acc[q];
-        }
-      }
+      oz_epilogue_tile<S, OUTD>(p, term_i, mt * kOzBM + wq * 32 + lane, sc.nt * kOzBN + ch * 32, tl, t_full,
+                                tile & 1, [&] {
+                                  if (lane == 0) oz_mbar_arrive(t_empty);
+                                });
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+}
+
+// ---- CTA-pair GEMM (tcgen05.mma.cta_group::2) ----
+// The two CTAs of a cluster own adjacent 128-fiber tiles (UMMA M = 256) of the same
+// 64-row E tile.  Each MMA a_s × [b_t0 | … | b_t1-1] reads its A rows from the CTA
+// that owns them and the N = 64(t1 − t0) B rows half from each CTA: CTA r holds rows
+// [r·N/2, (r+1)·N/2) of the concatenation, so every chunk (t0, t1) the MMAs use is
+// stored per CTA as its half (7 chunks, 16 × 32 rows per 128-byte k-stage).  The
+// accumulator columns keep the 1-CTA layout (diagonal g at [64g, 64g + 64)), so the
+// epilogue is shared.  Per SM and k-step the tensor cores read 40 KB of A and 28 KB
+// of B from shared memory instead of 40 + 56 KB.
+// chunk c: digits [t0, t0 + m) of B; off = 32-row pieces of the chunks before it
+struct OzChunks {
+  static constexpr int NC = 7;
+  static constexpr int PIECES = 16;  // per CTA and k-stage
+  __host__ __device__ static constexpr int t0(int c) { return (c >= 1 && c <= 3) ? 4 : 0; }
+  __host__ __device__ static constexpr int m(int c) { return c == 0 ? 4 : (c <= 3 ? 4 - c : 7 - c); }
+  __host__ __device__ static constexpr int off(int c) {
+    return c == 0 ? 0 : c == 1 ? 4 : c == 2 ? 7 : c == 3 ? 9 : c == 4 ? 10 : c == 5 ? 13 : 15;
+  }
+  // chunks of digit s of A (S = 7): [0, min(4, 7 − s)) and [4, 7 − s)
+  __host__ __device__ static constexpr int first(int s) { return s <= 3 ? 0 : s; }
+  __host__ __device__ static constexpr int second(int s) { return s <= 2 ? s + 1 : -1; }
+};
+static_assert(OzChunks::off(6) + OzChunks::m(6) == OzChunks::PIECES, "chunk pieces");
+
+struct OzGeom2 {
+  static constexpr int S = 7;
+  static constexpr int A_BYTES = kOzBM * kOzBK;              // one digit × 128 fibers × 128 k
+  static constexpr int NST = 4;
+  static constexpr int E_KB = OzChunks::PIECES * 32 * kOzBK;  // 64 KB of chunk halves per k-stage
+  static constexpr int E_BYTES = (kOzMaxN / kOzBK) * E_KB;
+  static constexpr int SMEM = NST * A_BYTES + E_BYTES + 1024 + 512;
+  static constexpr int EPI_WARPS = 8;
+  static constexpr int THREADS = 64 + EPI_WARPS * 32;
+  static_assert(SMEM <= 232448, "shared memory");
+};
+
+__device__ __forceinline__ uint32_t oz_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t oz_mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(oz_smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void oz_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// TMA load into this CTA's shared memory whose completion is counted on the pair
+// leader's barrier (shared::cluster address)
+__device__ __forceinline__ void oz_tma_load_4d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                    uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6];\n" ::"r"(oz_smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void oz_mma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// arrive on the barrier at the same offset in both CTAs of the pair once the MMAs are done
+__device__ __forceinline__ void oz_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          oz_smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+__device__ __forceinline__ void oz_mbar_arrive_remote(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__host__ __device__ constexpr uint32_t oz_idesc_pair(int bn, bool amn) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (amn ? (1u << 15) : 0u) | (static_cast<uint32_t>(bn >> 3) << 17) |
+         ((256u >> 4) << 24);
+}
+
+template <bool AMN, bool OUTD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OzGeom2::THREADS, 1)
+    oz_gemm_pair_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
+                        const __grid_constant__ CUtensorMap te) {
+  using G = OzGeom2;
+  constexpr int S = G::S;
+  extern __shared__ uint8_t oz_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* eres = smem + G::NST * G::A_BYTES;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(eres + G::E_BYTES);
+  uint64_t* a_empty = a_full + G::NST;
+  uint64_t* b_full = a_empty + G::NST;
+  uint64_t* b_empty = b_full + 1;
+  uint64_t* t_full = b_empty + 1;
+  uint64_t* t_empty = t_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = oz_cluster_rank();
+  const bool leader = rank == 0;
+  // pair schedule: pair k works on n-tile k % ntn, units q, q + Q, … over (term, 256-fiber tile)
+  const int ntn = (p.n + kOzBN - 1) / kOzBN;
+  const int pi = static_cast<int>(blockIdx.x >> 1);
+  const int nt = pi % ntn, q = pi / ntn, Q = static_cast<int>(gridDim.x >> 1) / ntn;
+  if (q >= Q) return;  // both CTAs of the pair leave together
+  const int64_t C = p.L * p.R;
+  const int64_t Mt2 = (C + 2 * kOzBM - 1) / (2 * kOzBM);
+  const int64_t units = Mt2 * p.nterms;
+  const int nk = p.Kp / kOzBK;
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&te)) : "memory");
+    for (int s = 0; s < G::NST; ++s) {
+      oz_mbar_init(&a_full[s], 1);
+      oz_mbar_init(&a_empty[s], 1);
+    }
+    oz_mbar_init(b_full, 1);
+    oz_mbar_init(b_empty, 1);
+    oz_mbar_init(t_full, 1);
+    oz_mbar_init(t_empty, 2 * G::EPI_WARPS);  // the epilogue warps of both CTAs (leader's barrier)
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(oz_smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  oz_cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t a_full0 = oz_mapa(a_full, 0), b_full0 = oz_mapa(b_full, 0), t_empty0 = oz_mapa(t_empty, 0);
+
+  if (warp == 0) {
+    // ---- TMA producer of this CTA's operands (both CTAs); completions count on the leader ----
+    int cur_term = -1, bgen = 0, it = 0;
+    for (int64_t u = q; u < units; u += Q) {
+      const int term = static_cast<int>(u / Mt2);
+      const int64_t mt = (u % Mt2) * 2 + rank;
+      if (term != cur_term) {  // this CTA's halves of the E chunks of (term, n-tile)
+        if (bgen > 0) oz_mbar_wait(b_empty, (bgen - 1) & 1);
+        if (oz_elect()) {
+          if (leader) oz_mbar_expect_tx(b_full, static_cast<unsigned>(2 * nk * G::E_KB));
+          const int es = p.terms[term].eslot;
+          for (int kb = 0; kb < nk; ++kb)
+            for (int c = 0; c < OzChunks::NC; ++c) {
+              const int mm = OzChunks::m(c);
+              for (int v = 0; v < mm; ++v) {
+                const int piece = static_cast<int>(rank) * mm + v;  // 32-row piece of the concatenation
+                oz_tma_load_4d_pair(eres + kb * G::E_KB + (OzChunks::off(c) + v) * 32 * kOzBK, &te, kb * kOzBK,
+                                    nt * kOzBN + 32 * (piece & 1), OzChunks::t0(c) + (piece >> 1), es, b_full0);
+              }
+            }
+        }
+        __syncwarp();
+        cur_term = term;
+        ++bgen;
+      }
+      const int xs = p.terms[term].xslot;
+      for (int kb = 0; kb < nk; ++kb)
+        for (int s = 0; s < S; ++s, ++it) {
+          const int st = it % G::NST;
+          if (it >= G::NST) oz_mbar_wait(&a_empty[st], ((it / G::NST) & 1) ^ 1);
+          if (oz_elect()) {
+            if (leader) oz_mbar_expect_tx(&a_full[st], 2 * G::A_BYTES);
+            if (AMN) {
+              const int64_t c0 = mt * kOzBM;
+              oz_tma_load_4d_pair(smem + st * G::A_BYTES, &ta, static_cast<int>(c0 % p.L), kb * kOzBK,
+                                  static_cast<int>(c0 / p.L), xs * S + s, a_full0 + 8u * st);
+            } else {
+              oz_tma_load_4d_pair(smem + st * G::A_BYTES, &ta, kb * kOzBK, static_cast<int>(mt * kOzBM), s, xs,
+                                  a_full0 + 8u * st);
+            }
+          }
+          __syncwarp();
+        }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ---- MMA issuer of the pair ----
+      const uint64_t a_desc0 = AMN ? oz_desc_mn_sw128(smem) : oz_desc_sw128(smem), e_desc0 = oz_desc_sw128(eres);
+      constexpr uint64_t a_kstep = AMN ? (kOzUK * kOzBM) >> 4 : kOzUK >> 4;
+      int cur_term = -1, bgen = 0, it = 0, tile = 0;
+      for (int64_t u = q; u < units; u += Q, ++tile) {
+        const int term = static_cast<int>(u / Mt2);
+        if (term != cur_term) {
+          if (bgen > 0) {
+            if (oz_elect()) oz_commit_pair(b_empty);
+            __syncwarp();
+          }
+          oz_mbar_wait(b_full, bgen & 1);
+          cur_term = term;
+          ++bgen;
+        }
+        if (tile > 0) oz_mbar_wait(t_empty, (tile - 1) & 1);  // both epilogues drained the accumulators
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        for (int kb = 0; kb < nk; ++kb) {
+          const uint64_t ed0 = e_desc0 + static_cast<uint64_t>((kb * G::E_KB) >> 4);
+#pragma unroll
+          for (int s = 0; s < S; ++s, ++it) {
+            const int st = it & (G::NST - 1);
+            oz_mbar_wait(&a_full[st], (it / G::NST) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint64_t ad0 = a_desc0 + static_cast<uint64_t>((st * G::A_BYTES) >> 4);
+            if (oz_elect()) {
+#pragma unroll
+              for (int kk = 0; kk < kOzBK / kOzUK; ++kk) {
+                const uint32_t accf = (kb > 0 || s > 0 || kk > 0) ? 1u : 0u;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const int c = h == 0 ? OzChunks::first(s) : OzChunks::second(s);
+                  if (c < 0) continue;
+                  oz_mma_pair(tmem + static_cast<uint32_t>((s + OzChunks::t0(c)) * kOzBN), ad0 + kk * a_kstep,
+                              ed0 + static_cast<uint64_t>((OzChunks::off(c) * 32 * kOzBK) >> 4) +
+                                  static_cast<uint64_t>(kk * 2),
+                              oz_idesc_pair(64 * OzChunks::m(c), AMN), accf);
+                }
+              }
+              oz_commit_pair(&a_empty[st]);
+            }
+            __syncwarp();
+          }
+        }
+        if (oz_elect()) oz_commit_pair(t_full);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---- epilogue warps of both CTAs: this CTA's 128 fibers of the pair's tile ----
+    const int wq = warp & 3, ch = (warp - 2) >> 2;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16) + ch * 32;
+    int tile = 0;
+    for (int64_t u = q; u < units; u += Q, ++tile) {
+      const int term_i = static_cast<int>(u / Mt2);
+      const int64_t mt = (u % Mt2) * 2 + rank;
+      oz_epilogue_tile<S, OUTD>(p, term_i, mt * kOzBM + wq * 32 + lane, nt * kOzBN + ch * 32, tl, t_full, tile & 1,
+                                [&] {
+                                  if (lane == 0) oz_mbar_arrive_remote(t_empty0);
+                                });
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  oz_cluster_sync();  // no MMA of the pair targets this CTA's TMEM any more
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
 }
 
 typedef CUresult (*OzEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -948,8 +1263,46 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   return cudaGetLastError();
 }
 
+template <bool AMN, bool OUTD>
+cudaError_t oz_gemm_pair_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& te) {
+  using G = OzGeom2;
+  static bool gattr = false;
+  static int sms = 0;
+  if (!gattr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(oz_gemm_pair_kernel<AMN, OUTD>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    gattr = true;
+  }
+  const int64_t C = p.L * p.R;
+  const int ntn = (p.n + kOzBN - 1) / kOzBN;
+  const int64_t units = ((C + 2 * kOzBM - 1) / (2 * kOzBM)) * p.nterms;
+  int64_t per = (sms / 2) / ntn;  // pairs per n-tile
+  if (per > units) per = units;
+  if (per < 1) per = 1;
+  oz_gemm_pair_kernel<AMN, OUTD><<<static_cast<unsigned>(2 * per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, te);
+  return cudaGetLastError();
+}
+
+bool oz_pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PHIKS_OZ_PAIR");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
+
 template <int S>
-cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e, bool gemm) {
+cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool split_e, bool gemm) {
+  static const int dbg = [] {
+    const char* e = std::getenv("PHIKS_OZ_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  OzakiParams p = p0;
+  p.dbg = dbg;
   const int64_t C = p.L * p.R;
   if (split_x) {
     const size_t sm = static_cast<size_t>(32) * (p.n | 1) * sizeof(double);
@@ -990,6 +1343,11 @@ cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool 
       oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
     }
   }
+  if (split_e && p.eext) {  // min / max / flag slots of the row-norm exponents
+    cudaMemsetAsync(p.eext, 0x7f, sizeof(int) * p.ne, st);
+    cudaMemsetAsync(p.eext + p.ne, 0x80, sizeof(int) * p.ne, st);
+    cudaMemsetAsync(p.eext + 2 * p.ne, 0, sizeof(int) * p.ne, st);
+  }
   if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
   if (split_e && p.n_next > 0 && p.nterms > 0) {  // next-mode exponent bounds (chained modes)
     const int64_t m = C / p.n_next;
@@ -999,7 +1357,17 @@ cudaError_t oz_launch(const OzakiParams& p, cudaStream_t st, bool split_x, bool 
   CUtensorMap ta, tb;
   const bool amap = p.a_mn ? oz_encode_mn(&ta, p.xs, p.L, p.n, p.R, S * p.nx)
                            : oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS);
-  if (!amap || !oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S)) return cudaErrorInvalidValue;
+  if (!amap) return cudaErrorInvalidValue;
+  if (S == 7 && oz_pair_enabled()) {  // CTA-pair MMAs (§4e): E chunks as 32-row pieces of one digit
+    if (!oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, 32, 1)) return cudaErrorInvalidValue;
+    if (p.a_mn) {
+      if (p.n_next > 0) return oz_gemm_pair_go<true, true>(p, st, ta, tb);
+      return oz_gemm_pair_go<true, false>(p, st, ta, tb);
+    }
+    if (p.n_next > 0) return oz_gemm_pair_go<false, true>(p, st, ta, tb);
+    return oz_gemm_pair_go<false, false>(p, st, ta, tb);
+  }
+  if (!oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S)) return cudaErrorInvalidValue;
   if (p.a_mn) {
     if (p.n_next > 0) return oz_gemm_go<S, true, true>(p, st, ta, tb);
     return oz_gemm_go<S, true, false>(p, st, ta, tb);
@@ -1014,7 +1382,8 @@ size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne)
   const int64_t C = L * R, Kp = (n + kOzBK - 1) / kOzBK * kOzBK;
   auto al = [](size_t b) { return (b + 1023) & ~size_t(1023); };
   return al(static_cast<size_t>(nx) * S * C * Kp) + al(static_cast<size_t>(nx) * C * 8) +
-         al(static_cast<size_t>(ne) * S * n * Kp) + 2 * al(static_cast<size_t>(ne) * n * 8);
+         al(static_cast<size_t>(ne) * S * n * Kp) + 2 * al(static_cast<size_t>(ne) * n * 8) +
+         al(static_cast<size_t>(ne) * n * 4) + al(static_cast<size_t>(ne) * 3 * 4);
 }
 
 void ozaki_bind_workspace(OzakiParams& p, void* ws) {
@@ -1031,6 +1400,10 @@ void ozaki_bind_workspace(OzakiParams& p, void* ws) {
   p.esc = reinterpret_cast<double*>(w);
   w += al(static_cast<size_t>(p.ne) * p.n * 8);
   p.eb = reinterpret_cast<double*>(w);
+  w += al(static_cast<size_t>(p.ne) * p.n * 8);
+  p.ecol = reinterpret_cast<int*>(w);
+  w += al(static_cast<size_t>(p.ne) * p.n * 4);
+  p.eext = reinterpret_cast<int*>(w);
 }
 
 bool ozaki_supported(int64_t L, int n, int64_t R, int S) {

@@ -141,8 +141,11 @@ struct OzakiParams {
   int8_t* es;    // [ne][S][n][Kp]
   double* esc;   // [ne][n] row exponents
   double* eb;    // [ne][n] exponents b_j with ‖e_j‖₁ < 2^{b_j} (chained modes)
+  int* ecol;     // [ne][n] (ee_j − 30) − b_j (INT_MIN: non-finite row), the digit epilogue's column shift
+  int* eext;     // [3][ne] min_j b_j, max_j b_j, any non-finite row (chained modes' fast-path test)
   int a_mn;      // 1: xs holds [nx][S][L·n·R] digit planes in the fp64 layout (MN-major A, L % 128 == 0)
   int n_next;    // chained: n_{μ+1} (0: plain fp64 outputs)
+  int dbg;       // timing experiments only (PHIKS_OZ_DBG); 0 in production
 };
 bool ozaki_supported(int64_t L, int n, int64_t R, int S);
 size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne);
