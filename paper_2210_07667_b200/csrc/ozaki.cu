@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(512, 1)
 // One output tile of the epilogue (both GEMM kernels): fiber c (TMEM lane), columns
 // j0 .. j0+31 of term term_i; waits for the accumulators (t_full, phase), drains them,
 // releases TMEM through release(), then scales and stores (fp64 or the next mode's digits).
-template <int S, bool OUTD, class Release>
+template <int S, bool OUTD, int EPC, class Release>
 __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_i, int64_t c, int j0, uint32_t tl,
                                              uint64_t* t_full, unsigned phase, Release release) {
   const int lane = threadIdx.x & 31;
@@ -550,22 +550,22 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
   const bool rvalid = c < C;
   const int64_t l = c % L, r = c / L;
   // per-tile operands issued before the accumulator wait: the fiber exponent, the
-  // 32 column scales of this half (lane q holds column j0 + q, broadcast by shuffles)
+  // EPC column scales of this warp's columns (lane q holds column j0 + q, broadcast by shuffles)
   // and, for chained modes, the row-norm exponents b_j and the fiber's Mx
   const double xsv = rvalid ? p.xsc[static_cast<int64_t>(term.xslot) * C + c] : 0.0;
   const int jn = p.n - j0;  // valid columns of this half
   const double esc_l = lane < jn ? __ldg(p.esc + static_cast<int64_t>(term.eslot) * p.n + j0 + lane) : 0.0;
   double eb_l = 0.0, mx = 0.0;
-  int colk[OUTD ? 32 : 1];
+  int colk[OUTD ? EPC : 1];
   bool ebad = false;
   int emin = 0, emax = 0;
   if (OUTD) {
     eb_l = lane < jn ? __ldg(p.eb + static_cast<int64_t>(term.eslot) * p.n + j0 + lane) : 0.0;
     mx = rvalid ? term.nmx[l + L * (r / p.n_next)] : 0.0;
     const int* ec = p.ecol + static_cast<int64_t>(term.eslot) * p.n + j0;
-    if (jn >= 32) {
+    if (jn >= EPC) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < EPC / 4; ++i) {
         const int4 v4 = __ldg(reinterpret_cast<const int4*>(ec) + i);
         colk[4 * i] = v4.x;
         colk[4 * i + 1] = v4.y;
@@ -574,7 +574,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
       }
     } else {
 #pragma unroll
-      for (int q = 0; q < 32; ++q) colk[q] = q < jn ? __ldg(ec + q) : 0;
+      for (int q = 0; q < EPC; ++q) colk[q] = q < jn ? __ldg(ec + q) : 0;
     }
     emin = __ldg(p.eext + term.eslot);
     emax = __ldg(p.eext + p.ne + term.eslot);
@@ -584,9 +584,9 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   // drain: per column, 2^16 Σ_g 256^{-g} D_g from three exact int64 partial sums
   // (D_0·2^16 + D_1·2^8 + D_2, D_3·2^16 + D_4·2^8 + D_5, D_6; each < 2^42) and two fp64 fmas
-  double acc[32];
+  double acc[EPC];
 #pragma unroll
-  for (int cb = 0; cb < 4; ++cb) {
+  for (int cb = 0; cb < EPC / 8; ++cb) {
     uint32_t v[S][8];
 #pragma unroll
     for (int g = 0; g < S; ++g) oz_ld8(tl + g * kOzBN + cb * 8, v[g]);
@@ -623,7 +623,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     const int64_t N = C * p.n;
     if (term.beta != 1.0)
 #pragma unroll
-      for (int q = 0; q < 32; ++q) acc[q] *= term.beta;
+      for (int q = 0; q < EPC; ++q) acc[q] *= term.beta;
     // column pair (b_j, ee_j - 30) packed in 16-bit halves, INT_MIN for a non-finite row of E
     const int cp_l = (isnan(esc_l) || isnan(eb_l))
                          ? INT_MIN
@@ -657,10 +657,10 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
       return (rbad || cpq == INT_MIN) ? 0ull : h;
     };
     const bool st_ok = rvalid && jn > 0;
-    if (L == 1) {  // 32 consecutive bytes of each digit plane per thread: two 16-byte stores
+    if (L == 1) {  // EPC consecutive bytes of each digit plane per thread: 16-byte stores
       int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
+      for (int h2 = 0; h2 < EPC / 16; ++h2) {
         uint32_t pk[4][S];
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -668,7 +668,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
                                   digits(16 * h2 + 4 * g + 3)};
           pack4<S>(h4, pk[g]);
         }
-        if (st_ok && jn >= 32) {
+        if (st_ok && jn >= EPC) {
 #pragma unroll
           for (int sd = 0; sd < S; ++sd)
             *reinterpret_cast<uint4*>(dg + sd * N + 16 * h2) = make_uint4(pk[0][sd], pk[1][sd], pk[2][sd], pk[3][sd]);
@@ -688,7 +688,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
       const uint32_t sel1 = (qi & 1) ? 0x3715u : 0x6240u, sel2 = (qi & 2) ? 0x3276u : 0x5410u;
       int8_t* dq = term.dig + (l - qi) + L * (j0 + qi + static_cast<int64_t>(p.n) * r);
 #pragma unroll
-      for (int q0 = 0; q0 < 32; q0 += 4) {
+      for (int q0 = 0; q0 < EPC; q0 += 4) {
         const uint64_t h4[4] = {digits(q0), digits(q0 + 1), digits(q0 + 2), digits(q0 + 3)};
         uint32_t pk[S];
         pack4<S>(h4, pk);
@@ -702,21 +702,21 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < 32; ++q) acc[q] = (acc[q] * __shfl_sync(0xffffffffu, esc_l, q)) * rb;  // exact, then rounded
+    for (int q = 0; q < EPC; ++q) acc[q] = (acc[q] * __shfl_sync(0xffffffffu, esc_l, q)) * rb;  // exact, then rounded
   }
   if (!OUTD && rvalid && jn > 0) {
     double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
-    if (jn >= 32) {
+    if (jn >= EPC) {
       if (L == 1 && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
 #pragma unroll
-        for (int q = 0; q < 32; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(acc[q], acc[q + 1]);
+        for (int q = 0; q < EPC; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(acc[q], acc[q + 1]);
       } else {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) outp[L * q] = acc[q];
+        for (int q = 0; q < EPC; ++q) outp[L * q] = acc[q];
       }
     } else {
 #pragma unroll
-      for (int q = 0; q < 32; ++q)
+      for (int q = 0; q < EPC; ++q)
         if (q < jn) outp[L * q] = acc[q];
     }
   }
@@ -733,7 +733,8 @@ struct OzGeom {
   static constexpr int B_KB = S * kOzBN * kOzBK;              // resident E slices per k-block
   static constexpr int B_BYTES = (kOzMaxN / kOzBK) * B_KB;    // Kp ≤ kOzMaxN
   static constexpr int SMEM = NST * A_BYTES + B_BYTES + 1024 /*align*/ + 512 /*barriers*/;
-  static constexpr int EPI_WARPS = 8;                          // 2 per TMEM lane quarter (column halves)
+  static constexpr int EPC = 32;                               // columns per epilogue warp (16: measured slower)
+  static constexpr int EPI_WARPS = 4 * kOzBN / EPC;             // 4 per TMEM lane quarter (column quarters)
   static constexpr int THREADS = 64 + EPI_WARPS * 32;
   static_assert(S * kOzBN <= 512, "TMEM holds one 64-column accumulator per diagonal");
   static_assert(SMEM <= 232448, "shared memory");
@@ -887,12 +888,12 @@ __global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
   } else {
     // ---- epilogue warps: lane quarter wq = warp % 4 (TMEM lanes 32wq..), column half ch ----
     const int wq = warp & 3, ch = (warp - 2) >> 2;
-    const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16) + ch * 32;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16) + ch * G::EPC;
     int tile = 0;
     for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
       const int term_i = static_cast<int>(u / sc.Mt);
       const int64_t mt = u % sc.Mt;
-      oz_epilogue_tile<S, OUTD>(p, term_i, mt * kOzBM + wq * 32 + lane, sc.nt * kOzBN + ch * 32, tl, t_full,
+      oz_epilogue_tile<S, OUTD, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, sc.nt * kOzBN + ch * G::EPC, tl, t_full,
                                 tile & 1, [&] {
                                   if (lane == 0) oz_mbar_arrive(t_empty);
                                 });
@@ -935,7 +936,8 @@ struct OzGeom2 {
   static constexpr int E_KB = OzChunks::PIECES * 32 * kOzBK;  // 64 KB of chunk halves per k-stage
   static constexpr int E_BYTES = (kOzMaxN / kOzBK) * E_KB;
   static constexpr int SMEM = NST * A_BYTES + E_BYTES + 1024 + 512;
-  static constexpr int EPI_WARPS = 8;
+  static constexpr int EPC = 32;
+  static constexpr int EPI_WARPS = 4 * kOzBN / EPC;
   static constexpr int THREADS = 64 + EPI_WARPS * 32;
   static_assert(SMEM <= 232448, "shared memory");
 };
@@ -1139,12 +1141,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OzGeom2::THREADS, 1)
   } else {
     // ---- epilogue warps of both CTAs: this CTA's 128 fibers of the pair's tile ----
     const int wq = warp & 3, ch = (warp - 2) >> 2;
-    const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16) + ch * 32;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16) + ch * G::EPC;
     int tile = 0;
     for (int64_t u = q; u < units; u += Q, ++tile) {
       const int term_i = static_cast<int>(u / Mt2);
       const int64_t mt = (u % Mt2) * 2 + rank;
-      oz_epilogue_tile<S, OUTD>(p, term_i, mt * kOzBM + wq * 32 + lane, nt * kOzBN + ch * 32, tl, t_full, tile & 1,
+      oz_epilogue_tile<S, OUTD, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, nt * kOzBN + ch * G::EPC, tl, t_full, tile & 1,
                                 [&] {
                                   if (lane == 0) oz_mbar_arrive_remote(t_empty0);
                                 });
@@ -1287,10 +1289,11 @@ cudaError_t oz_gemm_pair_go(const OzakiParams& p, cudaStream_t st, const CUtenso
   return cudaGetLastError();
 }
 
+// opt-in (PHIKS_OZ_PAIR=1): measured slower than the 1-CTA kernel on configs[3]
 bool oz_pair_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PHIKS_OZ_PAIR");
-    return !(e && std::strcmp(e, "0") == 0);
+    return e && std::strcmp(e, "1") == 0;
   }();
   return on;
 }
