@@ -649,6 +649,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     const bool fast = __all_sync(0xffffffffu, !rbad && !ebad && emin + mxi >= -1100 && emax + mxi <= 1025);
     const int rowk = rk - mxi;
     auto digits = [&](int q) -> uint64_t {
+      if (p.dbg & 4) return 0ull;  // timing experiment: no digit arithmetic
       if (fast) return digit_bits(acc[q], colk[q] + rowk);
       const int cpq = __shfl_sync(0xffffffffu, cp_l, q);
       const int e = min(max(((cpq >> 16) - 0x4000) + mxi, -1100), 1025);
@@ -656,28 +657,53 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
       const uint64_t h = digit_bits(acc[q], k);
       return (rbad || cpq == INT_MIN) ? 0ull : h;
     };
-    const bool st_ok = rvalid && jn > 0;
-    if (L == 1) {  // EPC consecutive bytes of each digit plane per thread: 16-byte stores
+    const bool st_ok = rvalid && jn > 0 && !(p.dbg & 2);  // dbg & 2: timing experiment without stores
+    if (L == 1) {  // EPC consecutive bytes of each digit plane per thread
       int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
+      const bool full = st_ok && jn >= EPC;
+      if (EPC == 32 && ((reinterpret_cast<uintptr_t>(dg) | static_cast<uintptr_t>(N)) & 31) == 0) {
+        // one 32-byte store (STG.256, a whole sector) per digit plane
+        uint32_t pk[8][S];
 #pragma unroll
-      for (int h2 = 0; h2 < EPC / 16; ++h2) {
-        uint32_t pk[4][S];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const uint64_t h4[4] = {digits(16 * h2 + 4 * g), digits(16 * h2 + 4 * g + 1), digits(16 * h2 + 4 * g + 2),
-                                  digits(16 * h2 + 4 * g + 3)};
+        for (int g = 0; g < 8; ++g) {
+          const uint64_t h4[4] = {digits(4 * g), digits(4 * g + 1), digits(4 * g + 2), digits(4 * g + 3)};
           pack4<S>(h4, pk[g]);
         }
-        if (st_ok && jn >= EPC) {
 #pragma unroll
-          for (int sd = 0; sd < S; ++sd)
-            *reinterpret_cast<uint4*>(dg + sd * N + 16 * h2) = make_uint4(pk[0][sd], pk[1][sd], pk[2][sd], pk[3][sd]);
-        } else if (st_ok) {
+        for (int sd = 0; sd < S; ++sd) {
+          if (full) {
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"l"(dg + sd * N),
+                         "r"(pk[0][sd]), "r"(pk[1][sd]), "r"(pk[2][sd]), "r"(pk[3][sd]), "r"(pk[4][sd]),
+                         "r"(pk[5][sd]), "r"(pk[6][sd]), "r"(pk[7][sd])
+                         : "memory");
+          } else if (st_ok) {
 #pragma unroll
-          for (int sd = 0; sd < S; ++sd)
+            for (int q = 0; q < 32; ++q)
+              if (q < jn) dg[sd * N + q] = static_cast<int8_t>(pk[q >> 2][sd] >> (8 * (q & 3)));
+          }
+        }
+      } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (16 * h2 + q < jn) dg[sd * N + 16 * h2 + q] = static_cast<int8_t>(pk[q >> 2][sd] >> (8 * (q & 3)));
+        for (int h2 = 0; h2 < EPC / 16; ++h2) {
+          uint32_t pk[4][S];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint64_t h4[4] = {digits(16 * h2 + 4 * g), digits(16 * h2 + 4 * g + 1),
+                                    digits(16 * h2 + 4 * g + 2), digits(16 * h2 + 4 * g + 3)};
+            pack4<S>(h4, pk[g]);
+          }
+          if (full) {
+#pragma unroll
+            for (int sd = 0; sd < S; ++sd)
+              *reinterpret_cast<uint4*>(dg + sd * N + 16 * h2) =
+                  make_uint4(pk[0][sd], pk[1][sd], pk[2][sd], pk[3][sd]);
+          } else if (st_ok) {
+#pragma unroll
+            for (int sd = 0; sd < S; ++sd)
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (16 * h2 + q < jn) dg[sd * N + 16 * h2 + q] = static_cast<int8_t>(pk[q >> 2][sd] >> (8 * (q & 3)));
+          }
         }
       }
     } else {
