@@ -322,7 +322,10 @@ struct Exec {
   static constexpr int kOzDigits = 7;
   template <class Terms>
   bool ozaki_route(int64_t L, int n, int64_t R, const Terms& terms, const Remap* rm) const {
-    if (rm || in_expm || h->cplx || h->sharded() || rec || h->gemm_path == PHIKS_GEMM_DMMA) return false;
+    // slab-sharded handles (local modes and the two peer-store stages) take it too; complex
+    // handles and the exponential stage's small GEMMs stay on DMMA
+    if (in_expm || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA) return false;
+    if (rm && rm->world > kMaxRanks) return false;
     if (!ozaki_supported(L, n, R, kOzDigits)) return false;
     // auto: where it measured faster (configs[2], n = 128: DMMA 1.00 ms vs int8 1.02 ms per apply)
     if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 192 || L * R * n < (int64_t(1) << 20))) return false;
@@ -334,7 +337,7 @@ struct Exec {
     return true;
   }
   template <class Terms>
-  void ozaki_launch(int64_t L, int n, int64_t R, const Terms& terms) {
+  void ozaki_launch(int64_t L, int n, int64_t R, const Terms& terms, const Remap* rm = nullptr) {
     constexpr int kChunkX = 8;  // distinct inputs split per launch (bounds the digit workspace)
     size_t i = 0;
     while (i < terms.size() && ok()) {
@@ -345,6 +348,7 @@ struct Exec {
       p.R = R;
       p.n = n;
       p.S = kOzDigits;
+      if (rm) p.remap = *rm;
       size_t j = i;
       for (; j < terms.size() && p.nterms < kMaxTerms; ++j) {
         int xs = -1, es = -1;
@@ -542,7 +546,7 @@ struct Exec {
   void mode_launch(int64_t L, int n, int64_t R, const std::vector<LaunchTerm>& terms, const Remap* rm = nullptr) {
     if (!ok() || terms.empty()) return;
     if (ozaki_route(L, n, R, terms, rm)) {
-      ozaki_launch(L, n, R, terms);
+      ozaki_launch(L, n, R, terms, rm);
       return;
     }
     // chunk so every launch fits ModeParams; a group's terms stay in order

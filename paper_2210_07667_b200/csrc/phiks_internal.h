@@ -146,6 +146,7 @@ struct OzakiParams {
   int a_mn;      // 1: xs holds [nx][S][L·n·R] digit planes in the fp64 layout (MN-major A, L % 128 == 0)
   int n_next;    // chained: n_{μ+1} (0: plain fp64 outputs)
   int dbg;       // timing experiments only (PHIKS_OZ_DBG); 0 in production
+  Remap remap;   // slab-sharded stage (world > 0): fp64 outputs go to the owner rank; out = byte offset
 };
 bool ozaki_supported(int64_t L, int n, int64_t R, int S);
 size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne);

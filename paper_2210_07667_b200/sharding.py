@@ -117,6 +117,10 @@ class ShardedPhiKS:
     def set_profiling(self, on: bool = True):
         self.op.set_profiling(on)
 
+    def set_gemm_path(self, path: str):
+        """int8 / DMMA / auto for the Tucker products of this rank (phiks_set_gemm_path)."""
+        self.op.set_gemm_path(path)
+
     def wait(self):
         self.op.wait()
 

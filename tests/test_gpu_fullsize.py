@@ -111,10 +111,21 @@ def test_config3_full_sharded8_equals_single():
     ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
     ShardedPhiKS.connect_local(ranks)
     vecs = [[torch.from_numpy(np.ascontiguousarray(s)).to(DEV)] for s in split_slabs(x, world)]
+    for r in ranks:
+        r.set_gemm_path("dmma")
     outs = apply_ranks_serial(ranks, pb.tau, pb.ells, vecs, mode="same", n_scales=1)
     torch.cuda.synchronize()
     for i in range(len(pb.ells)):
         got = torch.cat([outs[r][i] for r in range(world)]).cpu().numpy()
         assert np.array_equal(got, single[i]), i
+    # the default (int8) path on the sharded handle: peer-store epilogues of the int8 GEMM
+    for r in ranks:
+        r.set_gemm_path("auto")
+    outs = apply_ranks_serial(ranks, pb.tau, pb.ells, vecs, mode="same", n_scales=1)
+    torch.cuda.synchronize()
+    assert all(r.stats()["i8_mode_launches"] > 0 for r in ranks)
+    for i in range(len(pb.ells)):
+        got = torch.cat([outs[r][i] for r in range(world)]).cpu().numpy()
+        assert rel2(got, single[i]) <= 1e-13, i
     for r in ranks:
         r.close()

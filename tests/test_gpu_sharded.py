@@ -28,10 +28,12 @@ def rel2(got, ref):
     return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
 
 
-def run_sharded(pb, world, n_scales=None, force=None):
+def run_sharded(pb, world, n_scales=None, force=None, path="dmma"):
     n_scales = pb.n_scales if n_scales is None else n_scales
     ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
     ShardedPhiKS.connect_local(ranks)
+    for r in ranks:
+        r.set_gemm_path(path)
     flat = [W.as_flat(v) for v in pb.vs]
     vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, world)[r])).to(DEV) for x in flat]
             for r in range(world)]
@@ -47,7 +49,7 @@ def run_sharded(pb, world, n_scales=None, force=None):
 def run_single(pb, n_scales=None):
     n_scales = pb.n_scales if n_scales is None else n_scales
     op = PhiKS(pb.A)
-    op.set_gemm_path("dmma")  # sharded handles run the DMMA kernel; compare like with like
+    op.set_gemm_path("dmma")  # like with like: both on the DMMA kernel (same accumulation order)
     outs = op.apply(pb.tau, pb.ells, [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).to(DEV) for v in pb.vs],
                     mode=pb.mode, n_scales=n_scales)
     torch.cuda.synchronize()
@@ -184,3 +186,23 @@ def test_sharded_complex(dims, world, mode):
     torch.cuda.synchronize()
     for a, b in zip(gathered, single):
         assert rel2(a, b.cpu().numpy()) <= 1e-15
+
+
+# ---- the int8 tensor-core path on sharded handles: local modes
+# split + GEMM, the two transposition stages as int8 GEMMs whose fp64 epilogue stores into
+# the owner ranks' regions ----
+@pytest.mark.parametrize("dims,world,mode", [((24, 40, 16), 2, "same"), ((20, 32, 24), 4, "lincomb"),
+                                             ((16, 24, 40), 8, "same"), ((36, 20), 4, "same"),
+                                             ((12, 10, 18, 16), 8, "lincomb"), ((30, 27, 24), 4, "same")])
+def test_sharded_int8_path(dims, world, mode):
+    seed = 1300 + sum(dims) + world
+    fac = W.random_factors(dims, seed=seed, scale=5.0)
+    ells = (0, 1, 2) if mode == "same" else (0, 1, 2, 3)
+    vs = [W.random_tensor(dims, seed=seed + 1 + k) for k in range(1 if mode == "same" else len(ells))]
+    pb = W.Problem(f"si8_{dims}_{world}_{mode}", dims, fac, 0.7, mode, ells, vs, 2)
+    outs, stats = run_sharded(pb, world, path="i8")
+    assert all(s["i8_mode_launches"] > 0 for s in stats)
+    compare_oracle(pb, outs, pb.n_scales)
+    single, _ = run_single(pb)
+    for a, b in zip(outs, single):
+        assert rel2(a, b) <= 1e-13
