@@ -8,7 +8,7 @@ import os
 from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libphiks.so")
+LIB_PATH = os.environ.get("PHIKS_LIB_PATH") or os.path.join(_HERE, "libphiks.so")  # override: experiments only
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "phiks.h")
 
 MODE_SAME_VECTOR = 0

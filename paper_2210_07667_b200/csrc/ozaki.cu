@@ -765,17 +765,22 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
 
 // Persistent GEMM geometry: the E-digit tile of a (term, n-tile) stays resident
 // (S × 64 rows × Kp bytes); fiber digits stream through an NST-stage ring of
-// SPS-digit units (k-block kb, digit group sg).
-template <int S>
+// SPS-digit units (k-block kb, digit group sg).  Ring depth per variant, measured on the
+// configs[3] launches (ms per 19-term batch at NST = 4 / 5 / 6 / 7): mode 1 with digit
+// epilogue 2.01 / 2.02 / 2.09 / 2.14, chained mode 2 2.15 / 2.13 / 2.12 / 2.14, fp64-output
+// mode 1.87 / 1.72 / 1.64 / 1.57 (the shared-memory carve-out also sizes the L1 the
+// digit epilogue's stores go through)
+__host__ __device__ constexpr int oz_nst(bool amn, bool outd) { return outd ? (amn ? 6 : 4) : 7; }
+template <int S, int NST_ = 6>
 struct OzGeom {
   static constexpr int SPS = 1;                                // digits per stage
   static constexpr int A_BYTES = SPS * kOzBM * kOzBK;         // one stage
-  static constexpr int NST = 6;                                // 96 KB ring (L2 latency cover for the short digit stages)
+  static constexpr int NST = NST_;
   static constexpr int B_KB = S * kOzBN * kOzBK;              // resident E slices per k-block
   static constexpr int B_BYTES = (kOzMaxN / kOzBK) * B_KB;    // Kp ≤ kOzMaxN
   static constexpr int SMEM = NST * A_BYTES + B_BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int EPC = 32;                               // columns per epilogue warp (16: measured slower)
-  static constexpr int EPI_WARPS = 4 * kOzBN / EPC;             // 4 per TMEM lane quarter (column quarters)
+  static constexpr int EPI_WARPS = 4 * kOzBN / EPC;             // 2 per TMEM lane quarter (column halves)
   static constexpr int THREADS = 64 + EPI_WARPS * 32;
   static_assert(S * kOzBN <= 512, "TMEM holds one 64-column accumulator per diagonal");
   static_assert(SMEM <= 232448, "shared memory");
@@ -801,10 +806,10 @@ struct OzSched {
 };
 
 template <int S, bool AMN, bool OUTD>
-__global__ void __launch_bounds__(OzGeom<S>::THREADS, 1)
+__global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb) {
-  using G = OzGeom<S>;
+  using G = OzGeom<S, oz_nst(AMN, OUTD)>;
   extern __shared__ uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* bres = smem + G::NST * G::A_BYTES;
@@ -1290,7 +1295,7 @@ bool oz_split_tma_ok(const OzakiParams& p) {
 
 template <int S, bool AMN, bool OUTD>
 cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
-  using G = OzGeom<S>;
+  using G = OzGeom<S, oz_nst(AMN, OUTD)>;
   static bool gattr = false;
   static int sms = 0;
   if (!gattr) {
