@@ -429,13 +429,16 @@ struct Exec {
     }();
     return on;
   }
-  bool ozaki_chain_route(const std::vector<TuckerItem>& items, size_t c0, size_t c1) const {
-    if (in_expm || h->cplx || h->sharded() || rec || h->gemm_path == PHIKS_GEMM_DMMA || !chain_env()) return false;
+  // modes 0..mlast of the batch chained (mlast = d − 1: whole operators; sharded handles stop at
+  // the mode-(d−1) stage, whose epilogue stores into the owner ranks)
+  bool ozaki_chain_route(const std::vector<TuckerItem>& items, size_t c0, size_t c1, int mlast = -1) const {
+    if (in_expm || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA || !chain_env()) return false;
     const int d = h->d;
-    if (d < 2) return false;
+    if (mlast < 0) mlast = d - 1;
+    if (d < 2 || mlast < 1) return false;
     const int64_t N = h->N;
     int64_t L = 1;
-    for (int mu = 0; mu < d; ++mu) {
+    for (int mu = 0; mu <= mlast; ++mu) {
       const int n = h->n[mu];
       const int64_t R = N / (L * n);
       if (!ozaki_supported(L, n, R, kOzDigits) || n % 16 != 0) return false;
@@ -455,8 +458,12 @@ struct Exec {
     const double per = 2.0 * kOzDigits * static_cast<double>(h->N);
     return static_cast<size_t>(std::max(1.0, std::min(24.0, std::floor(8e9 / per))));
   }
-  void tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size_t c1) {
+  // last mode mlast writes fp64: the items' outputs (mlast = d − 1), or with rm set the
+  // sharded stage-0 peer stores into symmetric-region offset kCtrlBytes + b·sym_slot
+  void tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size_t c1, int mlast = -1,
+                       const Remap* rm = nullptr) {
     const int d = h->d, S = kOzDigits;
+    if (mlast < 0) mlast = d - 1;
     const int64_t N = h->N;
     const int nt = static_cast<int>(c1 - c0);
     int nmin = h->n[0];
@@ -471,7 +478,7 @@ struct Exec {
       oz_chain_cap = cap;
     }
     int64_t L = 1;
-    for (int mu = 0; mu < d && ok(); ++mu) {
+    for (int mu = 0; mu <= mlast && ok(); ++mu) {
       const int n = h->n[mu];
       const int64_t R = N / (L * n);
       auto pp = std::make_shared<OzakiParams>();
@@ -481,8 +488,9 @@ struct Exec {
       p.R = R;
       p.n = n;
       p.S = S;
-      p.n_next = mu + 1 < d ? h->n[mu + 1] : 0;
-      const int64_t Cn = mu + 1 < d ? N / h->n[mu + 1] : 0;
+      p.n_next = mu < mlast ? h->n[mu + 1] : 0;
+      if (mu == mlast && rm) p.remap = *rm;
+      const int64_t Cn = mu < mlast ? N / h->n[mu + 1] : 0;
       for (int b = 0; b < nt; ++b) {
         const TuckerItem& it = items[c0 + b];
         int xs = b, es = -1;
@@ -502,10 +510,12 @@ struct Exec {
           p.e[p.ne++] = it.mats[mu];
         }
         OzakiTerm t{xs, es, nullptr, 1.0, nullptr, nullptr, nullptr};
-        if (mu + 1 < d) {
+        if (mu < mlast) {
           t.dig = oz_dig[mu % 2] + static_cast<int64_t>(b) * S * N;
           t.nex = oz_ex[mu % 2] + static_cast<int64_t>(b) * Cn;
           t.nmx = oz_mx + static_cast<int64_t>(b) * (N / (static_cast<int64_t>(n) * h->n[mu + 1]));
+        } else if (rm) {
+          t.out = reinterpret_cast<double*>(kCtrlBytes + static_cast<size_t>(c0 + b) * h->sym_slot);
         } else {
           t.out = it.outs[0].dst;
           t.beta = it.outs[0].beta * it.in_scale;
@@ -528,10 +538,11 @@ struct Exec {
       oz_emit(pp, mu == 0);
       L *= n;
     }
+    i8_chained += nt;
+    if (mlast < d - 1) return;  // the sharded caller completes and counts the operators
     int64_t nsum = 0;
     for (int mu = 0; mu < d; ++mu) nsum += h->n[mu];
     tucker_ops += nt;
-    i8_chained += nt;
     mu_flops += static_cast<double>(nt) * 2.0 * static_cast<double>(N) * static_cast<double>(nsum);
   }
 
@@ -987,13 +998,15 @@ struct Exec {
     const int d = h->d, P = h->world, rk = h->rank;
     const int64_t N = h->N;
     const size_t nb = items.size();
+    // int8 chain over the local modes into stage 0 (DESIGN.md §4d, §0(e))
+    const bool chained = d >= 3 && ozaki_chain_route(items, 0, nb, d - 2);
     auto& scr = scr_pool;
-    if (d >= 3)
+    if (d >= 3 && !chained)
       while (scr[0].size() < nb) scr[0].push_back(ar->alloc_doubles(N));
-    if (d >= 4)
+    if (d >= 4 && !chained)
       while (scr[1].size() < nb) scr[1].push_back(ar->alloc_doubles(N));
     int64_t L = 1;
-    for (int mu = 0; mu + 2 < d; ++mu) {
+    for (int mu = 0; mu + 2 < d && !chained; ++mu) {
       const int n = h->n[mu];
       std::vector<LaunchTerm> terms;
       for (size_t b = 0; b < nb; ++b) {
@@ -1025,7 +1038,12 @@ struct Exec {
     };
     const Remap ra = remap_of(s0), rb = remap_of(s1);
     (void)L;
-    {
+    if (chained) {
+      // modes 1..d−2 chained on the slab, stage 0 (mode d−1) reading their digits and
+      // storing fp64 into the owners' T pools
+      const size_t cap = chain_cap();
+      for (size_t s0c = 0; s0c < nb && ok(); s0c += cap) tucker_chain_i8(items, s0c, std::min(nb, s0c + cap), d - 2, &ra);
+    } else {
       std::vector<LaunchTerm> terms;
       for (size_t b = 0; b < nb; ++b) {
         LaunchTerm t;

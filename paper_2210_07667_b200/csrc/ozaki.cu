@@ -735,14 +735,24 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     // element (l, j, r) goes to base[k] + out + l + kstride[k]·r + kroff[k] + colstride·(j − kstart[k])
     const Remap& rm = p.remap;
     const int big = (rm.cq + 1) * rm.crem;
+    auto owner = [&](int j) { return j < big ? j / (rm.cq + 1) : rm.crem + (j - big) / rm.cq; };
+    const int kf = owner(j0), kl = owner(j0 + (jn < EPC ? jn : EPC) - 1);
+    if (kf == kl) {  // the warp's columns share one owner: one base, then a stride per column
+      double* b = reinterpret_cast<double*>(rm.base[kf] + reinterpret_cast<uintptr_t>(term.out)) + rm.kroff[kf] + l +
+                  rm.kstride[kf] * r + rm.colstride * static_cast<int64_t>(j0 - rm.kstart[kf]);
 #pragma unroll
-    for (int q = 0; q < EPC; ++q) {
-      const int j = j0 + q;
-      if (q < jn) {
-        const int k = j < big ? j / (rm.cq + 1) : rm.crem + (j - big) / rm.cq;
-        double* colp = reinterpret_cast<double*>(rm.base[k] + reinterpret_cast<uintptr_t>(term.out)) + rm.kroff[k] +
-                       rm.colstride * static_cast<int64_t>(j - rm.kstart[k]);
-        colp[l + rm.kstride[k] * r] = acc[q];
+      for (int q = 0; q < EPC; ++q)
+        if (q < jn) b[rm.colstride * q] = acc[q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < EPC; ++q) {
+        const int j = j0 + q;
+        if (q < jn) {
+          const int k = owner(j);
+          double* colp = reinterpret_cast<double*>(rm.base[k] + reinterpret_cast<uintptr_t>(term.out)) + rm.kroff[k] +
+                         rm.colstride * static_cast<int64_t>(j - rm.kstart[k]);
+          colp[l + rm.kstride[k] * r] = acc[q];
+        }
       }
     }
   } else if (!OUTD && rvalid && jn > 0) {

@@ -193,7 +193,9 @@ def test_sharded_complex(dims, world, mode):
 # the owner ranks' regions ----
 @pytest.mark.parametrize("dims,world,mode", [((24, 40, 16), 2, "same"), ((20, 32, 24), 4, "lincomb"),
                                              ((16, 24, 40), 8, "same"), ((36, 20), 4, "same"),
-                                             ((12, 10, 18, 16), 8, "lincomb"), ((30, 27, 24), 4, "same")])
+                                             ((12, 10, 18, 16), 8, "lincomb"), ((30, 27, 24), 4, "same"),
+                                             ((128, 32, 16), 2, "same"), ((128, 48, 24), 8, "lincomb"),
+                                             ((128, 48, 32, 16), 4, "same")])
 def test_sharded_int8_path(dims, world, mode):
     seed = 1300 + sum(dims) + world
     fac = W.random_factors(dims, seed=seed, scale=5.0)
@@ -202,6 +204,8 @@ def test_sharded_int8_path(dims, world, mode):
     pb = W.Problem(f"si8_{dims}_{world}_{mode}", dims, fac, 0.7, mode, ells, vs, 2)
     outs, stats = run_sharded(pb, world, path="i8")
     assert all(s["i8_mode_launches"] > 0 for s in stats)
+    if dims[0] == 128:  # modes 1..d−2 chained into the peer-store stage
+        assert all(s["i8_chained_ops"] > 0 for s in stats)
     compare_oracle(pb, outs, pb.n_scales)
     single, _ = run_single(pb)
     for a, b in zip(outs, single):
