@@ -658,7 +658,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
       return (rbad || cpq == INT_MIN) ? 0ull : h;
     };
     const bool st_ok = rvalid && jn > 0 && !(p.dbg & 2);  // dbg & 2: timing experiment without stores
-    if (L == 1) {  // EPC consecutive bytes of each digit plane per thread
+    if (L == 1 && !p.out_kmajor) {  // EPC consecutive bytes of each digit plane per thread
       int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
       const bool full = st_ok && jn >= EPC;
       if (EPC == 32 && ((reinterpret_cast<uintptr_t>(dg) | static_cast<uintptr_t>(N)) & 31) == 0) {
@@ -707,12 +707,24 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
         }
       }
     } else {
-      // lanes hold consecutive l (L % 128 == 0): per 4 columns, the 4×4 byte blocks of each
-      // lane quad are transposed by two shuffle rounds, so lane i of a quad stores the
-      // 4 consecutive rows of column q0 + i as one 32-bit word
+      // lanes hold consecutive rows of the next mode's layout: consecutive l (MN-major,
+      // L % 128 == 0: row offset l + L·n·r, column stride L) or, for the mode-1 product with
+      // K-major next-mode digits (p.out_kmajor), consecutive k = i of fibre c' = j + n·r'
+      // (r = i + n'·r', row offset i + n·n'·r', column stride n').  Per 4 columns, the 4×4
+      // byte blocks of each lane quad are transposed by two shuffle rounds, so lane qi of a
+      // quad stores the 4 consecutive rows of column q0 + qi as one 32-bit word
       const int qi = lane & 3;
       const uint32_t sel1 = (qi & 1) ? 0x3715u : 0x6240u, sel2 = (qi & 2) ? 0x3276u : 0x5410u;
-      int8_t* dq = term.dig + (l - qi) + L * (j0 + qi + static_cast<int64_t>(p.n) * r);
+      int64_t rowoff, cs;
+      if (L == 1) {
+        const int64_t i = r % p.n_next, rq = r / p.n_next;
+        rowoff = i + static_cast<int64_t>(p.n) * p.n_next * rq;
+        cs = p.n_next;
+      } else {
+        rowoff = l + L * static_cast<int64_t>(p.n) * r;
+        cs = L;
+      }
+      int8_t* dq = term.dig + (rowoff - qi) + cs * (j0 + qi);
 #pragma unroll
       for (int q0 = 0; q0 < EPC; q0 += 4) {
         const uint64_t h4[4] = {digits(q0), digits(q0 + 1), digits(q0 + 2), digits(q0 + 3)};
@@ -722,7 +734,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
         for (int sd = 0; sd < S; ++sd) {
           const uint32_t t1 = __byte_perm(pk[sd], __shfl_xor_sync(0xffffffffu, pk[sd], 1), sel1);
           const uint32_t t2 = __byte_perm(t1, __shfl_xor_sync(0xffffffffu, t1, 2), sel2);
-          if (st_ok && q0 + qi < jn) *reinterpret_cast<uint32_t*>(dq + sd * N + L * q0) = t2;
+          if (st_ok && q0 + qi < jn) *reinterpret_cast<uint32_t*>(dq + sd * N + cs * q0) = t2;
         }
       }
     }

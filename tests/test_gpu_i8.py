@@ -205,7 +205,9 @@ def test_i8_path_selection_api():
 
 # ---- chained modes: every mode on the int8 path, each product
 # writing the next mode's digits with exponents bounded before the product ----
-CHAIN_SHAPES = [(128, 96), (128, 48, 32), (256, 16, 64), (128, 16, 16, 16)]
+# n_2 % 128 == 0 hands K-major digits from the mode-1 product to mode 2; the others MN-major
+CHAIN_SHAPES = [(128, 96), (128, 48, 32), (256, 16, 64), (128, 16, 16, 16), (256, 128), (128, 128, 16),
+                (128, 256, 32, 16)]
 
 
 @pytest.mark.parametrize("dims", CHAIN_SHAPES)
