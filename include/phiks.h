@@ -205,7 +205,11 @@ phiks_status phiks_set_profiling(phiks_handle h, int on);
    PHIKS_GEMM_DMMA: the fp64 DMMA kernel for every product;
    PHIKS_GEMM_I8: the int8 tensor-core kernel (7 balanced base-256 digits per
      operand, exact int32 accumulation: fp64-class error) wherever it applies
-     (real handles, unsharded, n_μ ≤ 256, plain outputs), DMMA elsewhere;
+     (real handles, sharded or not, n_μ ≤ 256, plain outputs), DMMA elsewhere;
+     when every mode of a Tucker batch qualifies (n_μ % 16 == 0, L_μ % 128 == 0
+     for μ ≥ 2) the modes run chained: each product writes the next mode's
+     digits, split with exponent bounds (reading R15; the
+     environment variable PHIKS_CHAIN=0 restores per-mode splits);
    PHIKS_GEMM_AUTO (default, or the PHIKS_GEMM environment variable "dmma" /
      "i8" / "auto" at create): the int8 kernel for products with n_μ ≥ 192 on
      tensors of N ≥ 2^20 elements, where it is faster.  Invalidates the handle's captured
