@@ -442,13 +442,13 @@ __global__ void __launch_bounds__(512, 1)
   const int n = p.n, Kp = p.Kp;
   const int64_t L = p.L, C = p.L * p.R;
   const int tile_elems = 32 * n;
-  double* red = oz_sx_raw + 2 * 32 * kOzMaxN + S * 2 * 4096 / 8;  // [16][32] partial maxima
+  double* red = oz_sx_raw + 2 * 32 * kOzMaxNRes + S * 2 * 4096 / 8;  // [16][32] partial maxima
   int* redbad = reinterpret_cast<int*>(red + 16 * 32);             // [16][32]
   uint64_t* full = reinterpret_cast<uint64_t*>(redbad + 16 * 32);
   // digit staging: per digit s and 128-byte k-half h, a SWIZZLE_128B image of the
   // 32 fibers × 128 bytes box (16-byte chunk q of row r at q ^ (r & 7)), written
   // conflict-free and stored by TMA (which undoes the swizzle)
-  uint8_t* stage = reinterpret_cast<uint8_t*>(oz_sx_raw) + 2 * 32 * kOzMaxN * 8;  // 1 KB aligned
+  uint8_t* stage = reinterpret_cast<uint8_t*>(oz_sx_raw) + 2 * 32 * kOzMaxNRes * 8;  // 1 KB aligned
   const int nh = Kp > 128 ? 2 : 1;  // k-halves (Kp ≤ 256)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntc = C / 32;
@@ -799,7 +799,7 @@ struct OzGeom {
   static constexpr int A_BYTES = SPS * kOzBM * kOzBK;         // one stage
   static constexpr int NST = NST_;
   static constexpr int B_KB = S * kOzBN * kOzBK;              // resident E slices per k-block
-  static constexpr int B_BYTES = (kOzMaxN / kOzBK) * B_KB;    // Kp ≤ kOzMaxN
+  static constexpr int B_BYTES = (kOzMaxNRes / kOzBK) * B_KB; // resident (Kp ≤ 256) or a 2-block ring (SE)
   static constexpr int SMEM = NST * A_BYTES + B_BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int EPC = 32;                               // columns per epilogue warp (16: measured slower)
   static constexpr int EPI_WARPS = 4 * kOzBN / EPC;             // 2 per TMEM lane quarter (column halves)
@@ -827,7 +827,9 @@ struct OzSched {
   }
 };
 
-template <int S, bool AMN, bool OUTD>
+// SE: n > 256, the E digits stream through a 2-block ring (one 128-k block per stage
+// group) instead of staying resident per term
+template <int S, bool AMN, bool OUTD, bool SE>
 __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb) {
@@ -841,7 +843,9 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
   uint64_t* b_empty = b_full + 1;
   uint64_t* t_full = b_empty + 1;
   uint64_t* t_empty = t_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 1);
+  uint64_t* e_full = t_empty + 1;  // SE: [2]
+  uint64_t* e_empty = e_full + 2;   // SE: [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const OzSched sc(p);
   if (sc.q >= sc.Q) return;  // idle CTA (grid not a multiple of the n-tile count)
@@ -859,6 +863,10 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     oz_mbar_init(b_empty, 1);
     oz_mbar_init(t_full, 1);
     oz_mbar_init(t_empty, G::EPI_WARPS);
+    for (int b = 0; b < 2; ++b) {
+      oz_mbar_init(&e_full[b], 1);
+      oz_mbar_init(&e_empty[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
@@ -873,11 +881,11 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
 
   if (warp == 0) {
     // ---- TMA producer (whole warp in lockstep, one elected lane issues) ----
-    int cur_term = -1, bgen = 0, it = 0;
+    int cur_term = -1, bgen = 0, it = 0, ek = 0;
     for (int64_t u = sc.q; u < sc.units; u += sc.Q) {
       const int term = static_cast<int>(u / sc.Mt);
       const int mt = static_cast<int>(u % sc.Mt);
-      if (term != cur_term) {  // (re)load the resident E slices of this (term, n-tile)
+      if (!SE && term != cur_term) {  // (re)load the resident E slices of this (term, n-tile)
         if (bgen > 0) oz_mbar_wait(b_empty, (bgen - 1) & 1);
         if (oz_elect()) {
           oz_mbar_expect_tx(b_full, static_cast<unsigned>(nk * G::B_KB));
@@ -889,7 +897,17 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
         ++bgen;
       }
       const int xs = p.terms[term].xslot;
-      for (int kb = 0; kb < nk; ++kb)
+      for (int kb = 0; kb < nk; ++kb) {
+        if (SE) {  // this k-block's E digits (all S digit planes × 64 rows) into ring slot ek & 1
+          const int es = ek & 1;
+          if (ek >= 2) oz_mbar_wait(&e_empty[es], ((ek >> 1) & 1) ^ 1);
+          if (oz_elect()) {
+            oz_mbar_expect_tx(&e_full[es], static_cast<unsigned>(G::B_KB));
+            oz_tma_load_4d(bres + es * G::B_KB, &tb, kb * kOzBK, sc.nt * kOzBN, 0, p.terms[term].eslot, &e_full[es]);
+          }
+          __syncwarp();
+          ++ek;
+        }
         for (int sg = 0; sg < NSG; ++sg, ++it) {
           const int st = it % G::NST;
           if (it >= G::NST) oz_mbar_wait(&a_empty[st], ((it / G::NST) & 1) ^ 1);
@@ -905,6 +923,7 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
           }
           __syncwarp();
         }
+      }
     }
   } else if (warp == 1) {
     // ---- MMA issuer (whole warp in lockstep, one elected lane issues) ----
@@ -912,10 +931,10 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     // advance by adding (byte offset >> 4) to their start-address field
     const uint64_t a_desc0 = AMN ? oz_desc_mn_sw128(smem) : oz_desc_sw128(smem), b_desc0 = oz_desc_sw128(bres);
     constexpr uint64_t a_kstep = AMN ? (kOzUK * kOzBM) >> 4 : kOzUK >> 4;  // one UMMA k-step of A
-    int cur_term = -1, bgen = 0, it = 0, tile = 0;
+    int cur_term = -1, bgen = 0, it = 0, tile = 0, ek = 0;
     for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
       const int term = static_cast<int>(u / sc.Mt);
-      if (term != cur_term) {
+      if (!SE && term != cur_term) {
         if (bgen > 0) {
           if (oz_elect()) oz_commit(b_empty);  // the previous E tile is free once its MMAs are done
           __syncwarp();
@@ -929,7 +948,12 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
       // fully unrolled over the digits: every MMA's column offset, N and instruction
       // descriptor are compile-time constants (the issue loop is a few uniform adds per MMA)
       for (int kb = 0; kb < nk; ++kb) {
-        const uint64_t bd0 = b_desc0 + static_cast<uint64_t>((kb * G::B_KB) >> 4);
+        const int es = ek & 1;
+        if (SE) {
+          oz_mbar_wait(&e_full[es], (ek >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        }
+        const uint64_t bd0 = b_desc0 + static_cast<uint64_t>(((SE ? es : kb) * G::B_KB) >> 4);
 #pragma unroll
         for (int s = 0; s < S; ++s, ++it) {
           const int st = it % G::NST;
@@ -952,6 +976,11 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
             oz_commit(&a_empty[st]);
           }
           __syncwarp();
+        }
+        if (SE) {  // the k-block's E slot is free once its MMAs are done
+          if (oz_elect()) oz_commit(&e_empty[es]);
+          __syncwarp();
+          ++ek;
         }
       }
       if (oz_elect()) oz_commit(t_full);
@@ -1007,7 +1036,7 @@ struct OzGeom2 {
   static constexpr int A_BYTES = kOzBM * kOzBK;              // one digit × 128 fibers × 128 k
   static constexpr int NST = 4;
   static constexpr int E_KB = OzChunks::PIECES * 32 * kOzBK;  // 64 KB of chunk halves per k-stage
-  static constexpr int E_BYTES = (kOzMaxN / kOzBK) * E_KB;
+  static constexpr int E_BYTES = (kOzMaxNRes / kOzBK) * E_KB;
   static constexpr int SMEM = NST * A_BYTES + E_BYTES + 1024 + 512;
   static constexpr int EPC = 32;
   static constexpr int EPI_WARPS = 4 * kOzBN / EPC;
@@ -1315,14 +1344,14 @@ bool oz_split_tma_ok(const OzakiParams& p) {
   return p.R < (int64_t(1) << 31) && p.L < (int64_t(1) << 31);
 }
 
-template <int S, bool AMN, bool OUTD>
+template <int S, bool AMN, bool OUTD, bool SE>
 cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
   using G = OzGeom<S, oz_nst(AMN, OUTD)>;
   static bool gattr = false;
   static int sms = 0;
   if (!gattr) {
     cudaError_t e =
-        cudaFuncSetAttribute(oz_gemm_kernel<S, AMN, OUTD>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaFuncSetAttribute(oz_gemm_kernel<S, AMN, OUTD, SE>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1335,7 +1364,7 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   int64_t per = sms / ntn;  // CTAs per n-tile
   if (per > units) per = units;
   if (per < 1) per = 1;
-  oz_gemm_kernel<S, AMN, OUTD><<<static_cast<unsigned>(per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, tb);
+  oz_gemm_kernel<S, AMN, OUTD, SE><<<static_cast<unsigned>(per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, tb);
   return cudaGetLastError();
 }
 
@@ -1395,7 +1424,7 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
     } else if (p.L % 32 == 0 && p.n <= 256 && p.Kp >= 128 && oz_split_tma_ok(p)) {
       static bool tattr = false;
       static int sms = 0;
-      const int smem = 2 * 32 * kOzMaxN * 8 + S * 2 * 4096 + 16 * 32 * 8 + 16 * 32 * 4 + 64;
+      const int smem = 2 * 32 * kOzMaxNRes * 8 + S * 2 * 4096 + 16 * 32 * 8 + 16 * 32 * 4 + 64;
       if (!tattr) {
         cudaError_t e = cudaFuncSetAttribute(oz_split_x_tma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              smem);
@@ -1435,7 +1464,7 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
   const bool amap = p.a_mn ? oz_encode_mn(&ta, p.xs, p.L, p.n, p.R, S * p.nx)
                            : oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS);
   if (!amap) return cudaErrorInvalidValue;
-  if (S == 7 && oz_pair_enabled()) {  // CTA-pair MMAs (§4e): E chunks as 32-row pieces of one digit
+  if (S == 7 && p.Kp <= kOzMaxNRes && oz_pair_enabled()) {  // CTA-pair MMAs (§4e): E chunks as 32-row pieces of one digit
     if (!oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, 32, 1)) return cudaErrorInvalidValue;
     if (p.a_mn) {
       if (p.n_next > 0) return oz_gemm_pair_go<true, true>(p, st, ta, tb);
@@ -1445,12 +1474,20 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
     return oz_gemm_pair_go<false, false>(p, st, ta, tb);
   }
   if (!oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S)) return cudaErrorInvalidValue;
-  if (p.a_mn) {
-    if (p.n_next > 0) return oz_gemm_go<S, true, true>(p, st, ta, tb);
-    return oz_gemm_go<S, true, false>(p, st, ta, tb);
+  if (p.Kp > kOzMaxNRes) {  // E streamed per k-block
+    if (p.a_mn) {
+      if (p.n_next > 0) return oz_gemm_go<S, true, true, true>(p, st, ta, tb);
+      return oz_gemm_go<S, true, false, true>(p, st, ta, tb);
+    }
+    if (p.n_next > 0) return oz_gemm_go<S, false, true, true>(p, st, ta, tb);
+    return oz_gemm_go<S, false, false, true>(p, st, ta, tb);
   }
-  if (p.n_next > 0) return oz_gemm_go<S, false, true>(p, st, ta, tb);
-  return oz_gemm_go<S, false, false>(p, st, ta, tb);
+  if (p.a_mn) {
+    if (p.n_next > 0) return oz_gemm_go<S, true, true, false>(p, st, ta, tb);
+    return oz_gemm_go<S, true, false, false>(p, st, ta, tb);
+  }
+  if (p.n_next > 0) return oz_gemm_go<S, false, true, false>(p, st, ta, tb);
+  return oz_gemm_go<S, false, false, false>(p, st, ta, tb);
 }
 
 }  // namespace

@@ -115,7 +115,8 @@ struct MultiCombineParams {
 // μ-mode products on the int8 tensor cores (ozaki.cu): every
 // term t computes out_t = beta_t · (x_{xslot} ×_μ e_{eslot}) (plain outputs, no
 // sources), each fiber / row written in S balanced base-256 digits.
-constexpr int kOzMaxN = 256;      // mode size limit (resident E tile, int32 exactness)
+constexpr int kOzMaxN = 512;      // mode size limit of the int8 path (E streamed per k-block above kOzMaxNRes)
+constexpr int kOzMaxNRes = 256;   // E tile resident in shared memory up to this n
 constexpr int kOzMaxSlices = 7;
 struct OzakiTerm {
   int xslot, eslot;

@@ -37,7 +37,8 @@ def dot_bound(xs, dims, mu, M):
 
 @pytest.mark.parametrize("dims,mu", [((40, 33, 17), 0), ((40, 33, 17), 1), ((40, 33, 17), 2), ((256, 9), 0),
                                      ((7, 250), 1), ((130, 64, 5), 1), ((3, 128, 129), 2), ((33, 200, 41), 1),
-                                     ((1, 1000, 96), 2), ((129,), 0), ((5, 1, 31), 1)])
+                                     ((1, 1000, 96), 2), ((129,), 0), ((5, 1, 31), 1), ((512, 40), 0),
+                                     ((24, 300, 8), 1), ((64, 7, 449), 2)])  # n > 256: E streamed
 @pytest.mark.parametrize("digits", [6, 7])
 def test_i8_mode_product_vs_numpy(dims, mu, digits):
     rng = np.random.default_rng(hash((dims, mu, digits)) % 2 ** 32)
@@ -117,10 +118,10 @@ def test_i8_matches_dmma_building_block_large():
 
 
 def test_i8_rejects_unsupported():
-    x = torch.zeros(300 * 4, dtype=torch.float64, device=DEV)
-    M = torch.zeros(300 * 300, dtype=torch.float64, device=DEV)
-    with pytest.raises(RuntimeError):
-        mode_product_i8((300, 4), 0, [x], [M], [x.clone()], slices=7)
+    x = torch.zeros(600 * 4, dtype=torch.float64, device=DEV)
+    M = torch.zeros(600 * 600, dtype=torch.float64, device=DEV)
+    with pytest.raises(RuntimeError):  # n_μ > 512
+        mode_product_i8((600, 4), 0, [x], [M], [x.clone()], slices=7)
     with pytest.raises(RuntimeError):
         mode_product_i8((4, 4), 0, [x[:16]], [M[:16]], [x[:16].clone()], slices=8)
 
@@ -174,8 +175,8 @@ def test_i8_path_apply_random_problems():
 
 
 def test_i8_path_blocks_handle_and_fallback():
-    # a block-diagonal handle on the int8 path; a mode with n_μ > 256 falls back to DMMA
-    dims = (300, 40)
+    # a block-diagonal handle on the int8 path; a mode with n_μ > 512 falls back to DMMA
+    dims = (520, 40)
     pbs = []
     for b in range(2):
         fac = W.random_factors(dims, seed=700 + b, scale=4.0 + 6 * b)
@@ -186,7 +187,7 @@ def test_i8_path_blocks_handle_and_fallback():
     outs = op.apply(0.5, (0, 1, 2), vs)
     torch.cuda.synchronize()
     st = op.stats()
-    assert st["i8_mode_launches"] > 0  # mode 2 (n = 40) on the int8 path, mode 1 (n = 300 > 256) on DMMA
+    assert st["i8_mode_launches"] > 0  # mode 2 (n = 40) on the int8 path, mode 1 (n = 520 > 512) on DMMA
     for b, pb in enumerate(pbs):
         for k, r in enumerate(_oracle_outs(pb)):
             assert rel(outs[b * 3 + k].cpu().numpy(), r) <= 1e-12
@@ -207,7 +208,7 @@ def test_i8_path_selection_api():
 # writing the next mode's digits with exponents bounded before the product ----
 # shapes with n_2 % 128 == 0 take the K-major hand-off when PHIKS_CHAIN_KMAJOR=1 (opt-in)
 CHAIN_SHAPES = [(128, 96), (128, 48, 32), (256, 16, 64), (128, 16, 16, 16), (256, 128), (128, 128, 16),
-                (128, 256, 32, 16)]
+                (128, 256, 32, 16), (512, 96), (128, 384, 16)]  # n > 256: E streamed per k-block
 
 
 @pytest.mark.parametrize("dims", CHAIN_SHAPES)
