@@ -12,26 +12,29 @@ from paper_2210_07667_b200 import PhiKS, ShardedPhiKS, apply_ranks_serial  # noq
 from paper_2210_07667_b200 import workloads as W  # noqa: E402
 from paper_2210_07667_b200.sharding import split_slabs  # noqa: E402
 
-wl = W.config(3)
+CFG = int(os.environ.get("CONFIG", "3"))  # 3: 256^3 Brusselator (bench); 4: 512x512x256 ADR lincomb (the 8-GPU config)
+wl = W.config(CFG)
 pb0 = wl.problems[0]
 blocks = [pb.A for pb in wl.problems]
+mode = pb0.mode
 res = []
 for P in [int(x) for x in os.environ.get("PS", "1,2,4,8").split(",")]:
-    xs = [W.as_flat(pb.vs[0]) for pb in wl.problems]
+    xs = [W.as_flat(v) for pb in wl.problems for v in pb.vs]
     if P == 1:
         ranks = [PhiKS(blocks)]
     else:
         ranks = [ShardedPhiKS(blocks, r, P, connect=None) for r in range(P)]
         ShardedPhiKS.connect_local(ranks)
     ins = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, P)[r])).cuda() for x in xs] for r in range(P)]
+    nout = len(wl.problems) * len(pb0.ells) if mode == "same" else pb0.n_scales
     outs = [[torch.empty(xs[0].size // P, dtype=torch.float64, device="cuda")
-             for _ in range(len(wl.problems) * len(pb0.ells))] for _ in range(P)]
+             for _ in range(nout)] for _ in range(P)]
 
     def step():
         if P == 1:
-            ranks[0].apply(pb0.tau, pb0.ells, ins[0], outs=outs[0])
+            ranks[0].apply(pb0.tau, pb0.ells, ins[0], mode=mode, n_scales=pb0.n_scales, outs=outs[0])
         else:
-            apply_ranks_serial(ranks, pb0.tau, pb0.ells, ins, outs=outs)
+            apply_ranks_serial(ranks, pb0.tau, pb0.ells, ins, mode=mode, n_scales=pb0.n_scales, outs=outs)
     for _ in range(3):
         step()
     torch.cuda.synchronize()
@@ -42,7 +45,7 @@ for P in [int(x) for x in os.environ.get("PS", "1,2,4,8").split(",")]:
     e1.record()
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 5
-    res.append({"P": P, "serial_ms": round(t, 3), "per_rank_ms": round(t / P, 3)})
+    res.append({"config": CFG, "P": P, "serial_ms": round(t, 3), "per_rank_ms": round(t / P, 3)})
     print(json.dumps(res[-1]), flush=True)
     del ranks, ins, outs
     torch.cuda.empty_cache()
