@@ -265,3 +265,22 @@ def test_i8_chain_zero_and_nonfinite_inputs():
     # a dense Tucker operator spreads the NaN to every output (as fp64 arithmetic does)
     for g in got:
         assert np.all(np.isnan(g))
+
+
+def test_i8_chain_graph_replay_bitwise():
+    # applies of ≤ 4M elements are captured as CUDA graphs the first time and replayed after
+    # (DESIGN.md §4): the chained path must replay bit for bit
+    dims = (128, 64, 32)
+    fac = W.random_factors(dims, seed=970, scale=6.0)
+    v = torch.from_numpy(W.as_flat(W.random_tensor(dims, seed=971)).copy()).to(DEV)
+    op = PhiKS(fac)
+    op.set_gemm_path("i8")
+    outs = [torch.empty_like(v) for _ in range(3)]
+    res = []
+    for _ in range(3):
+        op.apply(0.4, (0, 1, 2), [v], outs=outs)
+        torch.cuda.synchronize()
+        res.append([o.cpu().numpy().copy() for o in outs])
+    assert op.stats()["i8_chained_ops"] > 0
+    for a, b in zip(res[0], res[2]):
+        assert np.array_equal(a, b)

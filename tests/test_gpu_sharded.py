@@ -195,7 +195,8 @@ def test_sharded_complex(dims, world, mode):
                                              ((16, 24, 40), 8, "same"), ((36, 20), 4, "same"),
                                              ((12, 10, 18, 16), 8, "lincomb"), ((30, 27, 24), 4, "same"),
                                              ((128, 32, 16), 2, "same"), ((128, 48, 24), 8, "lincomb"),
-                                             ((128, 48, 32, 16), 4, "same"), ((128, 128, 16), 4, "lincomb")])
+                                             ((128, 48, 32, 16), 4, "same"), ((128, 128, 16), 4, "lincomb"),
+                                             ((512, 32, 16), 2, "same")])  # n > 256: E streamed
 def test_sharded_int8_path(dims, world, mode):
     seed = 1300 + sum(dims) + world
     fac = W.random_factors(dims, seed=seed, scale=5.0)
