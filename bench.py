@@ -193,8 +193,18 @@ def i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, g_ms, g_n, ex_n
     # algorithmic bytes of a GEMM launch: the fiber digits (7 B per element and distinct input, once)
     # + the fp64 outputs (8 B per element and term); elements per term = flops / (2·n), n = 256
     elems = i8_fl / max(g_n, 1) / (2.0 * 256)
+    burst = 2.0 * pk["bf16_tflops"] if pk.get("bf16_tflops") else None
+    # the tcgen05 kind::i8 issue rate measured by scripts/umma_probe.cu (profiles/r01_mma_probes.json):
+    # 7930 MACs/SM/clk with the GEMM's own MMA sequence and stage synchronisation, operands in smem
+    probe = 2.0 * 7930 * 148 * 1.965e9 / 1e12
     return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOP/s (int8)",
             "frac": (ach / peak) if ach else None, "traffic": traffic,
+            "frac_vs_burst": (ach / burst) if (ach and burst) else None,
+            "frac_vs_mma_probe": (ach / probe) if ach else None,
+            "other_peaks": {"burst_tops": burst, "mma_probe_tops": probe,
+                            "note": "frac uses the sustained bf16 figure x 2 (the kernel runs inside a long step); "
+                                    "the GEMM kept 1965 MHz SM clocks in the bench, so the burst figure and the "
+                                    "MMA-issue probe are given as stricter denominators"},
             "kernel": "oz_gemm_kernel<7, AMN, OUTD> (tcgen05.mma kind::i8, TMEM accumulators, TMA SWIZZLE_128B, chained modes: DESIGN.md §4d): "
                       "the Tucker-operator μ-mode products",
             "algorithmic_ops_per_launch": ops / max(g_n, 1),
