@@ -649,7 +649,6 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     const bool fast = __all_sync(0xffffffffu, !rbad && !ebad && emin + mxi >= -1100 && emax + mxi <= 1025);
     const int rowk = rk - mxi;
     auto digits = [&](int q) -> uint64_t {
-      if (p.dbg & 4) return 0ull;  // timing experiment: no digit arithmetic
       if (fast) return digit_bits(acc[q], colk[q] + rowk);
       const int cpq = __shfl_sync(0xffffffffu, cp_l, q);
       const int e = min(max(((cpq >> 16) - 0x4000) + mxi, -1100), 1025);
@@ -657,7 +656,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
       const uint64_t h = digit_bits(acc[q], k);
       return (rbad || cpq == INT_MIN) ? 0ull : h;
     };
-    const bool st_ok = rvalid && jn > 0 && !(p.dbg & 2);  // dbg & 2: timing experiment without stores
+    const bool st_ok = rvalid && jn > 0;
     if (L == 1 && !p.out_kmajor) {  // EPC consecutive bytes of each digit plane per thread
       int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
       const bool full = st_ok && jn >= EPC;
@@ -724,7 +723,13 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
         rowoff = l + L * static_cast<int64_t>(p.n) * r;
         cs = L;
       }
+      // one running pointer per digit plane (column stride 4·cs per group of 4 columns)
       int8_t* dq = term.dig + (rowoff - qi) + cs * (j0 + qi);
+      uint32_t* dqs[S];
+#pragma unroll
+      for (int sd = 0; sd < S; ++sd) dqs[sd] = reinterpret_cast<uint32_t*>(dq + sd * N);
+      const int64_t step = cs;  // in 32-bit words: 4·cs bytes
+      const bool full = st_ok && jn >= EPC;
 #pragma unroll
       for (int q0 = 0; q0 < EPC; q0 += 4) {
         const uint64_t h4[4] = {digits(q0), digits(q0 + 1), digits(q0 + 2), digits(q0 + 3)};
@@ -734,7 +739,8 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
         for (int sd = 0; sd < S; ++sd) {
           const uint32_t t1 = __byte_perm(pk[sd], __shfl_xor_sync(0xffffffffu, pk[sd], 1), sel1);
           const uint32_t t2 = __byte_perm(t1, __shfl_xor_sync(0xffffffffu, t1, 2), sel2);
-          if (st_ok && q0 + qi < jn) *reinterpret_cast<uint32_t*>(dq + sd * N + cs * q0) = t2;
+          if (full || (st_ok && q0 + qi < jn)) *dqs[sd] = t2;
+          dqs[sd] += step;
         }
       }
     }
