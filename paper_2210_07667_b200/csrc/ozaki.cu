@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(512, 1)
 // One output tile of the epilogue (both GEMM kernels): fiber c (TMEM lane), columns
 // j0 .. j0+31 of term term_i; waits for the accumulators (t_full, phase), drains them,
 // releases TMEM through release(), then scales and stores (fp64 or the next mode's digits).
-template <int S, bool OUTD, int EPC, class Release>
+template <int S, bool OUTD, bool AMN, int EPC, class Release>
 __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_i, int64_t c, int j0, uint32_t tl,
                                              uint64_t* t_full, unsigned phase, Release release) {
   const int lane = threadIdx.x & 31;
@@ -648,61 +648,48 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     // k = ((ee_j − 30) − b_j) + (ex_c + 8S − 1 − Mx) = colk[q] + rowk: one add per element
     const bool fast = __all_sync(0xffffffffu, !rbad && !ebad && emin + mxi >= -1100 && emax + mxi <= 1025);
     const int rowk = rk - mxi;
-    auto digits = [&](int q) -> uint64_t {
-      if (fast) return digit_bits(acc[q], colk[q] + rowk);
-      const int cpq = __shfl_sync(0xffffffffu, cp_l, q);
-      const int e = min(max(((cpq >> 16) - 0x4000) + mxi, -1100), 1025);
-      const int k = ((cpq & 0xffff) - 0x4000) + rk - e;
-      const uint64_t h = digit_bits(acc[q], k);
-      return (rbad || cpq == INT_MIN) ? 0ull : h;
-    };
+    if (!fast) {
+      // rare (non-finite rows or fibres, clamped exponents): fold the general exponent into
+      // colk and zero the accumulators of non-finite entries (zero digits), so that the
+      // per-element code below stays a single short path (the kernel's instruction footprint
+      // bounds the epilogue: DESIGN.md §4e)
+#pragma unroll
+      for (int q = 0; q < EPC; ++q) {
+        const int cpq = __shfl_sync(0xffffffffu, cp_l, q);
+        const int e = min(max(((cpq >> 16) - 0x4000) + mxi, -1100), 1025);
+        colk[q] = ((cpq & 0xffff) - 0x4000) + rk - e - rowk;
+        if (rbad || cpq == INT_MIN) acc[q] = 0.0;
+      }
+    }
+    auto digits = [&](int q) -> uint64_t { return digit_bits(acc[q], colk[q] + rowk); };
     const bool st_ok = rvalid && jn > 0;
-    if (L == 1 && !p.out_kmajor) {  // EPC consecutive bytes of each digit plane per thread
+    if (!AMN && !p.out_kmajor) {  // mode-1 product (L = 1): EPC consecutive bytes of each digit plane per thread
       int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
       const bool full = st_ok && jn >= EPC;
-      if (EPC == 32 && ((reinterpret_cast<uintptr_t>(dg) | static_cast<uintptr_t>(N)) & 31) == 0) {
-        // one 32-byte store (STG.256, a whole sector) per digit plane
-        uint32_t pk[8][S];
+      const bool a32 = ((reinterpret_cast<uintptr_t>(dg) | static_cast<uintptr_t>(N)) & 31) == 0;
+      uint32_t pk[EPC / 4][S];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const uint64_t h4[4] = {digits(4 * g), digits(4 * g + 1), digits(4 * g + 2), digits(4 * g + 3)};
-          pack4<S>(h4, pk[g]);
-        }
+      for (int g = 0; g < EPC / 4; ++g) {
+        const uint64_t h4[4] = {digits(4 * g), digits(4 * g + 1), digits(4 * g + 2), digits(4 * g + 3)};
+        pack4<S>(h4, pk[g]);
+      }
 #pragma unroll
-        for (int sd = 0; sd < S; ++sd) {
-          if (full) {
-            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"l"(dg + sd * N),
-                         "r"(pk[0][sd]), "r"(pk[1][sd]), "r"(pk[2][sd]), "r"(pk[3][sd]), "r"(pk[4][sd]),
-                         "r"(pk[5][sd]), "r"(pk[6][sd]), "r"(pk[7][sd])
-                         : "memory");
-          } else if (st_ok) {
+      for (int sd = 0; sd < S; ++sd) {
+        int8_t* ds = dg + sd * N;
+        if (EPC == 32 && full && a32) {  // one 32-byte store (STG.256, a whole sector)
+          asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"l"(ds), "r"(pk[0][sd]),
+                       "r"(pk[1][sd]), "r"(pk[2][sd]), "r"(pk[3][sd]), "r"(pk[4][sd]), "r"(pk[5][sd]),
+                       "r"(pk[6][sd]), "r"(pk[7][sd])
+                       : "memory");
+        } else if (full) {  // 16-byte aligned rows (n % 16 == 0 on chained modes)
 #pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q < jn) dg[sd * N + q] = static_cast<int8_t>(pk[q >> 2][sd] >> (8 * (q & 3)));
-          }
-        }
-      } else {
+          for (int h2 = 0; h2 < EPC / 16; ++h2)
+            *reinterpret_cast<uint4*>(ds + 16 * h2) =
+                make_uint4(pk[4 * h2][sd], pk[4 * h2 + 1][sd], pk[4 * h2 + 2][sd], pk[4 * h2 + 3][sd]);
+        } else if (st_ok) {  // last n-tile of n % 64 != 0: jn is a multiple of 16
 #pragma unroll
-        for (int h2 = 0; h2 < EPC / 16; ++h2) {
-          uint32_t pk[4][S];
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const uint64_t h4[4] = {digits(16 * h2 + 4 * g), digits(16 * h2 + 4 * g + 1),
-                                    digits(16 * h2 + 4 * g + 2), digits(16 * h2 + 4 * g + 3)};
-            pack4<S>(h4, pk[g]);
-          }
-          if (full) {
-#pragma unroll
-            for (int sd = 0; sd < S; ++sd)
-              *reinterpret_cast<uint4*>(dg + sd * N + 16 * h2) =
-                  make_uint4(pk[0][sd], pk[1][sd], pk[2][sd], pk[3][sd]);
-          } else if (st_ok) {
-#pragma unroll
-            for (int sd = 0; sd < S; ++sd)
-#pragma unroll
-              for (int q = 0; q < 16; ++q)
-                if (16 * h2 + q < jn) dg[sd * N + 16 * h2 + q] = static_cast<int8_t>(pk[q >> 2][sd] >> (8 * (q & 3)));
-          }
+          for (int g = 0; g < EPC / 4; ++g)
+            if (4 * g < jn) *reinterpret_cast<uint32_t*>(ds + 4 * g) = pk[g][sd];
         }
       }
     } else {
@@ -1000,7 +987,7 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
       const int term_i = static_cast<int>(u / sc.Mt);
       const int64_t mt = u % sc.Mt;
-      oz_epilogue_tile<S, OUTD, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, sc.nt * kOzBN + ch * G::EPC, tl, t_full,
+      oz_epilogue_tile<S, OUTD, AMN, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, sc.nt * kOzBN + ch * G::EPC, tl, t_full,
                                 tile & 1, [&] {
                                   if (lane == 0) oz_mbar_arrive(t_empty);
                                 });
@@ -1254,7 +1241,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OzGeom2::THREADS, 1)
     for (int64_t u = q; u < units; u += Q, ++tile) {
       const int term_i = static_cast<int>(u / Mt2);
       const int64_t mt = (u % Mt2) * 2 + rank;
-      oz_epilogue_tile<S, OUTD, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, nt * kOzBN + ch * G::EPC, tl, t_full, tile & 1,
+      oz_epilogue_tile<S, OUTD, AMN, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, nt * kOzBN + ch * G::EPC, tl, t_full, tile & 1,
                                 [&] {
                                   if (lane == 0) oz_mbar_arrive_remote(t_empty0);
                                 });
