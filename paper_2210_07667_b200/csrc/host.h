@@ -422,15 +422,6 @@ struct Exec {
   double* oz_ex[2] = {nullptr, nullptr};
   double* oz_mx = nullptr;  // Mx of the current product (read by its own epilogue only)
   size_t oz_chain_cap = 0;  // Tucker operators the buffers hold
-  // opt-in (PHIKS_CHAIN_KMAJOR=1): K-major mode-2 digits from the mode-1 epilogue; measured
-  // slower on configs[3] (mode-1 / mode-2 launches 2.33 / 2.23 ms against 1.99 / 2.13 ms)
-  static bool kmajor_env() {
-    static const bool on = [] {
-      const char* e = std::getenv("PHIKS_CHAIN_KMAJOR");
-      return e && std::strcmp(e, "1") == 0;
-    }();
-    return on;
-  }
   static bool chain_env() {
     static const bool on = [] {
       const char* e = std::getenv("PHIKS_CHAIN");
@@ -499,11 +490,6 @@ struct Exec {
       p.S = S;
       p.n_next = mu < mlast ? h->n[mu + 1] : 0;
       if (mu == mlast && rm) p.remap = *rm;
-      // the mode-1 product hands K-major digits to mode 2 when its fibres tile evenly
-      // (each warp store then covers 4 rows of 32 bytes instead of 32 rows)
-      const bool kmaj_out = mu == 0 && mu < mlast && p.n_next % 128 == 0 && kmajor_env();
-      const bool kmaj_in = mu == 1 && h->n[1] % 128 == 0 && kmajor_env();
-      p.out_kmajor = kmaj_out ? 1 : 0;
       const int64_t Cn = mu < mlast ? N / h->n[mu + 1] : 0;
       for (int b = 0; b < nt; ++b) {
         const TuckerItem& it = items[c0 + b];
@@ -545,7 +531,7 @@ struct Exec {
         p.nx = nt;
         p.xs = oz_dig[(mu - 1) % 2];
         p.xsc = oz_ex[(mu - 1) % 2];
-        p.a_mn = kmaj_in ? 0 : 1;  // K-major [slot][S][c][Kp = n_2] after a K-major mode-1 epilogue
+        p.a_mn = 1;
       } else {
         p.nx = nx_keep;
       }

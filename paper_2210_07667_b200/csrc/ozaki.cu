@@ -663,7 +663,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     }
     auto digits = [&](int q) -> uint64_t { return digit_bits(acc[q], colk[q] + rowk); };
     const bool st_ok = rvalid && jn > 0;
-    if (!AMN && !p.out_kmajor) {  // mode-1 product (L = 1): EPC consecutive bytes of each digit plane per thread
+    if (!AMN) {  // mode-1 product (L = 1): EPC consecutive bytes of each digit plane per thread
       int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
       const bool full = st_ok && jn >= EPC;
       const bool a32 = ((reinterpret_cast<uintptr_t>(dg) | static_cast<uintptr_t>(N)) & 31) == 0;
@@ -693,24 +693,13 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
         }
       }
     } else {
-      // lanes hold consecutive rows of the next mode's layout: consecutive l (MN-major,
-      // L % 128 == 0: row offset l + L·n·r, column stride L) or, for the mode-1 product with
-      // K-major next-mode digits (p.out_kmajor), consecutive k = i of fibre c' = j + n·r'
-      // (r = i + n'·r', row offset i + n·n'·r', column stride n').  Per 4 columns, the 4×4
-      // byte blocks of each lane quad are transposed by two shuffle rounds, so lane qi of a
-      // quad stores the 4 consecutive rows of column q0 + qi as one 32-bit word
+      // lanes hold consecutive l (MN-major next-mode digits, L % 128 == 0: row offset l + L·n·r,
+      // column stride L).  Per 4 columns, the 4×4 byte blocks of each lane quad are transposed
+      // by two shuffle rounds, so lane qi of a quad stores the 4 consecutive rows of column
+      // q0 + qi as one 32-bit word
       const int qi = lane & 3;
       const uint32_t sel1 = (qi & 1) ? 0x3715u : 0x6240u, sel2 = (qi & 2) ? 0x3276u : 0x5410u;
-      int64_t rowoff, cs;
-      if (L == 1) {
-        const int64_t i = r % p.n_next, rq = r / p.n_next;
-        rowoff = i + static_cast<int64_t>(p.n) * p.n_next * rq;
-        cs = p.n_next;
-      } else {
-        rowoff = l + L * static_cast<int64_t>(p.n) * r;
-        cs = L;
-      }
-      // one running pointer per digit plane (column stride 4·cs per group of 4 columns)
+      const int64_t rowoff = l + L * static_cast<int64_t>(p.n) * r, cs = L;
       int8_t* dq = term.dig + (rowoff - qi) + cs * (j0 + qi);
       uint32_t* dqs[S];
 #pragma unroll
@@ -748,12 +737,13 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
 #pragma unroll
       for (int q = 0; q < EPC; ++q)
         if (q < jn) b[rm.colstride * q] = acc[q];
-    } else {
+    } else {  // the owner advances by at most one rank per column (every block has ≥ 1 column)
+      int k = kf;
 #pragma unroll
       for (int q = 0; q < EPC; ++q) {
         const int j = j0 + q;
         if (q < jn) {
-          const int k = owner(j);
+          if (k + 1 < rm.world && j >= rm.kstart[k + 1]) ++k;
           double* colp = reinterpret_cast<double*>(rm.base[k] + reinterpret_cast<uintptr_t>(term.out)) + rm.kroff[k] +
                          rm.colstride * static_cast<int64_t>(j - rm.kstart[k]);
           colp[l + rm.kstride[k] * r] = acc[q];
@@ -762,15 +752,10 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     }
   } else if (!OUTD && rvalid && jn > 0) {
     double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
-    if (jn >= EPC) {
-      if (L == 1 && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
+    if (!AMN && L == 1 && jn >= EPC && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
 #pragma unroll
-        for (int q = 0; q < EPC; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(acc[q], acc[q + 1]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < EPC; ++q) outp[L * q] = acc[q];
-      }
-    } else {
+      for (int q = 0; q < EPC; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(acc[q], acc[q + 1]);
+    } else {  // one predicated loop (full and partial column ranges): a small instruction footprint
 #pragma unroll
       for (int q = 0; q < EPC; ++q)
         if (q < jn) outp[L * q] = acc[q];

@@ -146,7 +146,6 @@ struct OzakiParams {
   int* eext;     // [3][ne] min_j b_j, max_j b_j, any non-finite row (chained modes' fast-path test)
   int a_mn;      // 1: xs holds [nx][S][L·n·R] digit planes in the fp64 layout (MN-major A, L % 128 == 0)
   int n_next;    // chained: n_{μ+1} (0: plain fp64 outputs)
-  int out_kmajor; // chained mode-1 product (L = 1, n_{μ+1} % 128 == 0): next-mode digits K-major [c'][k]
   int dbg;       // timing experiments only (PHIKS_OZ_DBG); 0 in production
   Remap remap;   // slab-sharded stage (world > 0): fp64 outputs go to the owner rank; out = byte offset
 };

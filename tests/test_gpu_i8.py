@@ -206,7 +206,6 @@ def test_i8_path_selection_api():
 
 # ---- chained modes: every mode on the int8 path, each product
 # writing the next mode's digits with exponents bounded before the product ----
-# shapes with n_2 % 128 == 0 take the K-major hand-off when PHIKS_CHAIN_KMAJOR=1 (opt-in)
 CHAIN_SHAPES = [(128, 96), (128, 48, 32), (256, 16, 64), (128, 16, 16, 16), (256, 128), (128, 128, 16),
                 (128, 256, 32, 16), (512, 96), (128, 384, 16)]  # n > 256: E streamed per k-block
 
