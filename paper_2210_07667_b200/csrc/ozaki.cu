@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(512, 1)
 // One output tile of the epilogue (both GEMM kernels): fiber c (TMEM lane), columns
 // j0 .. j0+31 of term term_i; waits for the accumulators (t_full, phase), drains them,
 // releases TMEM through release(), then scales and stores (fp64 or the next mode's digits).
-template <int S, bool OUTD, bool AMN, int EPC, class Release>
+template <int S, bool OUTD, bool AMN, bool REM, int EPC, class Release>
 __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_i, int64_t c, int j0, uint32_t tl,
                                              uint64_t* t_full, unsigned phase, Release release) {
   const int lane = threadIdx.x & 31;
@@ -724,7 +724,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
 #pragma unroll
     for (int q = 0; q < EPC; ++q) acc[q] = (acc[q] * __shfl_sync(0xffffffffu, esc_l, q)) * rb;  // exact, then rounded
   }
-  if (!OUTD && rvalid && jn > 0 && p.remap.world > 0) {
+  if (!OUTD && REM && rvalid && jn > 0) {
     // slab-sharded stage: column j of the product belongs to rank k = owner(j);
     // element (l, j, r) goes to base[k] + out + l + kstride[k]·r + kroff[k] + colstride·(j − kstart[k])
     const Remap& rm = p.remap;
@@ -750,7 +750,7 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
         }
       }
     }
-  } else if (!OUTD && rvalid && jn > 0) {
+  } else if (!OUTD && !REM && rvalid && jn > 0) {
     double* outp = term.out + l + L * (j0 + static_cast<int64_t>(p.n) * r);
     if (!AMN && L == 1 && jn >= EPC && (reinterpret_cast<uintptr_t>(outp) & 15) == 0) {
 #pragma unroll
@@ -807,7 +807,7 @@ struct OzSched {
 
 // SE: n > 256, the E digits stream through a 2-block ring (one 128-k block per stage
 // group) instead of staying resident per term
-template <int S, bool AMN, bool OUTD, bool SE>
+template <int S, bool AMN, bool OUTD, bool SE, bool REM>
 __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb) {
@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
       const int term_i = static_cast<int>(u / sc.Mt);
       const int64_t mt = u % sc.Mt;
-      oz_epilogue_tile<S, OUTD, AMN, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, sc.nt * kOzBN + ch * G::EPC, tl, t_full,
+      oz_epilogue_tile<S, OUTD, AMN, REM, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, sc.nt * kOzBN + ch * G::EPC, tl, t_full,
                                 tile & 1, [&] {
                                   if (lane == 0) oz_mbar_arrive(t_empty);
                                 });
@@ -1226,7 +1226,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OzGeom2::THREADS, 1)
     for (int64_t u = q; u < units; u += Q, ++tile) {
       const int term_i = static_cast<int>(u / Mt2);
       const int64_t mt = (u % Mt2) * 2 + rank;
-      oz_epilogue_tile<S, OUTD, AMN, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, nt * kOzBN + ch * G::EPC, tl, t_full, tile & 1,
+      oz_epilogue_tile<S, OUTD, AMN, false, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, nt * kOzBN + ch * G::EPC, tl, t_full, tile & 1,
                                 [&] {
                                   if (lane == 0) oz_mbar_arrive_remote(t_empty0);
                                 });
@@ -1322,14 +1322,15 @@ bool oz_split_tma_ok(const OzakiParams& p) {
   return p.R < (int64_t(1) << 31) && p.L < (int64_t(1) << 31);
 }
 
-template <int S, bool AMN, bool OUTD, bool SE>
+template <int S, bool AMN, bool OUTD, bool SE, bool REM = false>
 cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
+  if (!OUTD && !REM && p.remap.world > 0) return oz_gemm_go<S, AMN, OUTD, SE, !OUTD>(p, st, ta, tb);
   using G = OzGeom<S, oz_nst(AMN, OUTD)>;
   static bool gattr = false;
   static int sms = 0;
   if (!gattr) {
     cudaError_t e =
-        cudaFuncSetAttribute(oz_gemm_kernel<S, AMN, OUTD, SE>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaFuncSetAttribute(oz_gemm_kernel<S, AMN, OUTD, SE, REM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1342,7 +1343,7 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   int64_t per = sms / ntn;  // CTAs per n-tile
   if (per > units) per = units;
   if (per < 1) per = 1;
-  oz_gemm_kernel<S, AMN, OUTD, SE><<<static_cast<unsigned>(per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, tb);
+  oz_gemm_kernel<S, AMN, OUTD, SE, REM><<<static_cast<unsigned>(per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, tb);
   return cudaGetLastError();
 }
 
@@ -1442,7 +1443,7 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
   const bool amap = p.a_mn ? oz_encode_mn(&ta, p.xs, p.L, p.n, p.R, S * p.nx)
                            : oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS);
   if (!amap) return cudaErrorInvalidValue;
-  if (S == 7 && p.Kp <= kOzMaxNRes && oz_pair_enabled()) {  // CTA-pair MMAs (§4e): E chunks as 32-row pieces of one digit
+  if (S == 7 && p.Kp <= kOzMaxNRes && p.remap.world == 0 && oz_pair_enabled()) {  // CTA-pair MMAs (§4e): E chunks as 32-row pieces of one digit
     if (!oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, 32, 1)) return cudaErrorInvalidValue;
     if (p.a_mn) {
       if (p.n_next > 0) return oz_gemm_pair_go<true, true>(p, st, ta, tb);
