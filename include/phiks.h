@@ -211,7 +211,7 @@ phiks_status phiks_set_profiling(phiks_handle h, int on);
      digits, split with exponent bounds (reading R15; the
      environment variable PHIKS_CHAIN=0 restores per-mode splits);
    PHIKS_GEMM_AUTO (default, or the PHIKS_GEMM environment variable "dmma" /
-     "i8" / "auto" at create): the int8 kernel for products with n_μ ≥ 192 on
+     "i8" / "auto" at create): the int8 kernel for products with n_μ ≥ 128 on
      tensors of N ≥ 2^20 elements, where it is faster.  Invalidates the handle's captured
      graphs.  PHIKS_ERR_ARG for an unknown path. */
 #define PHIKS_GEMM_AUTO 0

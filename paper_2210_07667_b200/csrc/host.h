@@ -327,8 +327,9 @@ struct Exec {
     if (in_expm || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA) return false;
     if (rm && rm->world > kMaxRanks) return false;
     if (!ozaki_supported(L, n, R, kOzDigits)) return false;
-    // auto: where it measured faster (configs[2], n = 128: DMMA 1.00 ms vs int8 1.02 ms per apply)
-    if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 192 || L * R * n < (int64_t(1) << 20))) return false;
+    // auto: where it measured faster (configs[2], n = 128: int8 chained 0.93 ms vs DMMA 0.99 ms per
+    // apply; below n = 128 or 2^20 elements the launches are too small for the digit splits to pay)
+    if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 128 || L * R * n < (int64_t(1) << 20))) return false;
     std::set<int> groups;
     for (const auto& t : terms) {
       if (t.cswap || t.outs.size() != 1 || !t.outs[0].srcs.empty()) return false;
@@ -443,7 +444,7 @@ struct Exec {
       const int64_t R = N / (L * n);
       if (!ozaki_supported(L, n, R, kOzDigits) || n % 16 != 0) return false;
       if (mu > 0 && (L % 128 != 0 || L >= (int64_t(1) << 31) || R >= (int64_t(1) << 31))) return false;
-      if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 192 || N < (int64_t(1) << 20))) return false;
+      if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 128 || N < (int64_t(1) << 20))) return false;
       L *= n;
     }
     std::set<int> groups;  // last mode: one plain output per operator, distinct groups
