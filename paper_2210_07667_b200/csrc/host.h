@@ -324,9 +324,11 @@ struct Exec {
   bool ozaki_route(int64_t L, int n, int64_t R, const Terms& terms, const Remap* rm) const {
     // slab-sharded handles (local modes and the two peer-store stages) take it too; complex
     // handles and the exponential stage's small GEMMs stay on DMMA
-    if (in_expm || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA) return false;
+    if (in_expm || h->gemm_path == PHIKS_GEMM_DMMA) return false;
     if (rm && rm->world > kMaxRanks) return false;
     if (!ozaki_supported(L, n, R, kOzDigits)) return false;
+    for (const auto& t : terms)
+      if (t.kcat && (2 * n > kOzMaxN || !terms[0].kcat)) return false;
     // auto: where it measured faster (configs[2], n = 128: int8 chained 0.93 ms vs DMMA 0.99 ms per
     // apply; below n = 128 or 2^20 elements the launches are too small for the digit splits to pay)
     if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 128 || L * R * n < (int64_t(1) << 20))) return false;
@@ -350,6 +352,7 @@ struct Exec {
       p.n = n;
       p.S = kOzDigits;
       if (rm) p.remap = *rm;
+      p.cplx_j = terms[i].kcat ? 1 : 0;
       size_t j = i;
       for (; j < terms.size() && p.nterms < kMaxTerms; ++j) {
         int xs = -1, es = -1;
@@ -368,7 +371,7 @@ struct Exec {
         }
         p.terms[p.nterms++] = OzakiTerm{xs, es, terms[j].outs[0].dst, terms[j].outs[0].beta};
       }
-      const size_t need = ozaki_workspace_bytes(L, n, R, p.S, p.nx, p.ne);
+      const size_t need = ozaki_workspace_bytes(L, n, R, p.S, p.nx, p.ne, p.cplx_j ? 2 * n : n);
       if (need > oz_ws_bytes) {
         oz_ws = ar->alloc_doubles(static_cast<int64_t>((need + 7) / 8));
         oz_ws_bytes = need;
@@ -554,6 +557,7 @@ struct Exec {
     int group;
     std::vector<Out> outs;
     int cswap = 0;  // complex: J applied to the accumulator (TermSpec::cswap)
+    int kcat = 0;   // complex μ ≥ 2 on the int8 path: M = [Re | Im] (n × 2n), fibres [x ; Jx]
   };
   void mode_launch(int64_t L, int n, int64_t R, const std::vector<LaunchTerm>& terms, const Remap* rm = nullptr) {
     if (!ok() || terms.empty()) return;
@@ -1114,6 +1118,21 @@ struct Exec {
         const int n = h->n[mu];
         const int64_t R = h->Nc / (L * n);
         std::vector<LaunchTerm> terms;
+        // complex μ ≥ 2 on the int8 path (plain outputs only): DESIGN.md §4f
+        bool cplx_i8 = cx && mu > 0;
+        if (cplx_i8) {
+          std::vector<LaunchTerm> probe(1);
+          probe[0].kcat = 1;
+          probe[0].outs.push_back(Out{nullptr, 1.0, {}});
+          cplx_i8 = ozaki_route(2 * L, n, R, probe, nullptr);
+          for (size_t b = c0; b < c1 && cplx_i8; ++b) {
+            const TuckerItem& it = items[b];
+            if (mu == d - 1 && (it.outs.size() != 1 || !it.outs[0].srcs.empty())) cplx_i8 = false;
+          }
+          std::set<int> gs;
+          for (size_t b = c0; b < c1 && cplx_i8; ++b)
+            if (mu == d - 1 && !gs.insert(items[b].group).second) cplx_i8 = false;
+        }
         for (size_t b = c0; b < c1; ++b) {
           const TuckerItem& it = items[b];
           LaunchTerm t;
@@ -1128,7 +1147,11 @@ struct Exec {
             if (it.in_scale != 1.0)
               for (Out& o : t.outs) o.beta *= it.in_scale;
           }
-          if (cx && mu > 0) {
+          if (cx && mu > 0 && cplx_i8) {  // one int8 product with K = 2n: [Re M | Im M]·[x ; Jx]
+            t.M = complex_parts(it.mats[mu], n).first;
+            t.kcat = 1;
+            terms.push_back(std::move(t));
+          } else if (cx && mu > 0) {
             const auto parts = complex_parts(it.mats[mu], n);
             LaunchTerm ti = t;
             t.M = parts.first;
@@ -1163,8 +1186,9 @@ struct Exec {
   std::pair<const double*, const double*> complex_parts(const double* Rm, int n) {
     auto itp = cparts.find(Rm);
     if (itp != cparts.end()) return itp->second;
-    double* mr = ar->alloc_doubles(static_cast<int64_t>(n) * n);
-    double* mi = ar->alloc_doubles(static_cast<int64_t>(n) * n);
+    // contiguous: [Re M | Im M] is the n × 2n matrix of the int8 complex products (§4f)
+    double* mr = ar->alloc_doubles(2 * static_cast<int64_t>(n) * n);
+    double* mi = mr + static_cast<int64_t>(n) * n;
     emit("complex_parts", [Rm, n, mr, mi](cudaStream_t s) { return launch_complex_parts(Rm, n, mr, mi, s); });
     cparts[Rm] = {mr, mi};
     return {mr, mi};

@@ -135,12 +135,19 @@ __global__ void __launch_bounds__(256) oz_split_x_kernel(const OzakiParams p) {
   }
   __syncthreads();
   int8_t* xs = p.xs + static_cast<int64_t>(slot) * S * C * Kp;
+  // complex products (cplx_j): fibre f is [x_f ; (Jx)_f], (Jx)_f = −x_{f+1} for the real part
+  // (f even), +x_{f−1} for the imaginary part (f odd); the blocks start at even fibres
+  const int K = p.cplx_j ? 2 * n : n;
+  auto val = [&](int f, int k) -> double {
+    if (k < n) return tile[f * P + k];
+    return (f & 1) ? tile[(f - 1) * P + k - n] : -tile[(f + 1) * P + k - n];
+  };
   for (int f = warp; f < nf; f += 8) {
     const int64_t c = c0 + f;
     double m = 0.0;
     bool bad = false;
-    for (int k = lane; k < n; k += 32) {
-      const double v = tile[f * P + k];
+    for (int k = lane; k < K; k += 32) {
+      const double v = val(f, k);
       m = fmax(m, fabs(v));
       bad |= !isfinite(v);
     }
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(256) oz_split_x_kernel(const OzakiParams p) {
     for (int k0 = 4 * lane; k0 < Kp; k0 += 128) {
       double v[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = (k0 + q < n && !bad) ? tile[f * P + k0 + q] : 0.0;
+      for (int q = 0; q < 4; ++q) v[q] = (k0 + q < K && !bad) ? val(f, k0 + q) : 0.0;
       uint32_t pk[S];
       split4<S>(v, ex, pk);
 #pragma unroll
@@ -209,9 +216,10 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (j >= n) return;
+  const int K = p.cplx_j ? 2 * n : n;  // complex products: row j of [Re M | Im M]
   double m = 0.0, a1 = 0.0;
   bool bad = false;
-  for (int k = lane; k < n; k += 32) {
+  for (int k = lane; k < K; k += 32) {
     const double v = E[j + static_cast<int64_t>(k) * n];
     m = fmax(m, fabs(v));
     a1 += fabs(v);
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
   for (int k0 = 4 * lane; k0 < Kp; k0 += 128) {
     double v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = (k0 + q < n && !bad) ? E[j + static_cast<int64_t>(k0 + q) * n] : 0.0;
+    for (int q = 0; q < 4; ++q) v[q] = (k0 + q < K && !bad) ? E[j + static_cast<int64_t>(k0 + q) * n] : 0.0;
     uint32_t pk[S];
     split4<S>(v, ex, pk);
 #pragma unroll
@@ -1398,7 +1406,9 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    if (p.L == 1) {
+    if (p.cplx_j) {
+      oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
+    } else if (p.L == 1) {
       oz_split_x_contig_kernel<S><<<dim3(static_cast<unsigned>((C + 7) / 8), p.nx), 256, 0, st>>>(p);
     } else if (p.L % 32 == 0 && p.n <= 256 && p.Kp >= 128 && oz_split_tma_ok(p)) {
       static bool tattr = false;
@@ -1471,8 +1481,9 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
 
 }  // namespace
 
-size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne) {
-  const int64_t C = L * R, Kp = (n + kOzBK - 1) / kOzBK * kOzBK;
+size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne, int K) {
+  if (K <= 0) K = n;
+  const int64_t C = L * R, Kp = (K + kOzBK - 1) / kOzBK * kOzBK;
   auto al = [](size_t b) { return (b + 1023) & ~size_t(1023); };
   return al(static_cast<size_t>(nx) * S * C * Kp) + al(static_cast<size_t>(nx) * C * 8) +
          al(static_cast<size_t>(ne) * S * n * Kp) + 2 * al(static_cast<size_t>(ne) * n * 8) +
@@ -1481,7 +1492,8 @@ size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne)
 
 void ozaki_bind_workspace(OzakiParams& p, void* ws) {
   const int64_t C = p.L * p.R;
-  p.Kp = (p.n + kOzBK - 1) / kOzBK * kOzBK;
+  const int K = p.cplx_j ? 2 * p.n : p.n;
+  p.Kp = (K + kOzBK - 1) / kOzBK * kOzBK;
   auto al = [](size_t b) { return (b + 1023) & ~size_t(1023); };
   char* w = static_cast<char*>(ws);
   p.xs = reinterpret_cast<int8_t*>(w);

@@ -145,12 +145,14 @@ struct OzakiParams {
   int* ecol;     // [ne][n] (ee_j − 30) − b_j (INT_MIN: non-finite row), the digit epilogue's column shift
   int* eext;     // [3][ne] min_j b_j, max_j b_j, any non-finite row (chained modes' fast-path test)
   int a_mn;      // 1: xs holds [nx][S][L·n·R] digit planes in the fp64 layout (MN-major A, L % 128 == 0)
+  int cplx_j;    // complex μ ≥ 2 product: fibres [x ; Jx] of length K = 2n against
+                 // E = [Re M | Im M] (n × 2n, column-major, Im M right after Re M), so y = Re M·x + J·Im M·x
   int n_next;    // chained: n_{μ+1} (0: plain fp64 outputs)
   int dbg;       // timing experiments only (PHIKS_OZ_DBG); 0 in production
   Remap remap;   // slab-sharded stage (world > 0): fp64 outputs go to the owner rank; out = byte offset
 };
 bool ozaki_supported(int64_t L, int n, int64_t R, int S);
-size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne);
+size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne, int K = 0);  // K: contraction (0: n)
 void ozaki_bind_workspace(OzakiParams& p, void* ws);  // sets Kp and the workspace pointers
 cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_x = true, bool split_e = true,
                               bool gemm = true);

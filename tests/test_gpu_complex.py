@@ -123,3 +123,29 @@ def test_complex_validation_operator_d6():
         V = np.multiply.outer(V, f)
     pb = W.Problem("validation_d6", (n,) * d, [A] * d, 1.0, "same", (0, 1, 2, 3), [V], 1)
     run_and_compare(pb)
+
+
+# ---- complex handles on the int8 tensor-core path: mode 1 through the 2n × 2n
+# real form, modes μ ≥ 2 as one product with K = 2n, [Re M | Im M]·[x ; Jx] ----
+@pytest.mark.parametrize("dims,mode", [((40, 48, 24), "same"), ((64, 150), "lincomb"), ((33, 130, 20), "same"),
+                                       ((128, 96), "same")])
+def test_complex_int8_path(dims, mode):
+    seed = 1700 + sum(dims)
+    fac = W.random_factors(dims, seed=seed, scale=4.0, complex_=True)
+    ells = (0, 1, 2) if mode == "same" else (0, 1, 2, 3)
+    vs = [W.random_tensor(dims, seed=seed + 1 + k, complex_=True) for k in range(1 if mode == "same" else len(ells))]
+    pb = W.Problem(f"ci8{dims}{mode}", dims, fac, 0.6, mode, ells, vs, 2)
+    op = PhiKS(pb.A)
+    op.set_gemm_path("i8")
+    outs = op.apply(pb.tau, pb.ells, [cdev(v) for v in pb.vs], mode=pb.mode, n_scales=pb.n_scales)
+    torch.cuda.synchronize()
+    assert op.stats()["i8_mode_launches"] > 0
+    ref = O.phiks(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, n_scales=pb.n_scales)
+    for j in range(pb.n_scales):
+        if pb.mode == "same":
+            for i, ell in enumerate(pb.ells):
+                e = rel2(outs[j * len(pb.ells) + i].cpu().numpy(), W.as_flat(ref.out[(ell, j)]))
+                assert e <= 1e-12, (pb.name, ell, j, e)
+        else:
+            e = rel2(outs[j].cpu().numpy(), W.as_flat(ref.out[j]))
+            assert e <= 1e-12, (pb.name, j, e)
