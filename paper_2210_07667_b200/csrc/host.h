@@ -888,6 +888,34 @@ struct Exec {
     gv[0] = 2;
     for (int mu = 0; mu < d; ++mu) gv[mu + 1] = h->gn[mu];
     // one complex μ-mode product on the local layout whose dims are dims[0..d-1]
+    // with rm set (a transposition stage, μ ≥ 2): one int8 product with K = 2n (§4f) whose
+    // epilogue stores straight into the owners' regions at byte offsets off0 + b·sym_slot;
+    // returns false when that route does not apply (the caller then copies)
+    auto cproduct_remote = [&](int mu, const int* dims, std::vector<const double*> in,
+                               std::vector<const double*> mats, const Remap& rm, size_t off0) -> bool {
+      if (mu == 0) return false;
+      int64_t Lc = 1, Nc = 1;
+      for (int k = 0; k < d; ++k) Nc *= dims[k];
+      for (int k = 0; k < mu; ++k) Lc *= dims[k];
+      const int n = dims[mu];
+      const int64_t R = Nc / (Lc * n);
+      std::vector<LaunchTerm> probe(1);
+      probe[0].kcat = 1;
+      probe[0].outs.push_back(Out{nullptr, 1.0, {}});
+      if (!ozaki_route(2 * Lc, n, R, probe, &rm)) return false;
+      std::vector<LaunchTerm> terms;
+      for (size_t b = 0; b < nb; ++b) {
+        LaunchTerm t;
+        t.in = in[b];
+        t.group = static_cast<int>(b);
+        t.M = complex_parts(mats[b], n).first;
+        t.kcat = 1;
+        t.outs.push_back(Out{reinterpret_cast<double*>(off0 + b * h->sym_slot), 1.0, {}});
+        terms.push_back(std::move(t));
+      }
+      mode_launch(2 * Lc, n, R, terms, &rm);
+      return true;
+    };
     auto cproduct = [&](int mu, const int* dims, std::vector<const double*> in, std::vector<double*> out,
                         std::vector<const double*> mats) {
       int64_t Lc = 1, Nc = 1;
@@ -920,7 +948,7 @@ struct Exec {
       else
         mode_launch(2 * Lc, n, R, terms);
     };
-    auto remap_copy = [&](const ShardStage& s, const double* src, size_t dst_off) {
+    auto remap_of_stage = [&](const ShardStage& s) {
       Remap r{};
       r.world = P;
       r.cq = static_cast<int>(s.n / P);
@@ -933,6 +961,10 @@ struct Exec {
         r.kroff[k] = s.kroff[k];
         r.base[k] = h->peer[k];
       }
+      return r;
+    };
+    auto remap_copy = [&](const ShardStage& s, const double* src, size_t dst_off) {
+      const Remap r = remap_of_stage(s);
       const int64_t L = s.L, R = s.R;
       const int n = static_cast<int>(s.n);
       emit("remap_copy", [src, L, n, R, dst_off, r](cudaStream_t st2) {
@@ -964,9 +996,12 @@ struct Exec {
         outv[b] = scr[ping][b];
         mats[b] = items[b].mats[d - 2];
       }
-      cproduct(d - 2, dimsS, cur, outv, mats);
       const ShardStage s0 = shard_stage(d + 1, gv, rk, P, 0);
-      for (size_t b = 0; b < nb; ++b) remap_copy(s0, outv[b], kCtrlBytes + b * h->sym_slot);
+      // the stage's (L, n, R) in the real view (2, n_1, …) is the K = 2n product's view
+      if (!cproduct_remote(d - 2, dimsS, cur, mats, remap_of_stage(s0), kCtrlBytes)) {
+        cproduct(d - 2, dimsS, cur, outv, mats);
+        for (size_t b = 0; b < nb; ++b) remap_copy(s0, outv[b], kCtrlBytes + b * h->sym_slot);
+      }
       ping ^= 1;
     }
     barrier();
@@ -983,9 +1018,11 @@ struct Exec {
         outv[b] = scr[ping][b];
         mats[b] = items[b].mats[d - 1];
       }
-      cproduct(d - 1, dimsT, in, outv, mats);
       const ShardStage s1 = shard_stage(d + 1, gv, rk, P, 1);
-      for (size_t b = 0; b < nb; ++b) remap_copy(s1, outv[b], kCtrlBytes + (kShardChunk + b) * h->sym_slot);
+      if (!cproduct_remote(d - 1, dimsT, in, mats, remap_of_stage(s1), kCtrlBytes + kShardChunk * h->sym_slot)) {
+        cproduct(d - 1, dimsT, in, outv, mats);
+        for (size_t b = 0; b < nb; ++b) remap_copy(s1, outv[b], kCtrlBytes + (kShardChunk + b) * h->sym_slot);
+      }
     }
     barrier();
     int64_t nsum = 0;

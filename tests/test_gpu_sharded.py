@@ -211,3 +211,28 @@ def test_sharded_int8_path(dims, world, mode):
     single, _ = run_single(pb)
     for a, b in zip(outs, single):
         assert rel2(a, b) <= 1e-13
+
+
+@pytest.mark.parametrize("dims,world,mode", [((6, 8, 8), 2, "same"), ((5, 9, 7), 3, "lincomb"),
+                                             ((40, 66, 48), 4, "same"), ((3, 4, 5, 8), 4, "lincomb")])
+def test_sharded_complex_int8(dims, world, mode):
+    # complex sharded handles on the int8 path: local K = 2n products, and the two transposition
+    # stages as K = 2n products whose epilogue stores into the owners (no copy pass, §4f)
+    fac = W.random_factors(dims, seed=3 + sum(dims), scale=3.0, complex_=True)
+    ells = (0, 1, 2)
+    vs = [W.random_tensor(dims, seed=21 + k, complex_=True) for k in range(1 if mode == "same" else 3)]
+    pb = W.Problem(f"cplx_shard_i8_{dims}_{world}", dims, fac, 0.7, mode, ells, vs, 2)
+    ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
+    ShardedPhiKS.connect_local(ranks)
+    for r in ranks:
+        r.set_gemm_path("i8")
+    flat = [W.as_flat(v) for v in pb.vs]
+    vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, world, dims)[r])).to(DEV) for x in flat]
+            for r in range(world)]
+    outs = apply_ranks_serial(ranks, pb.tau, pb.ells, vecs, mode=pb.mode, n_scales=pb.n_scales)
+    torch.cuda.synchronize()
+    assert all(r.stats()["i8_mode_launches"] > 0 for r in ranks)
+    gathered = [torch.cat([outs[r][i] for r in range(world)]).cpu().numpy() for i in range(len(outs[0]))]
+    for r in ranks:
+        r.close()
+    compare_oracle(pb, gathered, 2)
