@@ -296,20 +296,21 @@ __global__ void __launch_bounds__(256) oz_chain_kernel(const OzakiParams p) {
         t = (isnan(t) || isnan(u)) ? qnan : fmax(t, u);
       }
       smx[lane] = t;
-      if (m < M) term.nmx[m] = t;
+      if (m < M && blockIdx.z == 0) term.nmx[m] = t;
     }
     __syncthreads();
   }
-  // ex'(c') for c' = l + L·j + L·n·r' over the chunk's (l, r') and every j
+  // ex'(c') for c' = l + L·j + L·n·r' over the chunk's (l, r') and this block's 64 columns j
   const double* eb = p.eb + static_cast<int64_t>(term.eslot) * n;
   const int cnt = static_cast<int>(M - m0 < 32 ? M - m0 : 32);
-  for (int idx = threadIdx.x; idx < 32 * n; idx += 256) {
+  const int jb = blockIdx.z * 64, jc = n - jb < 64 ? n - jb : 64;
+  for (int idx = threadIdx.x; idx < 32 * jc; idx += 256) {
     int mi, j;
     if (L == 1) {
-      mi = idx / n;
-      j = idx - mi * n;
+      mi = idx / jc;
+      j = jb + idx - mi * jc;
     } else {
-      j = idx >> 5;
+      j = jb + (idx >> 5);
       mi = idx & 31;
     }
     if (mi >= cnt) continue;
@@ -1446,7 +1447,7 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
   if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
   if (split_e && p.n_next > 0 && p.nterms > 0) {  // next-mode exponent bounds (chained modes)
     const int64_t m = C / p.n_next;
-    oz_chain_kernel<<<dim3(static_cast<unsigned>((m + 31) / 32), p.nterms), 256, 0, st>>>(p);
+    oz_chain_kernel<<<dim3(static_cast<unsigned>((m + 31) / 32), p.nterms, (p.n + 63) / 64), 256, 0, st>>>(p);
   }
   if (p.nterms == 0 || !gemm) return cudaGetLastError();
   CUtensorMap ta, tb;
