@@ -181,12 +181,33 @@ __global__ void __launch_bounds__(256) oz_split_x_contig_kernel(const OzakiParam
   double v[kOzMaxN / 128][4];
   double m = 0.0;
   bool bad = false;
+  if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(p.x[slot]) & 15) == 0) {  // 16-byte aligned fibers: two 16-byte loads per lane and chunk
+#pragma unroll
+    for (int i = 0; i < kOzMaxN / 128; ++i) {
+      const int k = 128 * i + 4 * lane;
+      double2 a = make_double2(0.0, 0.0), b = a;
+      if (k < n) {
+        a = __ldcs(reinterpret_cast<const double2*>(src + k));
+        b = __ldcs(reinterpret_cast<const double2*>(src + k + 2));
+      }
+      v[i][0] = a.x;
+      v[i][1] = a.y;
+      v[i][2] = b.x;
+      v[i][3] = b.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kOzMaxN / 128; ++i)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = 128 * i + 4 * lane + q;
+        v[i][q] = k < n ? __ldg(src + k) : 0.0;
+      }
+  }
 #pragma unroll
   for (int i = 0; i < kOzMaxN / 128; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int k = 128 * i + 4 * lane + q;
-      v[i][q] = k < n ? __ldg(src + k) : 0.0;
       m = fmax(m, fabs(v[i][q]));
       bad |= !isfinite(v[i][q]);
     }
