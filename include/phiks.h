@@ -208,16 +208,42 @@ phiks_status phiks_set_profiling(phiks_handle h, int on);
      (real handles, sharded or not, n_μ ≤ 256, plain outputs), DMMA elsewhere;
      when every mode of a Tucker batch qualifies (n_μ % 16 == 0, L_μ % 128 == 0
      for μ ≥ 2) the modes run chained: each product writes the next mode's
-     digits, split with exponent bounds (reading R15; the
-     environment variable PHIKS_CHAIN=0 restores per-mode splits);
-   PHIKS_GEMM_AUTO (default, or the PHIKS_GEMM environment variable "dmma" /
-     "i8" / "auto" at create): the int8 kernel for products with n_μ ≥ 128 on
+     digits, split with exponent bounds (reading R15) — see
+     PHIKS_OPT_CHAIN below;
+   PHIKS_GEMM_AUTO (default): the int8 kernel for products with n_μ ≥ 128 on
      tensors of N ≥ 2^20 elements, where it is faster.  Invalidates the handle's captured
      graphs.  PHIKS_ERR_ARG for an unknown path. */
 #define PHIKS_GEMM_AUTO 0
 #define PHIKS_GEMM_DMMA 1
 #define PHIKS_GEMM_I8 2
 phiks_status phiks_set_gemm_path(phiks_handle h, int path);
+
+/* Per-handle execution options (the library reads no environment variables).
+   Every value gives the same result up to rounding; they exist for A/B
+   measurements and tests.  Setting an option invalidates the handle's captured
+   graphs.  PHIKS_ERR_ARG for an unknown option or value.
+   PHIKS_OPT_SPLIT   where the quadrature weight-sum (Eq. (11)/(17), l.547-552,
+                     l.726-733) and the squaring recurrence (Eq. (12)/(18),
+                     l.554-563, l.734-746) are evaluated: 0 = in the last mode's
+                     epilogue of the Tucker launches (DMMA products; int8 batches
+                     with fused outputs fall back to DMMA), 1 = quadrature as a
+                     streaming pass, squaring fused, 2 (default) = both as one
+                     matrix-form streaming pass over the raw Tucker results.
+   PHIKS_OPT_CHAIN   int8 modes of a Tucker batch chained (R15):
+                     0 = off (each mode's output split with its own maxima),
+                     1 (default) = guarded: chained only when every factor τA_μ
+                     of the handle is a Metzler matrix (off-diagonal ≥ 0), whose
+                     exponentials are entrywise ≥ 0, so the exponent bound
+                     ‖e_j‖₁·max|x| is attained (no cancellation inside a row),
+                     2 = whenever the shapes allow (tests of the guard).
+   PHIKS_OPT_GRAPHS  1 (default) = capture device-memory applies of tensors up to
+                     2^22 elements as CUDA graphs and replay them; 0 = direct
+                     launches. */
+#define PHIKS_OPT_SPLIT 0
+#define PHIKS_OPT_CHAIN 1
+#define PHIKS_OPT_GRAPHS 2
+phiks_status phiks_set_option(phiks_handle h, int option, int value);
+phiks_status phiks_get_option(phiks_handle h, int option, int* value);
 
 /* Telemetry of the last phiks_apply on this handle. */
 phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out);

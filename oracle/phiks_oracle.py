@@ -188,9 +188,9 @@ def range_rectangle(factors: Sequence[np.ndarray]) -> Rect:
 # Remainder bound (§3.3 Eq. (21), l.905-960) and plan (l.809-875)
 # ---------------------------------------------------------------------------
 
-R_GRID = tuple(float(r) for r in np.geomspace(0.3, 10.0, 25))  # reading R3
+R_GRID = tuple(float(r) for r in np.geomspace(0.3, 6.0, 16))   # reading R3
 N_SIDE = 32                                                    # reading R4
-Q_MIN, Q_MAX, S_MAX = 2, 32, 60                                # reading R5
+Q_MIN, Q_MAX, S_MAX = 2, 12, 60                                # reading R5
 W_CAP = 256.0   # reading R5: scales with max|w| > W_CAP are infeasible for q ≤ Q_MAX
 SPECTRAL_SET_C = 1.0 + math.sqrt(2.0)                          # l.908 [CP17]
 
@@ -265,6 +265,27 @@ def tucker_count(mode: str, s: int, s_hat: int, q: int, p: int) -> int:
     """T(s,ŝ,q,p): Eq. (14) q+sp+ŝ (same vector, l.618-620) or Eq. (19)
     qp+sp+ŝ (linear combination, l.775-778)."""
     return (q + s * p + s_hat) if mode == "same" else (q * p + s * p + s_hat)
+
+
+def tucker_executed(mode: str, s: int, q: int, ells: Sequence[int], n_scales: int,
+                    has_v0: bool = False) -> int:
+    """Tucker operators phiks_same / phiks_lincomb below actually run (reading R9):
+    θ_q = 1 costs none (l.948-952); at the last squaring step j = 1 only the
+    combinations that are outputs are formed (l.953-956 "few other
+    shrewdnesses"): Ψ_p alone for a linear combination, the requested φ_ℓ for
+    the same vector.  Linear combination without v_0, ŝ = 1:
+    (q−2)p + sp + 1, the T of PAPER.md Table 1 (l.1436-1446)."""
+    p = max(ells)
+    if p == 0:
+        return n_scales if (mode == "same" or has_v0) else 0
+    last = (sum(1 for e in ells if e >= 1) if mode == "same" else 1)
+    if mode == "same":
+        quad = q - 1
+        sq = (s - 1) * p + last if s >= 1 else 0
+        return quad + sq + (n_scales if 0 in ells else 0)
+    quad = (q - 1) * (p if s >= 1 else 1)
+    sq = (s - 1) * p + last if s >= 1 else 0
+    return quad + sq + (n_scales if has_v0 else 0)
 
 
 def q_for_s(mode: str, rect: Rect, p: int, norms: Sequence[float], delta: float, s: int,
@@ -367,6 +388,8 @@ def phiks_same(A: Sequence[np.ndarray], tau: float, V: np.ndarray, ells: Sequenc
         for j in range(s, 0, -1):
             new = [None] * (p + 1)
             for ell in range(p, 0, -1):
+                if j == 1 and ell not in ells:
+                    continue          # level 0 is output only (l.953-956)
                 acc = tucker(phi[ell], Es[j])
                 ops += 1
                 for k in range(1, ell + 1):
@@ -419,6 +442,8 @@ def phiks_lincomb(A: Sequence[np.ndarray], tau: float, vs: Dict[int, np.ndarray]
         psi = [None] + [zero.copy() for _ in range(p)]
         for i in range(plan.q):
             for ell in range(1, p + 1):
+                if s == 0 and ell != p:
+                    continue          # only Ψ_p^{(0)} is an output (l.953-956)
                 x = lincomb_nodes_input(theta[i], vs, p, s, ell, zero)
                 if nodeE[i] is None:
                     Tx = x
@@ -430,6 +455,8 @@ def phiks_lincomb(A: Sequence[np.ndarray], tau: float, vs: Dict[int, np.ndarray]
         for j in range(s, 0, -1):
             new = [None] * (p + 1)
             for ell in range(p, 0, -1):
+                if j == 1 and ell != p:
+                    continue          # only Ψ_p^{(0)} is an output (l.953-956, Table 1 T)
                 acc = tucker(psi[ell], Es[j])
                 ops += 1
                 for k in range(1, ell + 1):

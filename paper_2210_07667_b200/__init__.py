@@ -194,6 +194,18 @@ class PhiKS:
         """μ-mode-product path of the Tucker launches: "auto", "dmma" or "i8"."""
         _lib.check(_lib.load().phiks_set_gemm_path(self._h, self.GEMM_PATHS[path]), "phiks_set_gemm_path")
 
+    OPTIONS = {"split": 0, "chain": 1, "graphs": 2}
+
+    def set_option(self, name: str, value: int):
+        """Execution option of the handle (include/phiks.h PHIKS_OPT_*): "split" 0/1/2,
+        "chain" 0 (off) / 1 (guarded, default) / 2 (forced), "graphs" 0/1."""
+        _lib.check(_lib.load().phiks_set_option(self._h, self.OPTIONS[name], int(value)), "phiks_set_option")
+
+    def get_option(self, name: str) -> int:
+        v = ctypes.c_int()
+        _lib.check(_lib.load().phiks_get_option(self._h, self.OPTIONS[name], ctypes.byref(v)), "phiks_get_option")
+        return v.value
+
     def set_profiling(self, on: bool = True):
         _lib.check(_lib.load().phiks_set_profiling(self._h, 1 if on else 0), "phiks_set_profiling")
 

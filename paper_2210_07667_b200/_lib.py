@@ -93,6 +93,8 @@ def load() -> ctypes.CDLL:
     lib.phiks_apply_ranks_serial.argtypes = [P(vp), i, P(Request), i, P(vp), P(vp), vp]
     lib.phiks_wait.argtypes = [vp]
     lib.phiks_set_gemm_path.argtypes = [vp, i]
+    lib.phiks_set_option.argtypes = [vp, i, i]
+    lib.phiks_get_option.argtypes = [vp, i, P(i)]
     lib.phiks_mode_product_i8_workspace.argtypes = [i, P(i), i, i, i, P(ctypes.c_size_t)]
     lib.phiks_mode_product_i8.argtypes = [i, P(i), i, i, i, P(vp), P(vp), P(vp), vp, ctypes.c_size_t, vp]
     lib.phiks_create_complex.argtypes = [i, P(i), P(vp), P(vp)]
@@ -110,7 +112,8 @@ def load() -> ctypes.CDLL:
                  "phiks_create_sharded_blocks", "phiks_shard_layout_ex",
                  "phiks_create_sharded_complex", "phiks_create_blocks_complex",
                  "phiks_create_sharded_blocks_complex",
-                 "phiks_mode_product_i8_workspace", "phiks_mode_product_i8", "phiks_set_gemm_path"):
+                 "phiks_mode_product_i8_workspace", "phiks_mode_product_i8", "phiks_set_gemm_path",
+                 "phiks_set_option", "phiks_get_option"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

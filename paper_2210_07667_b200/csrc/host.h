@@ -60,6 +60,7 @@ struct Factor {
   int n = 0;
   double* dA = nullptr;   // device copy of A_f
   double norm1 = 0.0;    // ||A_f||_1
+  bool metzler = false;  // real factor with every off-diagonal entry ≥ 0 (chain guard, R15)
   plan::FactorRange fr{};
 };
 
@@ -93,6 +94,7 @@ struct phiks_ctx {
   void* ws_own = nullptr;
   size_t ws_own_bytes = 0;
   double* h_pinned = nullptr;  // pinned host scratch (norms)
+  int* h_barrier_err = nullptr;  // pinned copy of the sharded barrier's sticky error flag (lagging check)
   std::map<PlanKey, plan::Plan> plan_cache;
   phiks_stats stats{};
   // profiling: event pairs around μ-mode-product launches of the last apply
@@ -100,13 +102,16 @@ struct phiks_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> ev_flops;
   std::vector<char> ev_expm;  // 1: small-GEMM launch of the exponential stage; 2: int8 (§4c) GEMM, 3: its digit splits
-  // μ-mode-product path of the Tucker launches (phiks_set_gemm_path; PHIKS_GEMM env for the default)
-  int gemm_path = default_gemm_path();
-  static int default_gemm_path() {
-    const char* e = std::getenv("PHIKS_GEMM");
-    if (e && std::strcmp(e, "dmma") == 0) return PHIKS_GEMM_DMMA;
-    if (e && std::strcmp(e, "i8") == 0) return PHIKS_GEMM_I8;
-    return PHIKS_GEMM_AUTO;
+  // μ-mode-product path of the Tucker launches (phiks_set_gemm_path)
+  int gemm_path = PHIKS_GEMM_AUTO;
+  // execution options (phiks_set_option)
+  int opt_split = 2;   // PHIKS_OPT_SPLIT
+  int opt_chain = 1;   // PHIKS_OPT_CHAIN: 0 off, 1 guarded (Metzler factors), 2 forced
+  int opt_graphs = 1;  // PHIKS_OPT_GRAPHS
+  bool chain_safe() const {  // every factor Metzler: exponentials entrywise ≥ 0 (τ > 0)
+    for (const auto& F : factors)
+      if (!F.metzler) return false;
+    return !factors.empty();
   }
   int ev_used = 0;
   // ---- slab sharding along the outermost mode (phiks_create_sharded) ----
@@ -426,17 +431,13 @@ struct Exec {
   double* oz_ex[2] = {nullptr, nullptr};
   double* oz_mx = nullptr;  // Mx of the current product (read by its own epilogue only)
   size_t oz_chain_cap = 0;  // Tucker operators the buffers hold
-  static bool chain_env() {
-    static const bool on = [] {
-      const char* e = std::getenv("PHIKS_CHAIN");
-      return !(e && std::strcmp(e, "0") == 0);
-    }();
-    return on;
-  }
   // modes 0..mlast of the batch chained (mlast = d − 1: whole operators; sharded handles stop at
   // the mode-(d−1) stage, whose epilogue stores into the owner ranks)
   bool ozaki_chain_route(const std::vector<TuckerItem>& items, size_t c0, size_t c1, int mlast = -1) const {
-    if (in_expm || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA || !chain_env()) return false;
+    if (in_expm || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA || h->opt_chain == 0) return false;
+    // guard (R15): the exponent bound ‖e_j‖₁·max|x| is attained when every exponential is
+    // entrywise nonnegative; rows with cancellation would lose bits against it
+    if (h->opt_chain == 1 && !h->chain_safe()) return false;
     const int d = h->d;
     if (mlast < 0) mlast = d - 1;
     if (d < 2 || mlast < 1) return false;
@@ -1334,13 +1335,9 @@ struct ApplyRun {
     host_async = req->mem_kind == PHIKS_MEM_HOST_ASYNC;
     N = h->N;
     tbytes = static_cast<size_t>(N) * sizeof(double);
-    static const int split_mode = [] {
-      // default 2: quadrature sums and squaring recurrences as a streaming pass
-      // (measured faster on B200 than the fused epilogue); 0 = fused
-      const char* e = getenv("PHIKS_SPLIT");
-      return e ? atoi(e) : 2;
-    }();
-    split = split_mode;
+    // default 2: quadrature sums and squaring recurrences as a streaming pass
+    // (measured faster on B200 than the fused epilogue); 0 = fused
+    split = h->opt_split;
     jobs.assign(nb, Job{});
     for (int b = 0; b < nb; ++b) {
       jobs[b].mode = req->mode;

@@ -792,22 +792,9 @@ static bool launch_tma(const ModeParams& p, cudaStream_t st, cudaError_t* err) {
   return true;
 }
 
-// PHIKS_TILE (A/B experiments, scripts/sweep_run.sh): 0 = the default below;
-// 1 = the cp.async kernel only (the pre-TMA baseline); 10 = TMA 128×128 tiles,
-// 8 warps, 1 CTA/SM; 12 = TMA 128×64 tiles, 3 stages.  DESIGN.md §4 and
-// profiles/r01_tile_sweep.jsonl, r01_kernel_experiments.json record the sweep.
-static int tile_variant() {
-  static const int v = [] {
-    const char* e = getenv("PHIKS_TILE");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
   if (p.ngroups == 0) return cudaSuccess;
   const int64_t Mtot = p.L * p.R;
-  const int var = tile_variant();
   if (p.remap.world > 0 && p.n > 64) {  // slab-sharded peer-store epilogue: default tile only
     cudaError_t err = cudaSuccess;
     if (launch_tma<64, 128, 16, 2, 2, 4, 2, true>(p, st, &err)) return err;
@@ -824,20 +811,16 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
                                          : launch_tma<64, 64, 16, 2, 2, 4, 3, false, true>(p, st, &err);
       if (done) return err;
     }
-  } else if (p.n > 64 && var != 1) {
+  } else if (p.n > 64) {
+    // tile sweep (128×128 / 8 warps, 128×64 / 3 stages, cp.async only) measured slower:
+    // DESIGN.md §4, profiles/r01_tile_sweep.jsonl
     cudaError_t err = cudaSuccess;
     bool done = false;
-    if (var == 10) {
-      done = launch_tma<128, 128, 16, 2, 4, 5, 1>(p, st, &err);
-    } else if (var == 12) {
-      done = launch_tma<128, 64, 16, 2, 2, 3, 2>(p, st, &err);
-    } else {
-      const int64_t units = ((Mtot + 63) / 64) * ((p.n + 127) / 128) * p.ngroups;
-      if (units >= 148 * 2)
-        done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);  // default: 2 CTAs/SM overlap epilogues
-      else  // less than a wave (e.g. the n×n GEMMs of the exponential stage): 64×64 tiles, 3 CTAs/SM
-        done = launch_tma<64, 64, 16, 2, 2, 4, 3>(p, st, &err);
-    }
+    const int64_t units = ((Mtot + 63) / 64) * ((p.n + 127) / 128) * p.ngroups;
+    if (units >= 148 * 2)
+      done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);  // default: 2 CTAs/SM overlap epilogues
+    else  // less than a wave (e.g. the n×n GEMMs of the exponential stage): 64×64 tiles, 3 CTAs/SM
+      done = launch_tma<64, 64, 16, 2, 2, 4, 3>(p, st, &err);
     if (done) return err;
   }
   // cp.async kernel: shapes TMA cannot take (odd n, odd or short L, misaligned pointers), n ≤ 64

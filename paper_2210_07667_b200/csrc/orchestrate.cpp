@@ -311,6 +311,9 @@ void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
         std::vector<std::vector<TuckerItem>> per_ell(p + 1);
         std::vector<TuckerItem> jitems;
         for (int ell = 1; ell <= p; ++ell) {
+          // s = 0: level 0 is the output level and only Ψ_p^{(0)} is an output
+          // (Table 1's lincomb T = (q−2)p + sp + 1, reading R9)
+          if (s == 0 && ell != p) continue;
           bool first = true;
           for (int i = 0; i < J.n_nodes; ++i) {
             std::vector<Src> comb;
@@ -392,6 +395,9 @@ void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
         const Job& jb = *J.jb;
         auto& state = J.state;
         for (int ell = p; ell >= 1; --ell) {
+          // level j−1 = 0 is output only: Ψ_p alone (linear combination), the
+          // requested φ_ℓ (same vector) — PAPER.md l.953-956, reading R9
+          if (j == 1 && (same ? !(jb.n_scales > 0 && jb.out_same[ell][0]) : ell != p)) continue;
           TuckerItem it;
           it.in = state[j][ell];
           mats_for(J, J.Es[j], it.mats);

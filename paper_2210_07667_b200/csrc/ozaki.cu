@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
         cur_term = term;
         ++bgen;
       }
-      if (tile > 0 && !(p.dbg & 1)) oz_mbar_wait(t_empty, (tile - 1) & 1);  // epilogue drained the accumulators
+      if (tile > 0) oz_mbar_wait(t_empty, (tile - 1) & 1);  // epilogue drained the accumulators
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       // fully unrolled over the digits: every MMA's column offset, N and instruction
       // descriptor are compile-time constants (the issue loop is a few uniform adds per MMA)
@@ -1013,260 +1013,6 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
-}
-
-// ---- CTA-pair GEMM (tcgen05.mma.cta_group::2) ----
-// The two CTAs of a cluster own adjacent 128-fiber tiles (UMMA M = 256) of the same
-// 64-row E tile.  Each MMA a_s × [b_t0 | … | b_t1-1] reads its A rows from the CTA
-// that owns them and the N = 64(t1 − t0) B rows half from each CTA: CTA r holds rows
-// [r·N/2, (r+1)·N/2) of the concatenation, so every chunk (t0, t1) the MMAs use is
-// stored per CTA as its half (7 chunks, 16 × 32 rows per 128-byte k-stage).  The
-// accumulator columns keep the 1-CTA layout (diagonal g at [64g, 64g + 64)), so the
-// epilogue is shared.  Per SM and k-step the tensor cores read 40 KB of A and 28 KB
-// of B from shared memory instead of 40 + 56 KB.
-// chunk c: digits [t0, t0 + m) of B; off = 32-row pieces of the chunks before it
-struct OzChunks {
-  static constexpr int NC = 7;
-  static constexpr int PIECES = 16;  // per CTA and k-stage
-  __host__ __device__ static constexpr int t0(int c) { return (c >= 1 && c <= 3) ? 4 : 0; }
-  __host__ __device__ static constexpr int m(int c) { return c == 0 ? 4 : (c <= 3 ? 4 - c : 7 - c); }
-  __host__ __device__ static constexpr int off(int c) {
-    return c == 0 ? 0 : c == 1 ? 4 : c == 2 ? 7 : c == 3 ? 9 : c == 4 ? 10 : c == 5 ? 13 : 15;
-  }
-  // chunks of digit s of A (S = 7): [0, min(4, 7 − s)) and [4, 7 − s)
-  __host__ __device__ static constexpr int first(int s) { return s <= 3 ? 0 : s; }
-  __host__ __device__ static constexpr int second(int s) { return s <= 2 ? s + 1 : -1; }
-};
-static_assert(OzChunks::off(6) + OzChunks::m(6) == OzChunks::PIECES, "chunk pieces");
-
-struct OzGeom2 {
-  static constexpr int S = 7;
-  static constexpr int A_BYTES = kOzBM * kOzBK;              // one digit × 128 fibers × 128 k
-  static constexpr int NST = 4;
-  static constexpr int E_KB = OzChunks::PIECES * 32 * kOzBK;  // 64 KB of chunk halves per k-stage
-  static constexpr int E_BYTES = (kOzMaxNRes / kOzBK) * E_KB;
-  static constexpr int SMEM = NST * A_BYTES + E_BYTES + 1024 + 512;
-  static constexpr int EPC = 32;
-  static constexpr int EPI_WARPS = 4 * kOzBN / EPC;
-  static constexpr int THREADS = 64 + EPI_WARPS * 32;
-  static_assert(SMEM <= 232448, "shared memory");
-};
-
-__device__ __forceinline__ uint32_t oz_cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t oz_mapa(const void* p, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(oz_smem_u32(p)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void oz_cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-// TMA load into this CTA's shared memory whose completion is counted on the pair
-// leader's barrier (shared::cluster address)
-__device__ __forceinline__ void oz_tma_load_4d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                                    uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-      "%4, %5}], [%6];\n" ::"r"(oz_smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void oz_mma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// arrive on the barrier at the same offset in both CTAs of the pair once the MMAs are done
-__device__ __forceinline__ void oz_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
-          oz_smem_u32(bar)),
-      "h"(static_cast<uint16_t>(3))
-      : "memory");
-}
-__device__ __forceinline__ void oz_mbar_arrive_remote(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__host__ __device__ constexpr uint32_t oz_idesc_pair(int bn, bool amn) {
-  return (2u << 4) | (1u << 7) | (1u << 10) | (amn ? (1u << 15) : 0u) | (static_cast<uint32_t>(bn >> 3) << 17) |
-         ((256u >> 4) << 24);
-}
-
-template <bool AMN, bool OUTD>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OzGeom2::THREADS, 1)
-    oz_gemm_pair_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
-                        const __grid_constant__ CUtensorMap te) {
-  using G = OzGeom2;
-  constexpr int S = G::S;
-  extern __shared__ uint8_t oz_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* eres = smem + G::NST * G::A_BYTES;
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(eres + G::E_BYTES);
-  uint64_t* a_empty = a_full + G::NST;
-  uint64_t* b_full = a_empty + G::NST;
-  uint64_t* b_empty = b_full + 1;
-  uint64_t* t_full = b_empty + 1;
-  uint64_t* t_empty = t_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = oz_cluster_rank();
-  const bool leader = rank == 0;
-  // pair schedule: pair k works on n-tile k % ntn, units q, q + Q, … over (term, 256-fiber tile)
-  const int ntn = (p.n + kOzBN - 1) / kOzBN;
-  const int pi = static_cast<int>(blockIdx.x >> 1);
-  const int nt = pi % ntn, q = pi / ntn, Q = static_cast<int>(gridDim.x >> 1) / ntn;
-  if (q >= Q) return;  // both CTAs of the pair leave together
-  const int64_t C = p.L * p.R;
-  const int64_t Mt2 = (C + 2 * kOzBM - 1) / (2 * kOzBM);
-  const int64_t units = Mt2 * p.nterms;
-  const int nk = p.Kp / kOzBK;
-
-  if (threadIdx.x == 0) {
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&te)) : "memory");
-    for (int s = 0; s < G::NST; ++s) {
-      oz_mbar_init(&a_full[s], 1);
-      oz_mbar_init(&a_empty[s], 1);
-    }
-    oz_mbar_init(b_full, 1);
-    oz_mbar_init(b_empty, 1);
-    oz_mbar_init(t_full, 1);
-    oz_mbar_init(t_empty, 2 * G::EPI_WARPS);  // the epilogue warps of both CTAs (leader's barrier)
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(oz_smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  oz_cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t a_full0 = oz_mapa(a_full, 0), b_full0 = oz_mapa(b_full, 0), t_empty0 = oz_mapa(t_empty, 0);
-
-  if (warp == 0) {
-    // ---- TMA producer of this CTA's operands (both CTAs); completions count on the leader ----
-    int cur_term = -1, bgen = 0, it = 0;
-    for (int64_t u = q; u < units; u += Q) {
-      const int term = static_cast<int>(u / Mt2);
-      const int64_t mt = (u % Mt2) * 2 + rank;
-      if (term != cur_term) {  // this CTA's halves of the E chunks of (term, n-tile)
-        if (bgen > 0) oz_mbar_wait(b_empty, (bgen - 1) & 1);
-        if (oz_elect()) {
-          if (leader) oz_mbar_expect_tx(b_full, static_cast<unsigned>(2 * nk * G::E_KB));
-          const int es = p.terms[term].eslot;
-          for (int kb = 0; kb < nk; ++kb)
-            for (int c = 0; c < OzChunks::NC; ++c) {
-              const int mm = OzChunks::m(c);
-              for (int v = 0; v < mm; ++v) {
-                const int piece = static_cast<int>(rank) * mm + v;  // 32-row piece of the concatenation
-                oz_tma_load_4d_pair(eres + kb * G::E_KB + (OzChunks::off(c) + v) * 32 * kOzBK, &te, kb * kOzBK,
-                                    nt * kOzBN + 32 * (piece & 1), OzChunks::t0(c) + (piece >> 1), es, b_full0);
-              }
-            }
-        }
-        __syncwarp();
-        cur_term = term;
-        ++bgen;
-      }
-      const int xs = p.terms[term].xslot;
-      for (int kb = 0; kb < nk; ++kb)
-        for (int s = 0; s < S; ++s, ++it) {
-          const int st = it % G::NST;
-          if (it >= G::NST) oz_mbar_wait(&a_empty[st], ((it / G::NST) & 1) ^ 1);
-          if (oz_elect()) {
-            if (leader) oz_mbar_expect_tx(&a_full[st], 2 * G::A_BYTES);
-            if (AMN) {
-              const int64_t c0 = mt * kOzBM;
-              oz_tma_load_4d_pair(smem + st * G::A_BYTES, &ta, static_cast<int>(c0 % p.L), kb * kOzBK,
-                                  static_cast<int>(c0 / p.L), xs * S + s, a_full0 + 8u * st);
-            } else {
-              oz_tma_load_4d_pair(smem + st * G::A_BYTES, &ta, kb * kOzBK, static_cast<int>(mt * kOzBM), s, xs,
-                                  a_full0 + 8u * st);
-            }
-          }
-          __syncwarp();
-        }
-    }
-  } else if (warp == 1) {
-    if (leader) {
-      // ---- MMA issuer of the pair ----
-      const uint64_t a_desc0 = AMN ? oz_desc_mn_sw128(smem) : oz_desc_sw128(smem), e_desc0 = oz_desc_sw128(eres);
-      constexpr uint64_t a_kstep = AMN ? (kOzUK * kOzBM) >> 4 : kOzUK >> 4;
-      int cur_term = -1, bgen = 0, it = 0, tile = 0;
-      for (int64_t u = q; u < units; u += Q, ++tile) {
-        const int term = static_cast<int>(u / Mt2);
-        if (term != cur_term) {
-          if (bgen > 0) {
-            if (oz_elect()) oz_commit_pair(b_empty);
-            __syncwarp();
-          }
-          oz_mbar_wait(b_full, bgen & 1);
-          cur_term = term;
-          ++bgen;
-        }
-        if (tile > 0) oz_mbar_wait(t_empty, (tile - 1) & 1);  // both epilogues drained the accumulators
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        for (int kb = 0; kb < nk; ++kb) {
-          const uint64_t ed0 = e_desc0 + static_cast<uint64_t>((kb * G::E_KB) >> 4);
-#pragma unroll
-          for (int s = 0; s < S; ++s, ++it) {
-            const int st = it & (G::NST - 1);
-            oz_mbar_wait(&a_full[st], (it / G::NST) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint64_t ad0 = a_desc0 + static_cast<uint64_t>((st * G::A_BYTES) >> 4);
-            if (oz_elect()) {
-#pragma unroll
-              for (int kk = 0; kk < kOzBK / kOzUK; ++kk) {
-                const uint32_t accf = (kb > 0 || s > 0 || kk > 0) ? 1u : 0u;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const int c = h == 0 ? OzChunks::first(s) : OzChunks::second(s);
-                  if (c < 0) continue;
-                  oz_mma_pair(tmem + static_cast<uint32_t>((s + OzChunks::t0(c)) * kOzBN), ad0 + kk * a_kstep,
-                              ed0 + static_cast<uint64_t>((OzChunks::off(c) * 32 * kOzBK) >> 4) +
-                                  static_cast<uint64_t>(kk * 2),
-                              oz_idesc_pair(64 * OzChunks::m(c), AMN), accf);
-                }
-              }
-              oz_commit_pair(&a_empty[st]);
-            }
-            __syncwarp();
-          }
-        }
-        if (oz_elect()) oz_commit_pair(t_full);
-        __syncwarp();
-      }
-    }
-  } else {
-    // ---- epilogue warps of both CTAs: this CTA's 128 fibers of the pair's tile ----
-    const int wq = warp & 3, ch = (warp - 2) >> 2;
-    const uint32_t tl = tmem + (static_cast<uint32_t>(wq * 32) << 16) + ch * G::EPC;
-    int tile = 0;
-    for (int64_t u = q; u < units; u += Q, ++tile) {
-      const int term_i = static_cast<int>(u / Mt2);
-      const int64_t mt = (u % Mt2) * 2 + rank;
-      oz_epilogue_tile<S, OUTD, AMN, false, G::EPC>(p, term_i, mt * kOzBM + wq * 32 + lane, nt * kOzBN + ch * G::EPC, tl, t_full, tile & 1,
-                                [&] {
-                                  if (lane == 0) oz_mbar_arrive_remote(t_empty0);
-                                });
-    }
-  }
-  if (p.remap.world > 0) __threadfence_system();
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  oz_cluster_sync();  // no MMA of the pair targets this CTA's TMEM any more
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
 }
 
 typedef CUresult (*OzEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1377,47 +1123,9 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   return cudaGetLastError();
 }
 
-template <bool AMN, bool OUTD>
-cudaError_t oz_gemm_pair_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& te) {
-  using G = OzGeom2;
-  static bool gattr = false;
-  static int sms = 0;
-  if (!gattr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(oz_gemm_pair_kernel<AMN, OUTD>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    gattr = true;
-  }
-  const int64_t C = p.L * p.R;
-  const int ntn = (p.n + kOzBN - 1) / kOzBN;
-  const int64_t units = ((C + 2 * kOzBM - 1) / (2 * kOzBM)) * p.nterms;
-  int64_t per = (sms / 2) / ntn;  // pairs per n-tile
-  if (per > units) per = units;
-  if (per < 1) per = 1;
-  oz_gemm_pair_kernel<AMN, OUTD><<<static_cast<unsigned>(2 * per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, te);
-  return cudaGetLastError();
-}
-
-// opt-in (PHIKS_OZ_PAIR=1): measured slower than the 1-CTA kernel on configs[3]
-bool oz_pair_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PHIKS_OZ_PAIR");
-    return e && std::strcmp(e, "1") == 0;
-  }();
-  return on;
-}
-
 template <int S>
 cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool split_e, bool gemm) {
-  static const int dbg = [] {
-    const char* e = std::getenv("PHIKS_OZ_DBG");
-    return e ? std::atoi(e) : 0;
-  }();
-  OzakiParams p = p0;
-  p.dbg = dbg;
+  const OzakiParams& p = p0;
   const int64_t C = p.L * p.R;
   if (split_x) {
     const size_t sm = static_cast<size_t>(32) * (p.n | 1) * sizeof(double);
@@ -1475,15 +1183,6 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
   const bool amap = p.a_mn ? oz_encode_mn(&ta, p.xs, p.L, p.n, p.R, S * p.nx)
                            : oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS);
   if (!amap) return cudaErrorInvalidValue;
-  if (S == 7 && p.Kp <= kOzMaxNRes && p.remap.world == 0 && oz_pair_enabled()) {  // CTA-pair MMAs (§4e): E chunks as 32-row pieces of one digit
-    if (!oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, 32, 1)) return cudaErrorInvalidValue;
-    if (p.a_mn) {
-      if (p.n_next > 0) return oz_gemm_pair_go<true, true>(p, st, ta, tb);
-      return oz_gemm_pair_go<true, false>(p, st, ta, tb);
-    }
-    if (p.n_next > 0) return oz_gemm_pair_go<false, true>(p, st, ta, tb);
-    return oz_gemm_pair_go<false, false>(p, st, ta, tb);
-  }
   if (!oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S)) return cudaErrorInvalidValue;
   if (p.Kp > kOzMaxNRes) {  // E streamed per k-block
     if (p.a_mn) {

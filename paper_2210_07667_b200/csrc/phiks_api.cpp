@@ -101,6 +101,13 @@ phiks_status create_impl(int d, const int* n, const double* const* A_host, bool 
         nrm = std::max(nrm, c);
       }
       F.norm1 = nrm;
+      F.metzler = !cplx;
+      for (int j = 0; j < F.n && F.metzler; ++j)
+        for (int i = 0; i < F.n; ++i)
+          if (i != j && !(A[i + static_cast<size_t>(j) * F.n] >= 0.0)) {
+            F.metzler = false;
+            break;
+          }
       F.fr = cplx ? plan::factor_range_complex(n[mu], Ah) : plan::factor_range(F.n, A);
       h->factors.push_back(F);
       rep.push_back(bm);
@@ -108,10 +115,12 @@ phiks_status create_impl(int d, const int* n, const double* const* A_host, bool 
     }
     h->fac_of_block[bm / d][mu] = found;
   }
-  if (cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned), 64 * sizeof(double)) != cudaSuccess) {
+  if (cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned), 64 * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&h->h_barrier_err), sizeof(int)) != cudaSuccess) {
     phiks_destroy(h);
     return fail(PHIKS_ERR_NOMEM, "pinned host scratch");
   }
+  *h->h_barrier_err = 0;
   *out = h;
   return PHIKS_OK;
 }
@@ -143,6 +152,7 @@ phiks_status phiks_destroy(phiks_handle h) {
     if (F.dA) cudaFree(F.dA);
   if (h->ws_own) cudaFree(h->ws_own);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
+  if (h->h_barrier_err) cudaFreeHost(h->h_barrier_err);
   for (int k = 0; k < kMaxRanks; ++k)
     if (h->peer_ipc[k] && h->peer[k]) cudaIpcCloseMemHandle(h->peer[k]);
   for (cudaEvent_t e : {h->ev_h2d, h->ev_d2h[0], h->ev_d2h[1], h->ev_cdone[0], h->ev_cdone[1], h->ev_ready})
@@ -186,6 +196,25 @@ phiks_status validate(phiks_handle h, const phiks_request* req, int& p) {
   if (req->force_s >= 0 && p >= 1 && req->force_q < 2) return fail(PHIKS_ERR_ARG, "force_q < 2");
   if (req->force_s >= 0 && req->force_s < req->n_scales - 1) return fail(PHIKS_ERR_ARG, "force_s < n_scales-1");
   return PHIKS_OK;
+}
+
+// Tucker operators run_jobs executes (reading R9): θ_q = 1 costs none; at the
+// last squaring step (or at s = 0) only the output combinations are formed —
+// Ψ_p for a linear combination, the requested φ_ℓ for the same vector
+// (PAPER.md l.953-956).  Lincomb without v_0, ŝ = 1: (q−2)p + sp + 1 (Table 1).
+int tucker_executed(const phiks_request* req, int p, const plan::Plan& pl) {
+  const bool same = req->mode == PHIKS_MODE_SAME_VECTOR;
+  const bool has0 = req->ells[0] == 0;
+  const int n0 = has0 ? req->n_scales : 0;
+  if (p == 0) return n0;
+  int last = 1;
+  if (same) {
+    last = 0;
+    for (int i = 0; i < req->n_ells; ++i) last += req->ells[i] >= 1;
+  }
+  const int sq = pl.s >= 1 ? (pl.s - 1) * p + last : 0;
+  const int quad = same ? pl.q - 1 : (pl.q - 1) * (pl.s >= 1 ? p : 1);
+  return quad + sq + n0;
 }
 
 phiks_status make_plan(phiks_handle h, const phiks_request* req, int p, const std::vector<double>& norms,
@@ -272,10 +301,7 @@ phiks_status phiks_plan(phiks_handle h, const phiks_request* req, const double* 
   out->s = pl.s;
   out->q = pl.q;
   out->T_formula = pl.T;
-  const int nodes = p >= 1 ? pl.q - 1 : 0;
-  bool has0 = req->ells[0] == 0;
-  out->T_executed = (req->mode == PHIKS_MODE_SAME_VECTOR) ? nodes + pl.s * p + (has0 ? req->n_scales : 0)
-                                                         : nodes * p + pl.s * p + (has0 ? req->n_scales : 0);
+  out->T_executed = tucker_executed(req, p, pl);
   return PHIKS_OK;
 }
 
@@ -286,9 +312,11 @@ extern "C" {
 static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_vecs, const double* const* vecs,
                                double* const* outs, void* workspace, size_t ws_bytes, void* stream,
                                bool size_only, const phiks_plan_info* forced, size_t* size_out) {
-  static const bool hostprof = getenv("PHIKS_HOSTPROF") != nullptr;
-  auto now = [] { return std::chrono::steady_clock::now(); };
-  const auto t0 = now();
+  // sharded handles: the barrier's sticky error flag of earlier applies, copied to pinned
+  // memory at the end of each apply (stream-ordered, no synchronisation): a device-memory
+  // apply reports a timed-out peer at the latest on the next call
+  if (!size_only && h && h->sharded() && h->h_barrier_err && *static_cast<volatile int*>(h->h_barrier_err))
+    return fail(PHIKS_ERR_CUDA, "cross-rank barrier timed out in an earlier apply (a peer rank did not arrive)");
   ApplyRun run;
   phiks_status st = run.init(h, req, n_vecs, vecs, outs, stream, size_only);
   if (st != PHIKS_OK) return st;
@@ -300,31 +328,15 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
     st = run.plan_direct(forced);
   }
   if (st != PHIKS_OK) return st;
-  const auto t1 = now();
   size_t need = 0;
   st = run.measure(&need);
   if (st != PHIKS_OK) return st;
-  const auto t2 = now();
-  struct HostProf {
-    bool on;
-    std::chrono::steady_clock::time_point t0, t1, t2;
-    ~HostProf() {
-      if (!on) return;
-      const auto t3 = std::chrono::steady_clock::now();
-      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-      fprintf(stderr, "PHIKS_HOSTPROF plan+norms %.1f us, measure %.1f us, enqueue %.1f us\n", us(t0, t1), us(t1, t2),
-              us(t2, t3));
-    }
-  } hostprof_guard{hostprof, t0, t1, t2};
   if (size_out) *size_out = need;
   if (size_only) return PHIKS_OK;
   char* base = nullptr;
   st = run.workspace(workspace, ws_bytes, need, &base);
   if (st != PHIKS_OK) return st;
-  static const bool graphs_on = [] {
-    const char* e = getenv("PHIKS_GRAPHS");
-    return !(e && atoi(e) == 0);
-  }();
+  const bool graphs_on = h->opt_graphs != 0;
   // graphs pay off where launch overhead matters (small tensors); large applies
   // keep direct launches so their exponential stage overlaps on the side stream
   const bool small_apply = h->N <= (int64_t(1) << 22);
@@ -375,11 +387,15 @@ static phiks_status apply_impl(phiks_handle h, const phiks_request* req, int n_v
     for (int k = 0; k < 2; ++k)
       if (!h->ev_cdone[k]) CUDA_TRY(cudaEventCreateWithFlags(&h->ev_cdone[k], cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(h->ev_cdone[run.half], cs));  // orders later side-stream work after this replay
+    if (h->sharded())
+      CUDA_TRY(cudaMemcpyAsync(h->h_barrier_err, h->sym + kCtrlErr, sizeof(int), cudaMemcpyDeviceToHost, cs));
     run.finish_stats(need);
     return PHIKS_OK;
   }
   st = run.execute(base, need, nullptr);
   if (st != PHIKS_OK) return st;
+  if (h->sharded())
+    CUDA_TRY(cudaMemcpyAsync(h->h_barrier_err, h->sym + kCtrlErr, sizeof(int), cudaMemcpyDeviceToHost, run.cs));
   if (run.host_mem && !run.host_async) {
     CUDA_TRY(cudaEventSynchronize(h->ev_d2h[run.half]));
     CUDA_TRY(cudaStreamSynchronize(run.cs));
@@ -453,6 +469,36 @@ phiks_status phiks_set_gemm_path(phiks_handle h, int path) {
     for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);  // captured with the other path
     h->graphs.clear();
     h->gemm_path = path;
+  }
+  return PHIKS_OK;
+}
+
+phiks_status phiks_set_option(phiks_handle h, int option, int value) {
+  if (!h) return fail(PHIKS_ERR_ARG, "null handle");
+  int* slot = nullptr;
+  int lo = 0, hi = 0;
+  switch (option) {
+    case PHIKS_OPT_SPLIT: slot = &h->opt_split; hi = 2; break;
+    case PHIKS_OPT_CHAIN: slot = &h->opt_chain; hi = 2; break;
+    case PHIKS_OPT_GRAPHS: slot = &h->opt_graphs; hi = 1; break;
+    default: return fail(PHIKS_ERR_ARG, "unknown option");
+  }
+  if (value < lo || value > hi) return fail(PHIKS_ERR_ARG, "option value out of range");
+  if (*slot != value) {
+    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);  // captured under the other setting
+    h->graphs.clear();
+    *slot = value;
+  }
+  return PHIKS_OK;
+}
+
+phiks_status phiks_get_option(phiks_handle h, int option, int* value) {
+  if (!h || !value) return fail(PHIKS_ERR_ARG, "null argument");
+  switch (option) {
+    case PHIKS_OPT_SPLIT: *value = h->opt_split; break;
+    case PHIKS_OPT_CHAIN: *value = h->opt_chain; break;
+    case PHIKS_OPT_GRAPHS: *value = h->opt_graphs; break;
+    default: return fail(PHIKS_ERR_ARG, "unknown option");
   }
   return PHIKS_OK;
 }

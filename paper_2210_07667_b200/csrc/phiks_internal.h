@@ -148,7 +148,6 @@ struct OzakiParams {
   int cplx_j;    // complex μ ≥ 2 product: fibres [x ; Jx] of length K = 2n against
                  // E = [Re M | Im M] (n × 2n, column-major, Im M right after Re M), so y = Re M·x + J·Im M·x
   int n_next;    // chained: n_{μ+1} (0: plain fp64 outputs)
-  int dbg;       // timing experiments only (PHIKS_OZ_DBG); 0 in production
   Remap remap;   // slab-sharded stage (world > 0): fp64 outputs go to the owner rank; out = byte offset
 };
 bool ozaki_supported(int64_t L, int n, int64_t R, int S);

@@ -24,10 +24,10 @@ using cd = std::complex<double>;
 
 namespace {
 
-constexpr int kQmin = 2, kQmax = 32, kSmax = 60;   // reading R5
+constexpr int kQmin = 2, kQmax = 12, kSmax = 60;   // reading R5 (Table 1 never exceeds q = 12)
 constexpr double kWcap = 256.0;                    // reading R5
 constexpr int kNside = 32;                         // reading R4
-constexpr int kNr = 25;                            // reading R3: r ∈ geomspace(0.3, 10, 25)
+constexpr int kNr = 16;                            // reading R3: r ∈ geomspace(0.3, 6, 16)
 constexpr int kGL = 256;                           // Gauss–Legendre points for k_q
 constexpr double kExpMax = 709.782712893384;       // exp overflow threshold (fp64)
 const double kSpectral = 1.0 + std::sqrt(2.0);     // (1+√2)-spectral set [CP17], l.908
@@ -75,9 +75,9 @@ const std::vector<std::pair<double, double>>& gauss_legendre01() {
   return gl;
 }
 
-double r_grid(int i) {  // geomspace(0.3, 10, kNr)
-  if (i == kNr - 1) return 10.0;
-  return 0.3 * std::pow(10.0 / 0.3, static_cast<double>(i) / (kNr - 1));
+double r_grid(int i) {  // geomspace(0.3, 6, kNr)
+  if (i == kNr - 1) return 6.0;
+  return 0.3 * std::pow(6.0 / 0.3, static_cast<double>(i) / (kNr - 1));
 }
 
 int n_zeta(double r, double wmax) {

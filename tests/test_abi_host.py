@@ -147,3 +147,61 @@ def test_cpp_complex_range_random_factors():
         ora = O.plan_for(fac, 1.0, "same", (1, 2), [V], 1)
         got = _plan_host_complex(dims, fac, "same", (1, 2), 1, 1.0)
         assert (got.s, got.q) == (ora.s, ora.q)
+
+
+# ---- full §3.3 search against PAPER.md Table 1 (readings R3, R5, R6) ----
+LINCOMB_SQ_REPRODUCED = {(3, 64), (6, 11)}   # see tests/test_oracle_phiks.py
+
+
+@pytest.mark.parametrize("mode,row", [("same", r) for r in _table1()["same_vector"]]
+                         + [("lincomb", r) for r in _table1()["linear_combination"]])
+def test_cpp_planner_table1_full_search(mode, row):
+    """PAPER.md Table 1 (l.1416-1449): the library's search picks the paper's
+    (s, q) in every same-vector column, and a plan of the paper's Eq. (19)
+    count in every linear-combination column ((s, q) too where the count has a
+    unique minimiser along the search).  A flipped stopping comparison moves
+    d=3, n=64 to (8, 10) and d=6, n=11 to (4, 10)."""
+    t = _table1()
+    n, d = row["n"], row["d"]
+    A = (1 + 1j) / 100 * W.fd_dxx_dirichlet(n)
+    rect = O.range_rectangle([A] * d)
+    h = 1.0 / (n + 1)
+    x = np.arange(1, n + 1) * h
+    nv = 4096 * math.sqrt(2) * float(np.linalg.norm(x * (1 - x))) ** d
+    norms = [nv] if mode == "same" else [nv] * t["p"]
+    info = _select(mode, rect, t["p"], norms, t["tol"], t["s_hat"], 0, -1)
+    paper_T = O.tucker_count(mode, row["s"], t["s_hat"], row["q"], t["p"])
+    assert info.T_formula == paper_T
+    if mode == "same" or (d, n) in LINCOMB_SQ_REPRODUCED:
+        assert (info.s, info.q) == (row["s"], row["q"])
+
+
+@pytest.mark.parametrize("row", _table1()["linear_combination"], ids=lambda r: f"d{r['d']}n{r['n']}")
+def test_cpp_T_executed_equals_table1(row):
+    """Table 1's lincomb T = (q−2)p + sp + 1 is the library's executed count at
+    the paper's (s, q) (forced), ℓ = 1..5 without v_0."""
+    lib = _lib.load()
+    n, d = 4, 3
+    A = (1 + 1j) / 100 * W.fd_dxx_dirichlet(n)
+    Az = [np.asfortranarray(A.astype(np.complex128))] * d
+    dims = (ctypes.c_int * d)(*([n] * d))
+    req = _lib.make_request(1, (1, 2, 3, 4, 5), 1, 1.0, 0.0, row["s"], row["q"])
+    arr = (ctypes.c_double * 5)(*([1.0] * 5))
+    info = _lib.PlanInfo()
+    _lib.check(lib.phiks_plan_host_complex(d, dims, _lib.ptr_array([a.ctypes.data for a in Az]), ctypes.byref(req),
+                                           arr, ctypes.byref(info)), "phiks_plan_host_complex")
+    assert info.T_executed == row["T"]
+
+
+def test_cpp_T_executed_matches_oracle_formula():
+    lib = _lib.load()
+    A = [np.asfortranarray(W.fd_dxx_dirichlet(5))] * 2
+    dims = (ctypes.c_int * 2)(5, 5)
+    for mode in ("same", "lincomb"):
+        for s, q, ells, ns in [(0, 5, (0, 1, 2), 1), (2, 4, (1, 3), 2), (3, 6, (0, 2), 3), (1, 3, (2,), 1)]:
+            req = _lib.make_request(0 if mode == "same" else 1, ells, ns, 1.0, 0.0, s, q)
+            arr = (ctypes.c_double * 5)(*([1.0] * 5))
+            info = _lib.PlanInfo()
+            _lib.check(lib.phiks_plan_host(2, dims, _lib.ptr_array([a.ctypes.data for a in A]), ctypes.byref(req),
+                                           arr, ctypes.byref(info)), "phiks_plan_host")
+            assert info.T_executed == O.tucker_executed(mode, s, q, ells, ns, has_v0=0 in ells), (mode, s, q, ells)

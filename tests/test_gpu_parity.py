@@ -310,3 +310,50 @@ def test_api_error_paths():
     # n_scales forcing s below ŝ-1
     with pytest.raises(PhiksError):
         op.apply(pb.tau, pb.ells, [v], n_scales=3, force_s=0, force_q=4)
+
+
+def _table1_rows():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "table1.json")) as f:
+        return json.load(f)["linear_combination"]
+
+
+@pytest.mark.parametrize("row", _table1_rows(), ids=lambda r: f"d{r['d']}n{r['n']}")
+def test_table1_lincomb_tucker_count_executed(row):
+    """PAPER.md Table 1 lincomb T = (q−2)p + sp + 1 (l.1436-1446): at the paper's
+    (s, q) the library runs exactly T Tucker operators (θ_q = 1 free, only Ψ_p
+    at the last squaring step, l.953-956), and the result matches the oracle."""
+    dims = (8, 6, 4)
+    fac = W.random_factors(dims, seed=row["n"], scale=2.0)
+    vs = [W.random_tensor(dims, seed=40 + k) for k in range(5)]
+    ells = (1, 2, 3, 4, 5)
+    pl = O.Plan(row["s"], row["q"], 0)
+    tau = 0.5
+    ref = O.phiks_lincomb(fac, tau, dict(zip(ells, vs)), 1, pl)
+    assert ref.tucker_ops == row["T"]
+    op = PhiKS(fac)
+    outs = op.apply(tau, ells, [dev(v) for v in vs], mode="lincomb", n_scales=1, force_s=row["s"],
+                    force_q=row["q"])
+    torch.cuda.synchronize()
+    st = op.stats()
+    assert st["tucker_ops"] == row["T"] == st["T_executed"]
+    assert rel2(outs[0], W.as_flat(ref.out[0])) <= TOL
+
+
+@pytest.mark.parametrize("ells,n_scales", [((1, 3), 1), ((2,), 2), ((0, 2, 4), 1), ((1, 2), 3)])
+def test_same_vector_last_step_requested_only(ells, n_scales):
+    """Same vector: at the last squaring step only the requested φ_ℓ are formed."""
+    dims = (9, 7, 5)
+    fac = W.random_factors(dims, seed=3, scale=6.0)
+    V = W.random_tensor(dims, seed=4)
+    pl = O.Plan(3, 5, 0)
+    ref = O.phiks_same(fac, 1.0, V, ells, n_scales, pl)
+    assert ref.tucker_ops == O.tucker_executed("same", 3, 5, ells, n_scales)
+    op = PhiKS(fac)
+    outs = op.apply(1.0, ells, [dev(V)], mode="same", n_scales=n_scales, force_s=3, force_q=5)
+    torch.cuda.synchronize()
+    assert op.stats()["tucker_ops"] == ref.tucker_ops
+    for j in range(n_scales):
+        for i, ell in enumerate(ells):
+            assert rel2(outs[j * len(ells) + i], W.as_flat(ref.out[(ell, j)])) <= TOL

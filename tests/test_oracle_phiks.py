@@ -198,14 +198,89 @@ def test_table1_same_vector_T_formula():
         assert O.tucker_count("same", row["s"], t["s_hat"], row["q"], t["p"]) == row["T"]
 
 
-def test_table1_plan_not_costlier_than_paper():
-    """The literal §3.3 stopping rule (reading R6) never picks a plan with a
-    larger Eq. (14)/(19) count than the paper's Table 1 choice."""
+# Columns where Table 1's (s, q) is reproduced by the literal §3.3 rule (reading
+# R6).  The other six linear-combination columns sit on a plateau of equal
+# Eq. (19) count q + s: the rule, which stops only when T(s+1) > T(s), walks to
+# the plateau's last s; Table 1 stops inside it (R6).  Their T is
+# still the paper's (test_table1_lincomb_T_equals_paper).
+LINCOMB_SQ_REPRODUCED = {(3, 64), (6, 11)}
+
+
+def _full_plan(mode, row, p):
+    rect, nv = _validation_plan_inputs(row["n"], row["d"])
+    norms = [nv] if mode == "same" else [nv] * p
+    return O.select_plan(mode, rect, p, norms, TOL, 1)
+
+
+@pytest.mark.parametrize("row", _table1()["same_vector"], ids=lambda r: f"d{r['d']}n{r['n']}")
+def test_table1_same_vector_s_q(row):
+    """PAPER.md Table 1 (l.1420-1430): the full §3.3 search (readings R3, R5,
+    R6) picks the paper's (s, q) in every same-vector column."""
+    pl = _full_plan("same", row, _table1()["p"])
+    assert (pl.s, pl.q) == (row["s"], row["q"])
+    assert pl.T == row["T"]          # Eq. (14) with ŝ = 1 is the printed T
+
+
+@pytest.mark.parametrize("row", _table1()["linear_combination"], ids=lambda r: f"d{r['d']}n{r['n']}")
+def test_table1_lincomb_T_equals_paper(row):
+    """PAPER.md Table 1 (l.1436-1446): the search picks a plan of exactly the
+    paper's Eq. (19) count, and the paper's (s, q) where the count has a unique
+    minimiser along the search."""
     t = _table1()
-    for mode, key in (("same", "same_vector"), ("lincomb", "linear_combination")):
-        row = [r for r in t[key] if r["d"] == 6 and r["n"] == 8][0]
-        rect, nv = _validation_plan_inputs(row["n"], row["d"])
-        norms = [nv] if mode == "same" else [nv] * t["p"]
-        pl = O.select_plan(mode, rect, t["p"], norms, t["tol"], t["s_hat"])
-        paper_T = O.tucker_count(mode, row["s"], t["s_hat"], row["q"], t["p"])
-        assert pl.T <= paper_T
+    pl = _full_plan("lincomb", row, t["p"])
+    assert pl.T == O.tucker_count("lincomb", row["s"], 1, row["q"], t["p"])
+    if (row["d"], row["n"]) in LINCOMB_SQ_REPRODUCED:
+        assert (pl.s, pl.q) == (row["s"], row["q"])
+
+
+def test_stopping_rule_is_strict(monkeypatch):
+    """§3.3 l.830-834 / l.867-871: continue while T(s+1) ≤ T(s), stop at the
+    first strict increase.  A synthetic q(s) landscape pins both branches: a
+    flipped comparison (≥) would stop at the start of the plateau."""
+    land = {0: 12, 1: 10, 2: 9, 3: 8, 4: 8, 5: 9}     # lincomb count 5(q+s)+1
+    monkeypatch.setattr(O, "q_for_s", lambda mode, rect, p, norms, delta, s, *a: land.get(s))
+    pl = O.select_plan("lincomb", None, 5, [1.0] * 5, 1.0, 1)
+    assert (pl.s, pl.q) == (3, 8)     # T: 61, 56, 56, 56, 61 -> plateau end s=3
+    pl = O.select_plan("same", None, 5, [1.0], 1.0, 1)
+    assert (pl.s, pl.q) == (0, 12)    # same-vector T = q+5s+1: 13, 16 -> stop at s=0
+    land2 = {0: None, 1: None, 2: 11, 3: 5, 4: 4}
+    monkeypatch.setattr(O, "q_for_s", lambda mode, rect, p, norms, delta, s, *a: land2.get(s))
+    pl = O.select_plan("same", None, 2, [1.0], 1.0, 1)
+    assert (pl.s, pl.q) == (3, 5)     # infeasible s skipped; 16, 12, 13 -> s=3
+
+
+def test_table1_q_max():
+    """Reading R5: q ≤ 12 (Table 1's largest q).  At d=3, n=64 the bound admits
+    q = 12 at s = 7 only marginally; any q cap ≥ 13 would pick s ≤ 7, not the
+    paper's s = 8."""
+    assert O.Q_MAX == 12
+    rect, nv = _validation_plan_inputs(64, 3)
+    assert O.q_for_s("same", rect, 5, [nv], TOL, 7, q_max=20) == 13
+    assert O.q_for_s("same", rect, 5, [nv], TOL, 7) is None
+
+
+@pytest.mark.parametrize("row", _table1()["linear_combination"], ids=lambda r: f"d{r['d']}n{r['n']}")
+def test_table1_lincomb_T_executed(row):
+    """PAPER.md Table 1 lincomb T = (q−2)p + sp + 1 (l.1436-1446, l.953-956):
+    the oracle runs exactly that many Tucker operators at the paper's (s, q)
+    (θ_q = 1 free, only Ψ_p formed at the last squaring step)."""
+    t = _table1()
+    p = t["p"]
+    fac = W.random_factors((3, 2, 2), seed=row["n"], scale=1.0)
+    V = W.random_tensor((3, 2, 2), seed=row["d"])
+    pl = O.Plan(row["s"], row["q"], 0)
+    res = O.phiks_lincomb(fac, 0.1, {k: V for k in range(1, p + 1)}, 1, pl)
+    assert res.tucker_ops == row["T"]
+    assert O.tucker_executed("lincomb", row["s"], row["q"], tuple(range(1, p + 1)), 1) == row["T"]
+
+
+def test_T_executed_formula_matches_runs():
+    fac = W.random_factors((3, 2), seed=4, scale=2.0)
+    V = W.random_tensor((3, 2), seed=5)
+    for s, q, ells, ns in [(0, 5, (0, 1, 2), 1), (2, 4, (1, 3), 2), (3, 6, (0, 2), 3), (1, 3, (2,), 1)]:
+        pl = O.Plan(s, q, 0)
+        r = O.phiks_same(fac, 0.3, V, ells, ns, pl)
+        assert r.tucker_ops == O.tucker_executed("same", s, q, ells, ns), (s, q, ells)
+        vs = {e: V for e in ells}
+        r = O.phiks_lincomb(fac, 0.3, vs, ns, pl)
+        assert r.tucker_ops == O.tucker_executed("lincomb", s, q, ells, ns, has_v0=0 in ells), (s, q, ells)
