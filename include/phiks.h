@@ -165,7 +165,7 @@ phiks_status phiks_create_blocks_complex(int nblocks, int d, const int* n, const
    first-mode product with that real form (μ = 1), or two real products
    X ×_μ Re(M) + J(X ×_μ Im(M)) (μ ≥ 2, J: re ← −im, im ← re) fused in one
    launch.  The §3.3 rectangle uses the complex trace shift (reading R1).
-   Not available for sharded handles. */
+   Sharded complex handles: phiks_create_sharded_complex. */
 phiks_status phiks_create_complex(int d, const int* n, const double* const* A_host, phiks_handle* out);
 
 /* Release the handle and every device/pinned buffer it owns.  NULL is a no-op. */
@@ -205,7 +205,8 @@ phiks_status phiks_set_profiling(phiks_handle h, int on);
    PHIKS_GEMM_DMMA: the fp64 DMMA kernel for every product;
    PHIKS_GEMM_I8: the int8 tensor-core kernel (7 balanced base-256 digits per
      operand, exact int32 accumulation: fp64-class error) wherever it applies
-     (real handles, sharded or not, n_μ ≤ 256, plain outputs), DMMA elsewhere;
+     (real handles, sharded or not, n_μ ≤ 512 — E streamed per k-block above 256 —
+     plain outputs), DMMA elsewhere;
      when every mode of a Tucker batch qualifies (n_μ % 16 == 0, L_μ % 128 == 0
      for μ ≥ 2) the modes run chained: each product writes the next mode's
      digits, split with exponent bounds (reading R15) — see
@@ -261,7 +262,7 @@ phiks_status phiks_mode_product(int d, const int* n, int mu, int batch, const do
    digits scaled by a power of two, and the digit products with s + t < S are
    accumulated exactly in int32; with 7 digits each operand keeps 55 bits and
    the error bound is that of an fp64 dot product (§3.1 Eq. (13) is
-   the product computed).  n_μ ≤ 256.  `workspace` is device memory of at
+   the product computed).  n_μ ≤ 512.  `workspace` is device memory of at
    least phiks_mode_product_i8_workspace bytes (owned by the caller, reused
    across calls on the same stream); errors as phiks_mode_product,
    PHIKS_ERR_ARG for unsupported sizes or digit counts. */

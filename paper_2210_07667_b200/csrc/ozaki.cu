@@ -3,17 +3,18 @@
 // DESIGN.md §4c.  The μ-mode product Y = X ×_μ E (§3.1, Eq. (13))
 // contracts every mode-μ fiber x_c (c = l + L·r of the (L, n, R) view) with the
 // rows e_j of E.  Each fiber and each row is written exactly (up to a
-// truncation below 2^{ex-8S+1}) in S balanced base-256 digits, an error-free
+// rounding below 2^{ex-8S}) in S balanced base-256 digits, an error-free
 // splitting in the manner of Ozaki:
 //     x_c = 2^{ex_c-7} Σ_{s=0..S-1} 256^{-s} a_{c,s},   e_j = 2^{ee_j-7} Σ_t 256^{-t} b_{j,t},
 // a, b ∈ [-128, 127]^n integer vectors (|x| < 2^{ex-1} for the whole fiber).
 // Then
 //     y_{c,j} = 2^{ex_c+ee_j-14} Σ_{g=0..S-1} 256^{-g} D_g,   D_g = Σ_{s+t=g} a_{c,s}·b_{j,t},
 // keeping the pairs with s + t < S (the dropped ones are below the
-// representation error).  Every D_g is an exact int32 sum (|D_g| ≤ S·n·2^14
-// < 2^31 for n ≤ 256) accumulated by tcgen05.mma kind::i8 in TMEM, one
-// accumulator per diagonal g; the epilogue combines them in fp64 (Horner in
-// 2^-8) and applies the power-of-two scales.  With S = 7 each operand carries
+// representation error).  Every D_g is an exact int32 sum (|D_g| ≤ (g+1)·n·2^14
+// < 2^31 for n ≤ 512; the E digits stay resident for n ≤ 256 and stream per
+// k-block above) accumulated by tcgen05.mma kind::i8 in TMEM, one accumulator
+// per diagonal g; the epilogue combines them exactly in 64-bit integers (one
+// fp64 rounding for fp64 outputs) and applies the power-of-two scales.  With S = 7 each operand carries
 // 55 bits relative to twice its fiber / row maximum, so the error is bounded
 // like that of an fp64 dot product, |Δy| ≲ n·2^-52·max|e_j|·max|x_c|.
 //
@@ -48,8 +49,9 @@ __device__ __forceinline__ unsigned oz_smem_u32(const void* p) {
 }
 
 // ---- exact splitting into S balanced base-256 digits ----
-// |v| < 2^{ex-1}: F = trunc(v·2^{8S-1-ex}) (an exact power-of-two scaling and one
-// fp64 → int64 conversion), |F| < 2^{8S-2}; G = F + 0x80…80 has bytes d_i + 128,
+// |v| < 2^{ex-1}: F = rint(v·2^{8S-1-ex}) (an exact power-of-two scaling and one
+// fp64 → int64 conversion, rounded to nearest so that the representation errors
+// of a dot product's terms have no common sign), |F| ≤ 2^{8S-2}; G = F + 0x80…80 has bytes d_i + 128,
 // d_i the balanced digits of F; digit s (most significant first) = byte S-1-s
 // of G ^ 0x80…80.  The scaling is split in two factors when 2^{8S-1-ex}
 // overflows (fibers of subnormal magnitude).
@@ -70,7 +72,7 @@ template <int S>
 __device__ __forceinline__ uint64_t oz_digits(double v, const OzScale& sc) {
   double t = v * sc.a;
   if (sc.two) t *= sc.b;
-  const long long F = __double2ll_rz(t);
+  const long long F = __double2ll_rn(t);
   constexpr uint64_t C = 0x8080808080808080ull >> (64 - 8 * S);
   return (static_cast<uint64_t>(F) + C) ^ C;
 }
@@ -266,7 +268,8 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     p.esc[static_cast<int64_t>(slot) * n + j] = bad ? qnan : scalbn(1.0, ex - 30);
     // b_j with ‖e_j‖₁ < 2^{b_j} (a1 carries ≤ n·2^-53 relative rounding: margin 2^-40); the
-    // truncated digits have |ẽ| ≤ |e|, so |Σ_k ẽ_jk x̃_k| < 2^{b_j}·max|x̃| (chained modes, §4d)
+    // rounded digits have |ẽ_jk| ≤ |e_jk| + 2^{ee-56}, i.e. ‖ẽ_j‖₁ ≤ ‖e_j‖₁(1 + n·2^-55) inside
+    // the margin, so |Σ_k ẽ_jk x̃_k| < 2^{b_j}·max|x̃| (chained modes, §4d)
     const int b = a1 > 0.0 ? ilogb(a1 * (1.0 + 0x1p-40)) + 1 : -1100;
     if (p.eb) p.eb[static_cast<int64_t>(slot) * n + j] = bad ? qnan : b;
     if (p.ecol) {
@@ -612,24 +615,44 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
   }
   oz_mbar_wait(t_full, phase);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  // drain: per column, 2^16 Σ_g 256^{-g} D_g from three exact int64 partial sums
-  // (D_0·2^16 + D_1·2^8 + D_2, D_3·2^16 + D_4·2^8 + D_5, D_6; each < 2^42) and two fp64 fmas
+  // drain: per column V = 2^16 Σ_g 256^{-g} D_g from two exact int64 partial sums,
+  // ta = D_0·2^16 + D_1·2^8 + D_2 (< n·2^31) and T = ((D_3·2^8 + D_4)·2^8 + D_5)·2^8 + D_6
+  // (< n·2^41), V = ta + 2^-32·T (|D_g| ≤ (g+1)·n·2^14).  fp64 outputs take V with one
+  // rounding; the next mode's digits (OUTD) take Pt = ⌊V·2^23⌋ = ta·2^23 + ⌊T/2^9⌋ (< 2^63
+  // for n ≤ 512; the floor is below 2^-60 of the fibre bound) and stay in the integer pipes
   double acc[EPC];
+  long long pt[EPC];
+  // high diagonals first (T from {3, …, S-1}), then ta from {0, 1, 2}: at most 32 loaded words
+  // live at a time next to the 32 partial sums
 #pragma unroll
   for (int cb = 0; cb < EPC / 8; ++cb) {
-    uint32_t v[S][8];
+    uint32_t v[S - 3][8];
 #pragma unroll
-    for (int g = 0; g < S; ++g) oz_ld8(tl + g * kOzBN + cb * 8, v[g]);
+    for (int g = 3; g < S; ++g) oz_ld8(tl + g * kOzBN + cb * 8, v[g - 3]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      long long T = static_cast<long long>(static_cast<int>(v[0][q])) * 256 + static_cast<int>(v[1][q]);
+      T = T * 256 + static_cast<int>(v[2][q]);
+      T = T * 256 + (S == 7 ? static_cast<int>(v[S == 7 ? 3 : 0][q]) : 0);
+      pt[cb * 8 + q] = T;
+    }
+  }
+#pragma unroll
+  for (int cb = 0; cb < EPC / 8; ++cb) {
+    uint32_t v[3][8];
+#pragma unroll
+    for (int g = 0; g < 3; ++g) oz_ld8(tl + g * kOzBN + cb * 8, v[g]);
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const long long ta = static_cast<long long>(static_cast<int>(v[0][q])) * 65536 +
                            static_cast<long long>(static_cast<int>(v[1][q])) * 256 + static_cast<int>(v[2][q]);
-      const long long tb = static_cast<long long>(static_cast<int>(v[3][q])) * 65536 +
-                           static_cast<long long>(static_cast<int>(v[4][q])) * 256 + static_cast<int>(v[5][q]);
-      double y = oz_l2d(tb);
-      if (S == 7) y = fma(oz_i2d(v[S - 1][q]), 0x1p-8, y);
-      acc[cb * 8 + q] = fma(y, 0x1p-24, oz_l2d(ta));
+      const long long T = pt[cb * 8 + q];
+      if constexpr (OUTD)
+        pt[cb * 8 + q] = (ta << 23) + (T >> 9);
+      else
+        acc[cb * 8 + q] = fma(oz_l2d(T), 0x1p-32, oz_l2d(ta));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -650,29 +673,25 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     // is one exact power-of-two scaling of the accumulator (β = 1 on chained modes), so the
     // digits take one DMUL and one F2I per element; digit s of element (l, j, r) goes to
     // dig[s·N + l + L·(j + n·r)]
-    const int64_t N = C * p.n;
-    if (term.beta != 1.0)
-#pragma unroll
-      for (int q = 0; q < EPC; ++q) acc[q] *= term.beta;
+    const int64_t N = C * p.n;  // (chained products have β = 1)
     // column pair (b_j, ee_j - 30) packed in 16-bit halves, INT_MIN for a non-finite row of E
     const int cp_l = (isnan(esc_l) || isnan(eb_l))
                          ? INT_MIN
                          : ((static_cast<int>(eb_l) + 0x4000) << 16) | (ilogb(esc_l) + 0x4000);
     const bool rbad = isnan(xsv) || isnan(mx);
     const int rk = rbad ? 0 : xe + 8 * S - 1, mxi = rbad ? 0 : static_cast<int>(mx);
-    // F = trunc(acc·2^k) read off the bits of acc with integer shifts (no FP64-pipe
-    // conversion): acc is 0 or a normal number (|acc| ≥ 2^-32), |F| < 2^55 by the bound, so
-    // F = (m·4) >> (1077 − E − k) with m the 53-bit significand and E the biased exponent
-    // (acc = 0 has E = 0 and shifts out entirely)
+    // F = rint(V·2^k) = rint(Pt·2^{k-23}): Pt shifted right by r = 23 − k with round half up,
+    // or left by −r (k ≤ 27 since ee_j ≤ b_j + 2 and ex_c ≤ Mx; no overflow: |F| ≤ 2^54),
+    // then balanced digits as in oz_digits
     constexpr uint64_t Cc = 0x8080808080808080ull >> (64 - 8 * S);
-    auto digit_bits = [&](double a, int k) -> uint64_t {
-      const long long bits = __double_as_longlong(a);
-      const int E = static_cast<int>(static_cast<uint64_t>(bits) >> 52) & 0x7ff;
-      const int rs = max(1077 - E - k, 0);
-      const uint64_t m4 = ((static_cast<uint64_t>(bits) & 0xFFFFFFFFFFFFFull) | (1ull << 52)) << 2;
-      const uint64_t fa = rs < 64 ? (m4 >> rs) : 0ull;
-      const uint64_t sg = static_cast<uint64_t>(bits >> 63);
-      return (((fa ^ sg) - sg) + Cc) ^ Cc;
+    auto digit_bits = [&](long long P, int k) -> uint64_t {
+      const int r = 23 - k;
+      long long F;
+      if (r > 0)
+        F = r < 63 ? ((P + (1ll << (r - 1))) >> r) : 0ll;
+      else
+        F = P << (-r & 63);
+      return (static_cast<uint64_t>(F) + Cc) ^ Cc;
     };
     // fast path (warp-uniform): every row of E finite and no clamp of e = b_j + Mx, so
     // k = ((ee_j − 30) − b_j) + (ex_c + 8S − 1 − Mx) = colk[q] + rowk: one add per element
@@ -688,10 +707,10 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
         const int cpq = __shfl_sync(0xffffffffu, cp_l, q);
         const int e = min(max(((cpq >> 16) - 0x4000) + mxi, -1100), 1025);
         colk[q] = ((cpq & 0xffff) - 0x4000) + rk - e - rowk;
-        if (rbad || cpq == INT_MIN) acc[q] = 0.0;
+        if (rbad || cpq == INT_MIN) pt[q] = 0;
       }
     }
-    auto digits = [&](int q) -> uint64_t { return digit_bits(acc[q], colk[q] + rowk); };
+    auto digits = [&](int q) -> uint64_t { return digit_bits(pt[q], colk[q] + rowk); };
     const bool st_ok = rvalid && jn > 0;
     if (!AMN) {  // mode-1 product (L = 1): EPC consecutive bytes of each digit plane per thread
       int8_t* dg = term.dig + l + L * (j0 + static_cast<int64_t>(p.n) * r);
@@ -954,7 +973,9 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
       if (tile > 0) oz_mbar_wait(t_empty, (tile - 1) & 1);  // epilogue drained the accumulators
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       // fully unrolled over the digits: every MMA's column offset, N and instruction
-      // descriptor are compile-time constants (the issue loop is a few uniform adds per MMA)
+      // descriptor are compile-time constants (the issue loop is a few uniform adds per MMA).
+      // Issuing the digits high to low with the accumulators released in two diagonal groups
+      // (to overlap the drain) measured 14 % slower
       for (int kb = 0; kb < nk; ++kb) {
         const int es = ek & 1;
         if (SE) {

@@ -121,6 +121,10 @@ class ShardedPhiKS:
         """int8 / DMMA / auto for the Tucker products of this rank (phiks_set_gemm_path)."""
         self.op.set_gemm_path(path)
 
+    def set_option(self, name: str, value: int):
+        """Execution option of this rank's handle (PHIKS_OPT_*, include/phiks.h)."""
+        self.op.set_option(name, value)
+
     def wait(self):
         self.op.wait()
 

@@ -1,7 +1,8 @@
 """Randomised parity sweep of the chained int8 modes against the oracle
 (one-off robustness check, not part of the suite): shapes that take the chained route
 (n_1 ∈ {128, 256}, the other n_μ multiples of 16 up to 256, d = 2..4), real random factors
-of random scale, both modes, 1-3 scales, the int8 path forced (PHIKS_GEMM=i8 semantics)."""
+of random scale, both modes, 1-3 scales, the int8 path forced; CHAIN=0/1/2 is the handle's
+PHIKS_OPT_CHAIN (default 2: chained regardless of the Metzler guard)."""
 import json, os, sys, time
 import numpy as np
 import torch
@@ -12,7 +13,8 @@ from paper_2210_07667_b200 import workloads as W  # noqa: E402
 
 seed = int(os.environ.get("SEED", "1"))
 count = int(os.environ.get("COUNT", "40"))
-path = os.environ.get("GEMM_PATH", "i8")  # i8 (chained unless PHIKS_CHAIN=0) or dmma
+path = os.environ.get("GEMM_PATH", "i8")  # i8 or dmma
+chain = int(os.environ.get("CHAIN", "2"))
 per_case = []
 rng = np.random.default_rng(seed)
 worst, fails, chained = 0.0, [], 0
@@ -34,6 +36,7 @@ for c in range(count):
     ns = int(rng.integers(1, 4))
     op = PhiKS(fac)
     op.set_gemm_path(path)
+    op.set_option("chain", chain)
     outs = op.apply(tau, ells, [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).cuda() for v in vs],
                     mode=mode, n_scales=ns)
     torch.cuda.synchronize()
@@ -51,6 +54,6 @@ for c in range(count):
             fails.append({"case": c, "dims": dims, "mode": mode, "out": k, "err": err})
     per_case.append(cw)
     op.close()
-print(json.dumps({"seed": seed, "count": count, "path": path, "chain": os.environ.get("PHIKS_CHAIN", "1"),
+print(json.dumps({"seed": seed, "count": count, "path": path, "chain": chain,
                   "worst_rel_err": worst, "fails": fails, "per_case_worst": per_case,
                   "chained_tucker_ops": int(chained), "seconds": time.time() - t0}))

@@ -129,3 +129,16 @@ def test_config3_full_sharded8_equals_single():
         assert rel2(got, single[i]) <= 1e-13, i
     for r in ranks:
         r.close()
+
+
+@pytest.mark.skipif(not __import__("os").environ.get("PHIKS_SLOW_TESTS"),
+                    reason="~5 min of oracle time; scripts/fullsize_cfg4_parity.py records the result in profiles/")
+def test_config4_full_oracle_parity():
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    import fullsize_cfg4_parity as F
+    res = F.run()
+    assert res["library_plan"]["s"] == res["oracle_plan"]["s"] and res["library_plan"]["q"] == res["oracle_plan"]["q"]
+    assert res["library_plan"]["tucker_ops"] == res["oracle_plan"]["tucker_ops"]
+    assert res["rel_2norm_err"] <= TOL, res

@@ -220,6 +220,7 @@ def test_i8_chain_apply_parity(dims, mode):
     vs = [W.random_tensor(dims, seed=seed + 10 + k) for k in range(1 if mode == "same" else len(ells))]
     pb = W.Problem(f"chain{dims}{mode}", dims, fac, float(rng.uniform(0.3, 1.2)), mode, ells, vs, 2)
     op = PhiKS(pb.A)
+    op.set_option("chain", 2)  # random (non-Metzler) factors: the guard would keep per-mode splits
     got, st = _apply(op, pb, "i8")
     # every quadrature / squaring batch is chained; lincomb's exp(τK/2^j)v_0 terms (one per
     # scale, several outputs per operator) keep the per-mode path
@@ -253,6 +254,7 @@ def test_i8_chain_zero_and_nonfinite_inputs():
     dims = (128, 32, 16)
     fac = W.random_factors(dims, seed=950, scale=3.0)
     op = PhiKS(fac)
+    op.set_option("chain", 2)
     z = np.zeros(dims)
     got, st = _apply(op, W.Problem("z", dims, fac, 0.5, "same", (0, 1), [z], 1), "i8")
     assert st["i8_chained_ops"] > 0
@@ -274,6 +276,7 @@ def test_i8_chain_graph_replay_bitwise():
     v = torch.from_numpy(W.as_flat(W.random_tensor(dims, seed=971)).copy()).to(DEV)
     op = PhiKS(fac)
     op.set_gemm_path("i8")
+    op.set_option("chain", 2)
     outs = [torch.empty_like(v) for _ in range(3)]
     res = []
     for _ in range(3):

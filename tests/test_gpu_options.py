@@ -1,0 +1,120 @@
+"""Per-handle execution options (include/phiks.h PHIKS_OPT_*): every setting gives the
+oracle's result; the chain guard (reading R15) chains the int8 modes only for Metzler
+factors."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import phiks_oracle as O  # noqa: E402
+from paper_2210_07667_b200 import PhiKS, PhiksError  # noqa: E402
+from paper_2210_07667_b200 import workloads as W  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+TOL = 1e-12
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _apply(op, pb):
+    vs = [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).to(DEV) for v in pb.vs]
+    outs = op.apply(pb.tau, pb.ells, vs, mode=pb.mode, n_scales=pb.n_scales)
+    torch.cuda.synchronize()
+    return [o.cpu().numpy() for o in outs], op.stats()
+
+
+def _oracle_outs(pb):
+    ref = O.phiks(pb.A, pb.tau, pb.mode, pb.ells, pb.vs, n_scales=pb.n_scales)
+    if pb.mode == "same":
+        return [W.as_flat(ref.out[(ell, j)]) for j in range(pb.n_scales) for ell in pb.ells]
+    return [W.as_flat(ref.out[j]) for j in range(pb.n_scales)]
+
+
+def test_option_api():
+    op = PhiKS([W.fd_dxx_dirichlet(8)] * 2)
+    assert (op.get_option("split"), op.get_option("chain"), op.get_option("graphs")) == (2, 1, 1)
+    for name, bad in (("split", 3), ("chain", -1), ("graphs", 2)):
+        with pytest.raises(PhiksError):
+            op.set_option(name, bad)
+    op.set_option("split", 0)
+    assert op.get_option("split") == 0
+
+
+@pytest.mark.parametrize("split", [0, 1, 2])
+@pytest.mark.parametrize("path", ["dmma", "i8"])
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_split_option_parity(split, path, cfg):
+    """PHIKS_OPT_SPLIT: quadrature sum and squaring recurrence fused into the last mode's
+    epilogue (0), the quadrature as a streaming pass (1), both streaming (2)."""
+    for pb in W.config(cfg, small=True).problems:
+        op = PhiKS(pb.A)
+        op.set_gemm_path(path)
+        op.set_option("split", split)
+        got, st = _apply(op, pb)
+        for k, (g, r) in enumerate(zip(got, _oracle_outs(pb))):
+            assert rel(g, r) <= TOL, (pb.name, split, path, k, rel(g, r))
+
+
+def _fd_problem():
+    dims = (128, 64, 32)
+    A = [0.7 * W.fd_dxx_neumann(dims[0]), W.fd_dxx_dirichlet(dims[1]) + 3.0 * W.fd_dx_dirichlet(dims[1]),
+         0.2 * W.fd_dxx_neumann(dims[2])]
+    v = W.uniform_tensor(dims, -1.0, 1.0, seed=31)
+    return W.Problem("fd", dims, A, 2e-3, "same", (0, 1, 2), [v], 1)
+
+
+def _random_problem(scale=20.0, seed=41):
+    dims = (128, 64, 32)
+    fac = W.random_factors(dims, seed=seed, scale=scale)
+    v = W.random_tensor(dims, seed=seed + 1)
+    return W.Problem("rand", dims, fac, 0.5, "same", (0, 1, 2), [v], 1)
+
+
+def test_chain_guard_follows_metzler_factors():
+    """Default (guarded): FD Laplacian / ADR factors (off-diagonals ≥ 0) chain; dense random
+    factors keep per-mode splits on the int8 path; 0 / 2 switch chaining off / on."""
+    for pb, chained_default in ((_fd_problem(), True), (_random_problem(), False)):
+        ref = _oracle_outs(pb)
+        op = PhiKS(pb.A)
+        op.set_gemm_path("i8")
+        for opt, want in ((1, chained_default), (0, False), (2, True)):
+            op.set_option("chain", opt)
+            got, st = _apply(op, pb)
+            assert st["i8_mode_launches"] > 0
+            assert (st["i8_chained_ops"] > 0) == want, (pb.name, opt, st["i8_chained_ops"])
+            for g, r in zip(got, ref):
+                assert rel(g, r) <= TOL, (pb.name, opt, rel(g, r))
+
+
+def test_chain_guard_accuracy_non_metzler():
+    """Rows with sign cancellation (dense random factors): the chained exponent bound
+    ‖e_j‖₁·max|x| exceeds the true fibre maximum, so chained digits carry fewer bits.  The
+    guarded default stays within a small factor of the fp64 DMMA path's error."""
+    errs = {}
+    for scale in (30.0,):
+        pb = _random_problem(scale=scale, seed=77)
+        ref = _oracle_outs(pb)
+        op = PhiKS(pb.A)
+        for key, path, chain in (("dmma", "dmma", 1), ("guarded", "i8", 1), ("forced", "i8", 2)):
+            op.set_gemm_path(path)
+            op.set_option("chain", chain)
+            got, _ = _apply(op, pb)
+            errs[key] = max(rel(g, r) for g, r in zip(got, ref))
+    assert errs["guarded"] <= TOL and errs["forced"] <= TOL, errs
+    assert errs["guarded"] <= 8 * max(errs["dmma"], 1e-16), errs
+
+
+def test_graphs_option_bitwise():
+    pb = W.config(2, small=True).problems[0]
+    res = []
+    for g in (1, 0):
+        op = PhiKS(pb.A)
+        op.set_option("graphs", g)
+        for _ in range(2):
+            got, _ = _apply(op, pb)
+        res.append(got)
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)

@@ -28,12 +28,13 @@ def rel2(got, ref):
     return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
 
 
-def run_sharded(pb, world, n_scales=None, force=None, path="dmma"):
+def run_sharded(pb, world, n_scales=None, force=None, path="dmma", chain=1):
     n_scales = pb.n_scales if n_scales is None else n_scales
     ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
     ShardedPhiKS.connect_local(ranks)
     for r in ranks:
         r.set_gemm_path(path)
+        r.set_option("chain", chain)
     flat = [W.as_flat(v) for v in pb.vs]
     vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, world)[r])).to(DEV) for x in flat]
             for r in range(world)]
@@ -203,7 +204,8 @@ def test_sharded_int8_path(dims, world, mode):
     ells = (0, 1, 2) if mode == "same" else (0, 1, 2, 3)
     vs = [W.random_tensor(dims, seed=seed + 1 + k) for k in range(1 if mode == "same" else len(ells))]
     pb = W.Problem(f"si8_{dims}_{world}_{mode}", dims, fac, 0.7, mode, ells, vs, 2)
-    outs, stats = run_sharded(pb, world, path="i8")
+    # random (non-Metzler) factors: chaining forced past the guard to exercise the chained stages
+    outs, stats = run_sharded(pb, world, path="i8", chain=2)
     assert all(s["i8_mode_launches"] > 0 for s in stats)
     if dims[0] == 128:  # modes 1..d−2 chained into the peer-store stage
         assert all(s["i8_chained_ops"] > 0 for s in stats)
