@@ -123,7 +123,9 @@ typedef struct {
   int64_t i8_chained_ops;         /* Tucker operators of the last apply whose modes ran
                                      chained on the int8 path (no fp64 intermediates:
                                      each product writes the next mode's digits,
-                                     DESIGN.md §4d; PHIKS_CHAIN=0 disables)          */
+                                     DESIGN.md §4d; PHIKS_OPT_CHAIN)                 */
+  int64_t shard_digit_ops;        /* sharded handles: Tucker operators whose stage 0 wrote
+                                     mode d's digit planes into the owners */
 } phiks_stats;
 
 /* Create a handle for K = A_d ⊕ … ⊕ A_1.

@@ -186,7 +186,7 @@ class PhiKS:
                 "block_plans": [(st.block_plan[b].s, st.block_plan[b].q) for b in range(max(st.nblocks, 1))],
                 "i8_mode_launches": st.i8_mode_launches, "i8_launches": st.i8_launches, "i8_ms": st.i8_ms,
                 "i8_flops": st.i8_flops, "i8_gemm_launches": st.i8_gemm_launches, "i8_gemm_ms": st.i8_gemm_ms,
-                "i8_chained_ops": st.i8_chained_ops}
+                "i8_chained_ops": st.i8_chained_ops, "shard_digit_ops": st.shard_digit_ops}
 
     GEMM_PATHS = {"auto": 0, "dmma": 1, "i8": 2}
 

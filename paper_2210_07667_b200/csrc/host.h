@@ -122,6 +122,8 @@ struct phiks_ctx {
   char* sym = nullptr;  // own symmetric region: control block + T/Y pools
   size_t sym_bytes = 0;
   size_t sym_slot = 0;  // bytes per pooled local tensor
+  size_t exch_off = 0;  // exponent exchange buffer of the sharded digit stages ([world][16][L0] doubles)
+  int64_t exch_l0 = 0;  // L0 = n_1⋯n_{d-2} it holds
   char* peer[kMaxRanks] = {nullptr};
   bool peer_ipc[kMaxRanks] = {false};
   bool peers_ready = false;
@@ -166,7 +168,7 @@ constexpr size_t kCtrlNormsBuf = kMaxRanks * kMaxBlocks * kMaxVecs * sizeof(doub
 constexpr size_t kCtrlBytes = 4096;
 static_assert(kCtrlNorms + 2 * kCtrlNormsBuf <= kCtrlBytes, "control block layout");
 static_assert(kCtrlErr + sizeof(int) <= kCtrlEpoch && kCtrlEpoch + 8 <= kCtrlNorms, "control block layout");
-constexpr int kShardChunk = 16;  // Tucker operators per sharded sub-batch (T and Y pools)
+constexpr int kShardChunk = kShardChunkMax;  // Tucker operators per sharded sub-batch (T and Y pools)
 constexpr uint64_t kBarrierTimeoutNs = 60ull * 1000 * 1000 * 1000;
 
 
@@ -322,6 +324,7 @@ struct Exec {
   // ---- int8 tensor-core route of plain mode products (ozaki.cu) ----
   int64_t i8_launches = 0;
   int64_t i8_chained = 0;  // Tucker operators run as chained int8 modes
+  int64_t shard_digit_ops = 0;  // sharded: Tucker operators whose stage 0 wrote digit planes to the owners
   double* oz_ws = nullptr;  // grown on demand, reused by every int8 launch of the apply (one stream)
   size_t oz_ws_bytes = 0;
   static constexpr int kOzDigits = 7;
@@ -393,10 +396,12 @@ struct Exec {
     }
   }
   // digit splits (+ chain exponents), then the GEMM (separate event pairs: kind 3 splits, kind 2 GEMM)
-  void oz_emit(const std::shared_ptr<OzakiParams>& pp, bool split_x) {
+  // mid: enqueued between the splits and the GEMM (the sharded stage-0 exponent exchange)
+  void oz_emit(const std::shared_ptr<OzakiParams>& pp, bool split_x, const std::function<void()>& mid = nullptr) {
     const OzakiParams& p = *pp;
     ++i8_launches;
     for (int phase = 0; phase < 2; ++phase) {
+      if (phase == 1 && mid) mid();
       const bool prof = !measure && h->profiling && !rec;
       if (prof) {
         if (h->ev_used == static_cast<int>(h->ev.size())) {
@@ -415,7 +420,7 @@ struct Exec {
       if (phase == 0) {
         emit("digits_i8", [pp, split_x](cudaStream_t s2) { return launch_ozaki_mode(*pp, s2, split_x, true, false); });
         if (split_x) ++launches;  // split_x + split_e (+ chain)
-        if (p.n_next > 0) ++launches;
+        if (p.n_next > 0 && !p.shard_stage0) ++launches;
       } else {
         emit("mode_product_i8", [pp](cudaStream_t s2) { return launch_ozaki_mode(*pp, s2, false, false, true); });
       }
@@ -465,12 +470,17 @@ struct Exec {
   }
   // last mode mlast writes fp64: the items' outputs (mlast = d − 1), or with rm set the
   // sharded stage-0 peer stores into symmetric-region offset kCtrlBytes + b·sym_slot
+  // With rm1 set (slab-sharded digit stages, shard_digits_ok): mode d−2 is stage 0, whose epilogue
+  // writes mode d's digit planes into the owners' T pools (rm: its peer-store geometry) after the
+  // cross-rank exponent exchange, then a barrier, and mode d−1 is stage 1 on the transposed slab,
+  // reading those planes and storing fp64 into the owners' Y pools (rm1)
   void tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size_t c1, int mlast = -1,
-                       const Remap* rm = nullptr) {
+                       const Remap* rm = nullptr, const Remap* rm1 = nullptr) {
     const int d = h->d, S = kOzDigits;
     if (mlast < 0) mlast = d - 1;
     const int64_t N = h->N;
     const int nt = static_cast<int>(c1 - c0);
+    const int st0 = rm1 ? d - 2 : -1;  // the stage-0 mode of the sharded digit path
     int nmin = h->n[0];
     for (int mu = 1; mu < d; ++mu) nmin = std::min(nmin, h->n[mu]);
     if (oz_chain_cap < static_cast<size_t>(nt)) {
@@ -484,8 +494,13 @@ struct Exec {
     }
     int64_t L = 1;
     for (int mu = 0; mu <= mlast && ok(); ++mu) {
-      const int n = h->n[mu];
-      const int64_t R = N / (L * n);
+      int n = h->n[mu];
+      int64_t R = N / (L * n);
+      if (rm1 && mu == d - 1) {  // stage 1: layout S_{d-1}, dims (L0·cb, n_d, 1)
+        n = h->gn[d - 1];
+        L = N / n;
+        R = 1;
+      }
       auto pp = std::make_shared<OzakiParams>();
       OzakiParams& p = *pp;
       std::memset(&p, 0, sizeof(p));
@@ -493,8 +508,12 @@ struct Exec {
       p.R = R;
       p.n = n;
       p.S = S;
-      p.n_next = mu < mlast ? h->n[mu + 1] : 0;
-      if (mu == mlast && rm) p.remap = *rm;
+      p.n_next = mu < mlast ? (mu == st0 ? h->gn[d - 1] : h->n[mu + 1]) : 0;
+      if (mu == mlast && rm) p.remap = rm1 ? *rm1 : *rm;
+      if (mu == st0) {
+        p.remap = *rm;
+        p.shard_stage0 = 1;
+      }
       const int64_t Cn = mu < mlast ? N / h->n[mu + 1] : 0;
       for (int b = 0; b < nt; ++b) {
         const TuckerItem& it = items[c0 + b];
@@ -515,10 +534,15 @@ struct Exec {
           p.e[p.ne++] = it.mats[mu];
         }
         OzakiTerm t{xs, es, nullptr, 1.0, nullptr, nullptr, nullptr};
-        if (mu < mlast) {
+        if (mu == st0) {  // the owners' T pools as digit pools: term b's plane s at (b·S + s)·N bytes
+          t.dig = reinterpret_cast<int8_t*>(kCtrlBytes + static_cast<size_t>(b) * S * N);
+          t.nmx = oz_mx + static_cast<int64_t>(b) * L;
+        } else if (mu < mlast) {
           t.dig = oz_dig[mu % 2] + static_cast<int64_t>(b) * S * N;
           t.nex = oz_ex[mu % 2] + static_cast<int64_t>(b) * Cn;
           t.nmx = oz_mx + static_cast<int64_t>(b) * (N / (static_cast<int64_t>(n) * h->n[mu + 1]));
+        } else if (rm1) {
+          t.out = reinterpret_cast<double*>(kCtrlBytes + static_cast<size_t>(kShardChunk + c0 + b) * h->sym_slot);
         } else if (rm) {
           t.out = reinterpret_cast<double*>(kCtrlBytes + static_cast<size_t>(c0 + b) * h->sym_slot);
         } else {
@@ -534,17 +558,44 @@ struct Exec {
       ozaki_bind_workspace(p, oz_ws);
       if (mu > 0) {  // A: the previous product's digit planes and exponent bounds
         p.nx = nt;
-        p.xs = oz_dig[(mu - 1) % 2];
+        p.xs = (rm1 && mu == d - 1) ? reinterpret_cast<int8_t*>(h->sym + kCtrlBytes) : oz_dig[(mu - 1) % 2];
         p.xsc = oz_ex[(mu - 1) % 2];
         p.a_mn = 1;
       } else {
         p.nx = nx_keep;
       }
-      oz_emit(pp, mu == 0);
+      if (mu == st0) {
+        // next-mode exponents across the ranks: partial maxima to every peer, barrier, tables
+        OzShardExch ex{};
+        ex.rank = h->rank;
+        ex.world = h->world;
+        ex.nterms = nt;
+        ex.L0 = L;
+        ex.R = R;
+        ex.kstart = static_cast<int>(blk_start(h->gn[d - 2], h->world, h->rank));
+        ex.cb = static_cast<int>(blk_cnt(h->gn[d - 2], h->world, h->rank));
+        ex.exch = reinterpret_cast<const double*>(h->sym + h->exch_off);
+        for (int k = 0; k < h->world; ++k) ex.dst[k] = reinterpret_cast<double*>(h->peer[k] + h->exch_off);
+        for (int b = 0; b < nt; ++b) {
+          ex.xsc[b] = p.xsc + static_cast<int64_t>(p.terms[b].xslot) * (L * R);
+          ex.eb[b] = p.eb + static_cast<int64_t>(p.terms[b].eslot) * n;
+          ex.nmx[b] = p.terms[b].nmx;
+          ex.xsc1[b] = oz_ex[mu % 2] + static_cast<int64_t>(b) * (L * ex.cb);
+        }
+        auto exs = std::make_shared<OzShardExch>(ex);
+        oz_emit(pp, mu == 0, [this, exs] {
+          emit("oz_shard_pmax", [exs](cudaStream_t s2) { return launch_oz_shard_pmax(*exs, s2); });
+          barrier();
+          emit("oz_shard_tables", [exs](cudaStream_t s2) { return launch_oz_shard_tables(*exs, s2); });
+        });
+        barrier();  // every rank's digit planes are in place before stage 1 reads them
+      } else {
+        oz_emit(pp, mu == 0);
+      }
       L *= n;
     }
     i8_chained += nt;
-    if (mlast < d - 1) return;  // the sharded caller completes and counts the operators
+    if (mlast < d - 1 || rm1) return;  // the sharded caller completes and counts the operators
     int64_t nsum = 0;
     for (int mu = 0; mu < d; ++mu) nsum += h->n[mu];
     tucker_ops += nt;
@@ -1032,6 +1083,22 @@ struct Exec {
     mu_flops += static_cast<double>(nb) * 8.0 * static_cast<double>(h->Nc) * static_cast<double>(nsum);
   }
 
+  // the sharded digit stages apply: uniform blocks (every warp's 32 columns of stage 0 on one
+  // owner), MN-major digit tiles on both stages (L0 % 128 == 0), mode d on the int8 path, the
+  // exchange buffer sized for L0, and the batch within the chain buffers
+  bool shard_digits_ok(size_t nb) const {
+    const int d = h->d, P = h->world;
+    if (d < 3 || !h->exch_off || nb > chain_cap()) return false;
+    int64_t L0 = 1;
+    for (int mu = 0; mu + 2 < d; ++mu) L0 *= h->gn[mu];
+    const int na = h->gn[d - 2], nd = h->gn[d - 1];
+    if (na % P || nd % P || (na / P) % 32 || L0 % 128) return false;
+    if (L0 > h->exch_l0) return false;
+    if (!ozaki_supported(L0 * (na / P), nd, 1, kOzDigits) || nd % 16) return false;
+    if (h->gemm_path == PHIKS_GEMM_AUTO && nd < 128) return false;
+    return true;
+  }
+
   void tucker_raw_sharded(const std::vector<TuckerItem>& items) {
     if (!ok() || items.empty()) return;
     if (h->cplx) {
@@ -1041,8 +1108,10 @@ struct Exec {
     const int d = h->d, P = h->world, rk = h->rank;
     const int64_t N = h->N;
     const size_t nb = items.size();
-    // int8 chain over the local modes into stage 0 (DESIGN.md §4d, §0(e))
+    // int8 chain over the local modes into stage 0 (DESIGN.md §4d, §0(e)); with shard_digits_ok
+    // also through stage 1 (stage 0 writes mode d's digit planes into the owners' pools)
     const bool chained = d >= 3 && ozaki_chain_route(items, 0, nb, d - 2);
+    const bool digits = chained && shard_digits_ok(items.size());
     auto& scr = scr_pool;
     if (d >= 3 && !chained)
       while (scr[0].size() < nb) scr[0].push_back(ar->alloc_doubles(N));
@@ -1081,6 +1150,18 @@ struct Exec {
     };
     const Remap ra = remap_of(s0), rb = remap_of(s1);
     (void)L;
+    if (digits) {
+      // every mode chained: stage 0 stores mode d's digit planes into the owners' T pools,
+      // stage 1 (after the exchange barriers inside) reads them and stores fp64 into the Y pools
+      tucker_chain_i8(items, 0, nb, d - 1, &ra, &rb);
+      barrier();
+      shard_digit_ops += static_cast<int64_t>(nb);
+      int64_t nsum = 0;
+      for (int mu = 0; mu < d; ++mu) nsum += h->gn[mu];
+      tucker_ops += static_cast<int64_t>(nb);
+      mu_flops += static_cast<double>(nb) * 2.0 * static_cast<double>(N) * static_cast<double>(nsum);
+      return;
+    }
     if (chained) {
       // modes 1..d−2 chained on the slab, stage 0 (mode d−1) reading their digits and
       // storing fp64 into the owners' T pools
@@ -1621,6 +1702,7 @@ struct ApplyRun {
     S.tucker_ops = ex.tucker_ops;
     S.i8_mode_launches = ex.i8_launches;
     S.i8_chained_ops = ex.i8_chained;
+    S.shard_digit_ops = ex.shard_digit_ops;
     S.mu_mode_flops = ex.mu_flops;
     S.expm_flops = ex.expm_flops;
     S.workspace_bytes = need;

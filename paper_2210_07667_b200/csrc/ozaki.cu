@@ -345,6 +345,44 @@ __global__ void __launch_bounds__(256) oz_chain_kernel(const OzakiParams p) {
   }
 }
 
+// ---- slab-sharded chained stage 0: cross-rank next-mode exponents (phiks_internal.h) ----
+__global__ void __launch_bounds__(256) oz_shard_pmax_kernel(const OzShardExch e) {
+  const int t = blockIdx.y;
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (l >= e.L0) return;
+  const double* x = e.xsc[t] + l;
+  double m = -2000.0;
+  bool nan = false;
+  for (int64_t r = 0; r < e.R; ++r) {
+    const double v = x[e.L0 * r];
+    nan |= isnan(v);
+    m = fmax(m, v);
+  }
+  if (nan) m = __longlong_as_double(0x7ff8000000000000ll);
+  const int64_t off = (static_cast<int64_t>(e.rank) * kShardChunkMax + t) * e.L0 + l;
+  for (int k = 0; k < e.world; ++k) e.dst[k][off] = m;  // NVLink peer stores (own buffer at k == rank)
+}
+
+__global__ void __launch_bounds__(256) oz_shard_tables_kernel(const OzShardExch e) {
+  const int t = blockIdx.y;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (idx >= e.L0 * e.cb) return;
+  const int64_t l = idx % e.L0;
+  const int jl = static_cast<int>(idx / e.L0);
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  double m = -2000.0;
+  bool nan = false;
+  for (int k = 0; k < e.world; ++k) {
+    const double v = e.exch[(static_cast<int64_t>(k) * kShardChunkMax + t) * e.L0 + l];
+    nan |= isnan(v);
+    m = fmax(m, v);
+  }
+  if (nan) m = qnan;
+  if (jl == 0) e.nmx[t][l] = m;
+  const double x = __ldg(e.eb[t] + e.kstart + jl) + m;
+  e.xsc1[t][idx] = isnan(x) ? qnan : fmin(fmax(x, -1100.0), 1025.0);
+}
+
 // ---- tcgen05 / TMA / mbarrier helpers ----
 __device__ __forceinline__ void oz_mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(oz_smem_u32(bar)), "r"(count) : "memory");
@@ -748,8 +786,22 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
       // q0 + qi as one 32-bit word
       const int qi = lane & 3;
       const uint32_t sel1 = (qi & 1) ? 0x3715u : 0x6240u, sel2 = (qi & 2) ? 0x3276u : 0x5410u;
-      const int64_t rowoff = l + L * static_cast<int64_t>(p.n) * r, cs = L;
-      int8_t* dq = term.dig + (rowoff - qi) + cs * (j0 + qi);
+      int64_t rowoff = l + L * static_cast<int64_t>(p.n) * r, cs = L;
+      int8_t* dbase = term.dig;
+      int jrel = j0;
+      if constexpr (REM) {
+        // slab-sharded stage 0: the next mode's digit planes go to the owner
+        // k of column j in its transposed layout (uniform blocks of cq ≥ EPC columns, so the
+        // warp's columns share one owner): plane offset l + kstride[k]·r + kroff[k] +
+        // colstride·(j − kstart[k]); the owners' planes have the local plane stride N
+        const Remap& rm = p.remap;
+        const int k = j0 / rm.cq;
+        dbase = reinterpret_cast<int8_t*>(rm.base[k] + reinterpret_cast<uintptr_t>(term.dig));
+        rowoff = l + rm.kstride[k] * r + rm.kroff[k];
+        cs = rm.colstride;
+        jrel = j0 - rm.kstart[k];
+      }
+      int8_t* dq = dbase + (rowoff - qi) + cs * (jrel + qi);
       uint32_t* dqs[S];
 #pragma unroll
       for (int sd = 0; sd < S; ++sd) dqs[sd] = reinterpret_cast<uint32_t*>(dq + sd * N);
@@ -1121,7 +1173,11 @@ bool oz_split_tma_ok(const OzakiParams& p) {
 
 template <int S, bool AMN, bool OUTD, bool SE, bool REM = false>
 cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
-  if (!OUTD && !REM && p.remap.world > 0) return oz_gemm_go<S, AMN, OUTD, SE, !OUTD>(p, st, ta, tb);
+  if constexpr (!REM && (AMN || !OUTD)) {  // peer-store epilogues: fp64 outputs, or AMN next-mode digits
+    if (p.remap.world > 0) return oz_gemm_go<S, AMN, OUTD, SE, true>(p, st, ta, tb);
+  } else if constexpr (!REM) {
+    if (p.remap.world > 0) return cudaErrorInvalidValue;
+  }
   using G = OzGeom<S, oz_nst(AMN, OUTD)>;
   static bool gattr = false;
   static int sms = 0;
@@ -1195,7 +1251,7 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
     cudaMemsetAsync(p.eext + 2 * p.ne, 0, sizeof(int) * p.ne, st);
   }
   if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
-  if (split_e && p.n_next > 0 && p.nterms > 0) {  // next-mode exponent bounds (chained modes)
+  if (split_e && p.n_next > 0 && p.nterms > 0 && !p.shard_stage0) {  // next-mode exponent bounds (chained modes)
     const int64_t m = C / p.n_next;
     oz_chain_kernel<<<dim3(static_cast<unsigned>((m + 31) / 32), p.nterms, (p.n + 63) / 64), 256, 0, st>>>(p);
   }
@@ -1256,6 +1312,18 @@ void ozaki_bind_workspace(OzakiParams& p, void* ws) {
 bool ozaki_supported(int64_t L, int n, int64_t R, int S) {
   const int64_t C = L * R;
   return S >= 6 && S <= 7 && n >= 1 && n <= kOzMaxN && C >= 1 && C < (int64_t(1) << 31);
+}
+
+cudaError_t launch_oz_shard_pmax(const OzShardExch& e, cudaStream_t st) {
+  if (e.nterms == 0) return cudaSuccess;
+  oz_shard_pmax_kernel<<<dim3(static_cast<unsigned>((e.L0 + 255) / 256), e.nterms), 256, 0, st>>>(e);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_oz_shard_tables(const OzShardExch& e, cudaStream_t st) {
+  if (e.nterms == 0) return cudaSuccess;
+  oz_shard_tables_kernel<<<dim3(static_cast<unsigned>((e.L0 * e.cb + 255) / 256), e.nterms), 256, 0, st>>>(e);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_x, bool split_e, bool gemm) {

@@ -148,8 +148,35 @@ struct OzakiParams {
   int cplx_j;    // complex μ ≥ 2 product: fibres [x ; Jx] of length K = 2n against
                  // E = [Re M | Im M] (n × 2n, column-major, Im M right after Re M), so y = Re M·x + J·Im M·x
   int n_next;    // chained: n_{μ+1} (0: plain fp64 outputs)
-  Remap remap;   // slab-sharded stage (world > 0): fp64 outputs go to the owner rank; out = byte offset
+  Remap remap;   // slab-sharded stage (world > 0): fp64 outputs (out) or next-mode digit planes (dig,
+                 // AMN only) go to the owner rank; out / dig = byte offsets in the owners' regions
+  int shard_stage0;  // 1: the next-mode exponents come from the cross-rank exchange
+                     // (launch_oz_shard_pmax / launch_oz_shard_tables), not oz_chain_kernel
 };
+// Slab-sharded chained stage 0: the next mode (d) runs along i_d, which the
+// ranks' slabs partition, so its fibre exponents e(l, j) = b_j + Mx(l), Mx(l) = max over all i_d
+// of the stage-0 input fibre exponents ex(l, i_d), need a cross-rank max.  pmax: every rank writes
+// its slab's partial max of term t into slot [rank][t][l] (kShardChunkMax terms per rank) of every
+// peer's exchange buffer; after a barrier, tables: Mx(l) over the ranks' slots → nmx[t][l] (the
+// stage-0 epilogue's digit exponents) and the stage-1 A fibre exponents of this rank's transposed
+// slab, xsc1[t][l + L0·jl] = b_{kstart + jl} + Mx(l), jl < cb (clamped like oz_chain_kernel;
+// NaN if any input fibre was non-finite).
+constexpr int kShardChunkMax = 16;
+struct OzShardExch {
+  int rank, world, nterms;
+  int64_t L0, R;                       // stage-0 launch geometry (L0, n_{d-1}, R = local slab of i_d)
+  const double* xsc[kMaxTerms];        // per term: its input fibre exponents, L0·R entries
+  double* dst[kMaxRanks];              // peers' exchange buffers [world][kShardChunkMax][L0]
+  // tables (own buffer)
+  const double* exch;
+  int kstart, cb;
+  const double* eb[kMaxTerms];         // per term: b_j of its stage-0 matrix (n_{d-1} entries)
+  double* nmx[kMaxTerms];              // per term: Mx, L0 entries
+  double* xsc1[kMaxTerms];             // per term: stage-1 fibre exponents, L0·cb entries
+};
+cudaError_t launch_oz_shard_pmax(const OzShardExch& e, cudaStream_t st);
+cudaError_t launch_oz_shard_tables(const OzShardExch& e, cudaStream_t st);
+
 bool ozaki_supported(int64_t L, int n, int64_t R, int S);
 size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne, int K = 0);  // K: contraction (0: n)
 void ozaki_bind_workspace(OzakiParams& p, void* ws);  // sets Kp and the workspace pointers

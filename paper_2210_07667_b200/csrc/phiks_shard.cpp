@@ -64,6 +64,11 @@ static phiks_status create_sharded_impl(int nblocks, int d, const int* n, const 
     if (cplx) slot *= 2;
     h->sym_slot = (static_cast<size_t>(slot) * sizeof(double) + 255) & ~size_t(255);
     h->sym_bytes = kCtrlBytes + 2 * kShardChunk * h->sym_slot;
+    if (!cplx && d >= 3) {  // exponent exchange of the sharded int8 digit stages (host.h shard_digits_ok)
+      h->exch_off = h->sym_bytes;
+      h->exch_l0 = L0;
+      h->sym_bytes += (static_cast<size_t>(world) * kShardChunk * L0 * sizeof(double) + 255) & ~size_t(255);
+    }
     if (cudaMalloc(reinterpret_cast<void**>(&h->sym), h->sym_bytes) != cudaSuccess) {
       phiks_destroy(h);
       return fail(PHIKS_ERR_NOMEM, "symmetric region cudaMalloc");

@@ -238,3 +238,46 @@ def test_sharded_complex_int8(dims, world, mode):
     for r in ranks:
         r.close()
     compare_oracle(pb, gathered, 2)
+
+
+# ---- sharded digit stages: stage 0 exchanges the next-mode exponent maxima
+# across the ranks and writes mode d's digit planes straight into the owners' pools; stage 1
+# reads them (no fp64 transposition buffer, no re-split) ----
+def _fd_factors(dims):
+    out = []
+    for k, n in enumerate(dims):
+        if k % 2 == 0:
+            out.append((0.5 + 0.3 * k) * W.fd_dxx_neumann(n))
+        else:
+            out.append(W.fd_dxx_dirichlet(n) + (2.0 + k) * W.fd_dx_dirichlet(n))
+    return out
+
+
+@pytest.mark.parametrize("dims,world,mode,kind", [((128, 64, 16), 2, "same", "fd"),
+                                                  ((256, 64, 32), 2, "lincomb", "fd"),
+                                                  ((128, 128, 16), 4, "same", "rand"),
+                                                  ((128, 256, 16), 8, "lincomb", "fd"),
+                                                  ((128, 16, 64, 16), 2, "same", "rand"),
+                                                  ((256, 256, 32), 8, "same", "fd")])
+def test_sharded_digit_stages(dims, world, mode, kind):
+    seed = 1700 + sum(dims) + world
+    fac = _fd_factors(dims) if kind == "fd" else W.random_factors(dims, seed=seed, scale=4.0)
+    tau = 2e-3 if kind == "fd" else 0.6
+    ells = (0, 1, 2) if mode == "same" else (0, 1, 2, 3)
+    vs = [W.random_tensor(dims, seed=seed + 1 + k) for k in range(1 if mode == "same" else len(ells))]
+    pb = W.Problem(f"sdig_{dims}_{world}_{mode}", dims, fac, tau, mode, ells, vs, 2)
+    chain = 1 if kind == "fd" else 2  # Metzler FD factors chain under the default guard
+    outs, stats = run_sharded(pb, world, path="i8", chain=chain)
+    assert all(s["shard_digit_ops"] == s["tucker_ops"] > 0 for s in stats), \
+        [(s["shard_digit_ops"], s["tucker_ops"]) for s in stats]
+    compare_oracle(pb, outs, pb.n_scales)
+    # one GPU, chained int8: the same digits (the exponent maxima are global either way) and
+    # exact integer products; only the combination passes group their sums differently
+    op = PhiKS(pb.A)
+    op.set_gemm_path("i8")
+    op.set_option("chain", chain)
+    single = op.apply(pb.tau, pb.ells, [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).to(DEV) for v in pb.vs],
+                      mode=pb.mode, n_scales=pb.n_scales)
+    torch.cuda.synchronize()
+    for a, b in zip(outs, single):
+        assert rel2(a, b.cpu().numpy()) <= 1e-13
