@@ -124,6 +124,7 @@ struct phiks_ctx {
   size_t sym_slot = 0;  // bytes per pooled local tensor
   size_t exch_off = 0;  // exponent exchange buffer of the sharded digit stages ([world][16][L0] doubles)
   int64_t exch_l0 = 0;  // L0 = n_1⋯n_{d-2} it holds
+  size_t xpool_off = 0, xpool_half = 0;  // sharded exponential stage: all-gathered matrices, two halves
   char* peer[kMaxRanks] = {nullptr};
   bool peer_ipc[kMaxRanks] = {false};
   bool peers_ready = false;
@@ -165,8 +166,10 @@ constexpr size_t kCtrlErr = kMaxRanks * sizeof(uint64_t);          // int err
 constexpr size_t kCtrlEpoch = 128;                                 // uint64 barrier count
 constexpr size_t kCtrlNorms = 256;                                 // double norms[2][kMaxRanks][kMaxVecs]
 constexpr size_t kCtrlNormsBuf = kMaxRanks * kMaxBlocks * kMaxVecs * sizeof(double);
+constexpr size_t kCtrlFlags2 = kCtrlNorms + 2 * kCtrlNormsBuf;       // uint64 flags[kMaxRanks], barrier channel 1
+constexpr size_t kCtrlEpoch2 = kCtrlFlags2 + kMaxRanks * sizeof(uint64_t);  // uint64 channel-1 barrier count
 constexpr size_t kCtrlBytes = 4096;
-static_assert(kCtrlNorms + 2 * kCtrlNormsBuf <= kCtrlBytes, "control block layout");
+static_assert(kCtrlEpoch2 + 8 <= kCtrlBytes, "control block layout");
 static_assert(kCtrlErr + sizeof(int) <= kCtrlEpoch && kCtrlEpoch + 8 <= kCtrlNorms, "control block layout");
 constexpr int kShardChunk = kShardChunkMax;  // Tucker operators per sharded sub-batch (T and Y pools)
 constexpr uint64_t kBarrierTimeoutNs = 60ull * 1000 * 1000 * 1000;
@@ -269,6 +272,7 @@ struct Exec {
   std::vector<double*> scr_pool[2];  // N-sized scratch reused by every tucker_batch
   std::vector<double*> y_pool;       // per-item Tucker results of split batches
   int split = 0;                     // 1: quadrature sums as a separate pass, 2: also squaring
+  int half = 0;                      // workspace half of the apply (sharded: the expm pool half too)
   double mu_flops = 0.0, expm_flops = 0.0;
   phiks_status status = PHIKS_OK;
   int64_t barriers = 0;
@@ -302,7 +306,10 @@ struct Exec {
       check(fn(st), what);
   }
   // cross-rank barrier of a sharded handle (device-side, stream-ordered)
-  void barrier() {
+  // channel 1: the exponential stage's all-gather, which runs on the handle's pre stream
+  // concurrently with the previous apply's tail on the compute stream (its own flags and count,
+  // so the two streams' barriers never pair up across ranks)
+  void barrier(int channel = 0) {
     ++barriers;
     if (!ok() || !h->sharded()) return;
     ++launches;
@@ -314,9 +321,10 @@ struct Exec {
     BarrierParams bp{};
     bp.rank = h->rank;
     bp.world = h->world;
-    bp.epoch = reinterpret_cast<uint64_t*>(h->sym + kCtrlEpoch);
+    bp.epoch = reinterpret_cast<uint64_t*>(h->sym + (channel ? kCtrlEpoch2 : kCtrlEpoch));
     bp.timeout_ns = kBarrierTimeoutNs;
-    for (int k = 0; k < h->world; ++k) bp.peer_flags[k] = reinterpret_cast<uint64_t*>(h->peer[k] + kCtrlFlags);
+    for (int k = 0; k < h->world; ++k)
+      bp.peer_flags[k] = reinterpret_cast<uint64_t*>(h->peer[k] + (channel ? kCtrlFlags2 : kCtrlFlags));
     bp.err = reinterpret_cast<int*>(h->sym + kCtrlErr);
     check(launch_barrier(bp, st), "barrier");
   }
@@ -1088,7 +1096,8 @@ struct Exec {
   // exchange buffer sized for L0, and the batch within the chain buffers
   bool shard_digits_ok(size_t nb) const {
     const int d = h->d, P = h->world;
-    if (d < 3 || !h->exch_off || nb > chain_cap()) return false;
+    (void)nb;
+    if (d < 3 || !h->exch_off) return false;
     int64_t L0 = 1;
     for (int mu = 0; mu + 2 < d; ++mu) L0 *= h->gn[mu];
     const int na = h->gn[d - 2], nd = h->gn[d - 1];
@@ -1153,8 +1162,11 @@ struct Exec {
     if (digits) {
       // every mode chained: stage 0 stores mode d's digit planes into the owners' T pools,
       // stage 1 (after the exchange barriers inside) reads them and stores fp64 into the Y pools
-      tucker_chain_i8(items, 0, nb, d - 1, &ra, &rb);
-      barrier();
+      const size_t cap = chain_cap();
+      for (size_t s0c = 0; s0c < nb && ok(); s0c += cap) {  // each piece: both stages and their barriers
+        tucker_chain_i8(items, s0c, std::min(nb, s0c + cap), d - 1, &ra, &rb);
+        barrier();
+      }
       shard_digit_ops += static_cast<int64_t>(nb);
       int64_t nsum = 0;
       for (int mu = 0; mu < d; ++mu) nsum += h->gn[mu];
@@ -1338,6 +1350,7 @@ struct ExpReq {
 };
 
 void expm_batch(Exec& ex, double tau, std::vector<ExpReq>& reqs);
+void expm_stage(Exec& ex, double tau, std::vector<ExpReq>& reqs);  // expm_batch, split over the ranks of a sharded handle
 
 struct Job {
   int mode;
@@ -1609,6 +1622,7 @@ struct ApplyRun {
     ar.cap = need;
     ex = Exec{h, cs, false, &ar};
     ex.split = split;
+    ex.half = half;
     ex.rec = rec;
     bind(false);
     if (host_mem && rec) return fail(PHIKS_ERR_ARG, "recorded applies take device memory");

@@ -14,6 +14,8 @@
 
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "phiks_internal.h"
 
 namespace phiks {
@@ -1136,6 +1138,27 @@ __global__ void scatter_small_kernel(const __grid_constant__ ScatterParams p) {
 
 cudaError_t launch_scatter_small(const ScatterParams& p, cudaStream_t st) {
   scatter_small_kernel<<<1, 128, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+__global__ void peer_copy_kernel(const __grid_constant__ PeerCopyParams p) {
+  const int i = blockIdx.y;
+  const int64_t cnt = p.count[i];
+  const double* src = p.src[i];
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < cnt;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = src[e];
+    for (int k = 0; k < p.world; ++k) reinterpret_cast<double*>(p.base[k] + p.off[i])[e] = v;
+  }
+  __threadfence_system();  // peer stores visible before the barrier kernel that follows
+}
+
+cudaError_t launch_peer_copy(const PeerCopyParams& p, cudaStream_t st) {
+  if (p.nitems == 0) return cudaSuccess;
+  int64_t mx = 0;
+  for (int i = 0; i < p.nitems; ++i) mx = mx > p.count[i] ? mx : p.count[i];
+  const unsigned bx = static_cast<unsigned>(std::min<int64_t>((mx + 255) / 256, 64));
+  peer_copy_kernel<<<dim3(bx, p.nitems), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -123,6 +123,52 @@ void expm_batch(Exec& ex, double tau, std::vector<ExpReq>& reqs) {
   for (size_t i = 0; i < reqs.size(); ++i) reqs[i].result = sts[i].buf[sts[i].cur];
 }
 
+// Stage A of one apply.  Slab-sharded handles split it over the ranks:
+// request i is computed by rank i mod P, which stores the n×n result into slot i of every
+// rank's exponential pool (symmetric region, the apply's half) by NVLink peer stores; a
+// channel-1 barrier, then every rank reads all results from its own pool.  The request list
+// and the slot offsets are identical on every rank (same plans).
+void expm_stage(Exec& ex, double tau, std::vector<ExpReq>& reqs) {
+  phiks_ctx* h = ex.h;
+  const int P = h->world;
+  std::vector<size_t> off(reqs.size());
+  size_t need = 0;
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    off[i] = need;
+    const size_t n = static_cast<size_t>(h->factors[reqs[i].f].n);
+    need += (n * n * sizeof(double) + 255) & ~size_t(255);
+  }
+  if (!h->sharded() || !h->xpool_off || need > h->xpool_half || reqs.size() < 2) {
+    expm_batch(ex, tau, reqs);
+    return;
+  }
+  std::vector<ExpReq> mine;
+  std::vector<size_t> mine_idx;
+  for (size_t i = h->rank; i < reqs.size(); i += P) {
+    mine.push_back(reqs[i]);
+    mine_idx.push_back(i);
+  }
+  if (!mine.empty()) expm_batch(ex, tau, mine);
+  if (!ex.ok()) return;
+  const size_t pool = h->xpool_off + static_cast<size_t>(ex.half) * h->xpool_half;
+  for (size_t c0 = 0; c0 < mine.size(); c0 += kMaxPeerCopy) {
+    auto pc = std::make_shared<PeerCopyParams>();
+    std::memset(pc.get(), 0, sizeof(PeerCopyParams));
+    pc->world = P;
+    for (int k = 0; k < P; ++k) pc->base[k] = h->peer[k];
+    for (size_t i = c0; i < std::min(mine.size(), c0 + kMaxPeerCopy); ++i) {
+      const int64_t n = h->factors[mine[i].f].n;
+      pc->src[pc->nitems] = mine[i].result;
+      pc->off[pc->nitems] = pool + off[mine_idx[i]];
+      pc->count[pc->nitems] = n * n;
+      ++pc->nitems;
+    }
+    ex.emit("peer_copy_expm", [pc](cudaStream_t s) { return launch_peer_copy(*pc, s); });
+  }
+  ex.barrier(1);
+  for (size_t i = 0; i < reqs.size(); ++i) reqs[i].result = reinterpret_cast<double*>(h->sym + pool + off[i]);
+}
+
 // ---------------------------------------------------------------------------
 // The whole φ-action (stages A-D) on device pointers.
 // vin[ℓ] (ℓ = 0..p) device input tensors or nullptr; out_same[ℓ][j] / out_lin[j]
@@ -190,7 +236,7 @@ void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
     if (p == 0)
       for (int f : J.facs) reqs.push_back({f, 1.0 / std::ldexp(1.0, J.s)});
   }
-  expm_batch(ex, tau, reqs);
+  expm_stage(ex, tau, reqs);
   if (!ex.ok()) return;
   int max_lev = 0;
   for (JS& J : js) {

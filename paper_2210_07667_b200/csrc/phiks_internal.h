@@ -161,7 +161,7 @@ struct OzakiParams {
 // stage-0 epilogue's digit exponents) and the stage-1 A fibre exponents of this rank's transposed
 // slab, xsc1[t][l + L0·jl] = b_{kstart + jl} + Mx(l), jl < cb (clamped like oz_chain_kernel;
 // NaN if any input fibre was non-finite).
-constexpr int kShardChunkMax = 16;
+constexpr int kShardChunkMax = 24;
 struct OzShardExch {
   int rank, world, nterms;
   int64_t L0, R;                       // stage-0 launch geometry (L0, n_{d-1}, R = local slab of i_d)
@@ -217,6 +217,17 @@ struct ScatterParams {
   double* dst[kMaxRanks];
 };
 cudaError_t launch_scatter_small(const ScatterParams& p, cudaStream_t st);
+// item i: count[i] doubles from src[i] to byte offset off[i] of every rank's region base[k]
+// (the sharded exponential stage's all-gather of the small matrices)
+constexpr int kMaxPeerCopy = 32;
+struct PeerCopyParams {
+  int world, nitems;
+  const double* src[kMaxPeerCopy];
+  size_t off[kMaxPeerCopy];
+  int64_t count[kMaxPeerCopy];
+  char* base[kMaxRanks];
+};
+cudaError_t launch_peer_copy(const PeerCopyParams& p, cudaStream_t st);
 cudaError_t launch_fp64_peak(int kind, int blocks, int64_t iters, double* sink, cudaStream_t st,
                              double* flops);
 

@@ -64,6 +64,13 @@ static phiks_status create_sharded_impl(int nblocks, int d, const int* n, const 
     if (cplx) slot *= 2;
     h->sym_slot = (static_cast<size_t>(slot) * sizeof(double) + 255) & ~size_t(255);
     h->sym_bytes = kCtrlBytes + 2 * kShardChunk * h->sym_slot;
+    {  // exponential pool (orchestrate.cpp expm_stage): 12 matrices per distinct factor (q ≤ 12), two halves
+      size_t half = 0;
+      for (const auto& F : h->factors) half += 12 * ((static_cast<size_t>(F.n) * F.n * sizeof(double) + 255) & ~size_t(255));
+      h->xpool_off = h->sym_bytes;
+      h->xpool_half = half;
+      h->sym_bytes += 2 * half;
+    }
     if (!cplx && d >= 3) {  // exponent exchange of the sharded int8 digit stages (host.h shard_digits_ok)
       h->exch_off = h->sym_bytes;
       h->exch_l0 = L0;
