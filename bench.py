@@ -399,6 +399,28 @@ def b200_arm(args):
         t = float(tt.item())
     value = flops_step * world * args.steps / t / 1e9
 
+    # ---- N > 1: self-check of the gathered slabs of the last timed step against one GPU ----
+    parity = None
+    if world > 1:
+        torch.cuda.synchronize()
+        gathered = []
+        for o in outs:
+            parts = [torch.empty_like(o) for _ in range(world)]
+            dist.all_gather(parts, o)
+            gathered.append(torch.cat(parts) if rank == 0 else None)
+        if rank == 0:
+            ref_op = PhiKS(blocks)
+            full_in = [torch.from_numpy(W.as_flat(pb.vs[0]).copy()).to(dev) for pb in wl.problems]
+            ref = ref_op.apply(pb0.tau, pb0.ells, full_in, mode=pb0.mode, n_scales=pb0.n_scales, stream=stream)
+            torch.cuda.synchronize()
+            errs = [float(torch.linalg.norm(g - r) / torch.linalg.norm(r)) for g, r in zip(gathered, ref)]
+            parity = {"vs": "the same apply on one GPU (rank 0, unsharded handle)", "max_rel_2norm_err": max(errs),
+                      "tol": 1e-12, "pass": max(errs) <= 1e-12, "outputs": len(errs)}
+            del ref_op, full_in, ref
+        del gathered
+        torch.cuda.empty_cache()
+        dist.barrier()
+
     # ---- end-to-end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -451,7 +473,7 @@ def b200_arm(args):
                        "l2": "inputs larger than L2 (134 MB per vector > 126 MB L2)", "plans": plans,
                        "mu_mode_gflop_per_step": flops_step / 1e9},
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
-            "roofline": roof, "cpu_baseline": cpu,
+            "roofline": roof, "cpu_baseline": cpu, "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -880,7 +880,7 @@ struct OzGeom {
   static constexpr int B_KB = S * kOzBN * kOzBK;              // resident E slices per k-block
   static constexpr int B_BYTES = (kOzMaxNRes / kOzBK) * B_KB; // resident (Kp ≤ 256) or a 2-block ring (SE)
   static constexpr int SMEM = NST * A_BYTES + B_BYTES + 1024 /*align*/ + 512 /*barriers*/;
-  static constexpr int EPC = 32;                               // columns per epilogue warp (16: measured slower)
+  static constexpr int EPC = 32;  // columns per epilogue warp (16, i.e. 16 epilogue warps at 96 registers: 8 % slower, r02)
   static constexpr int EPI_WARPS = 4 * kOzBN / EPC;             // 2 per TMEM lane quarter (column halves)
   static constexpr int THREADS = 64 + EPI_WARPS * 32;
   static_assert(S * kOzBN <= 512, "TMEM holds one 64-column accumulator per diagonal");
