@@ -6,9 +6,10 @@ the merged squaring batch, 3 modes each, inputs split in chunks of 8):
 
   ncu --set full -k regex:oz_gemm -s 10 -c 10 python scripts/profile_bench.py
 
-with PHIKS_GEMM=dmma, 6 DMMA launches of the 64x128 instantiation:
+with GEMM_PATH=dmma (the handle's phiks_set_gemm_path), 6 DMMA launches of the 64x128
+instantiation:
 
-  PHIKS_GEMM=dmma ncu --set full --kernel-name-base demangled \
+  GEMM_PATH=dmma ncu --set full --kernel-name-base demangled \
       -k "regex:tma_kernel<.int.64, .int.128" -s 6 -c 6 python scripts/profile_bench.py
 """
 import os
@@ -24,6 +25,7 @@ from paper_2210_07667_b200 import workloads as W  # noqa: E402
 wl = W.config(3)
 pb = wl.problems[0]
 op = PhiKS([p.A for p in wl.problems])
+op.set_gemm_path(os.environ.get("GEMM_PATH", "auto"))
 vs = [torch.from_numpy(np.ascontiguousarray(W.as_flat(p.vs[0]))).cuda() for p in wl.problems]
 outs = [torch.empty_like(vs[0]) for _ in range(len(wl.problems) * len(pb.ells))]
 for _ in range(2):
