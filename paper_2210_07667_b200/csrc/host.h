@@ -501,6 +501,9 @@ struct Exec {
       oz_chain_cap = cap;
     }
     int64_t L = 1;
+    std::vector<const double*> prev_e;  // the previous mode's matrices, split in oz_ws (bind: E region first)
+    int prev_n = -1;
+    double* prev_ws = nullptr;
     for (int mu = 0; mu <= mlast && ok(); ++mu) {
       int n = h->n[mu];
       int64_t R = N / (L * n);
@@ -564,6 +567,12 @@ struct Exec {
       const int nx_keep = p.nx;
       p.nx = nx_split;
       ozaki_bind_workspace(p, oz_ws);
+      // the same factor in every mode (configs[2]-[4]): each distinct matrix is split once per batch
+      p.e_ready = (prev_ws == oz_ws && prev_n == n && prev_e.size() == static_cast<size_t>(p.ne) &&
+                   std::equal(prev_e.begin(), prev_e.end(), p.e)) ? 1 : 0;
+      prev_e.assign(p.e, p.e + p.ne);
+      prev_n = n;
+      prev_ws = oz_ws;
       if (mu > 0) {  // A: the previous product's digit planes and exponent bounds
         p.nx = nt;
         p.xs = (rm1 && mu == d - 1) ? reinterpret_cast<int8_t*>(h->sym + kCtrlBytes) : oz_dig[(mu - 1) % 2];

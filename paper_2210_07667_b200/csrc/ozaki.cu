@@ -1245,12 +1245,12 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
       oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
     }
   }
-  if (split_e && p.eext) {  // min / max / flag slots of the row-norm exponents
+  if (split_e && p.eext && !p.e_ready) {  // min / max / flag slots of the row-norm exponents
     cudaMemsetAsync(p.eext, 0x7f, sizeof(int) * p.ne, st);
     cudaMemsetAsync(p.eext + p.ne, 0x80, sizeof(int) * p.ne, st);
     cudaMemsetAsync(p.eext + 2 * p.ne, 0, sizeof(int) * p.ne, st);
   }
-  if (split_e) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
+  if (split_e && !p.e_ready) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
   if (split_e && p.n_next > 0 && p.nterms > 0 && !p.shard_stage0) {  // next-mode exponent bounds (chained modes)
     const int64_t m = C / p.n_next;
     oz_chain_kernel<<<dim3(static_cast<unsigned>((m + 31) / 32), p.nterms, (p.n + 63) / 64), 256, 0, st>>>(p);
@@ -1293,11 +1293,9 @@ void ozaki_bind_workspace(OzakiParams& p, void* ws) {
   const int K = p.cplx_j ? 2 * p.n : p.n;
   p.Kp = (K + kOzBK - 1) / kOzBK * kOzBK;
   auto al = [](size_t b) { return (b + 1023) & ~size_t(1023); };
+  // the matrices' digits first: two launches with the same (ne, n, Kp) find them at the same place,
+  // so a launch whose matrices the previous launch already split can skip that (e_ready)
   char* w = static_cast<char*>(ws);
-  p.xs = reinterpret_cast<int8_t*>(w);
-  w += al(static_cast<size_t>(p.nx) * p.S * C * p.Kp);
-  p.xsc = reinterpret_cast<double*>(w);
-  w += al(static_cast<size_t>(p.nx) * C * 8);
   p.es = reinterpret_cast<int8_t*>(w);
   w += al(static_cast<size_t>(p.ne) * p.S * p.n * p.Kp);
   p.esc = reinterpret_cast<double*>(w);
@@ -1307,6 +1305,10 @@ void ozaki_bind_workspace(OzakiParams& p, void* ws) {
   p.ecol = reinterpret_cast<int*>(w);
   w += al(static_cast<size_t>(p.ne) * p.n * 4);
   p.eext = reinterpret_cast<int*>(w);
+  w += al(static_cast<size_t>(p.ne) * 3 * 4);
+  p.xs = reinterpret_cast<int8_t*>(w);
+  w += al(static_cast<size_t>(p.nx) * p.S * C * p.Kp);
+  p.xsc = reinterpret_cast<double*>(w);
 }
 
 bool ozaki_supported(int64_t L, int n, int64_t R, int S) {

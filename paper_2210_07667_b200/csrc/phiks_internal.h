@@ -150,6 +150,7 @@ struct OzakiParams {
   int n_next;    // chained: n_{μ+1} (0: plain fp64 outputs)
   Remap remap;   // slab-sharded stage (world > 0): fp64 outputs (out) or next-mode digit planes (dig,
                  // AMN only) go to the owner rank; out / dig = byte offsets in the owners' regions
+  int e_ready;       // 1: es/esc/eb/ecol/eext already hold these matrices' split (the previous launch's)
   int shard_stage0;  // 1: the next-mode exponents come from the cross-rank exchange
                      // (launch_oz_shard_pmax / launch_oz_shard_tables), not oz_chain_kernel
 };
