@@ -347,20 +347,32 @@ __global__ void __launch_bounds__(256) oz_chain_kernel(const OzakiParams p) {
 
 // ---- slab-sharded chained stage 0: cross-rank next-mode exponents (phiks_internal.h) ----
 __global__ void __launch_bounds__(256) oz_shard_pmax_kernel(const OzShardExch e) {
-  const int t = blockIdx.y;
-  const int64_t l = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
-  if (l >= e.L0) return;
-  const double* x = e.xsc[t] + l;
+  // 32 consecutive l per CTA (lanes), the 8 warps splitting the slab's R; smem reduction
+  __shared__ double red[8][32];
+  const int t = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   double m = -2000.0;
   bool nan = false;
-  for (int64_t r = 0; r < e.R; ++r) {
-    const double v = x[e.L0 * r];
-    nan |= isnan(v);
-    m = fmax(m, v);
+  if (l < e.L0) {
+    const double* x = e.xsc[t] + l;
+    for (int64_t r = warp; r < e.R; r += 8) {
+      const double v = x[e.L0 * r];
+      nan |= isnan(v);
+      m = fmax(m, v);
+    }
   }
-  if (nan) m = __longlong_as_double(0x7ff8000000000000ll);
+  red[warp][lane] = nan ? qnan : m;
+  __syncthreads();
+  if (warp != 0 || l >= e.L0) return;
+  double v = red[0][lane];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) {
+    const double u = red[w][lane];
+    v = (isnan(v) || isnan(u)) ? qnan : fmax(v, u);
+  }
   const int64_t off = (static_cast<int64_t>(e.rank) * kShardChunkMax + t) * e.L0 + l;
-  for (int k = 0; k < e.world; ++k) e.dst[k][off] = m;  // NVLink peer stores (own buffer at k == rank)
+  for (int k = 0; k < e.world; ++k) e.dst[k][off] = v;  // NVLink peer stores (own buffer at k == rank)
 }
 
 __global__ void __launch_bounds__(256) oz_shard_tables_kernel(const OzShardExch e) {
@@ -1318,7 +1330,7 @@ bool ozaki_supported(int64_t L, int n, int64_t R, int S) {
 
 cudaError_t launch_oz_shard_pmax(const OzShardExch& e, cudaStream_t st) {
   if (e.nterms == 0) return cudaSuccess;
-  oz_shard_pmax_kernel<<<dim3(static_cast<unsigned>((e.L0 + 255) / 256), e.nterms), 256, 0, st>>>(e);
+  oz_shard_pmax_kernel<<<dim3(static_cast<unsigned>((e.L0 + 31) / 32), e.nterms), 256, 0, st>>>(e);
   return cudaGetLastError();
 }
 
