@@ -38,14 +38,18 @@ for P in [int(x) for x in os.environ.get("PS", "1,2,4,8").split(",")]:
     for _ in range(3):
         step()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(5):
-        step()
-    e1.record()
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 5
-    res.append({"config": CFG, "P": P, "serial_ms": round(t, 3), "per_rank_ms": round(t / P, 3)})
+    reps = []
+    for _ in range(int(os.environ.get("REPS", "3"))):  # best of REPS windows of 5 steps (power-cap noise)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        reps.append(e0.elapsed_time(e1) / 5)
+    t = min(reps)
+    res.append({"config": CFG, "P": P, "serial_ms": round(t, 3), "per_rank_ms": round(t / P, 3),
+                "windows_ms": [round(x, 3) for x in reps]})
     print(json.dumps(res[-1]), flush=True)
     del ranks, ins, outs
     torch.cuda.empty_cache()
