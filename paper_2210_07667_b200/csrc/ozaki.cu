@@ -735,12 +735,11 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
     // then balanced digits as in oz_digits
     constexpr uint64_t Cc = 0x8080808080808080ull >> (64 - 8 * S);
     auto digit_bits = [&](long long P, int k) -> uint64_t {
+      // branch-free: F = ((P << ls) + 2^{rs-1}) >> rs with rs = min(max(r, 0), 63), ls = max(−r, 0)
       const int r = 23 - k;
-      long long F;
-      if (r > 0)
-        F = r < 63 ? ((P + (1ll << (r - 1))) >> r) : 0ll;
-      else
-        F = P << (-r & 63);
+      const int rs = min(max(r, 0), 63), ls = max(-r, 0) & 63;
+      const long long half = rs > 0 ? (1ll << (rs - 1)) : 0ll;
+      const long long F = ((P << ls) + half) >> rs;
       return (static_cast<uint64_t>(F) + Cc) ^ Cc;
     };
     // fast path (warp-uniform): every row of E finite and no clamp of e = b_j + Mx, so
