@@ -34,7 +34,7 @@ for r in data:
               "registers": g(r, "launch__registers_per_thread"), "grid": g(r, "launch__grid_size")})
 old = json.load(open(out)) if len(sys.argv) < 4 else {}
 res = {"source": "ncu --set full --clock-control none --import-source on -k regex:oz_gemm -s 6 -c 3 python scripts/profile_bench.py "
-                 "(B200, round 1, final kernel): the three chained GEMM launches of the 19-term batch of one apply of the "
+                 "(B200, round 2 kernel): the three chained GEMM launches of the 19-term batch of one apply of the "
                  "block-diagonal configs[3] handle on the default path",
        "kernel": "oz_gemm_kernel<7, AMN, OUTD, SE=false> (tcgen05.mma kind::i8, M=128 x N<=256 x K=32 concatenated-diagonal "
                  "MMAs, fully unrolled issue, TMEM accumulators, TMA SWIZZLE_128B, A K-major (mode 1) or MN-major (chained "
