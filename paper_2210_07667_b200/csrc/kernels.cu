@@ -821,7 +821,7 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st) {
     const int64_t units = ((Mtot + 63) / 64) * ((p.n + 127) / 128) * p.ngroups;
     // far less than a wave of 64×64 tiles (the n×n GEMMs of a sharded rank's exponential stage,
     // a few matrices each): 32×32 tiles, 4× the CTAs, each a quarter of the serial K loop
-    if (((Mtot + 63) / 64) * ((p.n + 63) / 64) * p.ngroups < 148 / 2) return launch_cfg<32, 32, 16, 2, 2, 4, 4>(p, st);
+    if (p.n <= 256 && ((Mtot + 63) / 64) * ((p.n + 63) / 64) * p.ngroups < 148 / 2) return launch_cfg<32, 32, 16, 2, 2, 4, 4>(p, st);
     if (units >= 148 * 2)
       done = launch_tma<64, 128, 16, 2, 2, 4, 2>(p, st, &err);  // default: 2 CTAs/SM overlap epilogues
     else  // less than a wave (e.g. the n×n GEMMs of the exponential stage): 64×64 tiles, 3 CTAs/SM
