@@ -356,7 +356,56 @@ void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
         };
         std::vector<std::vector<TuckerItem>> per_ell(p + 1);
         std::vector<TuckerItem> jitems;
-        for (int ell = 1; ell <= p; ++ell) {
+        // s ≥ 1 (every Ψ_ℓ^{(s)} feeds the squaring): by the linearity of the Tucker operator,
+        // E_i x_iℓ = Σ_k c_iℓk E_i v_{p+1−k}, so one operator per node and GIVEN vector feeds every
+        // Ψ_ℓ that uses that vector — each v split once, no pre-combined inputs, and with only some
+        // v_ℓ given fewer operators than one per (node, ℓ) (reading R9).  s = 0: only Ψ_p is an
+        // output, from the pre-combined x_ip (one operator per node).
+        if (s >= 1) {
+          std::vector<char> started(p + 1, 0);
+          auto initial = [&](int ell, Out& o) {  // the θ_q = 1 term w_q x_qℓ
+            for (int k = 1; k <= ell; ++k) {
+              const double* v = jb.vin[p + 1 - k];
+              if (v) o.srcs.push_back(Src{v, wq * xcoef(1.0, ell, k)});
+            }
+          };
+          for (int i = 0; i < J.n_nodes; ++i)
+            for (int m = 1; m <= p; ++m) {
+              const double* v = jb.vin[m];
+              if (!v) continue;
+              const int k = p + 1 - m;
+              TuckerItem it;
+              it.in = v;
+              node_mats(J, i, it.mats);
+              it.group = J.gbase;
+              for (int ell = k; ell <= p; ++ell) {
+                const double c = xcoef(theta[i], ell, k);
+                if (c == 0.0) continue;
+                Out o;
+                o.dst = state[s][ell];
+                o.beta = w[i] * c;
+                if (!started[ell]) {
+                  initial(ell, o);
+                  started[ell] = 1;
+                } else {
+                  o.srcs.push_back(Src{o.dst, 1.0});
+                }
+                it.outs.push_back(o);
+              }
+              if (!it.outs.empty()) jitems.push_back(it);
+            }
+          for (int ell = 1; ell <= p; ++ell)
+            if (!started[ell]) {  // no node contributed: Ψ_ℓ = w_q x_qℓ
+              Out o{state[s][ell], 0.0, {}};
+              initial(ell, o);
+              prep.push_back(o);
+              if (ell == p && s < jb.n_scales && jb.out_lin[s]) {
+                o.dst = jb.out_lin[s];
+                prep.push_back(o);
+              }
+            }
+        }
+        for (int ell = 1; ell <= p && s == 0; ++ell) {
           // s = 0: level 0 is the output level and only Ψ_p^{(0)} is an output
           // (Table 1's lincomb T = (q−2)p + sp + 1, reading R9)
           if (s == 0 && ell != p) continue;
@@ -412,14 +461,17 @@ void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
           for (auto& it : per_ell[ell]) jitems.push_back(it);
         if (s < jb.n_scales && jb.out_lin[s]) {
           // scale s output = Ψ_p^{(s)} (+ exp term later): mirror the Ψ_p accumulation
-          for (auto& it : jitems)
-            if (it.group == J.gbase + p) {
-              Out o = it.outs[0];
-              o.dst = jb.out_lin[s];
-              for (auto& sr : o.srcs)
-                if (sr.ptr == state[s][p]) sr.ptr = jb.out_lin[s];
-              it.outs.push_back(o);
-            }
+          for (auto& it : jitems) {
+            const size_t no = it.outs.size();
+            for (size_t oi = 0; oi < no; ++oi)
+              if (it.outs[oi].dst == state[s][p]) {
+                Out o = it.outs[oi];
+                o.dst = jb.out_lin[s];
+                for (auto& sr : o.srcs)
+                  if (sr.ptr == state[s][p]) sr.ptr = jb.out_lin[s];
+                it.outs.push_back(o);
+              }
+          }
         }
         for (auto& it : jitems) items.push_back(it);
       }

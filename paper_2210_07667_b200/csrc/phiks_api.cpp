@@ -201,19 +201,19 @@ phiks_status validate(phiks_handle h, const phiks_request* req, int& p) {
 // Tucker operators run_jobs executes (reading R9): θ_q = 1 costs none; at the
 // last squaring step (or at s = 0) only the output combinations are formed —
 // Ψ_p for a linear combination, the requested φ_ℓ for the same vector
-// (PAPER.md l.953-956).  Lincomb without v_0, ŝ = 1: (q−2)p + sp + 1 (Table 1).
+// (PAPER.md l.953-956); a linear combination's quadrature at s ≥ 1 runs one
+// operator per node and given vector v_ℓ (ℓ ≥ 1).  Lincomb with v_1..v_p, without
+// v_0, ŝ = 1: (q−2)p + sp + 1 (Table 1).
 int tucker_executed(const phiks_request* req, int p, const plan::Plan& pl) {
   const bool same = req->mode == PHIKS_MODE_SAME_VECTOR;
   const bool has0 = req->ells[0] == 0;
   const int n0 = has0 ? req->n_scales : 0;
   if (p == 0) return n0;
-  int last = 1;
-  if (same) {
-    last = 0;
-    for (int i = 0; i < req->n_ells; ++i) last += req->ells[i] >= 1;
-  }
+  int given = 0;  // requested orders ℓ ≥ 1 (lincomb: the given vectors v_ℓ)
+  for (int i = 0; i < req->n_ells; ++i) given += req->ells[i] >= 1;
+  const int last = same ? given : 1;
   const int sq = pl.s >= 1 ? (pl.s - 1) * p + last : 0;
-  const int quad = same ? pl.q - 1 : (pl.q - 1) * (pl.s >= 1 ? p : 1);
+  const int quad = same ? pl.q - 1 : (pl.q - 1) * (pl.s >= 1 ? given : 1);
   return quad + sq + n0;
 }
 
