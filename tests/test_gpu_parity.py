@@ -357,3 +357,26 @@ def test_same_vector_last_step_requested_only(ells, n_scales):
     for j in range(n_scales):
         for i, ell in enumerate(ells):
             assert rel2(outs[j * len(ells) + i], W.as_flat(ref.out[(ell, j)])) <= TOL
+
+
+@pytest.mark.parametrize("ells", [(1, 3), (0, 2, 4), (4,), (0, 1, 2, 3, 4, 5)])
+@pytest.mark.parametrize("path", ["dmma", "i8"])
+def test_lincomb_given_vectors_subset(ells, path):
+    """Linear combination with only some v_ℓ given: the quadrature runs one Tucker operator per
+    node and GIVEN vector (linearity, reading R9) and matches the oracle's Eq. (17) result."""
+    dims = (128, 32, 16)
+    fac = [0.4 * W.fd_dxx_neumann(dims[0]), W.fd_dxx_dirichlet(dims[1]) + 2.0 * W.fd_dx_dirichlet(dims[1]),
+           0.3 * W.fd_dxx_neumann(dims[2])]
+    vs = [W.random_tensor(dims, seed=60 + k) for k in range(len(ells))]
+    tau, s, q = 2e-3, 2, 6
+    ref = O.phiks(fac, tau, "lincomb", ells, vs, n_scales=2, plan=O.Plan(s, q, 0))
+    op = PhiKS(fac)
+    op.set_gemm_path(path)
+    outs = op.apply(tau, ells, [dev(v) for v in vs], mode="lincomb", n_scales=2, force_s=s, force_q=q)
+    torch.cuda.synchronize()
+    st = op.stats()
+    given = sum(1 for e in ells if e >= 1)
+    p = max(ells)
+    assert st["tucker_ops"] == st["T_executed"] == (q - 1) * given + (s - 1) * p + 1 + (2 if 0 in ells else 0)
+    for j in range(2):
+        assert rel2(outs[j], W.as_flat(ref.out[j])) <= TOL, (ells, path, j)
