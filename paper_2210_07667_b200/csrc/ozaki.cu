@@ -171,62 +171,99 @@ __global__ void __launch_bounds__(256) oz_split_x_kernel(const OzakiParams p) {
 }
 
 // ---- split_x, contiguous fibers (L = 1): one warp per fiber, values in registers ----
-template <int S>
-__global__ void __launch_bounds__(256) oz_split_x_contig_kernel(const OzakiParams p) {
-  const int slot = blockIdx.y;
-  const int64_t C = p.R;
-  const int n = p.n, Kp = p.Kp;
-  const int lane = threadIdx.x & 31;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (c >= C) return;
-  const double* src = p.x[slot] + c * n;
-  double v[kOzMaxN / 128][4];
-  double m = 0.0;
-  bool bad = false;
-  if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(p.x[slot]) & 15) == 0) {  // 16-byte aligned fibers: two 16-byte loads per lane and chunk
+// Lane t holds the EPL = Kp/32 consecutive elements k ∈ [EPL·t, EPL·t + EPL) (zeros past n), so
+// every digit plane row is one EPL-byte store per lane.  The fibre exponent comes from the
+// maximum of the high words: for non-negative doubles the bit patterns order like the values,
+// so the largest high word carries the exponent field of max|x| (ilogb(max) + 2 = field − 1021),
+// and a field of 0x7ff marks a non-finite fibre (one REDUX instead of a shuffle tree of fp64
+// maxima and per-element finiteness tests: this kernel was integer-ALU bound).
+// Maxima of subnormal magnitude (field 0) take the exact fp64 path.
+template <int S, int EPL>
+__device__ __forceinline__ int oz_fibre_exponent(const double (&v)[EPL], bool& bad) {
+  unsigned hm = 0;
 #pragma unroll
-    for (int i = 0; i < kOzMaxN / 128; ++i) {
-      const int k = 128 * i + 4 * lane;
-      double2 a = make_double2(0.0, 0.0), b = a;
-      if (k < n) {
-        a = __ldcs(reinterpret_cast<const double2*>(src + k));
-        b = __ldcs(reinterpret_cast<const double2*>(src + k + 2));
-      }
-      v[i][0] = a.x;
-      v[i][1] = a.y;
-      v[i][2] = b.x;
-      v[i][3] = b.y;
+  for (int q = 0; q < EPL; ++q) hm = max(hm, static_cast<unsigned>(__double2hiint(v[q])) & 0x7fffffffu);
+  hm = __reduce_max_sync(0xffffffffu, hm);
+  bad = hm >= 0x7ff00000u;
+  if (bad) return 0;
+  if (hm >= 0x00100000u) return static_cast<int>(hm >> 20) - 1021;
+  double m = 0.0;
+#pragma unroll
+  for (int q = 0; q < EPL; ++q) m = fmax(m, fabs(v[q]));
+  return slice_exponent(warp_max(m));
+}
+// the S digit planes of EPL consecutive elements (EPL % 4 == 0): pk[g][s] holds digit s of
+// elements 4g..4g+3 (element q of the group in byte q)
+template <int S, int EPL>
+__device__ __forceinline__ void oz_split_lane(const double (&v)[EPL], int ex, bool zero, uint32_t (&pk)[EPL / 4][S]) {
+  const OzScale sc = oz_scale<S>(ex);
+  constexpr uint64_t Cc = 0x8080808080808080ull >> (64 - 8 * S);
+#pragma unroll
+  for (int g = 0; g < EPL / 4; ++g) {
+    uint64_t h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double t = v[4 * g + q] * sc.a;
+      if (sc.two) t *= sc.b;
+      const long long F = zero ? 0ll : __double2ll_rn(t);
+      h[q] = static_cast<uint64_t>(F) + Cc;  // bytes d_i + 128; the ^ 0x80 per packed word below
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int i = S - 1 - s;
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = static_cast<uint32_t>(h[q] >> (8 * (i & 4)));
+      const uint32_t sel = (i & 3) | (((i & 3) + 4) << 4);
+      pk[g][s] = __byte_perm(__byte_perm(w[0], w[1], sel), __byte_perm(w[2], w[3], sel), 0x5410) ^ 0x80808080u;
+    }
+  }
+}
+// one EPL-byte store per digit plane (dst: plane 0 of this lane's bytes, 4·EPL-aligned offsets)
+template <int S, int EPL>
+__device__ __forceinline__ void oz_store_lane(int8_t* dst, int64_t plane, const uint32_t (&pk)[EPL / 4][S]) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    int8_t* d = dst + s * plane;
+    if constexpr (EPL == 16)
+      *reinterpret_cast<uint4*>(d) = make_uint4(pk[0][s], pk[1][s], pk[2][s], pk[3][s]);
+    else if constexpr (EPL == 8)
+      *reinterpret_cast<uint2*>(d) = make_uint2(pk[0][s], pk[1][s]);
+    else
+#pragma unroll
+      for (int g = 0; g < EPL / 4; ++g) reinterpret_cast<uint32_t*>(d)[g] = pk[g][s];
+  }
+}
+template <int EPL>
+__device__ __forceinline__ void oz_load_lane(const double* src, int k0, int n, bool vec, double (&v)[EPL]) {
+  if (vec) {  // n == Kp, 16-byte aligned fibres
+#pragma unroll
+    for (int i = 0; i < EPL / 2; ++i) {
+      const double2 a = __ldcs(reinterpret_cast<const double2*>(src + k0) + i);
+      v[2 * i] = a.x;
+      v[2 * i + 1] = a.y;
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < kOzMaxN / 128; ++i)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = 128 * i + 4 * lane + q;
-        v[i][q] = k < n ? __ldg(src + k) : 0.0;
-      }
+    for (int q = 0; q < EPL; ++q) v[q] = k0 + q < n ? __ldg(src + k0 + q) : 0.0;
   }
-#pragma unroll
-  for (int i = 0; i < kOzMaxN / 128; ++i)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      m = fmax(m, fabs(v[i][q]));
-      bad |= !isfinite(v[i][q]);
-    }
-  m = warp_max(m);
-  bad = __any_sync(0xffffffffu, bad);
-  const int ex = bad ? 0 : slice_exponent(m);
-  int8_t* xs = p.xs + static_cast<int64_t>(slot) * S * C * Kp;
-#pragma unroll
-  for (int i = 0; i < kOzMaxN / 128; ++i) {
-    const int k0 = 128 * i + 4 * lane;
-    if (k0 < Kp) {
-      uint32_t pk[S];
-      split4<S>(v[i], ex, pk);
-#pragma unroll
-      for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(xs + (s * C + c) * Kp + k0) = pk[s];
-    }
-  }
+}
+template <int S, int EPL>
+__global__ void __launch_bounds__(256) oz_split_x_contig_kernel(const OzakiParams p) {
+  const int slot = blockIdx.y;
+  const int64_t C = p.R;
+  const int n = p.n, Kp = p.Kp;  // Kp = 32·EPL
+  const int lane = threadIdx.x & 31;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (c >= C) return;
+  const int k0 = EPL * lane;
+  double v[EPL];
+  oz_load_lane<EPL>(p.x[slot] + c * n, k0, n, n == Kp && (reinterpret_cast<uintptr_t>(p.x[slot]) & 15) == 0, v);
+  bool bad;
+  const int ex = oz_fibre_exponent<S, EPL>(v, bad);
+  uint32_t pk[EPL / 4][S];
+  oz_split_lane<S, EPL>(v, ex, bad, pk);
+  oz_store_lane<S, EPL>(p.xs + (static_cast<int64_t>(slot) * S * C + c) * Kp + k0, C * Kp, pk);
   if (lane == 0) p.xsc[static_cast<int64_t>(slot) * C + c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
 }
 
@@ -1227,7 +1264,14 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
     if (p.cplx_j) {
       oz_split_x_kernel<S><<<dim3(static_cast<unsigned>((C + 31) / 32), p.nx), 256, sm, st>>>(p);
     } else if (p.L == 1) {
-      oz_split_x_contig_kernel<S><<<dim3(static_cast<unsigned>((C + 7) / 8), p.nx), 256, 0, st>>>(p);
+      const dim3 g(static_cast<unsigned>((C + 7) / 8), p.nx);
+      switch (p.Kp) {  // Kp = n rounded up to 128
+        case 128: oz_split_x_contig_kernel<S, 4><<<g, 256, 0, st>>>(p); break;
+        case 256: oz_split_x_contig_kernel<S, 8><<<g, 256, 0, st>>>(p); break;
+        case 384: oz_split_x_contig_kernel<S, 12><<<g, 256, 0, st>>>(p); break;
+        case 512: oz_split_x_contig_kernel<S, 16><<<g, 256, 0, st>>>(p); break;
+        default: return cudaErrorInvalidValue;
+      }
     } else if (p.L % 32 == 0 && p.n <= 256 && p.Kp >= 128 && oz_split_tma_ok(p)) {
       static bool tattr = false;
       static int sms = 0;
