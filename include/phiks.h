@@ -126,6 +126,9 @@ typedef struct {
                                      DESIGN.md §4d; PHIKS_OPT_CHAIN)                 */
   int64_t shard_digit_ops;        /* sharded handles: Tucker operators whose stage 0 wrote
                                      mode d's digit planes into the owners */
+  int64_t presplit_inputs;        /* inputs of the last apply's chained batches whose mode-1
+                                     digits the previous batch's combination wrote (no
+                                     separate split pass)              */
 } phiks_stats;
 
 /* Create a handle for K = A_d ⊕ … ⊕ A_1.
@@ -241,10 +244,16 @@ phiks_status phiks_set_gemm_path(phiks_handle h, int path);
                      2 = whenever the shapes allow (tests of the guard).
    PHIKS_OPT_GRAPHS  1 (default) = capture device-memory applies of tensors up to
                      2^22 elements as CUDA graphs and replay them; 0 = direct
-                     launches. */
+                     launches.
+   PHIKS_OPT_PRESPLIT 1 (default) = the streaming combination that produces the
+                     next squaring level's inputs also writes their mode-1 int8
+                     digit planes (chained batches; stats presplit_inputs); 0 = the
+                     next batch splits them in a separate pass.  Same digits,
+                     same results bit for bit. */
 #define PHIKS_OPT_SPLIT 0
 #define PHIKS_OPT_CHAIN 1
 #define PHIKS_OPT_GRAPHS 2
+#define PHIKS_OPT_PRESPLIT 3
 phiks_status phiks_set_option(phiks_handle h, int option, int value);
 phiks_status phiks_get_option(phiks_handle h, int option, int* value);
 

@@ -143,7 +143,10 @@ void Exec::tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size
       }
       p.terms[p.nterms++] = t;
     }
-    const int nx_split = mu == 0 ? p.nx : 0;
+    // mode 1 of a batch whose inputs the previous batch's combination already split (pre_ready)
+    bool pre = mu == 0 && !rm && !pre_ready.empty();
+    for (int k = 0; pre && k < p.nx; ++k) pre = pre_ready.count(p.x[k]) != 0;
+    const int nx_split = mu == 0 && !pre ? p.nx : 0;
     oz_ws_reserve(ozaki_workspace_bytes(L, n, R, S, nx_split, p.ne));
     const int nx_keep = p.nx;
     p.nx = nx_split;
@@ -159,6 +162,12 @@ void Exec::tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size
       p.xs = (rm1 && mu == d - 1) ? reinterpret_cast<int8_t*>(h->sym + kCtrlBytes) : oz_dig[(mu - 1) % 2];
       p.xsc = oz_ex[(mu - 1) % 2];
       p.a_mn = 1;
+    } else if (pre) {  // A: the pre-split slots (same Kp: n rounded up to 128)
+      for (int b = 0; b < p.nterms; ++b) p.terms[b].xslot = pre_ready.at(p.x[p.terms[b].xslot]);
+      p.nx = pre_slots;
+      p.xs = pre_xs;
+      p.xsc = pre_xsc;
+      pre_hits += nx_keep;
     } else {
       p.nx = nx_keep;
     }
@@ -188,7 +197,7 @@ void Exec::tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size
       });
       barrier();  // every rank's digit planes are in place before stage 1 reads them
     } else {
-      oz_emit(pp, mu == 0);
+      oz_emit(pp, mu == 0 && !pre);
     }
     L *= n;
   }
@@ -325,9 +334,51 @@ void Exec::combine(int64_t count, const std::vector<Out>& outs) {
   }
 }
 
+bool Exec::pre_ok() const {
+  // the conditions of ozaki_chain_route on mode 1, for the pre-split's fibre layout
+  if (!h->opt_presplit || h->sharded() || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA || h->opt_chain == 0 || h->d < 2)
+    return false;
+  if (h->opt_chain == 1 && !h->chain_safe()) return false;
+  const int n = h->n[0];
+  if (n % 16 != 0 || n > kOzMaxN || !ozaki_supported(1, n, h->N / n, kOzDigits)) return false;
+  if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 128 || h->N < (int64_t(1) << 20))) return false;
+  return true;
+}
+
 void Exec::mcombine(int64_t count, const std::vector<const double*>& srcs, const std::vector<double*>& dsts,
-              const std::vector<std::vector<double>>& coef) {
+              const std::vector<std::vector<double>>& coef, const std::vector<int>* dslot) {
   if (!ok() || dsts.empty()) return;
+  bool any = false;
+  for (size_t o = 0; dslot && o < dsts.size(); ++o) any |= (*dslot)[o] >= 0;
+  if (any && static_cast<int>(srcs.size()) <= kMcMaxSrc && count == h->N) {
+    // the combination fused with the next batch's mode-1 split, up to 4 outputs per launch
+    const int n = h->n[0];
+    const int64_t C = count / n;
+    const int Kp = (n + 127) / 128 * 128;
+    for (size_t o0 = 0; o0 < dsts.size(); o0 += 4) {
+      MultiCombineParams* pp = new MultiCombineParams();
+      std::memset(pp, 0, sizeof(MultiCombineParams));
+      pp->count = count;
+      pp->fn = n;
+      pp->Kp = Kp;
+      pp->nsrc = static_cast<int>(srcs.size());
+      for (size_t k = 0; k < srcs.size(); ++k) pp->src[k] = srcs[k];
+      pp->nout = static_cast<int>(std::min(dsts.size() - o0, static_cast<size_t>(4)));
+      for (int o = 0; o < pp->nout; ++o) {
+        pp->dst[o] = dsts[o0 + o];
+        for (size_t k = 0; k < srcs.size(); ++k) pp->coef[o][k] = coef[o0 + o][k];
+        const int sl = (*dslot)[o0 + o];
+        if (sl >= 0) {
+          pp->dig[o] = pre_xs + static_cast<int64_t>(sl) * kOzDigits * C * Kp;
+          pp->dsc[o] = pre_xsc + static_cast<int64_t>(sl) * C;
+          pre_next[dsts[o0 + o]] = sl;
+        }
+      }
+      std::shared_ptr<MultiCombineParams> sp(pp);
+      emit("multi_combine_split", [sp](cudaStream_t s) { return launch_multi_combine_split(*sp, s); });
+    }
+    return;
+  }
   if (static_cast<int>(srcs.size()) <= kMcMaxSrc) {
     for (size_t o0 = 0; o0 < dsts.size(); o0 += kMcMaxOut) {
       MultiCombineParams* pp = new MultiCombineParams();
@@ -473,6 +524,21 @@ void Exec::tucker_batch_split(const std::vector<TuckerItem>& items) {
       touch(dsts[o]);
       for (auto& t : rows[o]) touch(t.first);
     }
+    // outputs the next batch splits (pre_want): their digit planes come out of the combination
+    std::vector<int> want_slot(dsts.size(), -1);
+    if (!shard && !pre_want.empty() && pre_ok()) {
+      const int ns = static_cast<int>(pre_want.size());
+      if (pre_slots < ns) {
+        const int n = h->n[0];
+        const int64_t C = N / n, Kp = (n + 127) / 128 * 128;
+        pre_xs = reinterpret_cast<int8_t*>(ar->alloc_doubles((static_cast<int64_t>(ns) * kOzDigits * C * Kp + 7) / 8));
+        pre_xsc = ar->alloc_doubles(static_cast<int64_t>(ns) * C);
+        pre_slots = ns;
+      }
+      for (size_t o = 0; o < dsts.size(); ++o)
+        for (int k = 0; k < ns; ++k)
+          if (pre_want[k] == dsts[o]) want_slot[o] = k;
+    }
     std::vector<int> done(dsts.size(), 0);
     for (size_t o0 = 0; o0 < dsts.size(); ++o0) {
       const int r0 = root(static_cast<int>(o0));
@@ -485,13 +551,15 @@ void Exec::tucker_batch_split(const std::vector<TuckerItem>& items) {
         for (auto& t : rows[o])
           if (std::find(srcs.begin(), srcs.end(), t.first) == srcs.end()) srcs.push_back(t.first);
       std::vector<double*> cd;
+      std::vector<int> cslot;
       std::vector<std::vector<double>> coef(members.size(), std::vector<double>(srcs.size(), 0.0));
       for (size_t m = 0; m < members.size(); ++m) {
         cd.push_back(dsts[members[m]]);
+        cslot.push_back(want_slot[members[m]]);
         for (auto& t : rows[members[m]])
           coef[m][std::find(srcs.begin(), srcs.end(), t.first) - srcs.begin()] += t.second;
       }
-      mcombine(N, srcs, cd, coef);
+      mcombine(N, srcs, cd, coef, &cslot);
       srcs.clear();
     }
   }

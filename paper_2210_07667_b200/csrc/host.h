@@ -108,6 +108,7 @@ struct phiks_ctx {
   int opt_split = 2;   // PHIKS_OPT_SPLIT
   int opt_chain = 1;   // PHIKS_OPT_CHAIN: 0 off, 1 guarded (Metzler factors), 2 forced
   int opt_graphs = 1;  // PHIKS_OPT_GRAPHS
+  int opt_presplit = 1;  // PHIKS_OPT_PRESPLIT
   bool chain_safe() const {  // every factor Metzler: exponentials entrywise ≥ 0 (τ > 0)
     for (const auto& F : factors)
       if (!F.metzler) return false;
@@ -445,8 +446,23 @@ struct Exec {
   void combine(int64_t count, const std::vector<Out>& outs);
 
   // ---- matrix-form combination dst_o = Σ_s coef[o][s] src_s ----
+  // dslot[o] ≥ 0: output o also written as mode-1 digit planes into slot dslot[o] of pre_xs
   void mcombine(int64_t count, const std::vector<const double*>& srcs, const std::vector<double*>& dsts,
-                const std::vector<std::vector<double>>& coef);
+                const std::vector<std::vector<double>>& coef, const std::vector<int>* dslot = nullptr);
+
+  // ---- next-batch digits from the streaming combination ----
+  // The orchestrator names the tensors the next batch takes as inputs (pre_want, set before a
+  // split batch); that batch's combination, which writes them, also writes their mode-1 digit
+  // planes and fibre exponents (slots of pre_xs / pre_xsc, layout of oz_split_x_contig), and the
+  // next batch's chained mode 1 reads them instead of splitting the tensors again.  pre_next
+  // (filled by the combination) becomes pre_ready for exactly the following batch.
+  std::vector<const double*> pre_want;
+  std::map<const double*, int> pre_ready, pre_next;
+  int8_t* pre_xs = nullptr;
+  double* pre_xsc = nullptr;
+  int pre_slots = 0;
+  int64_t pre_hits = 0;
+  bool pre_ok() const;  // the next batch's mode 1 can take pre-split digits
 
   // A batch whose last-mode epilogues run as a separate streaming pass: every
   // item writes its raw Tucker result Y_b, then the epilogue recurrences (in
@@ -481,10 +497,14 @@ struct Exec {
 
   // every batch of run_job: sharded handles always split
   void batch(const std::vector<TuckerItem>& items, bool split_it) {
+    pre_ready.swap(pre_next);
+    pre_next.clear();
     if (h->sharded() || h->cplx || split_it)
       tucker_batch_split(items);
     else
       tucker_batch(items);
+    pre_ready.clear();
+    pre_want.clear();
   }
 
   // ---- batched Tucker operators (Eq. (4)) ----
@@ -887,6 +907,7 @@ struct ApplyRun {
     S.i8_mode_launches = ex.i8_launches;
     S.i8_chained_ops = ex.i8_chained;
     S.shard_digit_ops = ex.shard_digit_ops;
+    S.presplit_inputs = ex.pre_hits;
     S.mu_mode_flops = ex.mu_flops;
     S.expm_flops = ex.expm_flops;
     S.workspace_bytes = need;

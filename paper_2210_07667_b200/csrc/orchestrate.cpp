@@ -476,17 +476,10 @@ void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
         for (auto& it : jitems) items.push_back(it);
       }
     }
-    ex.combine(N, prep);
-    for (auto& it : d_items) items.push_back(it);
-    ex.batch(items, ex.split >= 1);
-    if (!ex.ok()) return;
-    if (ex.on_outputs && !d_ready.empty()) ex.on_outputs(d_ready);
-    if (!ex.ok()) return;
-
     // ---- Stage C: squaring, level j for every job with s_b ≥ j ----
     int max_s = 0;
     for (const JS& J : js) max_s = std::max(max_s, J.s);
-    for (int j = max_s; j >= 1; --j) {
+    auto squaring_items = [&](int j) {
       std::vector<TuckerItem> sq;
       for (JS& J : js) {
         if (J.s < j) continue;
@@ -520,6 +513,26 @@ void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
           sq.push_back(it);
         }
       }
+      return sq;
+    };
+    // the inputs of the next squaring level come out of this batch's combination, which then
+    // also writes their mode-1 digits (Exec::pre_want)
+    auto want_next = [&](int j, bool producer_split) {
+      if (j < 1 || !producer_split) return;
+      for (const TuckerItem& it : squaring_items(j)) ex.pre_want.push_back(it.in);
+    };
+
+    ex.combine(N, prep);
+    for (auto& it : d_items) items.push_back(it);
+    want_next(max_s, ex.split >= 1);
+    ex.batch(items, ex.split >= 1);
+    if (!ex.ok()) return;
+    if (ex.on_outputs && !d_ready.empty()) ex.on_outputs(d_ready);
+    if (!ex.ok()) return;
+
+    for (int j = max_s; j >= 1; --j) {
+      std::vector<TuckerItem> sq = squaring_items(j);
+      want_next(j - 1, ex.split >= 2);
       ex.batch(sq, ex.split >= 2);
       if (!ex.ok()) return;
     }

@@ -267,6 +267,72 @@ __global__ void __launch_bounds__(256) oz_split_x_contig_kernel(const OzakiParam
   if (lane == 0) p.xsc[static_cast<int64_t>(slot) * C + c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
 }
 
+// ---- streaming combination fused with the next batch's mode-1 split ----
+// One warp per fibre of fn contiguous elements, lane t the EPL consecutive elements
+// [EPL·t, EPL·t + EPL): every source is read once, the NOUT sums stay in registers (the
+// accumulation order of multi_combine_kernel: sources in order, acc += c·x), the fp64 outputs
+// are stored, and the outputs with dig[o] set are also split into digit planes exactly as
+// oz_split_x_contig_kernel would split them after reading them back.
+template <int NOUT, int EPL>
+__global__ void __launch_bounds__(256) oz_multi_combine_split_kernel(const __grid_constant__ MultiCombineParams p) {
+  constexpr int S = 7;
+  const int n = p.fn, Kp = p.Kp;
+  const int64_t C = p.count / n;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (c >= C) return;
+  const int k0 = EPL * lane;
+  const bool vec = n == Kp;  // full lanes, 16-byte aligned rows (checked by the launcher)
+  double acc[NOUT][EPL];
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+    for (int q = 0; q < EPL; ++q) acc[o][q] = 0.0;
+  for (int s = 0; s < p.nsrc; ++s) {
+    double x[EPL];
+    const double* src = p.src[s] + c * n;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < EPL / 2; ++i) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(src + k0) + i);
+        x[2 * i] = a.x;
+        x[2 * i + 1] = a.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) x[q] = k0 + q < n ? __ldcs(src + k0 + q) : 0.0;
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) {
+      const double cf = p.coef[o][s];
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) acc[o][q] += cf * x[q];
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) {
+    if (o >= p.nout) break;
+    double* dst = p.dst[o] + c * n;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < EPL / 2; ++i)
+        reinterpret_cast<double2*>(dst + k0)[i] = make_double2(acc[o][2 * i], acc[o][2 * i + 1]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < EPL; ++q)
+        if (k0 + q < n) dst[k0 + q] = acc[o][q];
+    }
+    if (p.dig[o]) {
+      bool bad;
+      const int ex = oz_fibre_exponent<S, EPL>(acc[o], bad);
+      uint32_t pk[EPL / 4][S];
+      oz_split_lane<S, EPL>(acc[o], ex, bad, pk);
+      oz_store_lane<S, EPL>(p.dig[o] + c * Kp + k0, C * Kp, pk);
+      if (lane == 0) p.dsc[o][c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
+    }
+  }
+}
+
 // ---- split_e: one warp per row j of E (column-major, E[j + k·n]) ----
 template <int S>
 __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
@@ -1341,6 +1407,27 @@ size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne,
   return al(static_cast<size_t>(nx) * S * C * Kp) + al(static_cast<size_t>(nx) * C * 8) +
          al(static_cast<size_t>(ne) * S * n * Kp) + 2 * al(static_cast<size_t>(ne) * n * 8) +
          al(static_cast<size_t>(ne) * n * 4) + al(static_cast<size_t>(ne) * 3 * 4);
+}
+
+cudaError_t launch_multi_combine_split(const MultiCombineParams& p, cudaStream_t st) {
+  if (p.nout == 0 || p.count == 0) return cudaSuccess;
+  const int n = p.fn;
+  if (n < 1 || n > kOzMaxN || p.count % n != 0 || p.nout > 4 || p.Kp != (n + kOzBK - 1) / kOzBK * kOzBK)
+    return cudaErrorInvalidValue;
+  bool aligned = (n % 2) == 0;
+  for (int s = 0; s < p.nsrc; ++s) aligned &= (reinterpret_cast<uintptr_t>(p.src[s]) & 15) == 0;
+  for (int o = 0; o < p.nout; ++o) aligned &= (reinterpret_cast<uintptr_t>(p.dst[o]) & 15) == 0;
+  if (!aligned) return cudaErrorMisalignedAddress;
+  const int64_t C = p.count / n;
+  const dim3 g(static_cast<unsigned>((C + 7) / 8));
+  const bool two = p.nout <= 2;
+  switch (p.Kp) {
+    case 128: two ? oz_multi_combine_split_kernel<2, 4><<<g, 256, 0, st>>>(p) : oz_multi_combine_split_kernel<4, 4><<<g, 256, 0, st>>>(p); break;
+    case 256: two ? oz_multi_combine_split_kernel<2, 8><<<g, 256, 0, st>>>(p) : oz_multi_combine_split_kernel<4, 8><<<g, 256, 0, st>>>(p); break;
+    case 384: two ? oz_multi_combine_split_kernel<2, 12><<<g, 256, 0, st>>>(p) : oz_multi_combine_split_kernel<4, 12><<<g, 256, 0, st>>>(p); break;
+    default: two ? oz_multi_combine_split_kernel<2, 16><<<g, 256, 0, st>>>(p) : oz_multi_combine_split_kernel<4, 16><<<g, 256, 0, st>>>(p); break;
+  }
+  return cudaGetLastError();
 }
 
 void ozaki_bind_workspace(OzakiParams& p, void* ws) {

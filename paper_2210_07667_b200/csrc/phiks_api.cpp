@@ -481,6 +481,7 @@ phiks_status phiks_set_option(phiks_handle h, int option, int value) {
     case PHIKS_OPT_SPLIT: slot = &h->opt_split; hi = 2; break;
     case PHIKS_OPT_CHAIN: slot = &h->opt_chain; hi = 2; break;
     case PHIKS_OPT_GRAPHS: slot = &h->opt_graphs; hi = 1; break;
+    case PHIKS_OPT_PRESPLIT: slot = &h->opt_presplit; hi = 1; break;
     default: return fail(PHIKS_ERR_ARG, "unknown option");
   }
   if (value < lo || value > hi) return fail(PHIKS_ERR_ARG, "option value out of range");
@@ -498,6 +499,7 @@ phiks_status phiks_get_option(phiks_handle h, int option, int* value) {
     case PHIKS_OPT_SPLIT: *value = h->opt_split; break;
     case PHIKS_OPT_CHAIN: *value = h->opt_chain; break;
     case PHIKS_OPT_GRAPHS: *value = h->opt_graphs; break;
+    case PHIKS_OPT_PRESPLIT: *value = h->opt_presplit; break;
     default: return fail(PHIKS_ERR_ARG, "unknown option");
   }
   return PHIKS_OK;

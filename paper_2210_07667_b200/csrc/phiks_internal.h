@@ -110,6 +110,13 @@ struct MultiCombineParams {
   const double* src[kMcMaxSrc];
   double* dst[kMcMaxOut];
   double coef[kMcMaxOut][kMcMaxSrc];
+  // with dig[o] set (launch_multi_combine_split): output o also as the S = 7 mode-1 digit
+  // planes of the next batch's int8 products, fibres of fn contiguous elements: digit s of
+  // element k of fibre c at dig[o][(s·C + c)·Kp + k] (zeros for n ≤ k < Kp), the fibre exponent
+  // (NaN: non-finite fibre) at dsc[o][c], C = count / fn — the layout oz_split_x_contig writes
+  int8_t* dig[kMcMaxOut];
+  double* dsc[kMcMaxOut];
+  int fn, Kp;
 };
 
 // μ-mode products on the int8 tensor cores (ozaki.cu): every
@@ -188,6 +195,9 @@ cudaError_t launch_ozaki_mode(const OzakiParams& p, cudaStream_t st, bool split_
 cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st);
 cudaError_t launch_combine(const CombineParams& p, cudaStream_t st);
 cudaError_t launch_multi_combine(const MultiCombineParams& p, cudaStream_t st);
+// the same combination fused with the mode-1 digit split of the outputs that have dig[o] set
+// (ozaki.cu): count % fn == 0, fn ≤ 512, Kp = fn rounded up to 128, nout ≤ 4, 16-byte aligned
+cudaError_t launch_multi_combine_split(const MultiCombineParams& p, cudaStream_t st);
 // partial sums of squares of `count` doubles of each of `nvec` vectors
 // -> norms2[v] (device), deterministic two-pass reduction; scratch ≥ 1024*nvec doubles
 cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, double* scratch,

@@ -35,7 +35,7 @@ def _oracle_outs(pb):
 
 def test_option_api():
     op = PhiKS([W.fd_dxx_dirichlet(8)] * 2)
-    assert (op.get_option("split"), op.get_option("chain"), op.get_option("graphs")) == (2, 1, 1)
+    assert [op.get_option(k) for k in ("split", "chain", "graphs", "presplit")] == [2, 1, 1, 1]
     for name, bad in (("split", 3), ("chain", -1), ("graphs", 2)):
         with pytest.raises(PhiksError):
             op.set_option(name, bad)
@@ -116,5 +116,32 @@ def test_graphs_option_bitwise():
         for _ in range(2):
             got, _ = _apply(op, pb)
         res.append(got)
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("mode", ["same", "lincomb"])
+def test_presplit_option_bitwise(mode):
+    """PHIKS_OPT_PRESPLIT: the combination producing a squaring level's inputs also writes
+    their mode-1 digit planes (one pass fewer); the digits are the ones the split kernel
+    would write, so both settings agree bit for bit (and with the oracle)."""
+    pb = _fd_problem()
+    if mode == "lincomb":
+        v = pb.vs[0]
+        pb = W.Problem("fd_lin", pb.dims, pb.A, pb.tau, "lincomb", (0, 1, 2, 3),
+                       [v, 0.5 * v, W.uniform_tensor(pb.dims, -1.0, 1.0, seed=32), 0.25 * v], 2)
+    ref = _oracle_outs(pb)
+    res, hits = [], []
+    for pre in (1, 0):
+        op = PhiKS(pb.A)
+        op.set_gemm_path("i8")
+        op.set_option("presplit", pre)
+        got, st = _apply(op, pb)
+        assert st["i8_chained_ops"] > 0 and st["s"] >= 2
+        hits.append(st["presplit_inputs"])
+        res.append(got)
+        for g, r in zip(got, ref):
+            assert rel(g, r) <= TOL, (mode, pre, rel(g, r))
+    assert hits[0] > 0 and hits[1] == 0, hits
     for a, b in zip(*res):
         assert np.array_equal(a, b)
