@@ -31,6 +31,8 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id));
   if (KIND == 1 && PAIR == 0)
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id));
+  if (KIND == 2 && PAIR == 0)  // A operand in TMEM (column a of the allocation), int8
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d), "r"(static_cast<uint32_t>(a)), "l"(b), "r"(id));
   if (KIND == 0 && PAIR == 1)
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\ntcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id));
   if (KIND == 1 && PAIR == 1)
@@ -84,7 +86,10 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int nmix, int4 ns, ui
     for (int it = 0; it < iters; ++it) {
 #pragma unroll 1
       for (int j = 0; j < nmix; ++j) {
-        mma<KIND, PAIR>(tmem + c_col[j], a + (it & 3) * 2, b + (it & 3) * 2, idesc(KIND, M, c_n[j]));
+        if (KIND == 2)
+          mma<KIND, PAIR>(tmem + c_col[j], tmem + 448 + (it & 3) * 8, b + (it & 3) * 2, idesc(0, M, c_n[j]));
+        else
+          mma<KIND, PAIR>(tmem + c_col[j], a + (it & 3) * 2, b + (it & 3) * 2, idesc(KIND, M, c_n[j]));
         if (ns.x && (j % ns.x) == ns.x - 1) {
           if (ns.z & 1)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(&bar2))
@@ -250,7 +255,7 @@ void run(const char* name, int nmix, const int* cols, const int* nsz, int iters,
   cudaEventElapsedTime(&ms, e0, e1);
   cudaError_t err = cudaGetLastError();
   double macs = 0;
-  const int M = PAIR ? 256 : 128, K = KIND == 0 ? 32 : 16;
+  const int M = PAIR ? 256 : 128, K = KIND != 1 ? 32 : 16;
   for (int j = 0; j < nmix; ++j) macs += double(M) * nsz[j] * K;
   macs *= double(iters) * (PAIR ? sms / 2 : sms);
   uint64_t h[256];
@@ -271,7 +276,12 @@ int main() {
   const int n64[] = {256, 192, 256, 128, 256, 64, 256, 192, 128, 64};
   const int c32[] = {0, 32, 64, 96, 128, 160, 192};
   const int n32[] = {224, 192, 160, 128, 96, 64, 32};
+  const int c256[] = {0, 256, 0, 256, 0, 256, 0};
+  const int n256[] = {256, 192, 256, 192, 256, 192, 256};
   for (int rnd = 0; rnd < 2; ++rnd) {
+    run<2, 0>(rnd ? "BN64 seq, A in TMEM, random operands" : "BN64 seq, A in TMEM, zero operands", 10, c64, n64, 4000, make_int4(0, rnd, 0, 0));
+    run<0, 0>(rnd ? "N256/192 mix, random" : "N256/192 mix, zero", 7, c256, n256, 4000, make_int4(0, rnd, 0, 0));
+    run<2, 0>(rnd ? "N256/192 mix, A in TMEM, random" : "N256/192 mix, A in TMEM, zero", 7, c256, n256, 4000, make_int4(0, rnd, 0, 0));
     run<0, 0>(rnd ? "BN64 seq, random operands" : "BN64 seq, zero operands", 10, c64, n64, 4000, make_int4(0, rnd, 0, 0));
     run<0, 0>(rnd ? "BN32 seq, random operands" : "BN32 seq, zero operands", 7, c32, n32, 4000, make_int4(0, rnd, 0, 0));
   }
