@@ -15,6 +15,8 @@ for idx in [int(x) for x in os.environ.get("CONFIGS", "0,1,2,3,4").split(",")]:
     ops, vins, outs = [], [], []
     for pb in wl.problems:
         op = PhiKS(pb.A)
+        if os.environ.get("PRESPLIT") is not None:  # A/B of PHIKS_OPT_PRESPLIT
+            op.set_option("presplit", int(os.environ["PRESPLIT"]))
         ops.append(op)
         vins.append([torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).cuda() for v in pb.vs])
         nout = len(pb.ells) * pb.n_scales if pb.mode == "same" else pb.n_scales
@@ -55,6 +57,7 @@ for idx in [int(x) for x in os.environ.get("CONFIGS", "0,1,2,3,4").split(",")]:
                       "tucker_share": round(mp_ms / reps / 1e3 / tp, 3) if mp_ms else None,
                       "expm_share": round(sum(s["expm_ms"] for s in st) / reps / 1e3 / tp, 3),
                       "expm_launches": sum(s["expm_launches"] for s in st) // reps,
-                      "launches": sum(s["kernel_launches"] for s in st)}), flush=True)
+                      "launches": sum(s["kernel_launches"] for s in st),
+                      "presplit_inputs": sum(s["presplit_inputs"] for s in st)}), flush=True)
     del ops, vins, outs
     torch.cuda.empty_cache()
