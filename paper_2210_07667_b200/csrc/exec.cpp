@@ -340,7 +340,8 @@ bool Exec::pre_ok() const {
     return false;
   if (h->opt_chain == 1 && !h->chain_safe()) return false;
   const int n = h->n[0];
-  if (n % 16 != 0 || n > kOzMaxN || !ozaki_supported(1, n, h->N / n, kOzDigits)) return false;
+  // mode 2's A operand is MN-major over L = n_1 fibres: the chain needs n_1 % 128 == 0
+  if (n % 128 != 0 || n > kOzMaxN || !ozaki_supported(1, n, h->N / n, kOzDigits)) return false;
   if (h->gemm_path == PHIKS_GEMM_AUTO && (n < 128 || h->N < (int64_t(1) << 20))) return false;
   return true;
 }

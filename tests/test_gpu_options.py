@@ -145,3 +145,31 @@ def test_presplit_option_bitwise(mode):
     assert hits[0] > 0 and hits[1] == 0, hits
     for a, b in zip(*res):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dims,mode,ells", [
+    ((384, 128, 16), "same", (1, 2)),         # 12 elements per lane, two pre-split inputs
+    ((512, 128), "lincomb", (0, 1, 2, 3, 4)),  # 16 per lane, four inputs per squaring level, d = 2
+    ((256, 128, 16), "lincomb", (1, 2, 3)),    # no v_0
+])
+def test_presplit_shapes_bitwise(dims, mode, ells):
+    """The fused combination + split on the other lane widths and output counts: bitwise equal
+    to the separate split, and within the oracle's tolerance."""
+    A = [W.fd_dxx_neumann(n) * (0.3 / (k + 1)) for k, n in enumerate(dims)]
+    vs = [W.uniform_tensor(dims, -1.0, 1.0, seed=50 + k) for k in range(1 if mode == "same" else len(ells))]
+    pb = W.Problem("pre", dims, A, 4e-3, mode, ells, vs, 2)
+    ref = _oracle_outs(pb)
+    res, hits = [], []
+    for pre in (1, 0):
+        op = PhiKS(pb.A)
+        op.set_gemm_path("i8")
+        op.set_option("presplit", pre)
+        got, st = _apply(op, pb)
+        assert st["i8_chained_ops"] > 0 and st["s"] >= 2, st
+        hits.append(st["presplit_inputs"])
+        res.append(got)
+        for g, r in zip(got, ref):
+            assert rel(g, r) <= TOL, (dims, pre, rel(g, r))
+    assert hits[0] > 0 and hits[1] == 0, hits
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
