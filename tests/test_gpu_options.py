@@ -147,17 +147,18 @@ def test_presplit_option_bitwise(mode):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("dims,mode,ells", [
-    ((384, 128, 16), "same", (1, 2)),         # 12 elements per lane, two pre-split inputs
-    ((512, 128), "lincomb", (0, 1, 2, 3, 4)),  # 16 per lane, four inputs per squaring level, d = 2
-    ((256, 128, 16), "lincomb", (1, 2, 3)),    # no v_0
+@pytest.mark.parametrize("dims,mode,ells,tau,n_scales", [
+    ((384, 128, 16), "same", (1, 2), 4e-3, 2),          # 12 elements per lane, two pre-split inputs
+    ((512, 128), "lincomb", (0, 1, 2, 3, 4), 4e-3, 2),  # 16 per lane, four inputs per level, d = 2
+    ((256, 128, 16), "lincomb", (1, 2, 3), 4e-3, 2),    # no v_0
+    ((256, 128, 16), "lincomb", (0, 1, 2, 3, 4), 3e-5, 4),  # s = 3 < 4 scales: 5 outputs per pass
 ])
-def test_presplit_shapes_bitwise(dims, mode, ells):
+def test_presplit_shapes_bitwise(dims, mode, ells, tau, n_scales):
     """The fused combination + split on the other lane widths and output counts: bitwise equal
     to the separate split, and within the oracle's tolerance."""
     A = [W.fd_dxx_neumann(n) * (0.3 / (k + 1)) for k, n in enumerate(dims)]
     vs = [W.uniform_tensor(dims, -1.0, 1.0, seed=50 + k) for k in range(1 if mode == "same" else len(ells))]
-    pb = W.Problem("pre", dims, A, 4e-3, mode, ells, vs, 2)
+    pb = W.Problem("pre", dims, A, tau, mode, ells, vs, n_scales)
     ref = _oracle_outs(pb)
     res, hits = [], []
     for pre in (1, 0):
