@@ -352,11 +352,13 @@ void Exec::mcombine(int64_t count, const std::vector<const double*>& srcs, const
   bool any = false;
   for (size_t o = 0; dslot && o < dsts.size(); ++o) any |= (*dslot)[o] >= 0;
   if (any && static_cast<int>(srcs.size()) <= kMcMaxSrc && count == h->N) {
-    // the combination fused with the next batch's mode-1 split, up to 4 outputs per launch
+    // the combination fused with the next batch's mode-1 split (up to 8 outputs per launch for
+    // n_1 ≤ 256, 4 above)
     const int n = h->n[0];
     const int64_t C = count / n;
     const int Kp = (n + 127) / 128 * 128;
-    for (size_t o0 = 0; o0 < dsts.size(); o0 += 4) {
+    const size_t mo = static_cast<size_t>(oz_multi_combine_split_max_out(n));
+    for (size_t o0 = 0; o0 < dsts.size(); o0 += mo) {
       MultiCombineParams* pp = new MultiCombineParams();
       std::memset(pp, 0, sizeof(MultiCombineParams));
       pp->count = count;
@@ -364,7 +366,7 @@ void Exec::mcombine(int64_t count, const std::vector<const double*>& srcs, const
       pp->Kp = Kp;
       pp->nsrc = static_cast<int>(srcs.size());
       for (size_t k = 0; k < srcs.size(); ++k) pp->src[k] = srcs[k];
-      pp->nout = static_cast<int>(std::min(dsts.size() - o0, static_cast<size_t>(4)));
+      pp->nout = static_cast<int>(std::min(dsts.size() - o0, mo));
       for (int o = 0; o < pp->nout; ++o) {
         pp->dst[o] = dsts[o0 + o];
         for (size_t k = 0; k < srcs.size(); ++k) pp->coef[o][k] = coef[o0 + o][k];

@@ -1409,10 +1409,13 @@ size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne,
          al(static_cast<size_t>(ne) * n * 4) + al(static_cast<size_t>(ne) * 3 * 4);
 }
 
+int oz_multi_combine_split_max_out(int n) { return n <= 256 ? 8 : 4; }  // sums in registers: NOUT·n/32 doubles
+
 cudaError_t launch_multi_combine_split(const MultiCombineParams& p, cudaStream_t st) {
   if (p.nout == 0 || p.count == 0) return cudaSuccess;
   const int n = p.fn;
-  if (n < 1 || n > kOzMaxN || p.count % n != 0 || p.nout > 4 || p.Kp != (n + kOzBK - 1) / kOzBK * kOzBK)
+  if (n < 1 || n > kOzMaxN || p.count % n != 0 || p.nout > oz_multi_combine_split_max_out(n) ||
+      p.Kp != (n + kOzBK - 1) / kOzBK * kOzBK)
     return cudaErrorInvalidValue;
   bool aligned = (n % 2) == 0;
   for (int s = 0; s < p.nsrc; ++s) aligned &= (reinterpret_cast<uintptr_t>(p.src[s]) & 15) == 0;
@@ -1420,12 +1423,19 @@ cudaError_t launch_multi_combine_split(const MultiCombineParams& p, cudaStream_t
   if (!aligned) return cudaErrorMisalignedAddress;
   const int64_t C = p.count / n;
   const dim3 g(static_cast<unsigned>((C + 7) / 8));
-  const bool two = p.nout <= 2;
-  switch (p.Kp) {
-    case 128: two ? oz_multi_combine_split_kernel<2, 4><<<g, 256, 0, st>>>(p) : oz_multi_combine_split_kernel<4, 4><<<g, 256, 0, st>>>(p); break;
-    case 256: two ? oz_multi_combine_split_kernel<2, 8><<<g, 256, 0, st>>>(p) : oz_multi_combine_split_kernel<4, 8><<<g, 256, 0, st>>>(p); break;
-    case 384: two ? oz_multi_combine_split_kernel<2, 12><<<g, 256, 0, st>>>(p) : oz_multi_combine_split_kernel<4, 12><<<g, 256, 0, st>>>(p); break;
-    default: two ? oz_multi_combine_split_kernel<2, 16><<<g, 256, 0, st>>>(p) : oz_multi_combine_split_kernel<4, 16><<<g, 256, 0, st>>>(p); break;
+  const int no = p.nout <= 2 ? 2 : (p.nout <= 4 ? 4 : 8);
+  switch (p.Kp * 10 + no) {  // Kp = n rounded up to 128
+    case 1282: oz_multi_combine_split_kernel<2, 4><<<g, 256, 0, st>>>(p); break;
+    case 1284: oz_multi_combine_split_kernel<4, 4><<<g, 256, 0, st>>>(p); break;
+    case 1288: oz_multi_combine_split_kernel<8, 4><<<g, 256, 0, st>>>(p); break;
+    case 2562: oz_multi_combine_split_kernel<2, 8><<<g, 256, 0, st>>>(p); break;
+    case 2564: oz_multi_combine_split_kernel<4, 8><<<g, 256, 0, st>>>(p); break;
+    case 2568: oz_multi_combine_split_kernel<8, 8><<<g, 256, 0, st>>>(p); break;
+    case 3842: oz_multi_combine_split_kernel<2, 12><<<g, 256, 0, st>>>(p); break;
+    case 3844: oz_multi_combine_split_kernel<4, 12><<<g, 256, 0, st>>>(p); break;
+    case 5122: oz_multi_combine_split_kernel<2, 16><<<g, 256, 0, st>>>(p); break;
+    case 5124: oz_multi_combine_split_kernel<4, 16><<<g, 256, 0, st>>>(p); break;
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

@@ -196,8 +196,9 @@ cudaError_t launch_mode_product(const ModeParams& p, cudaStream_t st);
 cudaError_t launch_combine(const CombineParams& p, cudaStream_t st);
 cudaError_t launch_multi_combine(const MultiCombineParams& p, cudaStream_t st);
 // the same combination fused with the mode-1 digit split of the outputs that have dig[o] set
-// (ozaki.cu): count % fn == 0, fn ≤ 512, Kp = fn rounded up to 128, nout ≤ 4, 16-byte aligned
+// (ozaki.cu): count % fn == 0, fn ≤ 512, Kp = fn rounded up to 128, nout ≤ the max below, 16-byte aligned
 cudaError_t launch_multi_combine_split(const MultiCombineParams& p, cudaStream_t st);
+int oz_multi_combine_split_max_out(int n);  // outputs per launch of the fused variant for fibres of n
 // partial sums of squares of `count` doubles of each of `nvec` vectors
 // -> norms2[v] (device), deterministic two-pass reduction; scratch ≥ 1024*nvec doubles
 cudaError_t launch_sumsq(const double* const* vecs, int nvec, int64_t count, double* scratch,
