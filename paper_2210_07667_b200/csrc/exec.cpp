@@ -143,8 +143,9 @@ void Exec::tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size
       }
       p.terms[p.nterms++] = t;
     }
-    // mode 1 of a batch whose inputs the previous batch's combination already split (pre_ready)
-    bool pre = mu == 0 && !rm && !pre_ready.empty();
+    // mode 1 of a batch whose inputs the previous batch's combination already split (pre_ready;
+    // mode 1 is local on slab-sharded handles too)
+    bool pre = mu == 0 && !pre_ready.empty();
     for (int k = 0; pre && k < p.nx; ++k) pre = pre_ready.count(p.x[k]) != 0;
     const int nx_split = mu == 0 && !pre ? p.nx : 0;
     oz_ws_reserve(ozaki_workspace_bytes(L, n, R, S, nx_split, p.ne));
@@ -336,8 +337,7 @@ void Exec::combine(int64_t count, const std::vector<Out>& outs) {
 
 bool Exec::pre_ok() const {
   // the conditions of ozaki_chain_route on mode 1, for the pre-split's fibre layout
-  if (!h->opt_presplit || h->sharded() || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA || h->opt_chain == 0 || h->d < 2)
-    return false;
+  if (!h->opt_presplit || h->cplx || h->gemm_path == PHIKS_GEMM_DMMA || h->opt_chain == 0 || h->d < 2) return false;
   if (h->opt_chain == 1 && !h->chain_safe()) return false;
   const int n = h->n[0];
   // mode 2's A operand is MN-major over L = n_1 fibres: the chain needs n_1 % 128 == 0
@@ -528,8 +528,9 @@ void Exec::tucker_batch_split(const std::vector<TuckerItem>& items) {
       for (auto& t : rows[o]) touch(t.first);
     }
     // outputs the next batch splits (pre_want): their digit planes come out of the combination
+    // (sharded: of the chunk that completes the outputs)
     std::vector<int> want_slot(dsts.size(), -1);
-    if (!shard && !pre_want.empty() && pre_ok()) {
+    if (c1 == items.size() && !pre_want.empty() && pre_ok()) {
       const int ns = static_cast<int>(pre_want.size());
       if (pre_slots < ns) {
         const int n = h->n[0];

@@ -28,13 +28,15 @@ def rel2(got, ref):
     return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
 
 
-def run_sharded(pb, world, n_scales=None, force=None, path="dmma", chain=1):
+def run_sharded(pb, world, n_scales=None, force=None, path="dmma", chain=1, presplit=None):
     n_scales = pb.n_scales if n_scales is None else n_scales
     ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
     ShardedPhiKS.connect_local(ranks)
     for r in ranks:
         r.set_gemm_path(path)
         r.set_option("chain", chain)
+        if presplit is not None:
+            r.set_option("presplit", presplit)
     flat = [W.as_flat(v) for v in pb.vs]
     vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, world)[r])).to(DEV) for x in flat]
             for r in range(world)]
@@ -281,3 +283,23 @@ def test_sharded_digit_stages(dims, world, mode, kind):
     torch.cuda.synchronize()
     for a, b in zip(outs, single):
         assert rel2(a, b.cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("dims,world,mode", [((128, 64, 16), 2, "same"), ((256, 128, 32), 4, "lincomb")])
+def test_sharded_presplit_bitwise(dims, world, mode):
+    """PHIKS_OPT_PRESPLIT on slab-sharded handles: the combination that completes a squaring
+    level's inputs writes their mode-1 digits (mode 1 is local to the slab); same results bit for
+    bit as the separate split."""
+    fac = _fd_factors(dims)
+    ells = (0, 1, 2) if mode == "same" else (0, 1, 2, 3)
+    vs = [W.random_tensor(dims, seed=1900 + k) for k in range(1 if mode == "same" else len(ells))]
+    pb = W.Problem(f"spre_{dims}_{world}_{mode}", dims, fac, 2e-3, mode, ells, vs, 2)
+    res = []
+    for pre in (1, 0):
+        outs, stats = run_sharded(pb, world, path="i8", chain=1, presplit=pre)
+        hits = [st["presplit_inputs"] for st in stats]
+        assert all(h > 0 for h in hits) if pre else all(h == 0 for h in hits), (pre, hits)
+        res.append(outs)
+    compare_oracle(pb, res[0], pb.n_scales)
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
