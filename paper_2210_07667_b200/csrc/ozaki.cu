@@ -1314,6 +1314,20 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   return cudaGetLastError();
 }
 
+// fewer fibre tiles per term than this many per CTA of an n-tile: stream E (configs[3] sharded at
+// P = 8: 9.40 → 9.17 ms serial for the 8 emulated ranks; thresholds 2 / 4 / 8 equal, P = 1 and
+// configs[2] unchanged)
+constexpr int kOzSeUnits = 4;
+int oz_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
 template <int S>
 cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool split_e, bool gemm) {
   const OzakiParams& p = p0;
@@ -1382,7 +1396,11 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
                            : oz_encode(&ta, p.xs, p.Kp, C, S, p.nx, kOzBM, OzGeom<S>::SPS);
   if (!amap) return cudaErrorInvalidValue;
   if (!oz_encode(&tb, p.es, p.Kp, p.n, S, p.ne, kOzBN, S)) return cudaErrorInvalidValue;
-  if (p.Kp > kOzMaxNRes) {  // E streamed per k-block
+  // E streamed per k-block: required above 256; also when a CTA would process few units per term
+  // (short launches, e.g. a slab-sharded rank's), where every term switch would reload the
+  // resident E tile with the MMAs stalled behind it
+  const int64_t Mt = (C + kOzBM - 1) / kOzBM, Qn = oz_sms() / ((p.n + kOzBN - 1) / kOzBN);
+  if (p.Kp > kOzMaxNRes || Mt < kOzSeUnits * Qn) {
     if (p.a_mn) {
       if (p.n_next > 0) return oz_gemm_go<S, true, true, true>(p, st, ta, tb);
       return oz_gemm_go<S, true, false, true>(p, st, ta, tb);
