@@ -1020,8 +1020,8 @@ struct OzSched {
   }
 };
 
-// SE: n > 256, the E digits stream through a 2-block ring (one 128-k block per stage
-// group) instead of staying resident per term
+// SE: the E digits stream through a 2-block ring (one 128-k block per stage group) instead of
+// staying resident per term: always for n > 256, and for short launches (kOzSeUnits)
 template <int S, bool AMN, bool OUTD, bool SE, bool REM>
 __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
