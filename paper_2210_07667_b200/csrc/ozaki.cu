@@ -1159,10 +1159,13 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < kOzBK / kOzUK; ++kk) {
               const uint32_t accf = (kb > 0 || s > 0 || kk > 0) ? 1u : 0u;
-              // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA
+              // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA;
+              // above 256 columns two equal halves (448 = 224 + 224, 384, 320) rather than 256 + rest:
+              // two equal independent accumulation streams instead of a small tail MMA (−1.5 % per launch)
+              const int W = (S - s) * kOzBN, CW = W > 256 ? W / 2 : W;
 #pragma unroll
-              for (int c0 = 0; c0 < (S - s) * kOzBN; c0 += 256) {
-                const int nn = (S - s) * kOzBN - c0 < 256 ? (S - s) * kOzBN - c0 : 256;
+              for (int c0 = 0; c0 < W; c0 += CW) {
+                const int nn = CW;
                 oz_mma(tmem + static_cast<uint32_t>(s * kOzBN + c0), ad0 + static_cast<uint64_t>(kk) * a_kstep,
                        bd0 + static_cast<uint64_t>((c0 * kOzBK) >> 4) + static_cast<uint64_t>(kk * 2),
                        oz_idesc(nn, AMN), accf);
