@@ -981,11 +981,12 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
 // Persistent GEMM geometry: the E-digit tile of a (term, n-tile) stays resident
 // (S × 64 rows × Kp bytes); fiber digits stream through an NST-stage ring of
 // SPS-digit units (k-block kb, digit group sg).  Ring depth per variant, measured on the
-// configs[3] launches (ms per 19-term batch at NST = 4 / 5 / 6 / 7): mode 1 with digit
+// configs[3] launches (round 1, ms per 19-term batch at NST = 4 / 5 / 6 / 7): mode 1 with digit
 // epilogue 2.01 / 2.02 / 2.09 / 2.14, chained mode 2 2.15 / 2.13 / 2.12 / 2.14, fp64-output
 // mode 1.87 / 1.72 / 1.64 / 1.57 (the shared-memory carve-out also sizes the L1 the
-// digit epilogue's stores go through)
-__host__ __device__ constexpr int oz_nst(bool amn, bool outd) { return outd ? (amn ? 6 : 4) : 7; }
+// digit epilogue's stores go through).  Round 2 (integer epilogue, balanced MMA halves): mode 1
+// at 5 or 6 stages 3.4 % faster than at 4, mode 2 at 7 slightly slower than at 6
+__host__ __device__ constexpr int oz_nst(bool amn, bool outd) { return outd ? (amn ? 6 : 5) : 7; }
 template <int S, int NST_ = 6>
 struct OzGeom {
   static constexpr int SPS = 1;                                // digits per stage
