@@ -174,3 +174,27 @@ def test_presplit_shapes_bitwise(dims, mode, ells, tau, n_scales):
     assert hits[0] > 0 and hits[1] == 0, hits
     for a, b in zip(*res):
         assert np.array_equal(a, b)
+
+
+def test_presplit_nonfinite_inputs():
+    """A NaN and an Inf in the input: the fused combination + split marks non-finite fibres exactly
+    as the split kernel does, so both settings give the same outputs (every output entry depends on
+    every input entry through the dense exponentials, so here they are NaN throughout)."""
+    pb = _fd_problem()
+    v = pb.vs[0].copy()
+    v[3, 5, 7] = np.nan
+    v[100, 20, 1] = np.inf
+    res = []
+    for pre in (1, 0):
+        op = PhiKS(pb.A)
+        op.set_gemm_path("i8")
+        op.set_option("presplit", pre)
+        outs = op.apply(pb.tau, pb.ells, [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).to(DEV)],
+                        mode=pb.mode, n_scales=pb.n_scales)
+        torch.cuda.synchronize()
+        st = op.stats()
+        assert (st["presplit_inputs"] > 0) == bool(pre)
+        res.append([o.cpu().numpy() for o in outs])
+    for a, b in zip(*res):
+        np.testing.assert_array_equal(a, b)
+        assert np.isnan(a).any()
