@@ -42,7 +42,6 @@ constexpr int kOzBM = 128;  // fibers per tile (UMMA M, TMEM lanes)
 constexpr int kOzBN = 64;   // rows of E per tile (UMMA N)
 constexpr int kOzBK = 128;  // k per stage (bytes: one SWIZZLE_128B row = 4 UMMA K-steps of 32)
 constexpr int kOzUK = 32;   // k per UMMA (int8)
-constexpr int kOzStages = 4;
 
 __device__ __forceinline__ unsigned oz_smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -570,16 +569,6 @@ __device__ __forceinline__ void oz_commit(uint64_t* bar) {
                    oz_smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void oz_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
-        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-}
 
 __device__ __forceinline__ bool oz_elect() {
   uint32_t pred = 0;
@@ -599,10 +588,6 @@ __device__ __forceinline__ void oz_ld8(uint32_t taddr, uint32_t* v) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                : "r"(taddr));
-}
-// exact int32 → fp64 without I2F: 1.5·2^52 + 2^31 + v has v in its low mantissa bits
-__device__ __forceinline__ double oz_i2d(uint32_t v) {
-  return __hiloint2double(0x43380000, static_cast<int>(v ^ 0x80000000u)) - 6755401588539392.0;
 }
 // exact int64 → fp64 for |v| < 2^51: the bits of 1.5·2^52 + v
 __device__ __forceinline__ double oz_l2d(long long v) {
