@@ -380,3 +380,35 @@ def test_lincomb_given_vectors_subset(ells, path):
     assert st["tucker_ops"] == st["T_executed"] == (q - 1) * given + (s - 1) * p + 1 + (2 if 0 in ells else 0)
     for j in range(2):
         assert rel2(outs[j], W.as_flat(ref.out[j])) <= TOL, (ells, path, j)
+
+
+def test_host_async_chained_presplit():
+    """Host-memory applies on the chained int8 path with the pre-split combination (two handles in
+    flight, the bench's e2e pattern): equal bit for bit to the device-memory path."""
+    dims = (128, 128, 16)
+    pbs = []
+    for k, D in enumerate((2e-3, 1e-3)):
+        A = [D * 128.0 ** 2 * W.fd_dxx_neumann(n) / n ** 2 for n in dims]
+        pbs.append(W.Problem(f"hc{k}", dims, A, 0.05, "same", (0, 1, 2),
+                             [W.uniform_tensor(dims, 0.0, 3.0, seed=60 + k)], 1))
+    ops = [PhiKS(pb.A) for pb in pbs]
+    for op in ops:
+        op.set_gemm_path("i8")
+    pins, pouts, ref = [], [], []
+    for op, pb in zip(ops, pbs):
+        x = W.as_flat(pb.vs[0])
+        hi = torch.empty(x.size, dtype=torch.float64, pin_memory=True)
+        hi.numpy()[:] = x
+        pins.append(hi)
+        pouts.append([torch.empty(x.size, dtype=torch.float64, pin_memory=True) for _ in pb.ells])
+        ref.append([o.cpu().numpy() for o in op.apply(pb.tau, pb.ells, [dev(pb.vs[0])])])
+        st = op.stats()
+        assert st["i8_chained_ops"] > 0 and st["presplit_inputs"] > 0, st
+    for rep in range(2):
+        for op, pb, hi, ho in zip(ops, pbs, pins, pouts):
+            op.apply(pb.tau, pb.ells, [hi.numpy()], outs=[t.numpy() for t in ho], host_async=True)
+        for op in ops:
+            op.wait()
+        for ho, r in zip(pouts, ref):
+            for a, b in zip(ho, r):
+                assert np.array_equal(a.numpy(), b)
