@@ -356,7 +356,9 @@ phiks_status phiks_select_plan(int mode, double center_re, double center_im, dou
    the same sequence of applies with the same request (the applies meet in
    device-side barriers; a rank that does not arrive within 60 s makes the
    barrier give up and the handle report PHIKS_ERR_CUDA from
-   phiks_get_stats / host-memory applies). */
+   phiks_get_stats / host-memory applies). The timeout is sticky: every later
+   barrier of the handle returns at once (no second wait), and the handle keeps
+   reporting the error — destroy it and create the ranks' handles again. */
 phiks_status phiks_create_sharded(int d, const int* n, const double* const* A_host, int rank, int world,
                                   phiks_handle* out);
 

@@ -1092,6 +1092,12 @@ cudaError_t launch_fp64_peak(int kind, int blocks, int64_t iters, double* sink, 
 // ---------------------------------------------------------------------------
 __global__ void barrier_kernel(const __grid_constant__ BarrierParams p) {
   const int t = threadIdx.x;
+  // fail fast: once a barrier of this rank has timed out (sticky flag, reported by phiks_wait /
+  // phiks_get_stats / the next apply), later barriers return at once instead of waiting out
+  // their own timeouts one after another
+  int failed;
+  asm volatile("ld.volatile.global.s32 %0, [%1];\n" : "=r"(failed) : "l"(p.err));
+  if (failed) return;
   __shared__ uint64_t epoch;
   if (t == 0) {
     epoch = *p.epoch + 1;  // only this (stream-ordered) kernel touches the counter
