@@ -177,20 +177,26 @@ def dmma_roofline(args, t_local, mp_ms, mp_fl, mp_n, ex_n, ex_ms, peak_tf):
 I8_PAIRS = 28  # digit products per fp64 product: pairs (s, t) of 7 digits with s + t < 7
 
 
-def i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, g_ms, g_n, ex_n, ex_ms, dmma_peak, clocks=None):
+def i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, g_ms, g_n, ex_n, ex_ms, dmma_peak, clocks=None,
+                kblocks=(0, 0)):
     """Roofline of the dominant kernel, the int8 digit-product GEMM (ozaki.cu): algorithmic int8
     ops = 28 digit pairs × 2·rows·n² per fp64 product; peak = the measured bf16 dense peak of
     MEASURED_PEAKS.json × 2 (the guide's nominal int8 : bf16 ratio).  The denominator follows the
     clock the kernel actually ran at: the burst figure (measured at max SM clock) when the median
     SM clock sampled over the timed region is ≥ 0.95 of max, else the sustained figure (measured
-    at a power-capped 1342 MHz median)."""
+    at a power-capped 1342 MHz median).  With PHIKS_OPT_KSKIP the GEMM skips the digit blocks of E
+    that are all zero: `achieved` counts only the MMAs that ran (the library's
+    k-block counters), the dense count is reported beside it."""
     pk = measured_peaks()
     burst_bf16, sust_bf16 = pk.get("bf16_tflops"), pk.get("bf16_tflops_sustained")
     at_max = bool(clocks and clocks.get("sm_mhz") and clocks.get("sm_max_mhz")
                   and clocks["sm_mhz"] >= 0.95 * clocks["sm_max_mhz"])
     bf16 = (burst_bf16 if at_max else sust_bf16) or burst_bf16 or sust_bf16
     peak = 2.0 * bf16 if bf16 else 4500.0
-    ops = I8_PAIRS * i8_fl  # i8_flops counts 2·rows·n² per GEMM term
+    dense_ops = I8_PAIRS * i8_fl  # i8_flops counts 2·rows·n² per GEMM term
+    kb_tot, kb_run = kblocks
+    run_frac = kb_run / kb_tot if kb_tot else 1.0
+    ops = dense_ops * run_frac  # the MMAs that ran (equal work per (unit, k-block))
     ach = ops / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
     tr = load_i8_traffic()
     per_launch_gflop = i8_fl / max(g_n, 1) / 1e9
@@ -217,6 +223,10 @@ def i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, g_ms, g_n, ex_n
             "kernel": "oz_gemm_kernel<7, AMN, OUTD> (tcgen05.mma kind::i8, TMEM accumulators, TMA SWIZZLE_128B, chained modes: DESIGN.md §4d): "
                       "the Tucker-operator μ-mode products",
             "algorithmic_ops_per_launch": ops / max(g_n, 1),
+            "dense_ops_per_launch": dense_ops / max(g_n, 1),
+            "kblocks_run_fraction": run_frac,
+            "kblocks_note": "(fibre tile x 64-row n-tile, 128-wide k-block) units whose E digits are not all zero "
+                            "(PHIKS_OPT_KSKIP, DESIGN.md §4g); the skipped ones add exact integer zeros",
             "algorithmic_bytes_per_launch_max": elems * 15.0,
             "peak_source": (f"MEASURED_PEAKS.json {'bf16_tflops' if at_max else 'bf16_tflops_sustained'} × 2 "
                             "(int8 : bf16 dense = 2, B200_PROFILING.md)") if bf16
@@ -390,6 +400,7 @@ def b200_arm(args):
     i8_fl = sum(s["i8_flops"] for s in st)
     i8_gemm_ms = sum(s["i8_gemm_ms"] for s in st)
     i8_gemm_n = sum(s["i8_gemm_launches"] for s in st)
+    kblocks = (sum(s["i8_kblocks"] for s in st), sum(s["i8_kblocks_run"] for s in st))
     for op in ops:
         op.set_profiling(False)
     t = t_local
@@ -456,7 +467,7 @@ def b200_arm(args):
 
     if i8_gemm_n:
         roof = i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, i8_gemm_ms, i8_gemm_n, ex_n, ex_ms,
-                           peak_tf, clocks=clk.summary())
+                           peak_tf, clocks=clk.summary(), kblocks=kblocks)
     else:
         roof = dmma_roofline(args, t_local, mp_ms, mp_fl, mp_n, ex_n, ex_ms, peak_tf)
     if rank == 0:
@@ -471,7 +482,10 @@ def b200_arm(args):
                        "parallelism": f"slab{world} (mode-3 slabs, transposition fused into peer stores)"
                        if world > 1 else "single",
                        "l2": "inputs larger than L2 (134 MB per vector > 126 MB L2)", "plans": plans,
-                       "mu_mode_gflop_per_step": flops_step / 1e9},
+                       "mu_mode_gflop_per_step": flops_step / 1e9,
+                       "mu_mode_flops": "2*N*sum(n_mu) per executed Tucker operator (dense mu-mode products, the "
+                                        "metric's count); the int8 GEMM skips the E digit blocks that are all zero "
+                                        "(roofline.kblocks_run_fraction)"},
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
             "roofline": roof, "cpu_baseline": cpu, "parity": parity,
         }

@@ -129,6 +129,10 @@ typedef struct {
   int64_t presplit_inputs;        /* inputs of the last apply's chained batches whose mode-1
                                      digits the previous batch's combination wrote (no
                                      separate split pass)              */
+  int64_t i8_kblocks;             /* profiling: (fibre tile × 64-row n-tile, 128-wide k-block)
+                                     units of the int8 GEMM launches, and the subset  */
+  int64_t i8_kblocks_run;         /*   whose MMAs ran (the rest had all-zero E digits and
+                                     were skipped, PHIKS_OPT_KSKIP)                  */
 } phiks_stats;
 
 /* Create a handle for K = A_d ⊕ … ⊕ A_1.
@@ -249,11 +253,19 @@ phiks_status phiks_set_gemm_path(phiks_handle h, int path);
                      next squaring level's inputs also writes their mode-1 int8
                      digit planes (chained batches; stats presplit_inputs); 0 = the
                      next batch splits them in a separate pass.  Same digits,
-                     same results bit for bit. */
+                     same results bit for bit.
+   PHIKS_OPT_KSKIP   1 (default) = the int8 GEMM skips the (64-row n-tile,
+                     128-wide k-block) blocks of E whose digits are all zero —
+                     the exponentials of banded factors (the FD operators of
+                     every BASELINE config) are numerically banded, and a skipped
+                     block's MMAs would add exact integer zeros — and gives its
+                     n-tiles CTAs in proportion to the remaining work
+                     (DESIGN.md §4g); 0 = every block.  Same results bit for bit. */
 #define PHIKS_OPT_SPLIT 0
 #define PHIKS_OPT_CHAIN 1
 #define PHIKS_OPT_GRAPHS 2
 #define PHIKS_OPT_PRESPLIT 3
+#define PHIKS_OPT_KSKIP 4
 phiks_status phiks_set_option(phiks_handle h, int option, int value);
 phiks_status phiks_get_option(phiks_handle h, int option, int* value);
 

@@ -187,7 +187,8 @@ class PhiKS:
                 "i8_mode_launches": st.i8_mode_launches, "i8_launches": st.i8_launches, "i8_ms": st.i8_ms,
                 "i8_flops": st.i8_flops, "i8_gemm_launches": st.i8_gemm_launches, "i8_gemm_ms": st.i8_gemm_ms,
                 "i8_chained_ops": st.i8_chained_ops, "shard_digit_ops": st.shard_digit_ops,
-                "presplit_inputs": st.presplit_inputs}
+                "presplit_inputs": st.presplit_inputs,
+                "i8_kblocks": st.i8_kblocks, "i8_kblocks_run": st.i8_kblocks_run}
 
     GEMM_PATHS = {"auto": 0, "dmma": 1, "i8": 2}
 
@@ -195,11 +196,12 @@ class PhiKS:
         """μ-mode-product path of the Tucker launches: "auto", "dmma" or "i8"."""
         _lib.check(_lib.load().phiks_set_gemm_path(self._h, self.GEMM_PATHS[path]), "phiks_set_gemm_path")
 
-    OPTIONS = {"split": 0, "chain": 1, "graphs": 2, "presplit": 3}
+    OPTIONS = {"split": 0, "chain": 1, "graphs": 2, "presplit": 3, "kskip": 4}
 
     def set_option(self, name: str, value: int):
         """Execution option of the handle (include/phiks.h PHIKS_OPT_*): "split" 0/1/2,
-        "chain" 0 (off) / 1 (guarded, default) / 2 (forced), "graphs" 0/1, "presplit" 0/1."""
+        "chain" 0 (off) / 1 (guarded, default) / 2 (forced), "graphs" 0/1, "presplit" 0/1,
+        "kskip" 0/1 (zero E digit blocks skipped by the int8 GEMM, default 1)."""
         _lib.check(_lib.load().phiks_set_option(self._h, self.OPTIONS[name], int(value)), "phiks_set_option")
 
     def get_option(self, name: str) -> int:

@@ -51,7 +51,8 @@ class Stats(ctypes.Structure):
                 ("i8_mode_launches", ctypes.c_int64), ("i8_launches", ctypes.c_int64), ("i8_ms", ctypes.c_double),
                 ("i8_flops", ctypes.c_double), ("i8_gemm_launches", ctypes.c_int64), ("i8_gemm_ms", ctypes.c_double),
                 ("i8_chained_ops", ctypes.c_int64), ("shard_digit_ops", ctypes.c_int64),
-                ("presplit_inputs", ctypes.c_int64)]
+                ("presplit_inputs", ctypes.c_int64),
+                ("i8_kblocks", ctypes.c_int64), ("i8_kblocks_run", ctypes.c_int64)]
 
 
 _lib = None

@@ -100,6 +100,8 @@ void Exec::tucker_chain_i8(const std::vector<TuckerItem>& items, size_t c0, size
     p.R = R;
     p.n = n;
     p.S = S;
+    p.kskip = h->opt_kskip;
+    p.kcount = h->profiling ? h->d_kcount : nullptr;
     p.n_next = mu < mlast ? (mu == st0 ? h->gn[d - 1] : h->n[mu + 1]) : 0;
     if (mu == mlast && rm) p.remap = rm1 ? *rm1 : *rm;
     if (mu == st0) {

@@ -109,12 +109,14 @@ struct phiks_ctx {
   int opt_chain = 1;   // PHIKS_OPT_CHAIN: 0 off, 1 guarded (Metzler factors), 2 forced
   int opt_graphs = 1;  // PHIKS_OPT_GRAPHS
   int opt_presplit = 1;  // PHIKS_OPT_PRESPLIT
+  int opt_kskip = 1;     // PHIKS_OPT_KSKIP
   bool chain_safe() const {  // every factor Metzler: exponentials entrywise ≥ 0 (τ > 0)
     for (const auto& F : factors)
       if (!F.metzler) return false;
     return !factors.empty();
   }
   int ev_used = 0;
+  unsigned long long* d_kcount = nullptr;  // profiling: the int8 GEMM's k-block counters (OzakiParams::kcount)
   // ---- slab sharding along the outermost mode (phiks_create_sharded) ----
   // n[] holds the LOCAL dims of layout S_d (n[d-1] = gn[d-1]/world); the
   // transposed layout S_{d-1} has dims (n_1..n_{d-2}, gn[d-2]/world, gn[d-1]).
@@ -368,6 +370,8 @@ struct Exec {
       p.R = R;
       p.n = n;
       p.S = kOzDigits;
+      p.kskip = h->opt_kskip;
+      p.kcount = h->profiling ? h->d_kcount : nullptr;
       if (rm) p.remap = *rm;
       p.cplx_j = terms[i].kcat ? 1 : 0;
       size_t j = i;

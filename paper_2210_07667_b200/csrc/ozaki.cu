@@ -356,16 +356,21 @@ __global__ void __launch_bounds__(256) oz_split_e_kernel(const OzakiParams p) {
   bad = __any_sync(0xffffffffu, bad);
   const int ex = bad ? 0 : slice_exponent(m);
   int8_t* es = p.es + static_cast<int64_t>(slot) * S * n * Kp;
-  for (int k0 = 4 * lane; k0 < Kp; k0 += 128) {
+  unsigned kbm = 0;  // k-blocks (128 k each; iteration kb of this loop) with a nonzero digit in row j
+  for (int k0 = 4 * lane, kb = 0; k0 < Kp; k0 += 128, ++kb) {
     double v[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) v[q] = (k0 + q < K && !bad) ? E[j + static_cast<int64_t>(k0 + q) * n] : 0.0;
-    uint32_t pk[S];
+    uint32_t pk[S], nz = 0;
     split4<S>(v, ex, pk);
 #pragma unroll
-    for (int s = 0; s < S; ++s)
+    for (int s = 0; s < S; ++s) {
       *reinterpret_cast<uint32_t*>(es + (static_cast<int64_t>(s) * n + j) * Kp + k0) = pk[s];
+      nz |= pk[s];
+    }
+    if (__any_sync(0xffffffffu, nz != 0)) kbm |= 1u << kb;
   }
+  if (lane == 0 && p.eext && kbm) atomicOr(reinterpret_cast<unsigned*>(p.eext + 3 * p.ne + slot), kbm << (4 * (j / kOzBN)));
   if (lane == 0) {  // the row's scale 2^{ee-30} (the GEMM epilogue's 2^-30: 2^-14 of the digit scaling, 2^-16 of its sums)
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     p.esc[static_cast<int64_t>(slot) * n + j] = bad ? qnan : scalbn(1.0, ex - 30);
@@ -985,6 +990,7 @@ struct OzGeom {
   static constexpr int THREADS = 64 + EPI_WARPS * 32;
   static_assert(S * kOzBN <= 512, "TMEM holds one 64-column accumulator per diagonal");
   static_assert(SMEM <= 232448, "shared memory");
+  static_assert((2 * NST + 8) * 8 + 16 + 4 * kMaxTerms <= 512, "barriers, TMEM slot and block masks");
 };
 
 // work of CTA k: n-tile nt = k % ntn, units u = q, q + Q, … over (term, m-tile),
@@ -993,16 +999,69 @@ struct OzGeom {
 // so the ntn CTAs sharing q read the same fiber tiles together and all CTAs sweep one term's
 // tiles at a time (a contiguous run of units per CTA measured slower: 2.09 -> 2.97 ms on the
 // chained mode-2 launch of configs[3])
+// k-blocks of term i's E digits that n-tile t multiplies: the nonzero blocks split_e recorded
+// (at least one, so that every tile's accumulators are written), all of them without kskip;
+// skm = the matrices' block masks, copied to shared memory at the kernel's start (a global load per
+// tile on the MMA warp's path measured 9 % slower per launch)
+__device__ __forceinline__ unsigned oz_kmask(const OzakiParams& p, const uint32_t* skm, int i, int t, int nk) {
+  const unsigned full = (1u << nk) - 1u;
+  if (!p.kskip) return full;
+  const unsigned m = (skm[p.terms[i].eslot] >> (4 * t)) & full;
+  return m ? m : 1u;
+}
+// kskip: the n-tile groups get CTAs in proportion to their work, Σ_terms (16·#k-blocks + 12) (a tile
+// of the configs[3] launches: ~4,150 cycles of MMAs per k-block and a ~2,350-cycle hand-over,
+// DESIGN.md §4e), so that the groups sweep the fibre tiles at the same rate and the L2 still
+// serves each fibre tile once for all of them
 struct OzSched {
-  int ntn, nt, q, Q;
+  int ntn, nt, q, Q, nk;
   int64_t Mt, units;
-  __device__ OzSched(const OzakiParams& p) {
+  __device__ OzSched(const OzakiParams& p, const uint32_t* skm, int fix) {
     ntn = (p.n + kOzBN - 1) / kOzBN;
-    nt = static_cast<int>(blockIdx.x % ntn);
-    q = static_cast<int>(blockIdx.x / ntn);
-    Q = static_cast<int>(gridDim.x / ntn);
+    nk = p.Kp / kOzBK;
     Mt = (p.L * p.R + kOzBM - 1) / kOzBM;
     units = Mt * p.nterms;
+    const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+    if (!p.kskip) {
+      nt = b % ntn;
+      q = b / ntn;
+      Q = G / ntn;
+      return;
+    }
+    int64_t cost[8], tot = 0;
+    int size[8], sum = 0;
+    for (int t = 0; t < ntn; ++t) {
+      cost[t] = 0;
+      for (int i = 0; i < p.nterms; ++i) cost[t] += 16 * __popc(oz_kmask(p, skm, i, t, nk)) + fix;
+      tot += cost[t];
+    }
+    for (int t = 0; t < ntn; ++t) {
+      size[t] = max(1, static_cast<int>(G * cost[t] / tot));
+      sum += size[t];
+    }
+    while (sum < G) {  // largest remainder first
+      int bt = 0;
+      for (int t = 1; t < ntn; ++t)
+        if (G * cost[t] - size[t] * tot > G * cost[bt] - size[bt] * tot) bt = t;
+      ++size[bt];
+      ++sum;
+    }
+    while (sum > G) {
+      int bt = 0;
+      for (int t = 1; t < ntn; ++t)
+        if (size[t] > size[bt]) bt = t;
+      --size[bt];
+      --sum;
+    }
+    nt = ntn - 1;
+    q = b;
+    for (int t = 0, s0 = 0; t < ntn; s0 += size[t], ++t)
+      if (b < s0 + size[t]) {
+        nt = t;
+        q = b - s0;
+        break;
+      }
+    Q = size[nt];
   }
 };
 
@@ -1025,8 +1084,14 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
   uint64_t* e_full = t_empty + 1;  // SE: [2]
   uint64_t* e_empty = e_full + 2;   // SE: [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e_empty + 2);
+  uint32_t* skm = tmem_slot + 4;  // [ne ≤ kMaxTerms] nonzero E digit blocks (kskip)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const OzSched sc(p);
+  if (p.kskip && threadIdx.x < p.ne) skm[threadIdx.x] = static_cast<uint32_t>(p.eext[3 * p.ne + threadIdx.x]);
+  __syncthreads();
+#ifndef OZ_KS_FIX
+#define OZ_KS_FIX 12
+#endif
+  const OzSched sc(p, skm, OZ_KS_FIX);
   if (sc.q >= sc.Q) return;  // idle CTA (grid not a multiple of the n-tile count)
   const int nk = p.Kp / kOzBK;
   constexpr int NSG = S / G::SPS;
@@ -1076,7 +1141,9 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
         ++bgen;
       }
       const int xs = p.terms[term].xslot;
+      const unsigned km = oz_kmask(p, skm, term, sc.nt, nk);
       for (int kb = 0; kb < nk; ++kb) {
+        if (!((km >> kb) & 1u)) continue;  // all E digits zero in this k-block: no MMAs, no loads
         if (SE) {  // this k-block's E digits (all S digit planes × 64 rows) into ring slot ek & 1
           const int es = ek & 1;
           if (ek >= 2) oz_mbar_wait(&e_empty[es], ((ek >> 1) & 1) ^ 1);
@@ -1111,6 +1178,7 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     const uint64_t a_desc0 = AMN ? oz_desc_mn_sw128(smem) : oz_desc_sw128(smem), b_desc0 = oz_desc_sw128(bres);
     constexpr uint64_t a_kstep = AMN ? (kOzUK * kOzBM) >> 4 : kOzUK >> 4;  // one UMMA k-step of A
     int cur_term = -1, bgen = 0, it = 0, tile = 0, ek = 0;
+    unsigned long long kb_run = 0;
     for (int64_t u = sc.q; u < sc.units; u += sc.Q, ++tile) {
       const int term = static_cast<int>(u / sc.Mt);
       if (!SE && term != cur_term) {
@@ -1128,7 +1196,11 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
       // descriptor are compile-time constants (the issue loop is a few uniform adds per MMA).
       // Issuing the digits high to low with the accumulators released in two diagonal groups
       // (to overlap the drain) measured 14 % slower
+      const unsigned km = oz_kmask(p, skm, term, sc.nt, nk);
+      const int kb0 = __ffs(km) - 1;  // the first k-block initialises the accumulators
+      kb_run += __popc(km);
       for (int kb = 0; kb < nk; ++kb) {
+        if (!((km >> kb) & 1u)) continue;
         const int es = ek & 1;
         if (SE) {
           oz_mbar_wait(&e_full[es], (ek >> 1) & 1);
@@ -1144,7 +1216,7 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
           if (oz_elect()) {
 #pragma unroll
             for (int kk = 0; kk < kOzBK / kOzUK; ++kk) {
-              const uint32_t accf = (kb > 0 || s > 0 || kk > 0) ? 1u : 0u;
+              const uint32_t accf = (kb > kb0 || s > 0 || kk > 0) ? 1u : 0u;
               // a_s × [b_0 | … | b_{S-1-s}] → diagonals s … S-1 (contiguous columns), N ≤ 256 per MMA;
               // above 256 columns two equal halves (448 = 224 + 224, 384, 320) rather than 256 + rest:
               // two equal independent accumulation streams instead of a small tail MMA (−1.5 % per launch)
@@ -1169,6 +1241,10 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
       }
       if (oz_elect()) oz_commit(t_full);
       __syncwarp();
+    }
+    if (p.kcount && lane == 0) {
+      atomicAdd(p.kcount, static_cast<unsigned long long>(tile) * nk);
+      atomicAdd(p.kcount + 1, kb_run);
     }
   } else {
     // ---- epilogue warps: lane quarter wq = warp % 4 (TMEM lanes 32wq..), column half ch ----
@@ -1275,7 +1351,19 @@ bool oz_split_tma_ok(const OzakiParams& p) {
 }
 
 template <int S, bool AMN, bool OUTD, bool SE, bool REM = false>
-cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
+cudaError_t oz_gemm_go(const OzakiParams& p0, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
+  // zero-block skipping only where the MMAs pace the tile: the fp64-output launches.  In the digit-
+  // output (chained) launches the epilogue's per-tile work is as long as the MMAs',
+  // so a tile with fewer k-blocks is barely shorter, and the proportional CTA groups measured 3-20 %
+  // slower there (the groups drift apart and the fibre tiles are read from DRAM twice, §4g)
+  OzakiParams pc;
+  const OzakiParams* pp = &p0;
+  if (OUTD && p0.kskip) {
+    pc = p0;
+    pc.kskip = 0;
+    pp = &pc;
+  }
+  const OzakiParams& p = *pp;
   if constexpr (!REM && (AMN || !OUTD)) {  // peer-store epilogues: fp64 outputs, or AMN next-mode digits
     if (p.remap.world > 0) return oz_gemm_go<S, AMN, OUTD, SE, true>(p, st, ta, tb);
   } else if constexpr (!REM) {
@@ -1299,7 +1387,12 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   int64_t per = sms / ntn;  // CTAs per n-tile
   if (per > units) per = units;
   if (per < 1) per = 1;
-  oz_gemm_kernel<S, AMN, OUTD, SE, REM><<<static_cast<unsigned>(per * ntn), G::THREADS, G::SMEM, st>>>(p, ta, tb);
+  // kskip: every SM, the kernel splits them over the n-tiles by their work (OzSched)
+  int64_t grid = per * ntn;
+  if (p.kskip) {
+    grid = units * ntn < sms ? units * ntn : sms;
+  }
+  oz_gemm_kernel<S, AMN, OUTD, SE, REM><<<static_cast<unsigned>(grid), G::THREADS, G::SMEM, st>>>(p, ta, tb);
   return cudaGetLastError();
 }
 
@@ -1372,7 +1465,7 @@ cudaError_t oz_launch(const OzakiParams& p0, cudaStream_t st, bool split_x, bool
   if (split_e && p.eext && !p.e_ready) {  // min / max / flag slots of the row-norm exponents
     cudaMemsetAsync(p.eext, 0x7f, sizeof(int) * p.ne, st);
     cudaMemsetAsync(p.eext + p.ne, 0x80, sizeof(int) * p.ne, st);
-    cudaMemsetAsync(p.eext + 2 * p.ne, 0, sizeof(int) * p.ne, st);
+    cudaMemsetAsync(p.eext + 2 * p.ne, 0, sizeof(int) * 2 * p.ne, st);  // flags, nonzero digit blocks
   }
   if (split_e && !p.e_ready) oz_split_e_kernel<S><<<dim3((p.n + 7) / 8, p.ne), 256, 0, st>>>(p);
   if (split_e && p.n_next > 0 && p.nterms > 0 && !p.shard_stage0) {  // next-mode exponent bounds (chained modes)
@@ -1413,7 +1506,7 @@ size_t ozaki_workspace_bytes(int64_t L, int n, int64_t R, int S, int nx, int ne,
   auto al = [](size_t b) { return (b + 1023) & ~size_t(1023); };
   return al(static_cast<size_t>(nx) * S * C * Kp) + al(static_cast<size_t>(nx) * C * 8) +
          al(static_cast<size_t>(ne) * S * n * Kp) + 2 * al(static_cast<size_t>(ne) * n * 8) +
-         al(static_cast<size_t>(ne) * n * 4) + al(static_cast<size_t>(ne) * 3 * 4);
+         al(static_cast<size_t>(ne) * n * 4) + al(static_cast<size_t>(ne) * 4 * 4);
 }
 
 int oz_multi_combine_split_max_out(int n) { return n <= 256 ? 8 : 4; }  // sums in registers: NOUT·n/32 doubles
@@ -1464,7 +1557,7 @@ void ozaki_bind_workspace(OzakiParams& p, void* ws) {
   p.ecol = reinterpret_cast<int*>(w);
   w += al(static_cast<size_t>(p.ne) * p.n * 4);
   p.eext = reinterpret_cast<int*>(w);
-  w += al(static_cast<size_t>(p.ne) * 3 * 4);
+  w += al(static_cast<size_t>(p.ne) * 4 * 4);
   p.xs = reinterpret_cast<int8_t*>(w);
   w += al(static_cast<size_t>(p.nx) * p.S * C * p.Kp);
   p.xsc = reinterpret_cast<double*>(w);

@@ -153,6 +153,7 @@ phiks_status phiks_destroy(phiks_handle h) {
   if (h->ws_own) cudaFree(h->ws_own);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
   if (h->h_barrier_err) cudaFreeHost(h->h_barrier_err);
+  if (h->d_kcount) cudaFree(h->d_kcount);
   for (int k = 0; k < kMaxRanks; ++k)
     if (h->peer_ipc[k] && h->peer[k]) cudaIpcCloseMemHandle(h->peer[k]);
   for (cudaEvent_t e : {h->ev_h2d, h->ev_d2h[0], h->ev_d2h[1], h->ev_cdone[0], h->ev_cdone[1], h->ev_ready})
@@ -434,7 +435,14 @@ phiks_status phiks_get_stats(phiks_handle h, phiks_stats* out) {
   out->i8_flops = 0.0;
   out->i8_gemm_launches = 0;
   out->i8_gemm_ms = 0.0;
+  out->i8_kblocks = out->i8_kblocks_run = 0;
   if (h->profiling) {
+    if (h->d_kcount) {
+      unsigned long long kc[2] = {0, 0};
+      CUDA_TRY(cudaMemcpy(kc, h->d_kcount, sizeof(kc), cudaMemcpyDeviceToHost));
+      out->i8_kblocks = static_cast<int64_t>(kc[0]);
+      out->i8_kblocks_run = static_cast<int64_t>(kc[1]);
+    }
     for (int i = 0; i < h->ev_used; ++i) {
       CUDA_TRY(cudaEventSynchronize(h->ev[i].second));
       float ms = 0.f;
@@ -482,6 +490,7 @@ phiks_status phiks_set_option(phiks_handle h, int option, int value) {
     case PHIKS_OPT_CHAIN: slot = &h->opt_chain; hi = 2; break;
     case PHIKS_OPT_GRAPHS: slot = &h->opt_graphs; hi = 1; break;
     case PHIKS_OPT_PRESPLIT: slot = &h->opt_presplit; hi = 1; break;
+    case PHIKS_OPT_KSKIP: slot = &h->opt_kskip; hi = 1; break;
     default: return fail(PHIKS_ERR_ARG, "unknown option");
   }
   if (value < lo || value > hi) return fail(PHIKS_ERR_ARG, "option value out of range");
@@ -500,6 +509,7 @@ phiks_status phiks_get_option(phiks_handle h, int option, int* value) {
     case PHIKS_OPT_CHAIN: *value = h->opt_chain; break;
     case PHIKS_OPT_GRAPHS: *value = h->opt_graphs; break;
     case PHIKS_OPT_PRESPLIT: *value = h->opt_presplit; break;
+    case PHIKS_OPT_KSKIP: *value = h->opt_kskip; break;
     default: return fail(PHIKS_ERR_ARG, "unknown option");
   }
   return PHIKS_OK;
@@ -509,6 +519,10 @@ phiks_status phiks_set_profiling(phiks_handle h, int on) {
   if (!h) return fail(PHIKS_ERR_ARG, "null handle");
   h->profiling = on != 0;
   h->ev_used = 0;
+  if (h->profiling) {  // k-block counters since profiling was switched on
+    if (!h->d_kcount) CUDA_TRY(cudaMalloc(&h->d_kcount, 2 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(h->d_kcount, 0, 2 * sizeof(unsigned long long)));
+  }
   return PHIKS_OK;
 }
 
@@ -568,6 +582,7 @@ phiks_status phiks_mode_product_i8(int d, const int* n, int mu, int slices, int 
     p.R = R;
     p.n = n[mu];
     p.S = slices;
+    p.kskip = 1;
     p.nx = p.ne = p.nterms = 0;
     for (int i = i0; i < std::min(batch, i0 + kMaxTerms); ++i) {
       int xs = -1, es = -1;

@@ -150,7 +150,9 @@ struct OzakiParams {
   double* esc;   // [ne][n] row exponents
   double* eb;    // [ne][n] exponents b_j with ‖e_j‖₁ < 2^{b_j} (chained modes)
   int* ecol;     // [ne][n] (ee_j − 30) − b_j (INT_MIN: non-finite row), the digit epilogue's column shift
-  int* eext;     // [3][ne] min_j b_j, max_j b_j, any non-finite row (chained modes' fast-path test)
+  int* eext;     // [4][ne] min_j b_j, max_j b_j, any non-finite row (chained modes' fast-path test), and
+                 // the nonzero digit blocks of each matrix: bit 4·t + kb set when some digit of rows
+                 // [64t, 64t+64) × k ∈ [128kb, 128kb+128) is nonzero (the GEMM skips the others)
   int a_mn;      // 1: xs holds [nx][S][L·n·R] digit planes in the fp64 layout (MN-major A, L % 128 == 0)
   int cplx_j;    // complex μ ≥ 2 product: fibres [x ; Jx] of length K = 2n against
                  // E = [Re M | Im M] (n × 2n, column-major, Im M right after Re M), so y = Re M·x + J·Im M·x
@@ -158,6 +160,9 @@ struct OzakiParams {
   Remap remap;   // slab-sharded stage (world > 0): fp64 outputs (out) or next-mode digit planes (dig,
                  // AMN only) go to the owner rank; out / dig = byte offsets in the owners' regions
   int e_ready;       // 1: es/esc/eb/ecol/eext already hold these matrices' split (the previous launch's)
+  unsigned long long* kcount;  // profiling (or null): [0] += (unit, k-block) pairs, [1] += those run
+  int kskip;         // 1: the GEMM skips the k-blocks whose E digits are all zero (exact: their MMAs
+                     // add integer zeros) and sizes its n-tile CTA groups by the remaining work
   int shard_stage0;  // 1: the next-mode exponents come from the cross-rank exchange
                      // (launch_oz_shard_pmax / launch_oz_shard_tables), not oz_chain_kernel
 };

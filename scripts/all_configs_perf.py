@@ -17,6 +17,8 @@ for idx in [int(x) for x in os.environ.get("CONFIGS", "0,1,2,3,4").split(",")]:
         op = PhiKS(pb.A)
         if os.environ.get("PRESPLIT") is not None:  # A/B of PHIKS_OPT_PRESPLIT
             op.set_option("presplit", int(os.environ["PRESPLIT"]))
+        if os.environ.get("KSKIP") is not None:  # A/B of PHIKS_OPT_KSKIP
+            op.set_option("kskip", int(os.environ["KSKIP"]))
         ops.append(op)
         vins.append([torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).cuda() for v in pb.vs])
         nout = len(pb.ells) * pb.n_scales if pb.mode == "same" else pb.n_scales
