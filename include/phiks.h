@@ -254,8 +254,9 @@ phiks_status phiks_set_gemm_path(phiks_handle h, int path);
                      digit planes (chained batches; stats presplit_inputs); 0 = the
                      next batch splits them in a separate pass.  Same digits,
                      same results bit for bit.
-   PHIKS_OPT_KSKIP   1 (default) = the int8 GEMM skips the (64-row n-tile,
-                     128-wide k-block) blocks of E whose digits are all zero —
+   PHIKS_OPT_KSKIP   1 (default) = the int8 GEMM launches with fp64 outputs (the
+                     last mode of a chained Tucker operator) skip the (64-row
+                     n-tile, 128-wide k-block) blocks of E whose digits are all zero —
                      the exponentials of banded factors (the FD operators of
                      every BASELINE config) are numerically banded, and a skipped
                      block's MMAs would add exact integer zeros — and gives its
