@@ -1003,9 +1003,10 @@ struct OzGeom {
 // (at least one, so that every tile's accumulators are written), all of them without kskip;
 // skm = the matrices' block masks, copied to shared memory at the kernel's start (a global load per
 // tile on the MMA warp's path measured 9 % slower per launch)
+template <bool KS>
 __device__ __forceinline__ unsigned oz_kmask(const OzakiParams& p, const uint32_t* skm, int i, int t, int nk) {
   const unsigned full = (1u << nk) - 1u;
-  if (!p.kskip) return full;
+  if (!KS) return full;
   const unsigned m = (skm[p.terms[i].eslot] >> (4 * t)) & full;
   return m ? m : 1u;
 }
@@ -1016,13 +1017,13 @@ __device__ __forceinline__ unsigned oz_kmask(const OzakiParams& p, const uint32_
 struct OzSched {
   int ntn, nt, q, Q, nk;
   int64_t Mt, units;
-  __device__ OzSched(const OzakiParams& p, const uint32_t* skm, int fix) {
+  __device__ OzSched(const OzakiParams& p, const uint32_t* skm, int fix, bool ks) {
     ntn = (p.n + kOzBN - 1) / kOzBN;
     nk = p.Kp / kOzBK;
     Mt = (p.L * p.R + kOzBM - 1) / kOzBM;
     units = Mt * p.nterms;
     const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
-    if (!p.kskip) {
+    if (!ks) {
       nt = b % ntn;
       q = b / ntn;
       Q = G / ntn;
@@ -1032,7 +1033,7 @@ struct OzSched {
     int size[8], sum = 0;
     for (int t = 0; t < ntn; ++t) {
       cost[t] = 0;
-      for (int i = 0; i < p.nterms; ++i) cost[t] += 16 * __popc(oz_kmask(p, skm, i, t, nk)) + fix;
+      for (int i = 0; i < p.nterms; ++i) cost[t] += 16 * __popc(oz_kmask<true>(p, skm, i, t, nk)) + fix;
       tot += cost[t];
     }
     for (int t = 0; t < ntn; ++t) {
@@ -1067,7 +1068,8 @@ struct OzSched {
 
 // SE: the E digits stream through a 2-block ring (one 128-k block per stage group) instead of
 // staying resident per term: always for n > 256, and for short launches (kOzSeUnits)
-template <int S, bool AMN, bool OUTD, bool SE, bool REM>
+// KS: skip the all-zero E digit blocks (PHIKS_OPT_KSKIP, fp64-output launches only)
+template <int S, bool AMN, bool OUTD, bool SE, bool REM, bool KS>
 __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb) {
@@ -1086,12 +1088,14 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e_empty + 2);
   uint32_t* skm = tmem_slot + 4;  // [ne ≤ kMaxTerms] nonzero E digit blocks (kskip)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (p.kskip && threadIdx.x < p.ne) skm[threadIdx.x] = static_cast<uint32_t>(p.eext[3 * p.ne + threadIdx.x]);
-  __syncthreads();
+  if constexpr (KS) {
+    if (threadIdx.x < p.ne) skm[threadIdx.x] = static_cast<uint32_t>(p.eext[3 * p.ne + threadIdx.x]);
+    __syncthreads();
+  }
 #ifndef OZ_KS_FIX
 #define OZ_KS_FIX 12
 #endif
-  const OzSched sc(p, skm, OZ_KS_FIX);
+  const OzSched sc(p, skm, OZ_KS_FIX, KS);
   if (sc.q >= sc.Q) return;  // idle CTA (grid not a multiple of the n-tile count)
   const int nk = p.Kp / kOzBK;
   constexpr int NSG = S / G::SPS;
@@ -1141,9 +1145,9 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
         ++bgen;
       }
       const int xs = p.terms[term].xslot;
-      const unsigned km = oz_kmask(p, skm, term, sc.nt, nk);
+      const unsigned km = oz_kmask<KS>(p, skm, term, sc.nt, nk);
       for (int kb = 0; kb < nk; ++kb) {
-        if (!((km >> kb) & 1u)) continue;  // all E digits zero in this k-block: no MMAs, no loads
+        if (KS && !((km >> kb) & 1u)) continue;  // all E digits zero in this k-block: no MMAs, no loads
         if (SE) {  // this k-block's E digits (all S digit planes × 64 rows) into ring slot ek & 1
           const int es = ek & 1;
           if (ek >= 2) oz_mbar_wait(&e_empty[es], ((ek >> 1) & 1) ^ 1);
@@ -1196,11 +1200,11 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
       // descriptor are compile-time constants (the issue loop is a few uniform adds per MMA).
       // Issuing the digits high to low with the accumulators released in two diagonal groups
       // (to overlap the drain) measured 14 % slower
-      const unsigned km = oz_kmask(p, skm, term, sc.nt, nk);
-      const int kb0 = __ffs(km) - 1;  // the first k-block initialises the accumulators
-      kb_run += __popc(km);
+      const unsigned km = oz_kmask<KS>(p, skm, term, sc.nt, nk);
+      const int kb0 = KS ? __ffs(km) - 1 : 0;  // the first k-block initialises the accumulators
+      kb_run += KS ? __popc(km) : nk;
       for (int kb = 0; kb < nk; ++kb) {
-        if (!((km >> kb) & 1u)) continue;
+        if (KS && !((km >> kb) & 1u)) continue;
         const int es = ek & 1;
         if (SE) {
           oz_mbar_wait(&e_full[es], (ek >> 1) & 1);
@@ -1350,22 +1354,17 @@ bool oz_split_tma_ok(const OzakiParams& p) {
   return p.R < (int64_t(1) << 31) && p.L < (int64_t(1) << 31);
 }
 
-template <int S, bool AMN, bool OUTD, bool SE, bool REM = false>
-cudaError_t oz_gemm_go(const OzakiParams& p0, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
+template <int S, bool AMN, bool OUTD, bool SE, bool REM = false, bool KS = false>
+cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
   // zero-block skipping only where the MMAs pace the tile: the fp64-output launches.  In the digit-
   // output (chained) launches the epilogue's per-tile work is as long as the MMAs',
   // so a tile with fewer k-blocks is barely shorter, and the proportional CTA groups measured 3-20 %
   // slower there (the groups drift apart and the fibre tiles are read from DRAM twice, §4g)
-  OzakiParams pc;
-  const OzakiParams* pp = &p0;
-  if (OUTD && p0.kskip) {
-    pc = p0;
-    pc.kskip = 0;
-    pp = &pc;
+  if constexpr (!OUTD && !KS) {
+    if (p.kskip) return oz_gemm_go<S, AMN, OUTD, SE, REM, true>(p, st, ta, tb);
   }
-  const OzakiParams& p = *pp;
   if constexpr (!REM && (AMN || !OUTD)) {  // peer-store epilogues: fp64 outputs, or AMN next-mode digits
-    if (p.remap.world > 0) return oz_gemm_go<S, AMN, OUTD, SE, true>(p, st, ta, tb);
+    if (p.remap.world > 0) return oz_gemm_go<S, AMN, OUTD, SE, true, KS>(p, st, ta, tb);
   } else if constexpr (!REM) {
     if (p.remap.world > 0) return cudaErrorInvalidValue;
   }
@@ -1374,7 +1373,7 @@ cudaError_t oz_gemm_go(const OzakiParams& p0, cudaStream_t st, const CUtensorMap
   static int sms = 0;
   if (!gattr) {
     cudaError_t e =
-        cudaFuncSetAttribute(oz_gemm_kernel<S, AMN, OUTD, SE, REM>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaFuncSetAttribute(oz_gemm_kernel<S, AMN, OUTD, SE, REM, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1389,10 +1388,10 @@ cudaError_t oz_gemm_go(const OzakiParams& p0, cudaStream_t st, const CUtensorMap
   if (per < 1) per = 1;
   // kskip: every SM, the kernel splits them over the n-tiles by their work (OzSched)
   int64_t grid = per * ntn;
-  if (p.kskip) {
+  if (KS) {
     grid = units * ntn < sms ? units * ntn : sms;
   }
-  oz_gemm_kernel<S, AMN, OUTD, SE, REM><<<static_cast<unsigned>(grid), G::THREADS, G::SMEM, st>>>(p, ta, tb);
+  oz_gemm_kernel<S, AMN, OUTD, SE, REM, KS><<<static_cast<unsigned>(grid), G::THREADS, G::SMEM, st>>>(p, ta, tb);
   return cudaGetLastError();
 }
 

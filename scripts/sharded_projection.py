@@ -25,6 +25,9 @@ for P in [int(x) for x in os.environ.get("PS", "1,2,4,8").split(",")]:
     else:
         ranks = [ShardedPhiKS(blocks, r, P, connect=None) for r in range(P)]
         ShardedPhiKS.connect_local(ranks)
+    if os.environ.get("KSKIP") is not None:  # A/B of PHIKS_OPT_KSKIP
+        for r in ranks:
+            r.set_option("kskip", int(os.environ["KSKIP"]))
     ins = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, P)[r])).cuda() for x in xs] for r in range(P)]
     nout = len(wl.problems) * len(pb0.ells) if mode == "same" else pb0.n_scales
     outs = [[torch.empty(xs[0].size // P, dtype=torch.float64, device="cuda")
