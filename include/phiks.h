@@ -441,6 +441,17 @@ phiks_status phiks_shard_layout_ex(int d, const int* n, int rank, int world, int
    (rank-major); outs: world × (outputs per rank) device pointers. */
 phiks_status phiks_apply_ranks_serial(const phiks_handle* hs, int world, const phiks_request* req, int n_vecs,
                                       const double* const* vecs, double* const* outs, void* stream);
+/* The same with a filtered replay, for the multi-GPU projection only
+   (scripts/sharded_projection.py): which = 0 every kernel (= the call above),
+   1 only stage A (the exponential stage and its all-gather: what a real
+   apply runs on the handle's pre stream, overlapped with the previous apply),
+   2 everything but stage A.  With which = 2 the applies read the exponentials
+   an earlier full apply of the same handles left in their workspaces, so the
+   outputs are those of a full apply only when the same request ran with
+   which = 0 at least twice before (the two workspace halves).
+   PHIKS_ERR_ARG for another value. */
+phiks_status phiks_apply_ranks_serial_ex(const phiks_handle* hs, int world, const phiks_request* req, int n_vecs,
+                                         const double* const* vecs, double* const* outs, void* stream, int which);
 
 /* Message for the last error on the calling thread ("" if none). */
 const char* phiks_last_error(void);

@@ -93,6 +93,7 @@ def load() -> ctypes.CDLL:
     lib.phiks_shard_base.argtypes = [vp, P(vp)]
     lib.phiks_shard_set_peer_bases.argtypes = [vp, P(vp)]
     lib.phiks_apply_ranks_serial.argtypes = [P(vp), i, P(Request), i, P(vp), P(vp), vp]
+    lib.phiks_apply_ranks_serial_ex.argtypes = [P(vp), i, P(Request), i, P(vp), P(vp), vp, i]
     lib.phiks_wait.argtypes = [vp]
     lib.phiks_set_gemm_path.argtypes = [vp, i]
     lib.phiks_set_option.argtypes = [vp, i, i]
@@ -110,7 +111,7 @@ def load() -> ctypes.CDLL:
                  "phiks_get_stats", "phiks_mode_product", "phiks_tucker", "phiks_expm",
                  "phiks_fp64_peak_launch", "phiks_plan_host", "phiks_select_plan", "phiks_set_profiling",
                  "phiks_create_sharded", "phiks_shard_info", "phiks_shard_ipc_handle", "phiks_shard_open_peers",
-                 "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_shard_layout", "phiks_wait", "phiks_shard_peer_base", "phiks_create_complex", "phiks_plan_host_complex", "phiks_create_blocks",
+                 "phiks_shard_base", "phiks_shard_set_peer_bases", "phiks_apply_ranks_serial", "phiks_apply_ranks_serial_ex", "phiks_shard_layout", "phiks_wait", "phiks_shard_peer_base", "phiks_create_complex", "phiks_plan_host_complex", "phiks_create_blocks",
                  "phiks_create_sharded_blocks", "phiks_shard_layout_ex",
                  "phiks_create_sharded_complex", "phiks_create_blocks_complex",
                  "phiks_create_sharded_blocks_complex",

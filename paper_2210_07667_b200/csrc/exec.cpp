@@ -283,7 +283,7 @@ void Exec::mode_launch(int64_t L, int n, int64_t R, const std::vector<LaunchTerm
       ++launches;
       if (!measure) {
         std::shared_ptr<ModeParams> sp(pp);
-        rec->push_back(Op{false, [sp](cudaStream_t s) { return launch_mode_product(*sp, s); }, "mode_product"});
+        rec->push_back(Op{false, [sp](cudaStream_t s) { return launch_mode_product(*sp, s); }, "mode_product", stage_a});
       } else {
         delete pp;
       }

@@ -286,7 +286,9 @@ struct Exec {
     bool barrier;
     std::function<cudaError_t(cudaStream_t)> fn;
     const char* what;
+    bool pre = false;  // stage A (exponentials, before on_inputs): the part a real apply runs on s_pre
   };
+  bool stage_a = true;  // until on_inputs: the recorded ops belong to stage A
   std::vector<Op>* rec = nullptr;
   // host-memory applies: called (execute pass only) when the staged inputs are
   // first needed and when some outputs are final (their copy-out can start)
@@ -304,7 +306,7 @@ struct Exec {
     ++launches;
     if (measure || !ok()) return;
     if (rec)
-      rec->push_back(Op{false, std::move(fn), what});
+      rec->push_back(Op{false, std::move(fn), what, stage_a});
     else
       check(fn(st), what);
   }
@@ -318,7 +320,7 @@ struct Exec {
     ++launches;
     if (measure) return;
     if (rec) {
-      rec->push_back(Op{true, nullptr, "barrier"});
+      rec->push_back(Op{true, nullptr, "barrier", stage_a});
       return;
     }
     BarrierParams bp{};

@@ -272,6 +272,7 @@ void run_jobs(Exec& ex, const std::vector<Job>& jobs) {
   };
 
   // inputs staged from host memory are needed from here on (stage A overlaps their copy)
+  ex.stage_a = false;
   if (ex.on_inputs) ex.on_inputs();
 
   // ---- Stage D (same vector): exp(τK/2^j)v needs only the level matrices and

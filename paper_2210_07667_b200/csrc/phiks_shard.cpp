@@ -162,6 +162,12 @@ phiks_status phiks_shard_set_peer_bases(phiks_handle h, void* const* bases) {
 
 phiks_status phiks_apply_ranks_serial(const phiks_handle* hs, int world, const phiks_request* req, int n_vecs,
                                       const double* const* vecs, double* const* outs, void* stream) {
+  return phiks_apply_ranks_serial_ex(hs, world, req, n_vecs, vecs, outs, stream, 0);
+}
+
+phiks_status phiks_apply_ranks_serial_ex(const phiks_handle* hs, int world, const phiks_request* req, int n_vecs,
+                                         const double* const* vecs, double* const* outs, void* stream, int which) {
+  if (which < 0 || which > 2) return fail(PHIKS_ERR_ARG, "which must be 0, 1 or 2");
   if (!hs || world < 1 || world > kMaxRanks || !req || !vecs || !outs) return fail(PHIKS_ERR_ARG, "bad argument");
   for (int k = 0; k < world; ++k) {
     if (!hs[k] || hs[k]->world != world || hs[k]->rank != k) return fail(PHIKS_ERR_ARG, "hs[k] must be rank k of world");
@@ -211,6 +217,10 @@ phiks_status phiks_apply_ranks_serial(const phiks_handle* hs, int world, const p
     for (int k = 0; k < world; ++k) {
       auto& v = ops[k];
       while (pos[k] < v.size() && !v[pos[k]].barrier) {
+        if ((which == 1 && !v[pos[k]].pre) || (which == 2 && v[pos[k]].pre)) {  // filtered replay (timing)
+          ++pos[k];
+          continue;
+        }
         cudaError_t e = v[pos[k]].fn(cs);
         if (e != cudaSuccess) return fail(PHIKS_ERR_CUDA, std::string(v[pos[k]].what) + ": " + cudaGetErrorString(e));
         ++pos[k];

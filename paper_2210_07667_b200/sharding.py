@@ -133,9 +133,11 @@ class ShardedPhiKS:
 
 
 def apply_ranks_serial(ranks: Sequence[ShardedPhiKS], tau: float, ells: Sequence[int], vecs: Sequence[Sequence],
-                       mode: str = "same", n_scales: int = 1, tol: float = 0.0, outs=None, stream=None):
-    """Run every rank's apply phase by phase on ONE GPU (phiks_apply_ranks_serial).
-    vecs[k]: rank k's local input slabs (device tensors); returns outs[k]."""
+                       mode: str = "same", n_scales: int = 1, tol: float = 0.0, outs=None, stream=None,
+                       which: int = 0):
+    """Run every rank's apply phase by phase on ONE GPU (phiks_apply_ranks_serial_ex).
+    vecs[k]: rank k's local input slabs (device tensors); returns outs[k].  which: 0 every kernel,
+    1 / 2 only / all but stage A (projection timing, include/phiks.h)."""
     import torch
     from . import PhiKS, _check_dev, _stream_ptr
     world = len(ranks)
@@ -150,7 +152,7 @@ def apply_ranks_serial(ranks: Sequence[ShardedPhiKS], tau: float, ells: Sequence
     optr = [_check_dev(o, ranks[k].N, cplx) for k in range(world) for o in outs[k]]
     req = _lib.make_request(m, ells, n_scales, tau, tol)
     hs = (ctypes.c_void_p * world)(*[r.op._h.value for r in ranks])
-    _lib.check(_lib.load().phiks_apply_ranks_serial(hs, world, ctypes.byref(req), len(vecs[0]),
-                                                    _lib.ptr_array(vptr), _lib.ptr_array(optr),
-                                                    _stream_ptr(stream)), "phiks_apply_ranks_serial")
+    _lib.check(_lib.load().phiks_apply_ranks_serial_ex(hs, world, ctypes.byref(req), len(vecs[0]),
+                                                       _lib.ptr_array(vptr), _lib.ptr_array(optr),
+                                                       _stream_ptr(stream), int(which)), "phiks_apply_ranks_serial_ex")
     return outs

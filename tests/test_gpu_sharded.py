@@ -303,3 +303,33 @@ def test_sharded_presplit_bitwise(dims, world, mode):
     compare_oracle(pb, res[0], pb.n_scales)
     for a, b in zip(*res):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("path", ["dmma", "i8"])
+def test_ranks_serial_filtered_replay(path):
+    """phiks_apply_ranks_serial_ex (projection timing, include/phiks.h): stage A alone (which = 1)
+    then the rest (which = 2) reproduces a full apply bit for bit, and so does the rest alone once
+    both workspace halves hold the exponentials of earlier full applies."""
+    pb = W.config(3, small=True).problems[0]
+    world = 4
+    ranks = [ShardedPhiKS(pb.A, r, world, connect=None) for r in range(world)]
+    ShardedPhiKS.connect_local(ranks)
+    for r in ranks:
+        r.set_gemm_path(path)
+    flat = [W.as_flat(v) for v in pb.vs]
+    vecs = [[torch.from_numpy(np.ascontiguousarray(split_slabs(x, world)[r])).to(DEV) for x in flat]
+            for r in range(world)]
+
+    def run(which):
+        o = apply_ranks_serial(ranks, pb.tau, pb.ells, vecs, mode=pb.mode, n_scales=pb.n_scales, which=which)
+        torch.cuda.synchronize()
+        return [t.cpu().numpy() for k in range(world) for t in o[k]]
+    full = run(0)
+    run(0)
+    for which in (2, 2):
+        for a, b in zip(full, run(which)):
+            assert np.array_equal(a, b)
+    with pytest.raises(Exception):
+        run(3)
+    for r in ranks:
+        r.close()
