@@ -1095,7 +1095,13 @@ __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
 #ifndef OZ_KS_FIX
 #define OZ_KS_FIX 12
 #endif
-  const OzSched sc(p, skm, OZ_KS_FIX, KS);
+#ifndef OZ_KS_FIX_OUTD
+#define OZ_KS_FIX_OUTD 32
+#endif
+#ifndef OZ_KS_FIX_AMN_OUTD
+#define OZ_KS_FIX_AMN_OUTD 24
+#endif
+  const OzSched sc(p, skm, OUTD ? (AMN ? OZ_KS_FIX_AMN_OUTD : OZ_KS_FIX_OUTD) : OZ_KS_FIX, KS);
   if (sc.q >= sc.Q) return;  // idle CTA (grid not a multiple of the n-tile count)
   const int nk = p.Kp / kOzBK;
   constexpr int NSG = S / G::SPS;
@@ -1356,12 +1362,20 @@ bool oz_split_tma_ok(const OzakiParams& p) {
 
 template <int S, bool AMN, bool OUTD, bool SE, bool REM = false, bool KS = false>
 cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb) {
-  // zero-block skipping only where the MMAs pace the tile: the fp64-output launches.  In the digit-
-  // output (chained) launches the epilogue's per-tile work is as long as the MMAs',
-  // so a tile with fewer k-blocks is barely shorter, and the proportional CTA groups measured 3-20 %
-  // slower there (the groups drift apart and the fibre tiles are read from DRAM twice, §4g)
-  if constexpr (!OUTD && !KS) {
-    if (p.kskip) return oz_gemm_go<S, AMN, OUTD, SE, REM, true>(p, st, ta, tb);
+  // zero-block skipping where a tile with fewer k-blocks is shorter: the fp64-output
+  // launches (the MMAs pace the tile; CTA groups by 16·kb + 12), the mode-1 digit-output launches
+  // (K-major A, the lighter digit epilogue; 16·kb + 32), and the MN-major digit-output launches from
+  // four k-blocks on (n > 384: the MMAs outweigh the epilogue again; 16·kb + 24).  With two k-blocks
+  // the MN-major digit epilogue's per-tile work is as long as the MMAs' (§4e), a tile with fewer
+  // k-blocks is barely shorter, and every grouping measured 3-20 % slower (the groups drift apart and
+  // the fibre tiles are read from DRAM twice); with one k-block there is nothing to skip
+#ifndef OZ_KS_AMN_OUTD_MINK
+#define OZ_KS_AMN_OUTD_MINK 4
+#endif
+  if constexpr (!KS) {
+    const int nk = p.Kp / kOzBK;
+    if (p.kskip && nk >= 2 && (!OUTD || !AMN || nk >= OZ_KS_AMN_OUTD_MINK))
+      return oz_gemm_go<S, AMN, OUTD, SE, REM, true>(p, st, ta, tb);
   }
   if constexpr (!REM && (AMN || !OUTD)) {  // peer-store epilogues: fp64 outputs, or AMN next-mode digits
     if (p.remap.world > 0) return oz_gemm_go<S, AMN, OUTD, SE, true, KS>(p, st, ta, tb);
