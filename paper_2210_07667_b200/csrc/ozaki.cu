@@ -1010,10 +1010,10 @@ __device__ __forceinline__ unsigned oz_kmask(const OzakiParams& p, const uint32_
   const unsigned m = (skm[p.terms[i].eslot] >> (4 * t)) & full;
   return m ? m : 1u;
 }
-// kskip: the n-tile groups get CTAs in proportion to their work, Σ_terms (16·#k-blocks + 12) (a tile
+// kskip: the n-tile groups get CTAs in proportion to their work, Σ_terms (16·#k-blocks + fix) (a tile
 // of the configs[3] launches: ~4,150 cycles of MMAs per k-block and a ~2,350-cycle hand-over,
-// DESIGN.md §4e), so that the groups sweep the fibre tiles at the same rate and the L2 still
-// serves each fibre tile once for all of them
+// DESIGN.md §4e; fix per launch kind, measured: §4g), so that the groups sweep the fibre tiles at the
+// same rate and the L2 still serves each fibre tile once for all of them (ntn ≤ 8: n ≤ kOzMaxN)
 struct OzSched {
   int ntn, nt, q, Q, nk;
   int64_t Mt, units;
@@ -1068,7 +1068,7 @@ struct OzSched {
 
 // SE: the E digits stream through a 2-block ring (one 128-k block per stage group) instead of
 // staying resident per term: always for n > 256, and for short launches (kOzSeUnits)
-// KS: skip the all-zero E digit blocks (PHIKS_OPT_KSKIP, fp64-output launches only)
+// KS: skip the all-zero E digit blocks (PHIKS_OPT_KSKIP; oz_gemm_go picks the launches)
 template <int S, bool AMN, bool OUTD, bool SE, bool REM, bool KS>
 __global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
