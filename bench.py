@@ -224,6 +224,7 @@ def i8_roofline(args, t_local, mp_ms, mp_fl, mp_n, i8_ms, i8_fl, g_ms, g_n, ex_n
                       "the Tucker-operator μ-mode products",
             "algorithmic_ops_per_launch": ops / max(g_n, 1),
             "dense_ops_per_launch": dense_ops / max(g_n, 1),
+            "frac_dense_equivalent": (dense_ops / (g_ms / 1e3) / 1e12 / peak) if g_ms > 0 else None,
             "kblocks_run_fraction": run_frac,
             "kblocks_note": "(fibre tile x 64-row n-tile, 128-wide k-block) units whose E digits are not all zero "
                             "(PHIKS_OPT_KSKIP, DESIGN.md §4g); the skipped ones add exact integer zeros",
