@@ -272,23 +272,39 @@ __global__ void __launch_bounds__(256) oz_split_x_contig_kernel(const OzakiParam
 // accumulation order of multi_combine_kernel: sources in order, acc += c·x), the fp64 outputs
 // are stored, and the outputs with dig[o] set are also split into digit planes exactly as
 // oz_split_x_contig_kernel would split them after reading them back.
-template <int NOUT, int EPL>
-__global__ void __launch_bounds__(256) oz_multi_combine_split_kernel(const __grid_constant__ MultiCombineParams p) {
+#ifndef OZ_MC_UNROLL
+#define OZ_MC_UNROLL 2
+#endif
+// FS warps per fibre (1 or 2): with FS = 2 each warp sums half of the fibre (EPL = Kp/64 per lane), so
+// the wide variants need half the registers and twice the warps fit per SM; the two halves meet for
+// the fibre exponent in shared memory behind a named barrier of the warp pair
+template <int NOUT, int EPL, int WPB = 8, int FS = 1>
+__global__ void __launch_bounds__(WPB * 32) oz_multi_combine_split_kernel(const __grid_constant__ MultiCombineParams p) {
+  static_assert(FS == 1 || (FS == 2 && WPB % 2 == 0 && WPB <= 30), "warp pairs");
   constexpr int S = 7;
   const int n = p.fn, Kp = p.Kp;
   const int64_t C = p.count / n;
-  const int lane = threadIdx.x & 31;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (c >= C) return;
-  const int k0 = EPL * lane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = warp % FS;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * (WPB / FS) + warp / FS;
+  const bool active = c < C;  // uniform per warp pair (an idle pair still meets at its barriers)
+  if (FS == 1 && !active) return;
+  const int k0 = EPL * (32 * h + lane);
+  __shared__ unsigned s_hm[FS == 2 ? NOUT : 1][WPB];
+  __shared__ double s_m[FS == 2 ? NOUT : 1][WPB];
+  auto pair_sync = [&]() {
+    if constexpr (FS == 2) asm volatile("bar.sync %0, 64;\n" ::"r"(1 + (warp >> 1)) : "memory");
+  };
   const bool vec = n == Kp;  // full lanes, 16-byte aligned rows (checked by the launcher)
   double acc[NOUT][EPL];
 #pragma unroll
   for (int o = 0; o < NOUT; ++o)
 #pragma unroll
     for (int q = 0; q < EPL; ++q) acc[o][q] = 0.0;
-  for (int s = 0; s < p.nsrc; ++s) {
-    double x[EPL];
+  // U sources per iteration, all loads issued before the sums: with NOUT·EPL accumulators in registers
+  // the wide variants run one 8-warp block per SM, and one source in flight per warp left them at
+  // ~0.6 of the copy peak (configs[4]: NOUT 4, EPL 16)
+  constexpr int U = OZ_MC_UNROLL;
+  auto load = [&](int s, double (&x)[EPL]) {
     const double* src = p.src[s] + c * n;
     if (vec) {
 #pragma unroll
@@ -301,6 +317,25 @@ __global__ void __launch_bounds__(256) oz_multi_combine_split_kernel(const __gri
 #pragma unroll
       for (int q = 0; q < EPL; ++q) x[q] = k0 + q < n ? __ldcs(src + k0 + q) : 0.0;
     }
+  };
+  int s0 = 0;
+  const int nsrc = active ? p.nsrc : 0;
+  for (; s0 + U <= nsrc; s0 += U) {
+    double x[U][EPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) load(s0 + u, x[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) {
+        const double cf = p.coef[o][s0 + u];
+#pragma unroll
+        for (int q = 0; q < EPL; ++q) acc[o][q] += cf * x[u][q];
+      }
+  }
+  for (int s = s0; s < nsrc; ++s) {
+    double x[EPL];
+    load(s, x);
 #pragma unroll
     for (int o = 0; o < NOUT; ++o) {
       const double cf = p.coef[o][s];
@@ -312,7 +347,8 @@ __global__ void __launch_bounds__(256) oz_multi_combine_split_kernel(const __gri
   for (int o = 0; o < NOUT; ++o) {
     if (o >= p.nout) break;
     double* dst = p.dst[o] + c * n;
-    if (vec) {
+    if (!active) {
+    } else if (vec) {
 #pragma unroll
       for (int i = 0; i < EPL / 2; ++i)
         reinterpret_cast<double2*>(dst + k0)[i] = make_double2(acc[o][2 * i], acc[o][2 * i + 1]);
@@ -323,11 +359,38 @@ __global__ void __launch_bounds__(256) oz_multi_combine_split_kernel(const __gri
     }
     if (p.dig[o]) {
       bool bad;
-      const int ex = oz_fibre_exponent<S, EPL>(acc[o], bad);
+      int ex;
+      if constexpr (FS == 1) {
+        ex = oz_fibre_exponent<S, EPL>(acc[o], bad);
+      } else {  // oz_fibre_exponent over the two halves of the fibre
+        unsigned hm = 0;
+#pragma unroll
+        for (int q = 0; q < EPL; ++q) hm = max(hm, static_cast<unsigned>(__double2hiint(acc[o][q])) & 0x7fffffffu);
+        hm = __reduce_max_sync(0xffffffffu, hm);
+        if (lane == 0) s_hm[o][warp] = hm;
+        pair_sync();
+        hm = max(s_hm[o][warp & ~1], s_hm[o][warp | 1]);
+        bad = hm >= 0x7ff00000u;
+        if (bad) {
+          ex = 0;
+        } else if (hm >= 0x00100000u) {
+          ex = static_cast<int>(hm >> 20) - 1021;
+        } else {  // subnormal maxima: the exact fp64 path (hm is the pair's, so both warps take it)
+          double m = 0.0;
+#pragma unroll
+          for (int q = 0; q < EPL; ++q) m = fmax(m, fabs(acc[o][q]));
+          m = warp_max(m);
+          if (lane == 0) s_m[o][warp] = m;
+          pair_sync();
+          ex = slice_exponent(fmax(s_m[o][warp & ~1], s_m[o][warp | 1]));
+        }
+      }
       uint32_t pk[EPL / 4][S];
       oz_split_lane<S, EPL>(acc[o], ex, bad, pk);
-      oz_store_lane<S, EPL>(p.dig[o] + c * Kp + k0, C * Kp, pk);
-      if (lane == 0) p.dsc[o][c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
+      if (active) {
+        oz_store_lane<S, EPL>(p.dig[o] + c * Kp + k0, C * Kp, pk);
+        if (lane == 0 && h == 0) p.dsc[o][c] = bad ? __longlong_as_double(0x7ff8000000000000ll) : ex;
+      }
     }
   }
 }
@@ -1536,6 +1599,14 @@ cudaError_t launch_multi_combine_split(const MultiCombineParams& p, cudaStream_t
   if (!aligned) return cudaErrorMisalignedAddress;
   const int64_t C = p.count / n;
   const dim3 g(static_cast<unsigned>((C + 7) / 8));
+  // the wide variants (NOUT·EPL ≥ 48 sums in registers, ~180-220 registers) fit one 8-warp block per
+  // SM, whose load and store phases then alternate; smaller blocks let several blocks per SM overlap
+#ifndef OZ_MC_WPB_WIDE
+#define OZ_MC_WPB_WIDE 8
+#endif
+  constexpr int WW = OZ_MC_WPB_WIDE;
+  const dim3 gw(static_cast<unsigned>((C + WW - 1) / WW));
+  const dim3 g2(static_cast<unsigned>((C + 3) / 4));  // warp pairs: 4 fibres per 8-warp block
   const int no = p.nout <= 2 ? 2 : (p.nout <= 4 ? 4 : 8);
   switch (p.Kp * 10 + no) {  // Kp = n rounded up to 128
     case 1282: oz_multi_combine_split_kernel<2, 4><<<g, 256, 0, st>>>(p); break;
@@ -1543,11 +1614,11 @@ cudaError_t launch_multi_combine_split(const MultiCombineParams& p, cudaStream_t
     case 1288: oz_multi_combine_split_kernel<8, 4><<<g, 256, 0, st>>>(p); break;
     case 2562: oz_multi_combine_split_kernel<2, 8><<<g, 256, 0, st>>>(p); break;
     case 2564: oz_multi_combine_split_kernel<4, 8><<<g, 256, 0, st>>>(p); break;
-    case 2568: oz_multi_combine_split_kernel<8, 8><<<g, 256, 0, st>>>(p); break;
+    case 2568: oz_multi_combine_split_kernel<8, 4, 8, 2><<<g2, 256, 0, st>>>(p); break;
     case 3842: oz_multi_combine_split_kernel<2, 12><<<g, 256, 0, st>>>(p); break;
-    case 3844: oz_multi_combine_split_kernel<4, 12><<<g, 256, 0, st>>>(p); break;
+    case 3844: oz_multi_combine_split_kernel<4, 12, WW><<<gw, WW * 32, 0, st>>>(p); break;
     case 5122: oz_multi_combine_split_kernel<2, 16><<<g, 256, 0, st>>>(p); break;
-    case 5124: oz_multi_combine_split_kernel<4, 16><<<g, 256, 0, st>>>(p); break;
+    case 5124: oz_multi_combine_split_kernel<4, 8, 8, 2><<<g2, 256, 0, st>>>(p); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

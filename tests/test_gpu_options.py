@@ -198,3 +198,30 @@ def test_presplit_nonfinite_inputs():
     for a, b in zip(*res):
         np.testing.assert_array_equal(a, b)
         assert np.isnan(a).any()
+
+
+@pytest.mark.parametrize("dims,ells", [
+    ((512, 128), (0, 1, 2, 3, 4)),      # 4 inputs per level at n = 512: two warps per fibre (FS = 2)
+    ((256, 128, 16), (0, 1, 2, 3, 4)),  # up to 8 outputs per pass at n = 256: two warps per fibre
+])
+@pytest.mark.parametrize("scale", [1.0, 1e-310])
+def test_presplit_warp_pairs_bitwise(dims, ells, scale):
+    """The combination + split variants that sum each fibre with two warps (their fibre exponent
+    meets in shared memory): bitwise equal to the separate split, also for fibres of subnormal
+    magnitude (the exact fp64 maximum path, a second exchange between the two warps)."""
+    A = [W.fd_dxx_neumann(n) * (0.3 / (k + 1)) for k, n in enumerate(dims)]
+    vs = [W.uniform_tensor(dims, -1.0, 1.0, seed=90 + k) * scale for k in range(len(ells))]
+    res, hits = [], []
+    for pre in (1, 0):
+        op = PhiKS(A)
+        op.set_gemm_path("i8")
+        op.set_option("presplit", pre)
+        outs = op.apply(3e-5, ells, [torch.from_numpy(np.ascontiguousarray(W.as_flat(v))).to(DEV) for v in vs],
+                        mode="lincomb", n_scales=4)
+        torch.cuda.synchronize()
+        hits.append(op.stats()["presplit_inputs"])
+        res.append([o.cpu().numpy() for o in outs])
+    assert hits[0] > 0 and hits[1] == 0, hits
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+        assert np.all(np.isfinite(a))
