@@ -1039,7 +1039,15 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
 // mode 1.87 / 1.72 / 1.64 / 1.57 (the shared-memory carve-out also sizes the L1 the
 // digit epilogue's stores go through).  Round 2 (integer epilogue, balanced MMA halves): mode 1
 // at 5 or 6 stages 3.4 % faster than at 4, mode 2 at 7 slightly slower than at 6
-__host__ __device__ constexpr int oz_nst(bool amn, bool outd) { return outd ? (amn ? 6 : 5) : 7; }
+#ifndef OZ_NST_KS_K
+#define OZ_NST_KS_K 5
+#endif
+#ifndef OZ_NST_KS_D
+#define OZ_NST_KS_D 7
+#endif
+__host__ __device__ constexpr int oz_nst(bool amn, bool outd, bool ks = false) {
+  return outd ? (amn ? 6 : (ks ? OZ_NST_KS_K : 5)) : (ks ? OZ_NST_KS_D : 7);
+}
 template <int S, int NST_ = 6>
 struct OzGeom {
   static constexpr int SPS = 1;                                // digits per stage
@@ -1133,10 +1141,10 @@ struct OzSched {
 // staying resident per term: always for n > 256, and for short launches (kOzSeUnits)
 // KS: skip the all-zero E digit blocks (PHIKS_OPT_KSKIP; oz_gemm_go picks the launches)
 template <int S, bool AMN, bool OUTD, bool SE, bool REM, bool KS>
-__global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD)>::THREADS, 1)
+__global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD, KS)>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb) {
-  using G = OzGeom<S, oz_nst(AMN, OUTD)>;
+  using G = OzGeom<S, oz_nst(AMN, OUTD, KS)>;
   extern __shared__ uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* bres = smem + G::NST * G::A_BYTES;
@@ -1445,7 +1453,7 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   } else if constexpr (!REM) {
     if (p.remap.world > 0) return cudaErrorInvalidValue;
   }
-  using G = OzGeom<S, oz_nst(AMN, OUTD)>;
+  using G = OzGeom<S, oz_nst(AMN, OUTD, KS)>;
   static bool gattr = false;
   static int sms = 0;
   if (!gattr) {
