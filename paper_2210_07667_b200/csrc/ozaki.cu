@@ -1439,13 +1439,19 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   // four k-blocks on (n > 384: the MMAs outweigh the epilogue again; 16·kb + 24).  With two k-blocks
   // the MN-major digit epilogue's per-tile work is as long as the MMAs' (§4e), a tile with fewer
   // k-blocks is barely shorter, and every grouping measured 3-20 % slower (the groups drift apart and
-  // the fibre tiles are read from DRAM twice); with one k-block there is nothing to skip
+  // the fibre tiles are read from DRAM twice); with one k-block there is nothing to skip; nor in a
+  // slab-sharded rank's short peer-store launches (streamed E, few tiles per CTA: emulated P = 8
+  // 9.0-9.2 → 8.95-8.97 ms per step without skipping there, configs[4] 92.5-95.8 → 91.8-93.1)
 #ifndef OZ_KS_AMN_OUTD_MINK
 #define OZ_KS_AMN_OUTD_MINK 4
 #endif
+#ifndef OZ_KS_REM_SHORT
+#define OZ_KS_REM_SHORT 0
+#endif
   if constexpr (!KS) {
     const int nk = p.Kp / kOzBK;
-    if (p.kskip && nk >= 2 && (!OUTD || !AMN || nk >= OZ_KS_AMN_OUTD_MINK))
+    const bool rem_short = p.remap.world > 0 && SE && p.Kp <= kOzMaxNRes;  // a rank's short peer-store launch
+    if (p.kskip && nk >= 2 && (!OUTD || !AMN || nk >= OZ_KS_AMN_OUTD_MINK) && (OZ_KS_REM_SHORT || !rem_short))
       return oz_gemm_go<S, AMN, OUTD, SE, REM, true>(p, st, ta, tb);
   }
   if constexpr (!REM && (AMN || !OUTD)) {  // peer-store epilogues: fp64 outputs, or AMN next-mode digits
