@@ -1048,7 +1048,13 @@ __device__ __forceinline__ void oz_epilogue_tile(const OzakiParams& p, int term_
 __host__ __device__ constexpr int oz_nst(bool amn, bool outd, bool ks = false) {
   return outd ? (amn ? 6 : (ks ? OZ_NST_KS_K : 5)) : (ks ? OZ_NST_KS_D : 7);
 }
-template <int S, int NST_ = 6>
+#ifndef OZ_EPC_D
+#define OZ_EPC_D 32
+#endif
+// columns per epilogue warp: 32 (16, i.e. 16 epilogue warps at 96 registers: 8 % slower on every
+// kernel in r02; on the fp64-output kernels alone 7 % slower, profiles/r02_ab_kskip/ab12_epc16_fp64.txt)
+__host__ __device__ constexpr int oz_epc(bool outd) { return outd ? 32 : OZ_EPC_D; }
+template <int S, int NST_ = 6, int EPC_ = 32>
 struct OzGeom {
   static constexpr int SPS = 1;                                // digits per stage
   static constexpr int A_BYTES = SPS * kOzBM * kOzBK;         // one stage
@@ -1056,7 +1062,7 @@ struct OzGeom {
   static constexpr int B_KB = S * kOzBN * kOzBK;              // resident E slices per k-block
   static constexpr int B_BYTES = (kOzMaxNRes / kOzBK) * B_KB; // resident (Kp ≤ 256) or a 2-block ring (SE)
   static constexpr int SMEM = NST * A_BYTES + B_BYTES + 1024 /*align*/ + 512 /*barriers*/;
-  static constexpr int EPC = 32;  // columns per epilogue warp (16, i.e. 16 epilogue warps at 96 registers: 8 % slower, r02)
+  static constexpr int EPC = EPC_;
   static constexpr int EPI_WARPS = 4 * kOzBN / EPC;             // 2 per TMEM lane quarter (column halves)
   static constexpr int THREADS = 64 + EPI_WARPS * 32;
   static_assert(S * kOzBN <= 512, "TMEM holds one 64-column accumulator per diagonal");
@@ -1141,10 +1147,10 @@ struct OzSched {
 // staying resident per term: always for n > 256, and for short launches (kOzSeUnits)
 // KS: skip the all-zero E digit blocks (PHIKS_OPT_KSKIP; oz_gemm_go picks the launches)
 template <int S, bool AMN, bool OUTD, bool SE, bool REM, bool KS>
-__global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD, KS)>::THREADS, 1)
+__global__ void __launch_bounds__(OzGeom<S, oz_nst(AMN, OUTD, KS), oz_epc(OUTD)>::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ OzakiParams p, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb) {
-  using G = OzGeom<S, oz_nst(AMN, OUTD, KS)>;
+  using G = OzGeom<S, oz_nst(AMN, OUTD, KS), oz_epc(OUTD)>;
   extern __shared__ uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* bres = smem + G::NST * G::A_BYTES;
@@ -1459,7 +1465,7 @@ cudaError_t oz_gemm_go(const OzakiParams& p, cudaStream_t st, const CUtensorMap&
   } else if constexpr (!REM) {
     if (p.remap.world > 0) return cudaErrorInvalidValue;
   }
-  using G = OzGeom<S, oz_nst(AMN, OUTD, KS)>;
+  using G = OzGeom<S, oz_nst(AMN, OUTD, KS), oz_epc(OUTD)>;
   static bool gattr = false;
   static int sms = 0;
   if (!gattr) {
